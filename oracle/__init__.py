@@ -1,0 +1,165 @@
+"""ctypes wrapper of the plain-C RSI oracle (rsi_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: importable from tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  The product package
+(paper_2508_01485_b200) never imports this module, and this module never
+imports the product package.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_P = ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "rsi_oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        # -O2, no OpenMP, no -ffast-math: IEEE fp64, single thread
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-shared", "-fPIC", src, "-o", _LIB_PATH, "-lm"])
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        i64, i32 = ctypes.c_int64, ctypes.c_int32
+        lib.oracle_select_targets.restype = i64
+        lib.oracle_select_targets.argtypes = [i64, _P, i32, _P]
+        lib.oracle_border.restype = i64
+        lib.oracle_border.argtypes = [i64, _P, _P, _P, _P]
+        lib.oracle_counts.argtypes = [i64, _P, _P, _P, i32, _P, _P, _P]
+        lib.oracle_weights.argtypes = [i64, i32, _P, _P]
+        lib.oracle_weights_closed_form.argtypes = [i64, i32, _P, _P]
+        lib.oracle_omega_max.restype = ctypes.c_double
+        lib.oracle_omega_max.argtypes = [i64, i32, _P]
+        lib.oracle_pred.restype = i64
+        lib.oracle_pred.argtypes = [i64, _P, _P, _P, _P, _P]
+        lib.oracle_rsi.argtypes = [i64, _P, _P, _P, i32, _P, _P, ctypes.c_double, i64, _P, _P, _P, _P]
+        lib.oracle_topk.restype = i64
+        lib.oracle_topk.argtypes = [i64, _P, i64, _P, _P]
+        _lib = lib
+    return _lib
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def _ptr(a):
+    return a.ctypes.data
+
+
+def select_targets(comm, k):
+    comm = _c(comm, np.int32)
+    out = np.zeros(max(k, 1), dtype=np.int32)
+    nc = _load().oracle_select_targets(comm.size, _ptr(comm), k, _ptr(out))
+    if nc < 0:
+        raise ValueError(f"k={k} out of range")
+    return out[:k]
+
+
+def border(g):
+    out = np.zeros(g.n, dtype=np.uint8)
+    _load().oracle_border(g.n, _ptr(_c(g.rowptr, np.int64)), _ptr(_c(g.col, np.int32)),
+                          _ptr(_c(g.comm, np.int32)), _ptr(out))
+    return out
+
+
+def counts(g, targets):
+    targets = _c(targets, np.int32)
+    k = targets.size
+    f = np.zeros((g.n, k), dtype=np.int32)
+    T = np.zeros(g.n, dtype=np.int32)
+    _load().oracle_counts(g.n, _ptr(_c(g.rowptr, np.int64)), _ptr(_c(g.col, np.int32)),
+                          _ptr(_c(g.comm, np.int32)), k, _ptr(targets), _ptr(f), _ptr(T))
+    return f, T
+
+
+def weights(f, closed_form=False):
+    f = _c(f, np.int32)
+    n, k = f.shape
+    w = np.zeros((n, k), dtype=np.float64)
+    fn = _load().oracle_weights_closed_form if closed_form else _load().oracle_weights
+    fn(n, k, _ptr(f), _ptr(w))
+    return w
+
+
+def omega_max(w):
+    w = _c(w, np.float64)
+    return float(_load().oracle_omega_max(w.shape[0], w.shape[1], _ptr(w)))
+
+
+def pred(g):
+    off = np.zeros(g.n + 1, dtype=np.int64)
+    rp, cl, cm = _c(g.rowptr, np.int64), _c(g.col, np.int32), _c(g.comm, np.int32)
+    cnt = _load().oracle_pred(g.n, _ptr(rp), _ptr(cl), _ptr(cm), _ptr(off), None)
+    lists = np.zeros(max(cnt, 1), dtype=np.int32)
+    _load().oracle_pred(g.n, _ptr(rp), _ptr(cl), _ptr(cm), _ptr(off), _ptr(lists))
+    return off, lists[:cnt]
+
+
+def rsi(g, targets, w, wmax, heads=None):
+    targets = _c(targets, np.int32)
+    heads = np.arange(g.n, dtype=np.int64) if heads is None else _c(heads, np.int64)
+    R = np.zeros(heads.size, dtype=np.float64)
+    nI = np.zeros(heads.size, dtype=np.int64)
+    nII = np.zeros(heads.size, dtype=np.int64)
+    w = _c(w, np.float64)
+    _load().oracle_rsi(g.n, _ptr(_c(g.rowptr, np.int64)), _ptr(_c(g.col, np.int32)),
+                       _ptr(_c(g.comm, np.int32)), targets.size, _ptr(targets), _ptr(w), float(wmax),
+                       heads.size, _ptr(heads), _ptr(R), _ptr(nI), _ptr(nII))
+    return R, nI, nII
+
+
+def topk(R, K):
+    R = _c(R, np.float64)
+    ids = np.zeros(max(K, 1), dtype=np.int32)
+    sc = np.zeros(max(K, 1), dtype=np.float64)
+    cnt = _load().oracle_topk(R.size, _ptr(R), K, _ptr(ids), _ptr(sc))
+    return ids[:cnt], sc[:cnt]
+
+
+@dataclass
+class OracleResult:
+    targets: np.ndarray
+    border: np.ndarray
+    f: np.ndarray
+    T: np.ndarray
+    omega: np.ndarray
+    omega_max: float
+    pred_off: np.ndarray
+    pred: np.ndarray
+    R: np.ndarray
+    nI: np.ndarray
+    nII: np.ndarray
+    top_ids: np.ndarray
+    top_scores: np.ndarray
+
+
+def run(g, k=None, targets=None, K=25, heads=None) -> OracleResult:
+    """O0-O8 end to end.  ``heads`` limits O5-O7 to a sample;
+    top-K is then over the sampled heads' scores only (positions)."""
+    if targets is None:
+        targets = select_targets(g.comm, k)
+    targets = _c(targets, np.int32)
+    b = border(g)
+    f, T = counts(g, targets)
+    w = weights(f)
+    wmax = omega_max(w)
+    off, pl = pred(g)
+    R, nI, nII = rsi(g, targets, w, wmax, heads)
+    ids, sc = topk(R, K)
+    return OracleResult(targets, b, f, T, w, wmax, off, pl, R, nI, nII, ids, sc)

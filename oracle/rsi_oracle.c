@@ -1,0 +1,268 @@
+/*
+ * RSI ORACLE — plain, slow, single-threaded CPU definition of the method of
+ * arXiv 2508.01485 ("A Parallel Algorithm for Finding Robust Spanners in
+ * Large Social Networks"), written from PAPER.md.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load or call this
+ * library. The product path (paper_2508_01485_b200/, librs.so) never links,
+ * imports or executes it, and shares no code, header, helper or table with
+ * it. Citations "P:n" are PAPER.md line numbers; "C-n" are the readings
+ * listed in SURVEY.md §8(c) and DESIGN.md §3.
+ *
+ * Precision: IEEE fp64 everywhere (the paper states none; C-19), base-2
+ * logarithms (C-2, forced by the worked example's H = 1 at P:491), and the
+ * per-head triad sum taken exactly in 128-bit fixed point with quantum 2^-80
+ * so the sum is independent of enumeration order (C-12): each fp64 term is
+ * rounded once to the 2^-80 grid, summed exactly, and converted back with one
+ * rounding.
+ *
+ * Every function below is pinned by tests/test_oracle_*.py against values the
+ * paper prints, closed forms, special cases and an independent brute-force
+ * O(n^3) triple enumeration (tests/bruteforce.py). None is "parity unpinned".
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+/* ---- O0. Target communities ("sort ... by size in descending
+ * order and select the top k"; C-15 ties -> ascending community id). ---- */
+typedef struct { int32_t id; int64_t size; } comm_size;
+
+static int cmp_i32(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+static int cmp_size_desc_id_asc(const void *a, const void *b) {
+    const comm_size *x = a, *y = b;
+    if (x->size != y->size) return x->size > y->size ? -1 : 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+/* returns the number of distinct communities, or -1 if k is out of range */
+int64_t oracle_select_targets(int64_t n, const int32_t *C, int32_t k, int32_t *targets_out) {
+    int32_t *s = malloc(sizeof(int32_t) * (n ? n : 1));
+    memcpy(s, C, sizeof(int32_t) * n);
+    qsort(s, (size_t)n, sizeof(int32_t), cmp_i32);
+    comm_size *cs = malloc(sizeof(comm_size) * (n ? n : 1));
+    int64_t nc = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (i == 0 || s[i] != s[i - 1]) { cs[nc].id = s[i]; cs[nc].size = 0; nc++; }
+        cs[nc - 1].size++;
+    }
+    qsort(cs, (size_t)nc, sizeof(comm_size), cmp_size_desc_id_asc);
+    int64_t ret = nc;
+    if (k < 1 || k > nc) ret = -1;
+    else for (int32_t i = 0; i < k; i++) targets_out[i] = cs[i].id;
+    free(s); free(cs);
+    return ret;
+}
+
+/* column of community c among the k targets, or -1 (the symbol ⊥) */
+static int32_t column_of(int32_t c, int32_t k, const int32_t *targets) {
+    for (int32_t i = 0; i < k; i++) if (targets[i] == c) return i;
+    return -1;
+}
+
+/* ---- O1. Border vertices ("u is called a community border vertex if
+ * there exists at least one neighbor v in N(u) such that C(u) != C(v)";
+ * Algorithm 1 Step 1). Over ALL communities. ---- */
+int64_t oracle_border(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C,
+                      uint8_t *border_out) {
+    int64_t nb = 0;
+    for (int64_t u = 0; u < n; u++) {
+        uint8_t b = 0;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++)
+            if (C[col[e]] != C[u]) { b = 1; break; }
+        border_out[u] = b;
+        nb += b;
+    }
+    return nb;
+}
+
+/* ---- O2. Neighbour-community histogram (P:452-453 count_neighbor_community:
+ * "counting the number of neighbors belonging to each community"
+ * T = sum of the k considered communities; C-5: only the k targets count).
+ * f_out is n*k row-major, T_out is n. ---- */
+void oracle_counts(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C,
+                   int32_t k, const int32_t *targets, int32_t *f_out, int32_t *T_out) {
+    for (int64_t u = 0; u < n; u++) {
+        int32_t *f = f_out + u * k;
+        for (int32_t i = 0; i < k; i++) f[i] = 0;
+        int32_t T = 0;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) {
+            int32_t j = column_of(C[col[e]], k, targets);
+            if (j >= 0) { f[j]++; T++; }
+        }
+        T_out[u] = T;
+    }
+}
+
+/* ---- O3. Weights. Eq.3 entropy of L(u,v) with
+ * p(f_j) = f_j / sum_{l != i} f_l, summed directly over j != i with
+ * f_j > 0 in ascending j; Eq.5 omega = H * |L| with Algorithm 2's
+ * |L| = L_all - 1 (reading C-3); rows with L_all <= 1 are zero
+ * (C-4, C-6; this also makes Y = T - f_i > 0 for every remaining column).
+ * omega_out is n*k row-major, column i = omega_v(C_i) (Lemma 1). ---- */
+void oracle_weights(int64_t n, int32_t k, const int32_t *f_all, double *omega_out) {
+    for (int64_t v = 0; v < n; v++) {
+        const int32_t *f = f_all + v * k;
+        double *w = omega_out + v * k;
+        int64_t T = 0; int32_t L_all = 0;
+        for (int32_t j = 0; j < k; j++) { T += f[j]; if (f[j] > 0) L_all++; }
+        for (int32_t i = 0; i < k; i++) {
+            if (L_all <= 1) { w[i] = 0.0; continue; }
+            double Y = (double)(T - f[i]);
+            double H = 0.0;
+            for (int32_t j = 0; j < k; j++) {
+                if (j == i || f[j] == 0) continue;
+                double p = (double)f[j] / Y;
+                H -= p * log2(p);
+            }
+            w[i] = H * (double)(L_all - 1);
+        }
+    }
+}
+
+/* Algorithm 2 / Eq. H_optimal closed form, kept only so the
+ * tests can check it against the direct form. C-18: X sums
+ * f_i log f_i over the row; T is the row total. */
+void oracle_weights_closed_form(int64_t n, int32_t k, const int32_t *f_all, double *omega_out) {
+    for (int64_t v = 0; v < n; v++) {
+        const int32_t *f = f_all + v * k;
+        double *w = omega_out + v * k;
+        double X = 0.0; int64_t T = 0; int32_t L_all = 0;
+        for (int32_t i = 0; i < k; i++) {
+            T += f[i];
+            if (f[i] > 0) { X += (double)f[i] * log2((double)f[i]); L_all++; }
+        }
+        for (int32_t i = 0; i < k; i++) {
+            if (L_all <= 1) { w[i] = 0.0; continue; }
+            double Y = (double)(T - f[i]);
+            double last = f[i] > 0 ? (double)f[i] * log2((double)f[i] / Y) : 0.0;
+            double H = -(1.0 / Y) * (X - (double)T * log2(Y) - last);
+            w[i] = H * (double)(L_all - 1);
+        }
+    }
+}
+
+/* ---- O4. omega_max (Algorithm 1 line "Find max edge weight", P:279;
+ * normalize_weights divides every element by the maximum, P:485-486;
+ * reading C-7: max over all cells). ---- */
+double oracle_omega_max(int64_t n, int32_t k, const double *omega) {
+    double m = 0.0;
+    for (int64_t i = 0; i < n * (int64_t)k; i++) if (omega[i] > m) m = omega[i];
+    return m;
+}
+
+/* ---- O5a. G' predecessor lists ((v->u) in E_b iff (u,v) in E, both
+ * border and C(u) != C(v); adjacency + different communities already makes
+ * both endpoints border vertices). pred_off is n+1; pred_out receives the
+ * lists (ascending) when non-NULL. Returns the number of entries. ---- */
+int64_t oracle_pred(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C,
+                    int64_t *pred_off, int32_t *pred_out) {
+    int64_t cnt = 0;
+    for (int64_t u = 0; u < n; u++) {
+        pred_off[u] = cnt;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++)
+            if (C[col[e]] != C[u]) { if (pred_out) pred_out[cnt] = col[e]; cnt++; }
+    }
+    pred_off[n] = cnt;
+    return cnt;
+}
+
+/* ---- exact fixed-point helpers (C-12) ---- */
+typedef __int128 i128;
+
+/* round-half-even(t * 2^80) for finite t >= 0, from the fp64 bits. */
+static i128 quantize80(double t) {
+    if (t == 0.0) return 0;
+    int ex;
+    double mant = frexp(t, &ex);                  /* t = mant * 2^ex, mant in [0.5,1) */
+    int64_t m = (int64_t)ldexp(mant, 53);         /* exact 53-bit integer             */
+    int shift = ex - 53 + 80;                     /* t * 2^80 = m * 2^shift           */
+    if (shift >= 0) return (i128)m << shift;
+    int s = -shift;
+    if (s >= 64) return 0;                        /* m < 2^53 <= half ulp of 2^s    */
+    int64_t q = m >> s;
+    int64_t rem = m & (((int64_t)1 << s) - 1);
+    int64_t half = (int64_t)1 << (s - 1);
+    if (rem > half || (rem == half && (q & 1))) q++;
+    return q;
+}
+static double from_fixed80(i128 s) { return ldexp((double)s, -80); }
+
+/* ---- O5-O7. RSI (Eq.4) over valid triads (Eq.6, P:163-171;
+ * Type-I / Type-II), one head at a time.
+ *
+ * For head u with col(u) != ⊥ and d(u) >= 2 (C-9, C-22), enumerate ordered
+ * (w, v): w in N(u), C(w) != C(u); v in N(w), v != u, C(v) != C(w); and
+ *   Type-II  if C(v) == C(u)                                (C-10, C-21)
+ *   Type-I   else if v in N(u) and col(v) != ⊥               (C-9)
+ * Each valid triad adds t = ( omega_v(C(u))/wmax * omega_w(C(v))/wmax *
+ * omega_w(C(u))/wmax )^(1/3) (Eq.4 and Algorithm 1 line P:286; factor order
+ * pinned by the worked example P:506). Terms with a zero factor
+ * are 0 but the triad is still counted. R(u) = sum / (d(u)(d(u)-1)) with d the
+ * degree in G (C-16). If wmax <= 0 every score is +0.0.
+ *
+ * heads: list of nh vertex ids to score (all vertices for a full run);
+ * R_out / nI_out / nII_out are indexed like heads. ---- */
+void oracle_rsi(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C,
+                int32_t k, const int32_t *targets, const double *omega, double wmax,
+                int64_t nh, const int64_t *heads, double *R_out, int64_t *nI_out, int64_t *nII_out) {
+    int32_t *cols = malloc(sizeof(int32_t) * (n ? n : 1));
+    for (int64_t x = 0; x < n; x++) cols[x] = column_of(C[x], k, targets);
+    int64_t *mark = malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int64_t x = 0; x < n; x++) mark[x] = -1;
+
+    for (int64_t h = 0; h < nh; h++) {
+        int64_t u = heads[h];
+        int64_t d = rowptr[u + 1] - rowptr[u];
+        int32_t cu = cols[u];
+        R_out[h] = 0.0; nI_out[h] = 0; nII_out[h] = 0;
+        if (cu < 0 || d < 2) continue;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) mark[col[e]] = u;
+        i128 S = 0;
+        int64_t nI = 0, nII = 0;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) {
+            int32_t w = col[e];
+            if (C[w] == C[u]) continue;
+            for (int64_t e2 = rowptr[w]; e2 < rowptr[w + 1]; e2++) {
+                int32_t v = col[e2];
+                if (v == u || C[v] == C[w]) continue;
+                int32_t cv;
+                if (C[v] == C[u]) { cv = cu; nII++; }
+                else if (mark[v] == u && cols[v] >= 0) { cv = cols[v]; nI++; }
+                else continue;
+                double f1 = omega[(int64_t)v * k + cu];   /* omega_v(u) = omega_v(C(u)) */
+                double f2 = omega[(int64_t)w * k + cv];   /* omega_w(v) = omega_w(C(v)) */
+                double f3 = omega[(int64_t)w * k + cu];   /* omega_w(u) = omega_w(C(u)) */
+                if (wmax <= 0.0 || f1 == 0.0 || f2 == 0.0 || f3 == 0.0) continue;
+                double t = cbrt((f1 / wmax) * (f2 / wmax) * (f3 / wmax));
+                S += quantize80(t);
+            }
+        }
+        nI_out[h] = nI; nII_out[h] = nII;
+        R_out[h] = wmax > 0.0 ? from_fixed80(S) / ((double)d * (double)(d - 1)) : 0.0;
+    }
+    free(cols); free(mark);
+}
+
+/* ---- O8. Top-K (Algorithm 1 optional Step 4): the K highest R,
+ * ties by ascending vertex id (C-14: zeros eligible, K clamped to n). ---- */
+typedef struct { double r; int32_t id; } scored;
+static int cmp_scored(const void *a, const void *b) {
+    const scored *x = a, *y = b;
+    if (x->r != y->r) return x->r > y->r ? -1 : 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+int64_t oracle_topk(int64_t n, const double *R, int64_t K, int32_t *ids_out, double *scores_out) {
+    scored *s = malloc(sizeof(scored) * (n ? n : 1));
+    for (int64_t i = 0; i < n; i++) { s[i].r = R[i]; s[i].id = (int32_t)i; }
+    qsort(s, (size_t)n, sizeof(scored), cmp_scored);
+    int64_t cnt = K < n ? K : n;
+    for (int64_t i = 0; i < cnt; i++) { ids_out[i] = s[i].id; scores_out[i] = s[i].r; }
+    free(s);
+    return cnt;
+}
