@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""RSI hot-path benchmark (arXiv 2508.01485 on B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config orkut|lj|dblp|karate]
+                    [--impl ours|reference] [--K 25]
+
+One step = the whole hot path on one synthetic
+graph resident in HBM: rs_set_communities (target selection + labels) ->
+rs_score (border, histogram, weights, G' lists, Type-I/II triad sums,
+finalize) -> rs_topk (K = 25). Metric: RSI-scored edges/s (GTEPS) = m /
+step time. Each timed step is bracketed by CUDA events on the library's
+stream; L2 is flushed (a 512 MiB write) between steps, outside the events.
+For N > 1 (torchrun), heads are split into work-balanced ranges, ranks merge
+top-K with NCCL, and the time is the max over ranks.
+
+--impl reference times the CPU oracle (oracle/, single thread) on a bounded
+sample of the same workload (the reference arm of this tier).
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import gen  # noqa: E402
+
+METRIC = "RSI-scored edges/sec (GTEPS)"
+UNIT = "GTEPS"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="orkut", choices=["orkut", "lj", "dblp", "karate", "friendster"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--K", type=int, default=25)
+    p.add_argument("--k", type=int, default=5)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--phases", action="store_true", help="print per-phase ms to stderr")
+    return p.parse_args()
+
+
+def load_graph(name, alloc=None):
+    if name == "karate":
+        g, _ = gen.load_fixture("karate")
+        return g
+    return gen.config_graph(name, alloc=alloc)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def phase_bytes(n, D, Db, k, ntri, nb):
+    """Bytes each phase must move at least once."""
+    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 12 * k * n + 16 * n
+    C = 8 * n + 16 * n + 4 * Db + 16 * Db + 8 * k * n + 16 * k * nb + 2 * Db + 4 * n
+    D_ = 8 * n + 16 * n + 4 * Db + 16 * Db + 24 * n + 8 * n
+    return {"A": A, "C": C, "D": D_}
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return reference_arm(a, rank, world)
+    import torch
+    import torch.distributed as dist
+    import paper_2508_01485_b200 as rsb
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(dev)
+    sh = stream.cuda_stream
+
+    t0 = time.time()
+    g = load_graph(a.config)
+    gen_s = time.time() - t0
+    n, D, m = g.n, g.nnz, g.m
+
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(rsb.rs_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        sc = rsb.Scorer(local, sh, rank=rank, world=world, nccl_id=bytes(idt.cpu().numpy()))
+    else:
+        sc = rsb.Scorer(local, sh)
+
+    # device-resident inputs
+    rp_d = torch.from_numpy(g.rowptr).to(dev)
+    col_d = torch.from_numpy(g.col).to(dev)
+    comm_d = torch.from_numpy(g.comm).to(dev)
+    ids_d = torch.empty(a.K, dtype=torch.int32, device=dev)
+    sco_d = torch.empty(a.K, dtype=torch.float64, device=dev)
+    sc.load_csr(rp_d, col_d, validate=False)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        sc.set_communities(comm_d, a.k)
+        sc.score(gather=False)
+        sc.topk(a.K, ids_d, sco_d)
+
+    # warm-up (also sizes every buffer)
+    for _ in range(max(a.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+    st = sc.score(stats=True)
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    phase_ms = []
+    launches0 = sc.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xFF)            # L2 flush outside the timed events
+            ev[i][0].record(stream)
+            sc.set_communities(comm_d, a.k)
+            s = sc.score(stats=a.phases)
+            sc.topk(a.K, ids_d, sco_d)
+            ev[i][1].record(stream)
+            if a.phases:
+                phase_ms.append(s["ms_phase"][:5])
+        torch.cuda.synchronize(dev)
+    launches = sc.launches() - launches0
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / a.steps
+    value = m / (ms_per_step * 1e-3) / 1e9
+
+    # top-k latency (rs_topk alone, device-resident scores -> device ids)
+    tk_ms = []
+    for i in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sc.topk(a.K, ids_d, sco_d)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        tk_ms.append(e0.elapsed_time(e1))
+
+    # per-phase split of one step (stats on), for the roofline of the dominant phase
+    ph = []
+    for _ in range(3):
+        with torch.cuda.stream(stream):
+            flush.fill_(7)
+        sc.set_communities(comm_d, a.k)
+        s = sc.score(stats=True)
+        ph.append(s["ms_phase"][:5])
+    ph = np.median(np.array(ph), axis=0)
+    names = ["targets", "A_border_hist_weights", "C_btable_orient", "E_type1_triangles", "D_type2_finalize"]
+    Db, nb, ntri = st["n_pred_entries"], st["n_border"], st["n_triangles"]
+    pb = phase_bytes(n, D, Db, a.k, ntri, nb)
+    peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # dominant HBM-bound phase (A, C or D; E is reported separately)
+    cand = {"A_border_hist_weights": (ph[1], pb["A"]), "C_btable_orient": (ph[2], pb["C"]),
+            "D_type2_finalize": (ph[4], pb["D"])}
+    dom = max(cand, key=lambda x: cand[x][0])
+    dms, dbytes = cand[dom]
+    achieved = dbytes / (dms * 1e-3) / 1e9 if dms > 0 else 0.0
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "traffic": None,
+            "phase_ms": {nm: round(float(x), 4) for nm, x in zip(names, ph)},
+            "phase_bytes": pb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"}
+
+    e2e = None
+    if not a.no_e2e:
+        e2e = measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(g, a.k, budget_s=15.0)
+
+    if rank == 0:
+        clk_s = clk.summary()
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{a.config}-shape DC-SBM (SURVEY §8(d))", "n": n, "m": m, "nnz": D,
+                       "k_targets": a.k, "K": a.K, "seed": gen.CONFIGS.get(a.config, {}).get("seed"),
+                       "n_border": nb, "pred_entries": Db, "triangles": ntri, "omega_max": st["omega_max"],
+                       "l2": "flushed between timed steps (512 MiB write)", "gen_s": round(gen_s, 1),
+                       "parallelism": f"head-range x{world}" if world > 1 else "single GPU"},
+            "roofline": roof,
+            "topk_latency_ms": round(float(np.median(tk_ms)), 4),
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": clk_s, "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
+        }
+        print(json.dumps(line), flush=True)
+    sc.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st):
+    """Same metric through the public API from pinned HOST buffers: every step
+    copies the CSR + labels host->device (rs_load_csr, rs_set_communities),
+    scores, and reads the top-K ids back to the host."""
+    import torch
+    rp_h = torch.from_numpy(g.rowptr).pin_memory()
+    col_h = torch.from_numpy(g.col).pin_memory()
+    comm_h = torch.from_numpy(g.comm).pin_memory()
+    ids_h = torch.empty(a.K, dtype=torch.int32).pin_memory()
+    sco_h = torch.empty(a.K, dtype=torch.float64).pin_memory()
+    if world > 1:
+        import torch.distributed as dist
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(rsb.rs_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        sc = rsb.Scorer(int(dev.index), sh, rank=rank, world=world, nccl_id=bytes(idt.cpu().numpy()))
+    else:
+        sc = rsb.Scorer(int(dev.index), sh)
+
+    def step():
+        sc.load_csr(rp_h, col_h)
+        sc.set_communities(comm_h, a.k)
+        sc.score()
+        sc.topk(a.K, ids_h, sco_h)
+
+    for _ in range(2):
+        step()
+    steps = max(3, min(a.steps, 5))
+    ts = []
+    for _ in range(steps):
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ts.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(ts) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    sc.close()
+    h2d = g.rowptr.nbytes + g.col.nbytes + g.comm.nbytes
+    d2h = a.K * (4 + 8)
+    return {"value": round(g.m / (ms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+# ------------------------------------------------------------------ oracle arms
+def oracle_sample_step(g, k, n_heads, rng):
+    """O0-O4 over the whole graph + O5-O7 for n_heads sampled heads; returns
+    (seconds of O0-O4, seconds of the head sample, heads)."""
+    import oracle
+    t0 = time.perf_counter()
+    t = oracle.select_targets(g.comm, k)
+    oracle.border(g)
+    f, _ = oracle.counts(g, t)
+    w = oracle.weights(f)
+    wmax = oracle.omega_max(w)
+    oracle.pred(g)
+    t1 = time.perf_counter()
+    heads = rng.choice(g.n, size=min(n_heads, g.n), replace=False).astype(np.int64)
+    oracle.rsi(g, t, w, wmax, heads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, heads.size
+
+
+def oracle_rate(g, k, budget_s, rng):
+    # size the head sample so the whole sample takes about budget_s
+    glob_s, s_small, nh = oracle_sample_step(g, k, 200, rng)
+    per_head = max(s_small / nh, 1e-7)
+    nh2 = int(max(200, min(g.n, (max(budget_s - glob_s, 1.0)) / per_head)))
+    glob_s, head_s, nh2 = oracle_sample_step(g, k, nh2, rng)
+    full_s = glob_s + head_s * (g.n / nh2)       # extrapolated single-thread full run
+    return g.m / full_s / 1e9, glob_s, head_s, nh2, full_s
+
+
+def cpu_baseline(g, k, budget_s=15.0):
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(0)
+    val, glob_s, head_s, nh, full_s = oracle_rate(g, k, budget_s, rng)
+    return {"value": round(val, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"O0-O4 on the whole graph ({glob_s:.1f}s) + O5-O7 on {nh} random heads ({head_s:.1f}s), "
+                      f"extrapolated to all {g.n} heads: {full_s:.0f}s single-thread",
+            "host_cores": os.cpu_count()}
+
+
+def reference_arm(a, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    g = load_graph(a.config)
+    rng = np.random.default_rng(0)
+    budget = 8.0 if a.config in ("orkut", "lj", "friendster") else 2.0
+    # size the per-step head sample once
+    glob_s, s_small, nh = oracle_sample_step(g, a.k, 100, rng)
+    per_head = max(s_small / nh, 1e-7)
+    nh_step = int(max(100, min(g.n, max(budget - glob_s, 0.5) / per_head)))
+    vals = []
+    for i in range(a.warmup + a.steps):
+        gs, hs, nh2 = oracle_sample_step(g, a.k, nh_step, rng)
+        if i >= a.warmup:
+            vals.append(gs + hs * (g.n / nh2))
+    full_s = float(np.mean(vals))
+    value = g.m / full_s / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(full_s * 1e3, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{a.config}-shape DC-SBM (SURVEY §8(d))", "n": g.n, "m": g.m, "k_targets": a.k},
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "kind": "oracle", "cores": 1,
+                             "sample": f"per step: O0-O4 on the whole graph + O5-O7 on {nh_step} random heads, "
+                                       f"extrapolated to all {g.n} heads (single thread)"},
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

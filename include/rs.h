@@ -1,0 +1,185 @@
+/*
+ * rs.h — C-ABI of librs, the B200 (sm_100a) implementation of the hot path of
+ * arXiv 2508.01485, "A Parallel Algorithm for Finding Robust Spanners in Large
+ * Social Networks": per-vertex Robust Spanning Index (RSI, Eq. 4) scoring and
+ * top-K robust-spanner selection over a community-labelled graph.
+ *
+ * Citations "P:n" are lines of the paper's LaTeX source; "C-n" are
+ * the readings of ambiguous passages listed in DESIGN.md §3.
+ *
+ * Conventions for every entry point
+ *  - Returns rs_status; RS_OK = 0. On any other status, rs_last_error(ctx)
+ *    holds a one-line message naming the first offender. No call aborts the
+ *    process or throws across the ABI.
+ *  - Pointers are plain host or device addresses. Inputs are COPIED into
+ *    context-owned device memory: the caller keeps ownership and may free or
+ *    reuse its buffers when the call returns. Outputs go to caller-allocated
+ *    buffers; an output pointer may be host memory (the call then
+ *    synchronises the context stream before returning) or device memory
+ *    (cudaPointerGetAttributes decides; the call is then stream-ordered and
+ *    returns without synchronising).
+ *  - All device work is issued on the context's stream (rs_create).
+ *  - Call order: rs_load_csr -> rs_set_communities -> rs_score -> rs_topk /
+ *    getters. Anything else returns RS_ESTATE. rs_load_csr invalidates
+ *    communities and scores; rs_set_communities invalidates scores.
+ *  - One context per host thread. Contexts are independent.
+ */
+#ifndef RS_H_
+#define RS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RS_OK = 0,
+    RS_EINVAL = -1,   /* an argument or input violates the contract below     */
+    RS_ESTATE = -2,   /* call out of order (e.g. rs_score before communities)  */
+    RS_ENOMEM = -3,   /* device allocation failed                              */
+    RS_ECUDA = -4,    /* CUDA runtime / kernel error (message has cuda string) */
+    RS_ENCCL = -5     /* NCCL error in a multi-GPU context                     */
+} rs_status;
+
+typedef struct rs_ctx rs_ctx;
+
+/* Phase timings (device milliseconds, CUDA events on the context stream) and
+ * size statistics of the last rs_score. */
+typedef struct {
+    int64_t n;                /* |V|                                            */
+    int64_t m;                /* |E| undirected = nnz / 2                       */
+    int64_t n_border;         /* |V_b| over all communities              */
+    int64_t n_pred_entries;   /* sum over u of |P(u)| = |E_b|           */
+    int64_t n_triangles;      /* triangles of G' (3 distinct communities)       */
+    double omega_max;         /* max weight over all cells (C-7)  */
+    float ms_phase[8];        /* [0] targets+labels [1] border/histogram/weight
+                                 [2] B-table + orientation [3] Type-I triangles
+                                 [4] Type-II + finalize  [5..7] reserved        */
+} rs_stats;
+
+/* Flags for rs_load_csr. */
+#define RS_VALIDATE   1u   /* check the CSR contract on the device (see rs_load_csr) */
+
+/* Flags for rs_score. */
+#define RS_GATHER_SCORES 1u /* multi-GPU: make scores_out complete on every rank */
+
+/* Create a context on CUDA device `device`. `cuda_stream` is a cudaStream_t
+ * (NULL = the legacy default stream) on which all work is issued; the caller
+ * keeps ownership of the stream and must keep it alive while ctx lives.
+ * Errors: RS_EINVAL (out == NULL, bad device), RS_ECUDA. */
+rs_status rs_create(rs_ctx **out, int device, void *cuda_stream);
+
+/* Multi-GPU context: rank `rank` of `world` processes, one GPU each, that all
+ * call the same sequence with the same inputs. `nccl_id` is the
+ * 128-byte ncclUniqueId produced by rs_nccl_unique_id on rank 0 and broadcast
+ * by the caller (e.g. with torch.distributed). Heads are split into
+ * work-balanced contiguous ranges; the exchange steps are NCCL collectives on
+ * the context stream. Errors: RS_EINVAL, RS_ECUDA, RS_ENCCL. */
+rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream, int rank, int world,
+                         const uint8_t nccl_id[128]);
+/* Fill `id_out` (128 bytes, host) with a fresh ncclUniqueId. */
+rs_status rs_nccl_unique_id(uint8_t id_out[128]);
+
+/* Free every device buffer owned by ctx. NULL is a no-op. */
+void rs_destroy(rs_ctx *ctx);
+
+/* Message for the last non-OK status on ctx (never NULL; "" if none).
+ * ctx == NULL returns the message of the last failed rs_create. */
+const char *rs_last_error(const rs_ctx *ctx);
+
+/* Load the undirected input graph G = (V, E) in CSR form ("a row
+ * pointer array ... and a 1D flattened neighbor list array").
+ *   n            number of vertices, 1 <= n < 2^31.
+ *   row_offsets  int64[n+1]; row_offsets[0] = 0, non-decreasing; row u's
+ *                neighbours are col_idx[row_offsets[u] .. row_offsets[u+1]).
+ *   col_idx      int32[row_offsets[n]], neighbour ids in [0, n).
+ * Contract (P:81 simple undirected graph; C-17): every row strictly ascending
+ * (sorted, no duplicates), no self-loops, and symmetric (v in N(u) iff u in
+ * N(v)). With RS_VALIDATE the contract is checked on the device and a
+ * violation returns RS_EINVAL naming the first offending row; without it the
+ * input is trusted (results on a non-canonical input are unspecified).
+ * The graph is copied; degree binning of the rows (a property of the graph
+ * alone) is computed here. Errors: RS_EINVAL, RS_ENOMEM, RS_ECUDA. */
+rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offsets, const int32_t *col_idx,
+                      uint32_t flags);
+
+/* Set the non-overlapping community of every vertex ("community
+ * IDs are considered user input") and the k target communities whose weights
+ * omega_v(C_i) are computed.
+ *   community_of  int32[n], each in [0, 2^28).
+ *   targets       int32[k] distinct community ids present in community_of,
+ *                 in column order, or NULL = the k largest communities,
+ *                 ties by ascending community id (C-15).
+ *   k             2 <= k <= min(254, number of distinct communities).
+ * Target selection, the per-vertex column labels and the community-size
+ * histogram run on the device. Errors: RS_EINVAL, RS_ESTATE, RS_ENOMEM, RS_ECUDA. */
+rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of, const int32_t *targets,
+                             int32_t k);
+
+/* Compute the RSI of every vertex (Algorithm 1 Steps 1-3; Eq. 4):
+ *   R(u) = 1/(d(u)(d(u)-1)) * sum over valid triads (u,w,v) (Eq. 6, Type-I
+ *          and Type-II) of (omega_v(u) omega_w(v) omega_w(u))^(1/3),
+ * weights normalised by omega_max, d(u) the degree in G
+ * (C-16). R(u) = +0.0 when C(u) is not a target, d(u) < 2, u is not a border
+ * vertex, or omega_max = 0 (C-9, C-22). Each head's triad sum is accumulated
+ * exactly in fixed point (C-12), so scores are bitwise independent of thread
+ * schedule and GPU count.
+ *   scores_out  double[n] (host or device) or NULL (scores stay on the device
+ *               for rs_topk). In a multi-GPU context only the rank's head
+ *               range is filled unless flags has RS_GATHER_SCORES.
+ *   stats_out   rs_stats* (host) or NULL; requesting stats synchronises.
+ * Errors: RS_ESTATE, RS_ECUDA, RS_ENCCL. */
+rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_out, uint32_t flags);
+
+/* Top-K robust spanners (Algorithm 1 optional Step 4): the min(K, n)
+ * vertices of largest R, ordered by descending R, ties by ascending vertex id
+ * (C-14: zero scores are eligible). Radix select on the fp64 bit patterns.
+ *   K          >= 1.
+ *   ids_out    int32[min(K,n)] (host or device).
+ *   scores_out double[min(K,n)] (host or device) or NULL.
+ *   count_out  int64* (host) or NULL: receives min(K, n).
+ * Multi-GPU: identical result on every rank (NCCL allgather of per-rank
+ * candidates + the same deterministic merge). Errors: RS_EINVAL, RS_ESTATE,
+ * RS_ECUDA, RS_ENCCL. */
+rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *scores_out, int64_t *count_out);
+
+/* ---- parity getters (bit-exact artefacts of the last rs_score) ---- */
+
+/* Step 2a histogram: f_out int32[n*k] row-major, f[u*k+i] =
+ * |{x in N(u): C(x) = targets[i]}|; total_out int32[n] = sum_i f[u*k+i]
+ * (P:431 T). Either pointer may be NULL. Requires rs_score. */
+rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_out);
+
+/* Step 2b weights before normalisation (Eq. 3, Eq. 5, Algorithm 2 |L| rule):
+ * omega_out double[n*k] row-major (column i = omega_u(C_i), Lemma 1) or NULL;
+ * omega_max_out double* or NULL. Requires rs_score. */
+rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omega_max_out);
+
+/* Step 1 border vertices (over all communities): bv_out int32[|V_b|]
+ * ascending (or NULL); nb_out int64* receives |V_b|. Requires rs_score. */
+rs_status rs_get_border(rs_ctx *ctx, int32_t *bv_out, int64_t *nb_out);
+
+/* Step 2d G' predecessor lists ((w -> u) in E_b iff (u,w) in E and
+ * C(u) != C(w)): pred_off_out int64[n+1] and pred_out int32[|E_b|] (each list
+ * ascending), either may be NULL; n_entries_out int64* receives |E_b|.
+ * Requires rs_score. */
+rs_status rs_get_pred(rs_ctx *ctx, int64_t *pred_off_out, int32_t *pred_out, int64_t *n_entries_out);
+
+/* Step 3 valid-triad counts per head (the "removal" sets of P:236: triads in
+ * which removing any one edge keeps C(w) reachable from u), counted for every
+ * scored head (C(u) a target, d(u) >= 2) including zero-weight triads:
+ * type1_out int64[n] Type-I, type2_out int64[n] Type-II; either may be NULL.
+ * Requires rs_score. */
+rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_t *type2_out);
+
+/* Target communities in column order (int32[k]) and k. Requires communities. */
+rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out);
+
+/* Number of librs kernels launched on ctx since creation (bench accounting). */
+int64_t rs_kernel_launches(const rs_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_H_ */

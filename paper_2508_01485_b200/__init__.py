@@ -1,0 +1,286 @@
+"""Python binding of librs (include/rs.h): argument marshalling only.
+
+Every step of the RSI path (arXiv 2508.01485, Algorithm 1 + Eq. 4) runs in the
+CUDA kernels of librs.so (sm_100a). There is no CPU fallback: if librs.so is
+missing or no CUDA device is present, the calls raise.
+
+Low-level names mirror the C-ABI (``rs_create``, ``rs_load_csr``,
+``rs_set_communities``, ``rs_score``, ``rs_topk``, getters); ``Scorer`` is a
+thin object wrapper around one context. Arrays may be numpy arrays (host),
+torch CPU tensors (host; pinned or not) or torch CUDA tensors (device).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librs.so")
+
+RS_OK, RS_EINVAL, RS_ESTATE, RS_ENOMEM, RS_ECUDA, RS_ENCCL = 0, -1, -2, -3, -4, -5
+RS_VALIDATE = 1
+RS_GATHER_SCORES = 1
+_STATUS = {0: "RS_OK", -1: "RS_EINVAL", -2: "RS_ESTATE", -3: "RS_ENOMEM", -4: "RS_ECUDA", -5: "RS_ENCCL"}
+
+
+class RsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class rs_stats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("n_border", ctypes.c_int64),
+                ("n_pred_entries", ctypes.c_int64), ("n_triangles", ctypes.c_int64),
+                ("omega_max", ctypes.c_double), ("ms_phase", ctypes.c_float * 8)]
+
+    def as_dict(self):
+        return {"n": self.n, "m": self.m, "n_border": self.n_border, "n_pred_entries": self.n_pred_entries,
+                "n_triangles": self.n_triangles, "omega_max": self.omega_max,
+                "ms_phase": [float(x) for x in self.ms_phase]}
+
+
+_P = ctypes.c_void_p
+_lib = None
+
+# (name, restype, argtypes) for every symbol include/rs.h declares
+SIGNATURES = [
+    ("rs_create", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P]),
+    ("rs_create_dist", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, _P]),
+    ("rs_nccl_unique_id", ctypes.c_int, [_P]),
+    ("rs_destroy", None, [_P]),
+    ("rs_last_error", ctypes.c_char_p, [_P]),
+    ("rs_load_csr", ctypes.c_int, [_P, ctypes.c_int64, _P, _P, ctypes.c_uint32]),
+    ("rs_set_communities", ctypes.c_int, [_P, _P, _P, ctypes.c_int32]),
+    ("rs_score", ctypes.c_int, [_P, _P, ctypes.POINTER(rs_stats), ctypes.c_uint32]),
+    ("rs_topk", ctypes.c_int, [_P, ctypes.c_int64, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
+    ("rs_get_counts", ctypes.c_int, [_P, _P, _P]),
+    ("rs_get_weights", ctypes.c_int, [_P, _P, _P]),
+    ("rs_get_border", ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
+    ("rs_get_pred", ctypes.c_int, [_P, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
+    ("rs_get_triad_counts", ctypes.c_int, [_P, _P, _P]),
+    ("rs_get_targets", ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int32)]),
+    ("rs_kernel_launches", ctypes.c_int64, [_P]),
+]
+
+
+def load_library(path: str = LIB_PATH):
+    """Load librs.so (build it first with paper_2508_01485_b200.build). Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"librs.so not built at {path}; run `python -m paper_2508_01485_b200.build`")
+        lib = ctypes.CDLL(path)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    """Address of a numpy array / torch tensor (host or device); None -> NULL."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _check(ctx, status):
+    if status != RS_OK:
+        raise RsError(status, load_library().rs_last_error(ctx).decode())
+
+
+def _as(a, dtype):
+    if hasattr(a, "data_ptr"):
+        import torch
+        want = {np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}[dtype]
+        if a.dtype != want:
+            raise TypeError(f"expected {want}, got {a.dtype}")
+        return a.contiguous()
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# ------------------------------------------------------------------ C-ABI mirrors
+def rs_create(device: int = 0, stream: int | None = None):
+    lib = load_library()
+    h = _P()
+    st = lib.rs_create(ctypes.byref(h), device, stream)
+    if st != RS_OK:
+        raise RsError(st, lib.rs_last_error(None).decode())
+    return h
+
+
+def rs_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    st = load_library().rs_nccl_unique_id(buf)
+    if st != RS_OK:
+        raise RsError(st, load_library().rs_last_error(None).decode())
+    return bytes(buf)
+
+
+def rs_create_dist(device: int, stream, rank: int, world: int, nccl_id: bytes):
+    lib = load_library()
+    h = _P()
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+    st = lib.rs_create_dist(ctypes.byref(h), device, stream, rank, world, buf)
+    if st != RS_OK:
+        raise RsError(st, lib.rs_last_error(h if h.value else None).decode())
+    return h
+
+
+def rs_destroy(ctx):
+    load_library().rs_destroy(ctx)
+
+
+def rs_load_csr(ctx, row_offsets, col_idx, flags: int = 0):
+    ro, ci = _as(row_offsets, np.int64), _as(col_idx, np.int32)
+    _check(ctx, load_library().rs_load_csr(ctx, int(ro.shape[0]) - 1, _ptr(ro), _ptr(ci), flags))
+
+
+def rs_set_communities(ctx, community_of, k: int, targets=None):
+    c = _as(community_of, np.int32)
+    t = None if targets is None else _as(targets, np.int32)
+    _check(ctx, load_library().rs_set_communities(ctx, _ptr(c), _ptr(t), int(k)))
+
+
+def rs_score(ctx, scores_out=None, want_stats: bool = False, flags: int = 0):
+    st = rs_stats()
+    _check(ctx, load_library().rs_score(ctx, _ptr(scores_out), ctypes.byref(st) if want_stats else None, flags))
+    return st.as_dict() if want_stats else None
+
+
+def rs_topk(ctx, K: int, ids_out=None, scores_out=None):
+    """Returns (ids, scores) numpy arrays when no output buffers are given."""
+    n_alloc = ids_out is None
+    if n_alloc:
+        ids_out = np.empty(K, dtype=np.int32)
+        scores_out = np.empty(K, dtype=np.float64)
+    cnt = ctypes.c_int64(0)
+    _check(ctx, load_library().rs_topk(ctx, int(K), _ptr(ids_out), _ptr(scores_out), ctypes.byref(cnt)))
+    if n_alloc:
+        return ids_out[:cnt.value], scores_out[:cnt.value]
+    return cnt.value
+
+
+def rs_get_counts(ctx, n, k):
+    f = np.empty((n, k), dtype=np.int32)
+    t = np.empty(n, dtype=np.int32)
+    _check(ctx, load_library().rs_get_counts(ctx, _ptr(f), _ptr(t)))
+    return f, t
+
+
+def rs_get_weights(ctx, n, k):
+    w = np.empty((n, k), dtype=np.float64)
+    m = ctypes.c_double(0)
+    _check(ctx, load_library().rs_get_weights(ctx, _ptr(w), ctypes.byref(m)))
+    return w, m.value
+
+
+def rs_get_border(ctx, n):
+    bv = np.empty(n, dtype=np.int32)
+    nb = ctypes.c_int64(0)
+    _check(ctx, load_library().rs_get_border(ctx, _ptr(bv), ctypes.byref(nb)))
+    return bv[:nb.value]
+
+
+def rs_get_pred(ctx, n, nnz):
+    off = np.empty(n + 1, dtype=np.int64)
+    pr = np.empty(max(nnz, 1), dtype=np.int32)
+    ne = ctypes.c_int64(0)
+    _check(ctx, load_library().rs_get_pred(ctx, _ptr(off), _ptr(pr), ctypes.byref(ne)))
+    return off, pr[:ne.value]
+
+
+def rs_get_triad_counts(ctx, n):
+    t1 = np.empty(n, dtype=np.int64)
+    t2 = np.empty(n, dtype=np.int64)
+    _check(ctx, load_library().rs_get_triad_counts(ctx, _ptr(t1), _ptr(t2)))
+    return t1, t2
+
+
+def rs_get_targets(ctx):
+    buf = np.empty(254, dtype=np.int32)
+    k = ctypes.c_int32(0)
+    _check(ctx, load_library().rs_get_targets(ctx, _ptr(buf), ctypes.byref(k)))
+    return buf[:k.value].copy()
+
+
+def rs_kernel_launches(ctx) -> int:
+    return int(load_library().rs_kernel_launches(ctx))
+
+
+# ------------------------------------------------------------------ object wrapper
+class Scorer:
+    """One librs context. ``stream`` is a raw cudaStream_t (e.g.
+    ``torch.cuda.current_stream().cuda_stream``) or None for the default stream."""
+
+    def __init__(self, device: int = 0, stream: int | None = None, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None):
+        if world > 1:
+            self.ctx = rs_create_dist(device, stream, rank, world, nccl_id)
+        else:
+            self.ctx = rs_create(device, stream)
+        self.n = self.nnz = self.k = 0
+
+    def close(self):
+        if self.ctx is not None:
+            rs_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_csr(self, rowptr, col, validate: bool = False):
+        rs_load_csr(self.ctx, rowptr, col, RS_VALIDATE if validate else 0)
+        self.n = int(rowptr.shape[0]) - 1
+        self.nnz = int(col.shape[0])
+
+    def set_communities(self, comm, k: int, targets=None):
+        rs_set_communities(self.ctx, comm, k, targets)
+        self.k = int(k)
+
+    def score(self, scores_out=None, stats: bool = False, gather: bool = False):
+        return rs_score(self.ctx, scores_out, stats, RS_GATHER_SCORES if gather else 0)
+
+    def scores(self) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.float64)
+        rs_score(self.ctx, out)
+        return out
+
+    def topk(self, K: int, ids_out=None, scores_out=None):
+        return rs_topk(self.ctx, K, ids_out, scores_out)
+
+    def counts(self):
+        return rs_get_counts(self.ctx, self.n, self.k)
+
+    def weights(self):
+        return rs_get_weights(self.ctx, self.n, self.k)
+
+    def border(self):
+        return rs_get_border(self.ctx, self.n)
+
+    def pred(self):
+        return rs_get_pred(self.ctx, self.n, self.nnz)
+
+    def triad_counts(self):
+        return rs_get_triad_counts(self.ctx, self.n)
+
+    def targets(self):
+        return rs_get_targets(self.ctx)
+
+    def launches(self) -> int:
+        return rs_kernel_launches(self.ctx)

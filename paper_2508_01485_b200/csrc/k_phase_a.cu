@@ -1,0 +1,269 @@
+// Phase A — one streaming pass over the CSR:
+//   Step 1 border test (Algorithm 1 lines P:254-263),
+//   Step 2a neighbour-community histogram f[u][i] over the k targets,
+//   Step 2b weights omega_u(C_i) = H(L_i) * (L_all - 1) (Eq. 3, Eq. 5, Algorithm 2
+//           P:457-482, closed form of Eq. H_optimal P:417 with exact zeros),
+//   Step 2c omega_max partial maxima,
+//   Step 2d G' predecessor list P(u) = {x in N(u): C(x) != C(u)}, written
+//           in place at col offset rowptr[u] (no scan needed), ascending.
+// Labels are the 8-bit community codes of rs_set_communities; only vertices of
+// two uncoded ("other") communities fall back to comparing full int32 ids.
+// Degree-binned: a group of G lanes (or a whole CTA for hubs) owns a vertex.
+#include "rs_internal.cuh"
+#include "rs_device.cuh"
+
+namespace rs {
+
+struct PhaseAArgs {
+    const int64_t *__restrict__ rowptr;
+    const int32_t *__restrict__ col;
+    const int32_t *__restrict__ comm;
+    const uint8_t *__restrict__ lab;
+    const int32_t *__restrict__ verts;  // bin slice
+    int64_t nverts;
+    int32_t k;
+    const double *__restrict__ l2t;     // log2 of small integers
+    int64_t l2n;
+    int32_t *__restrict__ f;
+    double *__restrict__ omega;
+    VRec *__restrict__ vrec;
+    int32_t *__restrict__ pidx;
+    unsigned long long *scal;
+};
+
+__device__ __forceinline__ double lg2(const PhaseAArgs &a, int64_t x) {
+    return x < a.l2n ? __ldg(a.l2t + x) : log2((double)x);
+}
+
+// k <= 8: per-lane register histogram. Returns the vertex's max weight (group-uniform
+// only on the lanes that computed columns; callers max-reduce per thread anyway).
+template <class GR>
+__device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
+    const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
+    const uint8_t lu = a.lab[u];
+    const int32_t cfull = (lu == kOther) ? a.comm[u] : 0;
+    const int k = a.k;
+    int cnt[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) cnt[c] = 0;
+    int pc = 0;
+    for (int64_t base = beg; base < end; base += GR::size) {
+        const int64_t e = base + g.lane;
+        const bool valid = e < end;
+        int32_t x = 0;
+        uint8_t lx = kOther;
+        if (valid) {
+            x = __ldcs(a.col + e);            // streamed once: evict-first
+            lx = __ldg(a.lab + x);            // 1-byte gather, L2-resident table
+        }
+        bool foreign = valid && (lx != lu);
+        if (valid && lx == kOther && lu == kOther) foreign = __ldg(a.comm + x) != cfull;
+#pragma unroll
+        for (int c = 0; c < 8; c++) cnt[c] += (c < k && lx == c) ? 1 : 0;
+        int tot;
+        int r = g.rank(foreign, &tot);
+        if (foreign) a.pidx[beg + pc + r] = x;
+        pc += tot;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; c++) cnt[c] = g.sum(cnt[c]);
+    // row statistics (identical on every lane, fixed order)
+    int T = 0, L_all = 0;
+    double X = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+        T += cnt[c];
+        L_all += cnt[c] > 0;
+        if (cnt[c] > 1) X += (double)cnt[c] * lg2(a, cnt[c]);
+    }
+    const int64_t d = end - beg;
+    double wmax = 0.0;
+    double a_self = 0.0;
+    for (int c = g.lane; c < k; c += GR::size) {
+        int fc = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) fc = (j == c) ? cnt[j] : fc;
+        const int others = L_all - (fc > 0);   // nonzero columns of L(u, .) besides c
+        double w = 0.0;
+        if (L_all >= 2 && others >= 2) {
+            const int Y = T - fc;               // > 0
+            const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
+            const double H = lg2(a, Y) - (X - xc) / (double)Y;
+            w = H * (double)(L_all - 1);
+            w = w > 0.0 ? w : 0.0;              // canonical +0.0
+        }
+        a.omega[u * k + c] = w;
+        a.f[u * k + c] = fc;
+        wmax = w > wmax ? w : wmax;
+        if (c == (int)lu) a_self = cbrt(w);
+    }
+    // own column lives on lane (lu mod G); the lane holding it writes the record
+    const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
+    if ((int)g.lane == owner) {
+        VRec r;
+        r.a_self = a_self;
+        r.pcnt = pc;
+        r.lab = lu;
+        r.head = (lu < k && d >= 2) ? 1 : 0;
+        r.pad = 0;
+        a.vrec[u] = r;
+    }
+    return wmax;
+}
+
+// k > 8: histogram in shared memory (one warp or one CTA per vertex)
+template <class GR>
+__device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64_t u, GR &g, int *hist) {
+    const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
+    const uint8_t lu = a.lab[u];
+    const int32_t cfull = (lu == kOther) ? a.comm[u] : 0;
+    const int k = a.k;
+    for (int c = g.lane; c < k; c += GR::size) hist[c] = 0;
+    g.sync();
+    int pc = 0;
+    for (int64_t base = beg; base < end; base += GR::size) {
+        const int64_t e = base + g.lane;
+        const bool valid = e < end;
+        int32_t x = 0;
+        uint8_t lx = kOther;
+        if (valid) { x = __ldcs(a.col + e); lx = __ldg(a.lab + x); }
+        bool foreign = valid && (lx != lu);
+        if (valid && lx == kOther && lu == kOther) foreign = __ldg(a.comm + x) != cfull;
+        if (valid && lx < k) atomicAdd(&hist[lx], 1);
+        int tot;
+        int r = g.rank(foreign, &tot);
+        if (foreign) a.pidx[beg + pc + r] = x;
+        pc += tot;
+    }
+    g.sync();
+    int T = 0, L_all = 0;
+    double X = 0.0;
+    for (int c = 0; c < k; c++) {
+        int v = hist[c];
+        T += v;
+        L_all += v > 0;
+        if (v > 1) X += (double)v * lg2(a, v);
+    }
+    const int64_t d = end - beg;
+    double wmax = 0.0;
+    for (int c = g.lane; c < k; c += GR::size) {
+        const int fc = hist[c];
+        const int others = L_all - (fc > 0);
+        double w = 0.0;
+        if (L_all >= 2 && others >= 2) {
+            const int Y = T - fc;
+            const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
+            w = (lg2(a, Y) - (X - xc) / (double)Y) * (double)(L_all - 1);
+            w = w > 0.0 ? w : 0.0;
+        }
+        a.omega[u * k + c] = w;
+        a.f[u * k + c] = fc;
+        wmax = w > wmax ? w : wmax;
+    }
+    g.sync();
+    if (g.lane == 0) {
+        VRec r;
+        r.a_self = lu < k ? cbrt(a.omega[u * k + lu]) : 0.0;
+        r.pcnt = pc;
+        r.lab = lu;
+        r.head = (lu < k && d >= 2) ? 1 : 0;
+        r.pad = 0;
+        a.vrec[u] = r;
+    }
+    g.sync();
+    return wmax;
+}
+
+__device__ __forceinline__ void block_max_to_scal(double v, unsigned long long *scal) {
+    __shared__ double s[32];
+    for (int o = 16; o > 0; o >>= 1) { double x = __shfl_xor_sync(0xffffffffu, v, o); v = x > v ? x : v; }
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) m = s[i] > m ? s[i] : m;
+        if (m > 0.0) atomic_max_nonneg(&scal[kScalOmegaMaxBits], m);
+    }
+}
+
+template <int G, bool SMEM>
+__global__ void __launch_bounds__(256) k_phase_a_warp(PhaseAArgs a) {
+    __shared__ int hist[SMEM ? 8 * 256 : 1];
+    WarpGroup<G> g;
+    const int64_t groups_per_block = blockDim.x / G;
+    const int64_t gid = blockIdx.x * groups_per_block + threadIdx.x / G;
+    const int64_t ngroups = (int64_t)gridDim.x * groups_per_block;
+    double wmax = 0.0;
+    for (int64_t i = gid; i < a.nverts; i += ngroups) {
+        const int64_t u = a.verts[i];
+        double w;
+        if constexpr (SMEM) w = phase_a_vertex_smem(a, u, g, hist + (threadIdx.x / 32) * 256);
+        else w = phase_a_vertex(a, u, g);
+        wmax = w > wmax ? w : wmax;
+    }
+    block_max_to_scal(wmax, a.scal);
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kCtaThreads) k_phase_a_cta(PhaseAArgs a) {
+    __shared__ int s_i[kCtaWarps + 1];
+    __shared__ unsigned long long s_u[2 * kCtaWarps];
+    __shared__ int hist[SMEM ? 256 : 1];
+    CtaGroup g(s_i, s_u);
+    double wmax = 0.0;
+    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) {
+        const int64_t u = a.verts[i];
+        double w;
+        if constexpr (SMEM) w = phase_a_vertex_smem(a, u, g, hist);
+        else w = phase_a_vertex(a, u, g);
+        wmax = w > wmax ? w : wmax;
+    }
+    block_max_to_scal(wmax, a.scal);
+}
+
+template <int G, bool SMEM>
+static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
+    const int64_t gpb = 256 / G;
+    int64_t blocks = (a.nverts + gpb - 1) / gpb;
+    blocks = std::min<int64_t>(blocks, 148 * 16);
+    if (blocks < 1) return;
+    k_phase_a_warp<G, SMEM><<<(unsigned)blocks, 256, 0, s>>>(a);
+    c.launches++;
+}
+
+template <bool SMEM>
+static void launch_bins_a(Ctx &c, PhaseAArgs base) {
+    // class -> group: [0,8):4 [8,16):8 [16,32):16 [32,2048):32 [2048,inf):CTA
+    for (int cls = kNumBins - 1; cls >= 0; cls--) {
+        PhaseAArgs a = base;
+        a.verts = c.binv + c.bins.offset[cls];
+        a.nverts = c.bins.count[cls];
+        if (a.nverts == 0) continue;
+        cudaStream_t s = c.side[cls];
+        if (cls >= 6) {
+            int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
+            k_phase_a_cta<SMEM><<<(unsigned)blocks, kCtaThreads, 0, s>>>(a);
+            c.launches++;
+        } else if (SMEM || cls >= 3) {
+            launch_warp_bin<32, SMEM>(c, a, s);
+        } else if (cls == 2) {
+            launch_warp_bin<16, SMEM>(c, a, s);
+        } else if (cls == 1) {
+            launch_warp_bin<8, SMEM>(c, a, s);
+        } else {
+            launch_warp_bin<4, SMEM>(c, a, s);
+        }
+    }
+}
+
+cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
+    PhaseAArgs a;
+    a.rowptr = c.rowptr; a.col = c.col; a.comm = c.comm_id; a.lab = c.lab;
+    a.verts = nullptr; a.nverts = 0; a.k = c.k; a.l2t = l2t; a.l2n = l2n;
+    a.f = c.f; a.omega = c.omega; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
+    if (c.k <= 8) launch_bins_a<false>(c, a);
+    else launch_bins_a<true>(c, a);
+    return cudaGetLastError();
+}
+
+}  // namespace rs

@@ -1,0 +1,339 @@
+// Load-time and community-time kernels:
+//  - CSR contract check (C-17), degree classes for binned scheduling,
+//  - community-size histogram, target selection (C-15), 8-bit labels.
+#include "rs_internal.cuh"
+#include "rs_device.cuh"
+#include <cub/cub.cuh>
+
+namespace rs {
+
+// ---------------------------------------------------------------- validation
+// err codes: 1 row_offsets decreasing / bad, 2 col out of range, 3 not strictly
+// ascending (unsorted or duplicate), 4 self-loop, 5 not symmetric.
+__global__ void k_validate(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ col, int64_t n,
+                           unsigned long long *scal) {
+    int64_t u = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    for (; u < n; u += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        int64_t b = rowptr[u], e = rowptr[u + 1];
+        int code = 0;
+        if (e < b) code = 1;
+        for (int64_t i = b + lane; i < e && !code; i += 32) {
+            int32_t v = col[i];
+            if (v < 0 || v >= n) { code = 2; break; }
+            if (i > b && col[i - 1] >= v) { code = 3; break; }
+            if (v == u) { code = 4; break; }
+            // symmetric: u in N(v) (binary search in the sorted row of v)
+            int64_t lo = rowptr[v], hi = rowptr[v + 1];
+            while (lo < hi) {
+                int64_t mid = (lo + hi) >> 1;
+                if (col[mid] < u) lo = mid + 1; else hi = mid;
+            }
+            if (lo >= rowptr[v + 1] || col[lo] != u) { code = 5; break; }
+        }
+        unsigned any = __ballot_sync(0xffffffffu, code != 0);
+        if (any) {
+            int first = __ffs(any) - 1;
+            int c = __shfl_sync(0xffffffffu, code, first);
+            if (lane == 0) {
+                // keep the smallest offending row
+                unsigned long long old = atomicMin(&scal[kScalErrRow], (unsigned long long)u);
+                if ((unsigned long long)u <= old) atomicExch(&scal[kScalErr], (unsigned long long)c);
+            }
+        }
+    }
+}
+
+cudaError_t launch_validate(Ctx &c) {
+    k_validate<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.col, c.n, c.scal);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- degree classes
+__device__ __forceinline__ int degree_class(int64_t d) {
+    int b = 0;
+#pragma unroll
+    for (int i = 1; i < kNumBins; i++) b += (d >= bin_lo(i));
+    return b;
+}
+
+__global__ void k_bin_flags(const int64_t *__restrict__ rowptr, int64_t n, int cls, int32_t *flags) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        flags[u] = degree_class(rowptr[u + 1] - rowptr[u]) == cls;
+}
+
+__global__ void k_bin_scatter(const int32_t *__restrict__ flags, const int32_t *__restrict__ pos, int64_t n,
+                              int64_t base, int32_t *binv) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        if (flags[u]) binv[base + pos[u]] = (int32_t)u;
+}
+
+__global__ void k_dmax(const int64_t *__restrict__ rowptr, int64_t n, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long d = (unsigned long long)(rowptr[u + 1] - rowptr[u]);
+        m = d > m ? d : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) { unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o); m = x > m ? x : m; }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// vertices grouped by degree class, ascending id inside a class (stable)
+cudaError_t launch_bins(Ctx &c) {
+    const int64_t n = c.n;
+    int32_t *flags = (int32_t *)c.scratch;
+    int32_t *pos = flags + n;
+    void *tmp = pos + n;
+    size_t tmp_bytes = c.scratch_bytes - 2 * sizeof(int32_t) * (size_t)n;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (blocks < 1) blocks = 1;
+    int64_t base = 0;
+    for (int cls = 0; cls < kNumBins; cls++) {
+        k_bin_flags<<<blocks, 256, 0, c.stream>>>(c.rowptr, n, cls, flags);
+        c.launches++;
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, flags, pos, (int)n, c.stream);
+        if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+        cub::DeviceScan::ExclusiveSum(tmp, need, flags, pos, (int)n, c.stream);
+        c.launches++;
+        k_bin_scatter<<<blocks, 256, 0, c.stream>>>(flags, pos, n, base, c.binv);
+        c.launches++;
+        int32_t last_pos = 0, last_flag = 0;
+        cudaMemcpyAsync(&last_pos, pos + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaMemcpyAsync(&last_flag, flags + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaError_t e = cudaStreamSynchronize(c.stream);
+        if (e != cudaSuccess) return e;
+        int64_t cnt = (int64_t)last_pos + last_flag;
+        c.bins.count[cls] = cnt;
+        c.bins.offset[cls] = base;
+        base += cnt;
+    }
+    c.bins.offset[kNumBins] = base;
+    cudaMemsetAsync(c.scal + kScalCnt0, 0, sizeof(unsigned long long), c.stream);
+    k_dmax<<<blocks, 256, 0, c.stream>>>(c.rowptr, n, c.scal + kScalCnt0);
+    c.launches++;
+    unsigned long long dm = 0;
+    cudaMemcpyAsync(&dm, c.scal + kScalCnt0, sizeof(dm), cudaMemcpyDeviceToHost, c.stream);
+    cudaError_t e = cudaStreamSynchronize(c.stream);
+    c.d_max = (int64_t)dm;
+    return e;
+}
+
+// ---------------------------------------------------------------- log2 table
+__global__ void k_log2_table(double *t, int64_t len) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+        t[i] = i > 0 ? log2((double)i) : 0.0;
+}
+cudaError_t launch_log2_table(Ctx &c, double *t, int64_t len) {
+    k_log2_table<<<148, 256, 0, c.stream>>>(t, len);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- communities
+__global__ void k_minmax_i32(const int32_t *__restrict__ a, int64_t n, unsigned long long *out) {
+    // out[0] = max(-min) trick: track min as max of (INT_MAX - v) via two atomics
+    long long mn = INT64_MAX, mx = INT64_MIN;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        long long v = a[i];
+        mn = v < mn ? v : mn;
+        mx = v > mx ? v : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        long long x = __shfl_xor_sync(0xffffffffu, mn, o); mn = x < mn ? x : mn;
+        long long y = __shfl_xor_sync(0xffffffffu, mx, o); mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin((long long *)&out[0], mn);
+        atomicMax((long long *)&out[1], mx);
+    }
+}
+
+cudaError_t launch_minmax_i32(Ctx &c, const int32_t *a, int64_t n, int64_t *mn, int64_t *mx) {
+    long long init[2] = {INT64_MAX, INT64_MIN};
+    cudaMemcpyAsync(c.scal + kScalTk, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    if (blocks < 1) blocks = 1;
+    k_minmax_i32<<<blocks, 256, 0, c.stream>>>(a, n, c.scal + kScalTk);
+    c.launches++;
+    long long res[2];
+    cudaMemcpyAsync(res, c.scal + kScalTk, sizeof(res), cudaMemcpyDeviceToHost, c.stream);
+    cudaError_t e = cudaStreamSynchronize(c.stream);
+    *mn = res[0];
+    *mx = res[1];
+    return e;
+}
+
+constexpr int kHistSmem = 8192;
+
+__global__ void k_comm_hist(const int32_t *__restrict__ comm, int64_t n, int32_t *hist, int64_t nbins) {
+    __shared__ int s[kHistSmem];
+    const bool priv = nbins <= kHistSmem;
+    if (priv) for (int i = threadIdx.x; i < nbins; i += blockDim.x) s[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t cid = comm[i];
+        if (priv) atomicAdd(&s[cid], 1); else atomicAdd(&hist[cid], 1);
+    }
+    __syncthreads();
+    if (priv) for (int i = threadIdx.x; i < nbins; i += blockDim.x) if (s[i]) atomicAdd(&hist[i], s[i]);
+}
+
+// One CTA: target selection (k largest communities, ties ascending id, or the
+// user's list), distinct count, and the community -> 8-bit code map:
+// targets get their column 0..k-1; other present communities get k, k+1, ...
+// in ascending id while codes last (<= 254); the rest share kOther (0xFF).
+constexpr int kSelThreads = 1024;
+__global__ void __launch_bounds__(kSelThreads) k_select(const int32_t *__restrict__ hist, int64_t nbins, int32_t k,
+                                                        const int32_t *user_targets, int32_t *targets,
+                                                        uint8_t *code, unsigned long long *scal) {
+    __shared__ long long s_key[kSelThreads / 32];
+    __shared__ int s_cnt[kSelThreads / 32];
+    __shared__ int32_t s_t[kMaxK];
+    __shared__ int s_base;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // distinct communities
+    int cnt = 0;
+    for (int64_t i = tid; i < nbins; i += blockDim.x) cnt += hist[i] > 0;
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_cnt[wid] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int i = 0; i < kSelThreads / 32; i++) t += s_cnt[i];
+        scal[kScalCnt0] = (unsigned long long)t;
+        if (k > t) scal[kScalErr] = 10;   // k exceeds the number of communities
+    }
+    __syncthreads();
+    if (scal[kScalErr]) return;
+    if (user_targets) {
+        if (tid < k) {
+            int32_t t = user_targets[tid];
+            bool ok = t >= 0 && t < nbins && hist[t] > 0;
+            for (int j = 0; j < tid; j++) ok = ok && user_targets[j] != t;
+            if (!ok) atomicExch(&scal[kScalErr], 11ull);
+            s_t[tid] = t;
+        }
+        __syncthreads();
+    } else {
+        // k rounds of argmax over key = size * 2^32 + (2^31 - 1 - id): largest size, then smallest id
+        for (int r = 0; r < k; r++) {
+            long long best = -1;
+            for (int64_t i = tid; i < nbins; i += blockDim.x) {
+                int32_t h = hist[i];
+                if (h <= 0) continue;
+                bool taken = false;
+                for (int j = 0; j < r; j++) taken |= (s_t[j] == (int32_t)i);
+                if (taken) continue;
+                long long key = ((long long)h << 32) | (long long)(0x7fffffff - (int32_t)i);
+                best = key > best ? key : best;
+            }
+            for (int o = 16; o > 0; o >>= 1) { long long x = __shfl_xor_sync(0xffffffffu, best, o); best = x > best ? x : best; }
+            if (lane == 0) s_key[wid] = best;
+            __syncthreads();
+            if (tid == 0) {
+                long long b = -1;
+                for (int i = 0; i < kSelThreads / 32; i++) b = s_key[i] > b ? s_key[i] : b;
+                s_t[r] = 0x7fffffff - (int32_t)(b & 0xffffffffll);
+            }
+            __syncthreads();
+        }
+    }
+    if (scal[kScalErr]) return;
+    if (tid < k) targets[tid] = s_t[tid];
+    // codes: ascending-id rank of non-target present communities
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nbins; base += blockDim.x) {
+        int64_t i = base + tid;
+        int col = -1;
+        bool present = false;
+        if (i < nbins) {
+            present = hist[i] > 0;
+            for (int j = 0; j < k; j++) col = (s_t[j] == (int32_t)i) ? j : col;
+        }
+        bool other = present && col < 0;
+        unsigned b = __ballot_sync(0xffffffffu, other);
+        if (lane == 0) s_cnt[wid] = __popc(b);
+        __syncthreads();
+        int before = 0, all = 0;
+        for (int w = 0; w < kSelThreads / 32; w++) { before += w < wid ? s_cnt[w] : 0; all += s_cnt[w]; }
+        int rank = s_base + before + __popc(b & ((1u << lane) - 1u));
+        if (i < nbins) {
+            uint8_t cd = kOther;
+            if (col >= 0) cd = (uint8_t)col;
+            else if (other && k + rank < (int)kOther) cd = (uint8_t)(k + rank);
+            code[i] = cd;
+        }
+        __syncthreads();
+        if (tid == 0) s_base += all;
+        __syncthreads();
+    }
+}
+
+__global__ void k_labels(const int32_t *__restrict__ comm, const uint8_t *__restrict__ code, int64_t n, uint8_t *lab) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        lab[i] = code[comm[i]];
+}
+
+cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets) {
+    const int64_t nbins = max_comm + 1;
+    cudaMemsetAsync(c.chist, 0, sizeof(int32_t) * nbins, c.stream);
+    int blocks = (int)std::min<int64_t>((c.n + 255) / 256, 148 * 4);
+    if (blocks < 1) blocks = 1;
+    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_id, c.n, c.chist, nbins);
+    c.launches++;
+    k_select<<<1, kSelThreads, 0, c.stream>>>(c.chist, nbins, c.k, user_targets, c.targets, c.ccode, c.scal);
+    c.launches++;
+    k_labels<<<blocks, 256, 0, c.stream>>>(c.comm_id, c.ccode, c.n, c.lab);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace rs
+
+namespace rs {
+// ---------------------------------------------------------------- multi-GPU partition
+// Contiguous head ranges balanced by the work estimate d(u) + 1 (prefix sum,
+// then the first vertex whose prefix reaches r/world of the total).
+__global__ void k_work(const int64_t *__restrict__ rowptr, int64_t n, int64_t *w) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        w[u] = rowptr[u + 1] - rowptr[u] + 1;
+}
+__global__ void k_split(const int64_t *__restrict__ incl, int64_t n, int world, int64_t *bounds) {
+    const int r = threadIdx.x;
+    if (r > world) return;
+    if (r == 0) { bounds[0] = 0; return; }
+    if (r == world) { bounds[world] = n; return; }
+    const int64_t total = incl[n - 1];
+    const int64_t target = (total * r + world - 1) / world;
+    int64_t lo = 0, hi = n;   // first u with incl[u] >= target -> boundary u+1
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (incl[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    bounds[r] = lo + 1 < n ? lo + 1 : n;
+}
+cudaError_t launch_partition(Ctx &c) {
+    const int64_t n = c.n;
+    int64_t *w = (int64_t *)c.scratch;
+    int64_t *incl = w + n;
+    int64_t *bounds = incl + n;
+    void *tmp = bounds + (c.world + 1);
+    size_t tmp_bytes = c.scratch_bytes - sizeof(int64_t) * (size_t)(2 * n + c.world + 1);
+    k_work<<<148 * 4, 256, 0, c.stream>>>(c.rowptr, n, w);
+    size_t need = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, need, w, incl, (int)n, c.stream);
+    if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+    cub::DeviceScan::InclusiveSum(tmp, need, w, incl, (int)n, c.stream);
+    k_split<<<1, 1024, 0, c.stream>>>(incl, n, c.world, bounds);
+    c.launches += 3;
+    c.bounds.assign(c.world + 1, 0);
+    cudaMemcpyAsync(c.bounds.data(), bounds, sizeof(int64_t) * (c.world + 1), cudaMemcpyDeviceToHost, c.stream);
+    cudaError_t e = cudaStreamSynchronize(c.stream);
+    c.head_lo = c.bounds[c.rank];
+    c.head_hi = c.bounds[c.rank + 1];
+    return e;
+}
+}  // namespace rs

@@ -1,0 +1,223 @@
+// Step 4 (Algorithm 1, optional): top-K vertices by R, ties by ascending
+// vertex id (C-14). Radix select over the IEEE bit patterns of the
+// non-negative scores (monotone as unsigned integers once -0.0 is folded into
+// +0.0), 8 digit passes of 8 bits; ties at the threshold are resolved by an
+// id-ordered block scan; the K survivors are sorted (key desc, id asc).
+#include "rs_internal.cuh"
+#include "rs_device.cuh"
+#include <cub/cub.cuh>
+
+namespace rs {
+
+constexpr int kTkBlocks = 148 * 4;
+constexpr int kTkThreads = 256;
+constexpr int kTkSortMax = 4096;   // in-smem bitonic sort capacity
+
+// state slots at scal + kScalTk: [0] prefix, [1] krem (keys still to take at
+// the threshold), [2] count of keys strictly above the current prefix
+__device__ __forceinline__ unsigned long long score_key(double s) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(s);
+    return (b == 0x8000000000000000ull) ? 0ull : b;   // -0.0 -> +0.0
+}
+
+__global__ void __launch_bounds__(kTkThreads) k_tk_hist(const double *__restrict__ score, int64_t lo, int64_t hi,
+                                                        int pass, const unsigned long long *st,
+                                                        unsigned long long *hist) {
+    __shared__ unsigned int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long prefix = st[0];
+    const int shift = 56 - 8 * pass;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = score_key(score[i]);
+        const bool match = (pass == 0) || (((key ^ prefix) >> (shift + 8)) == 0ull);
+        if (match) atomicAdd(&h[(key >> shift) & 0xFF], 1u);
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+}
+
+// one warp: choose the digit of this pass
+__global__ void k_tk_pick(int pass, unsigned long long *st, unsigned long long *hist) {
+    if (threadIdx.x != 0) return;
+    const int shift = 56 - 8 * pass;
+    unsigned long long krem = st[1];
+    unsigned long long above = 0;
+    int t = 0;
+    for (int dgt = 255; dgt >= 0; dgt--) {
+        const unsigned long long h = hist[dgt];
+        if (above + h >= krem) { t = dgt; break; }
+        above += h;
+    }
+    st[0] |= ((unsigned long long)t) << shift;
+    st[1] = krem - above;
+    st[2] += above;
+    for (int i = 0; i < 256; i++) hist[i] = 0;   // ready for the next pass
+}
+
+// keys above the threshold -> cand[0, count_gt) (any order); ties counted per block
+__global__ void __launch_bounds__(kTkThreads) k_tk_above(const double *__restrict__ score, int64_t lo, int64_t hi,
+                                                         const unsigned long long *st, unsigned long long *cand_key,
+                                                         int32_t *cand_id, unsigned long long *cursor,
+                                                         unsigned int *tie_cnt, int64_t chunk) {
+    __shared__ unsigned int s_ties;
+    if (threadIdx.x == 0) s_ties = 0;
+    __syncthreads();
+    const unsigned long long T = st[0];
+    const int64_t b0 = lo + blockIdx.x * chunk;
+    const int64_t b1 = min(hi, b0 + chunk);
+    unsigned int ties = 0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        const unsigned long long key = score_key(score[i]);
+        if (key > T) {
+            const unsigned long long p = atomicAdd(cursor, 1ull);
+            cand_key[p] = key;
+            cand_id[p] = (int32_t)i;
+        } else if (key == T) {
+            ties++;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_ties, ties);
+    __syncthreads();
+    if (threadIdx.x == 0) tie_cnt[blockIdx.x] = s_ties;
+}
+
+// ties in id order: block b takes its ties while their global rank < krem
+__global__ void __launch_bounds__(kTkThreads) k_tk_ties(const double *__restrict__ score, int64_t lo, int64_t hi,
+                                                        const unsigned long long *st, unsigned long long *cand_key,
+                                                        int32_t *cand_id, const unsigned int *tie_cnt, int64_t chunk) {
+    __shared__ unsigned long long s_pre;
+    __shared__ int s_w[kTkThreads / 32];
+    const unsigned long long T = st[0];
+    const unsigned long long krem = st[1];
+    const unsigned long long gt = st[2];
+    unsigned long long pre = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += blockDim.x) pre += tie_cnt[b];
+    for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if (threadIdx.x == 0) s_pre = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_pre, pre);
+    __syncthreads();
+    unsigned long long base = s_pre;
+    if (base >= krem || tie_cnt[blockIdx.x] == 0) return;
+    const int64_t b0 = lo + blockIdx.x * chunk;
+    const int64_t b1 = min(hi, b0 + chunk);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t t0 = b0; t0 < b1 && base < krem; t0 += blockDim.x) {
+        const int64_t i = t0 + threadIdx.x;
+        const bool tie = i < b1 && score_key(score[i]) == T;
+        const unsigned m = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) s_w[wid] = __popc(m);
+        __syncthreads();
+        unsigned long long before = 0, all = 0;
+        for (int w = 0; w < kTkThreads / 32; w++) { before += (w < wid) ? s_w[w] : 0; all += s_w[w]; }
+        const unsigned long long r = base + before + __popc(m & ((1u << lane) - 1u));
+        if (tie && r < krem) {
+            cand_key[gt + r] = T;
+            cand_id[gt + r] = (int32_t)i;
+        }
+        __syncthreads();
+        base += all;
+    }
+}
+
+__device__ __forceinline__ bool tk_before(unsigned long long ka, int32_t ia, unsigned long long kb, int32_t ib) {
+    return ka > kb || (ka == kb && ia < ib);
+}
+
+// single CTA bitonic sort of cnt <= kTkSortMax candidates, writes the first `out` entries
+__global__ void __launch_bounds__(1024) k_tk_sort(const unsigned long long *cand_key, const int32_t *cand_id,
+                                                  int64_t cnt, int64_t out, int32_t *ids_out, double *scores_out) {
+    __shared__ unsigned long long sk[kTkSortMax];
+    __shared__ int32_t si[kTkSortMax];
+    int size = 1;
+    while (size < cnt) size <<= 1;
+    for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        if (i < cnt) { sk[i] = cand_key[i]; si[i] = cand_id[i]; }
+        else { sk[i] = 0ull; si[i] = 0x7fffffff; }
+    }
+    __syncthreads();
+    for (int len = 2; len <= size; len <<= 1) {
+        for (int j = len >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < size; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const bool asc = (i & len) == 0;   // "ascending" = our order
+                    const bool swap = asc ? tk_before(sk[p], si[p], sk[i], si[i]) : tk_before(sk[i], si[i], sk[p], si[p]);
+                    if (swap) {
+                        unsigned long long tk = sk[i]; sk[i] = sk[p]; sk[p] = tk;
+                        int32_t ti = si[i]; si[i] = si[p]; si[p] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < out; i += blockDim.x) {
+        ids_out[i] = si[i];
+        if (scores_out) scores_out[i] = __longlong_as_double((long long)sk[i]);
+    }
+}
+
+__global__ void k_tk_copy_out(const unsigned long long *key, const int32_t *id, int64_t out, int32_t *ids_out,
+                              double *scores_out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < out; i += (int64_t)gridDim.x * blockDim.x) {
+        ids_out[i] = id[i];
+        if (scores_out) scores_out[i] = __longlong_as_double((long long)key[i]);
+    }
+}
+
+// sort `cnt` (key, id) candidates by (key desc, id asc) and emit the first `out`
+cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
+                         double *scores_out) {
+    if (cnt <= kTkSortMax) {
+        k_tk_sort<<<1, 1024, 0, c.stream>>>(key, id, cnt, out, ids_out, scores_out);
+        c.launches++;
+        return cudaGetLastError();
+    }
+    // large K: two stable radix sorts (ids ascending, then keys descending)
+    unsigned long long *key2 = key + cnt;
+    int32_t *id2 = (int32_t *)(key2 + cnt);
+    size_t need1 = 0, need2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need1, id, id2, key, key2, (int)cnt, 0, 32, c.stream);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, need2, key2, key, id2, id, (int)cnt, 0, 64, c.stream);
+    size_t need = std::max(need1, need2);
+    if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
+    cub::DeviceRadixSort::SortPairs(c.scratch, need, id, id2, key, key2, (int)cnt, 0, 32, c.stream);
+    cub::DeviceRadixSort::SortPairsDescending(c.scratch, need, key2, key, id2, id, (int)cnt, 0, 64, c.stream);
+    c.launches += 2;
+    k_tk_copy_out<<<148, 256, 0, c.stream>>>(key, id, out, ids_out, scores_out);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+// local top-K of score[lo, hi) into (cand_key, cand_id)[0, K') sorted, K' = min(K, hi-lo)
+cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
+                               int32_t *cand_id) {
+    unsigned long long *st = c.scal + kScalTk;
+    unsigned long long *hist = c.tk_hist;
+    unsigned long long *cursor = hist + 256;
+    unsigned int *tie_cnt = (unsigned int *)(hist + 512);
+    const int64_t range = hi - lo;
+    unsigned long long init[3] = {0ull, (unsigned long long)K, 0ull};
+    cudaMemcpyAsync(st, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
+    cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 257, c.stream);
+    int blocks = (int)std::min<int64_t>((range + kTkThreads - 1) / kTkThreads, kTkBlocks);
+    if (blocks < 1) blocks = 1;
+    for (int pass = 0; pass < 8; pass++) {
+        k_tk_hist<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist);
+        k_tk_pick<<<1, 32, 0, c.stream>>>(pass, st, hist);
+        c.launches += 2;
+    }
+    const int64_t chunk = (range + kTkBlocks - 1) / kTkBlocks;
+    const int cblocks = (int)std::max<int64_t>(1, (range + chunk - 1) / std::max<int64_t>(chunk, 1));
+    k_tk_above<<<cblocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, cursor, tie_cnt,
+                                                     std::max<int64_t>(chunk, 1));
+    k_tk_ties<<<cblocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, tie_cnt,
+                                                    std::max<int64_t>(chunk, 1));
+    c.launches += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace rs

@@ -1,0 +1,595 @@
+// C-ABI of librs (include/rs.h): argument checking, device memory ownership,
+// call-order state machine, stream fork/join for the degree bins, phase
+// timing and the NCCL exchange steps of the multi-GPU path.
+#include "rs_internal.cuh"
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <dlfcn.h>
+
+namespace rs {
+cudaError_t launch_log2_table(Ctx &c, double *t, int64_t len);
+cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n);
+cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
+                               int32_t *cand_id);
+cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
+                         double *scores_out);
+cudaError_t launch_partition(Ctx &c);
+}  // namespace rs
+
+using rs::Ctx;
+
+#ifdef RS_WITH_NCCL
+const rs::NcclApi *rs::nccl_api(std::string *err) {
+    static rs::NcclApi api;
+    static int state = 0;   // 0 untried, 1 ok, -1 failed
+    static std::string why;
+    if (state == 0) {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char *path = getenv("RS_NCCL_LIBRARY");
+            h = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        }
+        state = -1;
+        if (!h) {
+            why = std::string("cannot load libnccl.so.2: ") + dlerror();
+        } else {
+            bool ok = true;
+            auto sym = [&](const char *name) { void *p = dlsym(h, name); ok = ok && p; return p; };
+            api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+            api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+            api.Broadcast = (decltype(api.Broadcast))sym("ncclBroadcast");
+            api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+            api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+            api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+            if (ok) state = 1; else why = "libnccl.so.2 lacks a required symbol";
+        }
+    }
+    if (state != 1) { if (err) *err = why; return nullptr; }
+    return &api;
+}
+#endif
+
+struct rs_ctx {
+    Ctx c;
+    double *l2t = nullptr;
+    int64_t l2n = 0;
+    int32_t *utargets = nullptr;     // device copy of user targets
+    int32_t *stage_i32 = nullptr;    // device staging for host outputs
+    double *stage_f64 = nullptr;
+    int64_t stage_cap = 0;
+    unsigned long long *cand_key = nullptr;
+    int32_t *cand_id = nullptr;
+    int64_t cand_cap = 0;
+    size_t tk_scratch = 0;
+};
+
+static std::string g_create_err;
+
+static rs_status fail(rs_ctx *ctx, rs_status s, const std::string &m) {
+    if (ctx) ctx->c.err = m; else g_create_err = m;
+    return s;
+}
+
+#define CK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess) return fail(ctx, RS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#ifdef RS_WITH_NCCL
+#define NK(expr)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (expr);                                                             \
+        if (r_ != ncclSuccess) return fail(ctx, RS_ENCCL, std::string(#expr) + ": " + rs::nccl_api(nullptr)->GetErrorString(r_)); \
+    } while (0)
+#define NCCL (*rs::nccl_api(nullptr))
+#endif
+
+static bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+static cudaError_t dalloc(T **p, size_t count) {
+    if (*p) { cudaFree(*p); *p = nullptr; }
+    if (count == 0) count = 1;
+    return cudaMalloc((void **)p, sizeof(T) * count);
+}
+template <class T>
+static void dfree(T *&p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+static void fork(Ctx &c) {
+    cudaEventRecord(c.ev_fork, c.stream);
+    for (int i = 0; i < rs::kNumBins; i++) cudaStreamWaitEvent(c.side[i], c.ev_fork, 0);
+}
+static void join(Ctx &c) {
+    for (int i = 0; i < rs::kNumBins; i++) {
+        cudaEventRecord(c.ev_join[i], c.side[i]);
+        cudaStreamWaitEvent(c.stream, c.ev_join[i], 0);
+    }
+}
+
+// ------------------------------------------------------------------ lifecycle
+static rs_status create_common(rs_ctx **out, int device, void *cuda_stream) {
+    rs_ctx *ctx = nullptr;
+    if (!out) return fail(nullptr, RS_EINVAL, "rs_create: out is NULL");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return fail(nullptr, RS_EINVAL, "rs_create: no CUDA device " + std::to_string(device));
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, RS_ECUDA, "rs_create: cudaSetDevice failed");
+    ctx = new rs_ctx();
+    Ctx &c = ctx->c;
+    c.device = device;
+    c.stream = (cudaStream_t)cuda_stream;
+    for (int i = 0; i < rs::kNumBins; i++) {
+        CK(cudaStreamCreateWithFlags(&c.side[i], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    for (int i = 0; i < 8; i++) CK(cudaEventCreate(&c.ev_phase[i]));
+    CK(dalloc(&c.scal, rs::kScalCount));
+    CK(cudaMemset(c.scal, 0, sizeof(unsigned long long) * rs::kScalCount));
+    CK(dalloc(&c.tk_hist, 2048));
+    CK(dalloc(&c.targets, rs::kMaxK));
+    CK(dalloc(&ctx->utargets, rs::kMaxK));
+    *out = ctx;
+    return RS_OK;
+}
+
+extern "C" rs_status rs_create(rs_ctx **out, int device, void *cuda_stream) {
+    return create_common(out, device, cuda_stream);
+}
+
+extern "C" rs_status rs_nccl_unique_id(uint8_t id_out[128]) {
+#ifdef RS_WITH_NCCL
+    if (!id_out) return fail(nullptr, RS_EINVAL, "rs_nccl_unique_id: NULL");
+    std::string why;
+    if (!rs::nccl_api(&why)) return fail(nullptr, RS_ENCCL, why);
+    ncclUniqueId id;
+    if (NCCL.GetUniqueId(&id) != ncclSuccess) return fail(nullptr, RS_ENCCL, "ncclGetUniqueId failed");
+    memcpy(id_out, &id, 128);
+    return RS_OK;
+#else
+    (void)id_out;
+    return fail(nullptr, RS_ENCCL, "librs built without NCCL");
+#endif
+}
+
+extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream, int rank, int world,
+                                    const uint8_t nccl_id[128]) {
+    if (world < 1 || rank < 0 || rank >= world || !nccl_id)
+        return fail(nullptr, RS_EINVAL, "rs_create_dist: bad rank/world/id");
+    rs_status s = create_common(out, device, cuda_stream);
+    if (s != RS_OK) return s;
+    rs_ctx *ctx = *out;
+    ctx->c.rank = rank;
+    ctx->c.world = world;
+#ifdef RS_WITH_NCCL
+    if (world > 1) {
+        std::string why;
+        if (!rs::nccl_api(&why)) return fail(ctx, RS_ENCCL, why);
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, 128);
+        NK(NCCL.CommInitRank(&ctx->c.comm, world, id, rank));
+    }
+    return RS_OK;
+#else
+    if (world > 1) return fail(ctx, RS_ENCCL, "librs built without NCCL");
+    return RS_OK;
+#endif
+}
+
+static void free_graph(rs_ctx *ctx) {
+    Ctx &c = ctx->c;
+    dfree(c.rowptr); dfree(c.col); dfree(c.binv); dfree(c.scratch); dfree(ctx->l2t);
+    dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.ppcnt);
+    dfree(c.acc1); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
+    c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
+}
+
+extern "C" void rs_destroy(rs_ctx *ctx) {
+    if (!ctx) return;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (c.stream) cudaStreamSynchronize(c.stream);
+    free_graph(ctx);
+    dfree(c.chist); dfree(c.ccode); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist);
+    dfree(ctx->utargets); dfree(ctx->stage_i32); dfree(ctx->stage_f64); dfree(ctx->cand_key); dfree(ctx->cand_id);
+    for (int i = 0; i < rs::kNumBins; i++) {
+        if (c.side[i]) cudaStreamDestroy(c.side[i]);
+        if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
+    }
+    if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+    for (int i = 0; i < 8; i++) if (c.ev_phase[i]) cudaEventDestroy(c.ev_phase[i]);
+#ifdef RS_WITH_NCCL
+    if (c.comm) NCCL.CommDestroy(c.comm);
+#endif
+    delete ctx;
+}
+
+extern "C" const char *rs_last_error(const rs_ctx *ctx) {
+    return ctx ? ctx->c.err.c_str() : g_create_err.c_str();
+}
+
+extern "C" int64_t rs_kernel_launches(const rs_ctx *ctx) { return ctx ? ctx->c.launches : 0; }
+
+// ------------------------------------------------------------------ load
+extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offsets, const int32_t *col_idx,
+                                 uint32_t flags) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (n < 1 || n >= (1ll << 31)) return fail(ctx, RS_EINVAL, "rs_load_csr: n must be in [1, 2^31)");
+    if (!row_offsets || !col_idx) return fail(ctx, RS_EINVAL, "rs_load_csr: NULL array");
+    const bool dev_ro = is_device_ptr(row_offsets), dev_ci = is_device_ptr(col_idx);
+    int64_t first = 0, nnz = 0;
+    if (dev_ro) {
+        CK(cudaMemcpy(&first, row_offsets, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&nnz, row_offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    } else {
+        first = row_offsets[0];
+        nnz = row_offsets[n];
+    }
+    if (first != 0) return fail(ctx, RS_EINVAL, "rs_load_csr: row_offsets[0] != 0");
+    if (nnz < 0) return fail(ctx, RS_EINVAL, "rs_load_csr: row_offsets[n] < 0");
+    free_graph(ctx);
+    c.n = n;
+    c.nnz = nnz;
+    CK(dalloc(&c.rowptr, n + 1));
+    CK(dalloc(&c.col, nnz));
+    CK(cudaMemcpyAsync(c.rowptr, row_offsets, sizeof(int64_t) * (n + 1),
+                       dev_ro ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    if (nnz) CK(cudaMemcpyAsync(c.col, col_idx, sizeof(int32_t) * nnz,
+                                dev_ci ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    if (flags & RS_VALIDATE) {
+        unsigned long long init[3] = {0ull, ~0ull, 0ull};
+        CK(cudaMemcpyAsync(c.scal + rs::kScalErr, init, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice, c.stream));
+        CK(rs::launch_validate(c));
+        unsigned long long er[2];
+        CK(cudaMemcpyAsync(er, c.scal + rs::kScalErr, sizeof(er), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        if (er[0]) {
+            static const char *what[] = {"", "row_offsets decreasing", "col_idx out of range",
+                                         "row not strictly ascending (unsorted or duplicate)", "self-loop",
+                                         "graph not symmetric"};
+            std::string m = std::string("rs_load_csr: ") + (er[0] < 6 ? what[er[0]] : "invalid") + " at row " +
+                            std::to_string((long long)er[1]);
+            free_graph(ctx);
+            return fail(ctx, RS_EINVAL, m);
+        }
+    }
+    // per-graph buffers (independent of communities)
+    size_t scratch = 24 * (size_t)(n + 1) + (64u << 20);
+    CK(cudaMalloc(&c.scratch, scratch));
+    c.scratch_bytes = scratch;
+    CK(dalloc(&c.binv, n));
+    CK(rs::launch_bins(c));
+    ctx->l2n = std::min<int64_t>(c.d_max + 1, 1ll << 20);
+    CK(dalloc(&ctx->l2t, ctx->l2n));
+    CK(rs::launch_log2_table(c, ctx->l2t, ctx->l2n));
+    CK(dalloc(&c.comm_id, n));
+    CK(dalloc(&c.lab, n));
+    CK(dalloc(&c.vrec, n));
+    CK(dalloc(&c.pidx, nnz));
+    CK(dalloc(&c.pplus, nnz));
+    CK(dalloc(&c.ppcnt, n));
+    CK(dalloc(&c.acc1, 3 * n));
+    CK(dalloc(&c.n1, n));
+    CK(dalloc(&c.score, n));
+    c.head_lo = 0;
+    c.head_hi = n;
+    if (c.world > 1) CK(rs::launch_partition(c));
+    CK(cudaStreamSynchronize(c.stream));
+    c.loaded = true;
+    return RS_OK;
+}
+
+// ------------------------------------------------------------------ communities
+extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of, const int32_t *targets, int32_t k) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.loaded) return fail(ctx, RS_ESTATE, "rs_set_communities: no graph loaded");
+    if (!community_of) return fail(ctx, RS_EINVAL, "rs_set_communities: community_of is NULL");
+    if (k < 2 || k > rs::kMaxK) return fail(ctx, RS_EINVAL, "rs_set_communities: k must be in [2, 254]");
+    c.scored = false;
+    c.has_comm = false;
+    CK(cudaMemcpyAsync(c.comm_id, community_of, sizeof(int32_t) * c.n,
+                       is_device_ptr(community_of) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    int64_t mn = 0, mx = 0;
+    CK(rs::launch_minmax_i32(c, c.comm_id, c.n, &mn, &mx));
+    if (mn < 0) return fail(ctx, RS_EINVAL, "rs_set_communities: negative community id");
+    if (mx >= (1ll << 28)) return fail(ctx, RS_EINVAL, "rs_set_communities: community id >= 2^28");
+    if (mx + 1 > c.ccap) {
+        int64_t cap = std::max<int64_t>(mx + 1, 1024);
+        CK(dalloc(&c.chist, cap));
+        CK(dalloc(&c.ccode, cap));
+        c.ccap = cap;
+    }
+    if (c.k_alloc != k) {
+        CK(dalloc(&c.f, (size_t)c.n * k));
+        CK(dalloc(&c.omega, (size_t)c.n * k));
+        CK(dalloc(&c.bq, (size_t)c.n * k));
+        c.k_alloc = k;
+    }
+    c.k = k;
+    const int32_t *ut = nullptr;
+    if (targets) {
+        CK(cudaMemcpyAsync(ctx->utargets, targets, sizeof(int32_t) * k,
+                           is_device_ptr(targets) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+        ut = ctx->utargets;
+    }
+    CK(cudaMemsetAsync(c.scal + rs::kScalErr, 0, sizeof(unsigned long long), c.stream));
+    CK(rs::launch_set_communities(c, mx, ut));
+    unsigned long long er = 0, ndist = 0;
+    CK(cudaMemcpyAsync(&er, c.scal + rs::kScalErr, sizeof(er), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&ndist, c.scal + rs::kScalCnt0, sizeof(ndist), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(c.h_targets, c.targets, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (er == 10)
+        return fail(ctx, RS_EINVAL, "rs_set_communities: k = " + std::to_string(k) + " exceeds the " +
+                                        std::to_string((long long)ndist) + " distinct communities");
+    if (er) return fail(ctx, RS_EINVAL, "rs_set_communities: targets must be distinct ids present in community_of");
+    c.has_comm = true;
+    return RS_OK;
+}
+
+// ------------------------------------------------------------------ score
+extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_out, uint32_t flags) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.has_comm) return fail(ctx, RS_ESTATE, "rs_score: call rs_load_csr and rs_set_communities first");
+    const int64_t n = c.n;
+    CK(cudaEventRecord(c.ev_phase[0], c.stream));
+    CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
+    CK(cudaMemsetAsync(c.n1, 0, sizeof(unsigned long long) * n, c.stream));
+    CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
+    CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, sizeof(unsigned long long), c.stream));
+    // Phase A: border + histogram + weights + P lists + omega_max partials
+    fork(c);
+    CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n));
+    join(c);
+    CK(cudaEventRecord(c.ev_phase[1], c.stream));
+    // Phase C: B table + orientation
+    fork(c);
+    CK(rs::launch_phase_c(c));
+    join(c);
+    CK(cudaEventRecord(c.ev_phase[2], c.stream));
+    // Phase E: Type-I triangles
+    CK(rs::launch_phase_e(c));
+    CK(cudaEventRecord(c.ev_phase[3], c.stream));
+    // Phase D: Type-II + finalize
+    fork(c);
+    CK(rs::launch_phase_d(c));
+    join(c);
+    CK(cudaEventRecord(c.ev_phase[4], c.stream));
+#ifdef RS_WITH_NCCL
+    if (c.world > 1 && (flags & RS_GATHER_SCORES)) {
+        // owned ranges are contiguous and of different sizes: one broadcast per rank
+        NK(NCCL.GroupStart());
+        for (int r = 0; r < c.world; r++) {
+            const int64_t lo = c.bounds[r], hi = c.bounds[r + 1];
+            if (hi > lo) NK(NCCL.Broadcast(c.score + lo, c.score + lo, (size_t)(hi - lo), ncclFloat64, r, c.comm, c.stream));
+        }
+        NK(NCCL.GroupEnd());
+    }
+#endif
+    c.scored = true;
+    if (scores_out) {
+        const bool dev = is_device_ptr(scores_out);
+        CK(cudaMemcpyAsync(scores_out, c.score, sizeof(double) * n,
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.stream));
+        if (!dev) CK(cudaStreamSynchronize(c.stream));
+    }
+    if (stats_out) {
+        int64_t st[3];
+        CK(rs::launch_stats(c, st));
+        rs_stats s;
+        memset(&s, 0, sizeof(s));
+        s.n = n;
+        s.m = c.nnz / 2;
+        s.n_border = st[0];
+        s.n_pred_entries = st[1];
+        s.n_triangles = st[2];
+        unsigned long long wb = 0;
+        CK(cudaMemcpy(&wb, c.scal + rs::kScalOmegaMaxBits, sizeof(wb), cudaMemcpyDeviceToHost));
+        memcpy(&s.omega_max, &wb, sizeof(double));
+        for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&s.ms_phase[i], c.ev_phase[i], c.ev_phase[i + 1]));
+        *stats_out = s;
+    }
+    (void)flags;
+    return RS_OK;
+}
+
+// ------------------------------------------------------------------ top-k
+static rs_status ensure_cand(rs_ctx *ctx, int64_t cap) {
+    if (cap <= ctx->cand_cap) return RS_OK;
+    CK(dalloc(&ctx->cand_key, 2 * (size_t)cap + (size_t)cap / 2 + 2));   // key, key2, id2 (large-K sort)
+    CK(dalloc(&ctx->cand_id, cap));
+    ctx->cand_cap = cap;
+    return RS_OK;
+}
+static rs_status ensure_stage(rs_ctx *ctx, int64_t cap) {
+    if (cap <= ctx->stage_cap) return RS_OK;
+    CK(dalloc(&ctx->stage_i32, cap));
+    CK(dalloc(&ctx->stage_f64, cap));
+    ctx->stage_cap = cap;
+    return RS_OK;
+}
+
+extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *scores_out, int64_t *count_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_topk: call rs_score first");
+    if (K < 1) return fail(ctx, RS_EINVAL, "rs_topk: K must be >= 1");
+    if (!ids_out) return fail(ctx, RS_EINVAL, "rs_topk: ids_out is NULL");
+    const int64_t Kc = std::min<int64_t>(K, c.n);
+    rs_status s = ensure_cand(ctx, Kc * c.world);
+    if (s != RS_OK) return s;
+    const bool dev_ids = is_device_ptr(ids_out);
+    const bool dev_sc = scores_out ? is_device_ptr(scores_out) : true;
+    int32_t *ids_d = ids_out;
+    double *sc_d = scores_out;
+    if (!dev_ids || !dev_sc) {
+        s = ensure_stage(ctx, Kc);
+        if (s != RS_OK) return s;
+        if (!dev_ids) ids_d = ctx->stage_i32;
+        if (scores_out && !dev_sc) sc_d = ctx->stage_f64;
+    }
+    if (c.world == 1) {
+        CK(rs::launch_topk_select(c, Kc, 0, c.n, ctx->cand_key, ctx->cand_id));
+        CK(rs::tk_sort_emit(c, ctx->cand_key, ctx->cand_id, Kc, Kc, ids_d, sc_d));
+    } else {
+#ifdef RS_WITH_NCCL
+        // local top-K of the owned head range, padded with sentinels, allgathered,
+        // then the same deterministic merge on every rank
+        const int64_t range = c.head_hi - c.head_lo;
+        const int64_t Kl = std::min<int64_t>(Kc, range);
+        unsigned long long *lk = ctx->cand_key;           // local sorted keys (Kc)
+        int32_t *li = ctx->cand_id;
+        s = ensure_stage(ctx, Kc);
+        if (s != RS_OK) return s;
+        // pad: keys 0, ids INT_MAX sort last
+        CK(cudaMemsetAsync(lk, 0, sizeof(unsigned long long) * Kc, c.stream));
+        CK(cudaMemsetAsync(li, 0x7f, sizeof(int32_t) * Kc, c.stream));
+        if (Kl > 0) {
+            CK(rs::launch_topk_select(c, Kl, c.head_lo, c.head_hi, lk, li));
+        }
+        unsigned long long *gk = (unsigned long long *)c.scratch;
+        int32_t *gi = (int32_t *)(gk + Kc * c.world * 3);
+        NK(NCCL.GroupStart());
+        NK(NCCL.AllGather(lk, gk, (size_t)Kc, ncclUint64, c.comm, c.stream));
+        NK(NCCL.AllGather(li, gi, (size_t)Kc, ncclInt32, c.comm, c.stream));
+        NK(NCCL.GroupEnd());
+        CK(rs::tk_sort_emit(c, gk, gi, Kc * c.world, Kc, ids_d, sc_d));
+#else
+        return fail(ctx, RS_ENCCL, "librs built without NCCL");
+#endif
+    }
+    if (!dev_ids) CK(cudaMemcpyAsync(ids_out, ids_d, sizeof(int32_t) * Kc, cudaMemcpyDeviceToHost, c.stream));
+    if (scores_out && !dev_sc)
+        CK(cudaMemcpyAsync(scores_out, sc_d, sizeof(double) * Kc, cudaMemcpyDeviceToHost, c.stream));
+    if (!dev_ids || !dev_sc) CK(cudaStreamSynchronize(c.stream));
+    if (count_out) *count_out = Kc;
+    return RS_OK;
+}
+
+// ------------------------------------------------------------------ getters
+template <class T>
+static rs_status out_copy(rs_ctx *ctx, T *dst, const T *src_dev, size_t count) {
+    Ctx &c = ctx->c;
+    CK(cudaMemcpyAsync(dst, src_dev, sizeof(T) * count,
+                       is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return RS_OK;
+}
+
+extern "C" rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_counts: call rs_score first");
+    if (f_out) { rs_status s = out_copy(ctx, f_out, c.f, (size_t)c.n * c.k); if (s) return s; }
+    if (total_out) {
+        int32_t *tmp = (int32_t *)c.scratch;
+        CK(rs::launch_counts_total(c, tmp));
+        return out_copy(ctx, total_out, tmp, (size_t)c.n);
+    }
+    return RS_OK;
+}
+
+extern "C" rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omega_max_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_weights: call rs_score first");
+    if (omega_out) { rs_status s = out_copy(ctx, omega_out, c.omega, (size_t)c.n * c.k); if (s) return s; }
+    if (omega_max_out) {
+        unsigned long long wb = 0;
+        CK(cudaMemcpyAsync(&wb, c.scal + rs::kScalOmegaMaxBits, 8, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        memcpy(omega_max_out, &wb, 8);
+    }
+    return RS_OK;
+}
+
+extern "C" rs_status rs_get_border(rs_ctx *ctx, int32_t *bv_out, int64_t *nb_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_border: call rs_score first");
+    int64_t nb = 0;
+    int32_t *tmp = nullptr;
+    CK(cudaMalloc(&tmp, sizeof(int32_t) * (size_t)c.n));
+    cudaError_t e = rs::launch_border_list(c, tmp, &nb);
+    if (e != cudaSuccess) { cudaFree(tmp); CK(e); }
+    rs_status s = RS_OK;
+    if (bv_out && nb) s = out_copy(ctx, bv_out, tmp, (size_t)nb);
+    cudaFree(tmp);
+    if (nb_out) *nb_out = nb;
+    return s;
+}
+
+extern "C" rs_status rs_get_pred(rs_ctx *ctx, int64_t *pred_off_out, int32_t *pred_out, int64_t *n_entries_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_pred: call rs_score first");
+    int64_t *off = nullptr;
+    int32_t *pr = nullptr;
+    int64_t ne = 0;
+    CK(cudaMalloc(&off, sizeof(int64_t) * (size_t)(c.n + 1)));
+    CK(cudaMalloc(&pr, sizeof(int32_t) * (size_t)std::max<int64_t>(c.nnz, 1)));
+    cudaError_t e = rs::launch_pred_export(c, off, pr, &ne);
+    if (e != cudaSuccess) { cudaFree(off); cudaFree(pr); CK(e); }
+    rs_status s = RS_OK;
+    if (pred_off_out) s = out_copy(ctx, pred_off_out, off, (size_t)(c.n + 1));
+    if (s == RS_OK && pred_out && ne) s = out_copy(ctx, pred_out, pr, (size_t)ne);
+    cudaFree(off);
+    cudaFree(pr);
+    if (n_entries_out) *n_entries_out = ne;
+    return s;
+}
+
+extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_t *type2_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_triad_counts: call rs_score first");
+    int64_t *tmp = (int64_t *)c.scratch;
+    if (type1_out) {
+        CK(rs::launch_type1_export(c, tmp));
+        rs_status s = out_copy(ctx, type1_out, tmp, (size_t)c.n);
+        if (s) return s;
+    }
+    if (type2_out) {
+        CK(rs::launch_type2_counts(c, tmp));
+        rs_status s = out_copy(ctx, type2_out, tmp, (size_t)c.n);
+        if (s) return s;
+    }
+    return RS_OK;
+}
+
+extern "C" rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    if (!c.has_comm) return fail(ctx, RS_ESTATE, "rs_get_targets: call rs_set_communities first");
+    if (targets_out) memcpy(targets_out, c.h_targets, sizeof(int32_t) * c.k);
+    if (k_out) *k_out = c.k;
+    return RS_OK;
+}

@@ -1,0 +1,184 @@
+// Device helpers of librs: exact fixed-point accumulation (reading C-12) and
+// vertex-group abstractions for degree-binned scheduling.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rs {
+
+// ---------------------------------------------------------------------------
+// Exact fixed point. A per-head triad sum is a sum of non-negative fp64 terms;
+// each term is rounded once onto the 2^-64 grid (round-half-even, from the
+// IEEE bits) and the grid integers are summed exactly in 128 bits, so the sum
+// does not depend on the order threads add them (C-12). Terms are
+// unnormalised (omega_max is applied once in the epilogue), bounded by
+// omega_max <= (k-1) log2(k-1) < 2^11, so every per-head sum is < 2^96.
+// ---------------------------------------------------------------------------
+struct U128 {
+    unsigned long long lo, hi;
+};
+
+__device__ __forceinline__ U128 u128_zero() { return U128{0ull, 0ull}; }
+
+__device__ __forceinline__ U128 u128_add(U128 a, U128 b) {
+    U128 r;
+    asm("add.cc.u64 %0, %2, %4;\n\taddc.u64 %1, %3, %5;"
+        : "=l"(r.lo), "=l"(r.hi)
+        : "l"(a.lo), "l"(a.hi), "l"(b.lo), "l"(b.hi));
+    return r;
+}
+
+// round-half-even(t * 2^64) for finite t >= 0 (t < 2^64).
+__device__ __forceinline__ U128 fx_quantize(double t) {
+    unsigned long long bits = (unsigned long long)__double_as_longlong(t);
+    int e = (int)((bits >> 52) & 0x7ff);
+    if (e == 0) return u128_zero();               // +-0 and subnormals (< 2^-1022)
+    unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+    int s = e - 1011;                             // t * 2^64 = m * 2^s
+    if (s >= 0) {
+        if (s == 0) return U128{m, 0ull};
+        if (s < 64) return U128{m << s, m >> (64 - s)};
+        return U128{0ull, m << (s - 64)};         // s < 128 by the bound above
+    }
+    int r = -s;
+    if (r >= 54) return u128_zero();              // m < 2^53 <= half of 2^r
+    unsigned long long q = m >> r;
+    unsigned long long rem = m & ((1ull << r) - 1ull);
+    unsigned long long half = 1ull << (r - 1);
+    if (rem > half || (rem == half && (q & 1ull))) q++;
+    return U128{q, 0ull};
+}
+
+// correctly rounded (round-to-nearest-even) conversion of v * 2^-64 to fp64
+__device__ __forceinline__ double fx_to_double(U128 v) {
+    if (v.hi == 0ull) return __ull2double_rn(v.lo) * 0x1p-64;
+    int lz = __clzll(v.hi);                       // 0..63
+    unsigned long long top, rest;
+    if (lz == 0) { top = v.hi; rest = v.lo; }
+    else { top = (v.hi << lz) | (v.lo >> (64 - lz)); rest = v.lo << lz; }
+    if (rest) top |= 1ull;                        // sticky bit below the rounding point
+    // v = top * 2^(64 - lz) (up to the sticky bit), times 2^-64
+    return __ull2double_rn(top) * exp2((double)(-lz));
+}
+
+// Type-I accumulators are three 64-bit limbs per head updated with
+// fire-and-forget RED (no carries between limbs): limb0 += bits[0,32),
+// limb1 += bits[32,64), limb2 += bits[64,128). Exact while a head receives
+// fewer than 2^32 terms.
+__device__ __forceinline__ void fx_red3(unsigned long long *acc3, U128 q) {
+    atomicAdd(acc3 + 0, q.lo & 0xFFFFFFFFull);
+    atomicAdd(acc3 + 1, q.lo >> 32);
+    if (q.hi) atomicAdd(acc3 + 2, q.hi);
+}
+__device__ __forceinline__ U128 fx_from3(const unsigned long long *acc3) {
+    unsigned long long l0 = acc3[0], l1 = acc3[1], l2 = acc3[2];
+    U128 a{l0, l2};
+    U128 b{l1 << 32, l1 >> 32};
+    return u128_add(a, b);
+}
+
+// ---------------------------------------------------------------------------
+// Vertex groups. A group of G lanes (G in {4, 8, 16, 32}) owns one vertex and
+// walks its adjacency G entries per step; 32/G groups share a warp. Lanes of
+// one group always execute the same trip count, so group-masked shuffles are
+// well defined even when the groups of a warp diverge.
+// ---------------------------------------------------------------------------
+template <int G>
+struct WarpGroup {
+    static constexpr int size = G;
+    unsigned lane;   // 0..G-1
+    unsigned shift;  // first lane of the group in the warp
+    unsigned gmask;  // the group's lanes
+    __device__ __forceinline__ WarpGroup() {
+        unsigned l = threadIdx.x & 31u;
+        lane = l & (G - 1);
+        shift = l & ~(unsigned)(G - 1);
+        gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << shift);
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(gmask); }
+    // exclusive rank of this lane among lanes with p set; total in *tot
+    __device__ __forceinline__ int rank(bool p, int *tot) const {
+        unsigned b = __ballot_sync(gmask, p) & gmask;
+        b >>= shift;
+        *tot = __popc(b);
+        return __popc(b & ((1u << lane) - 1u));
+    }
+    template <class T>
+    __device__ __forceinline__ T sum(T v) const {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o, G);
+        return v;
+    }
+    __device__ __forceinline__ U128 sum(U128 v) const {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            U128 w{__shfl_xor_sync(gmask, v.lo, o, G), __shfl_xor_sync(gmask, v.hi, o, G)};
+            v = u128_add(v, w);
+        }
+        return v;
+    }
+    template <class T>
+    __device__ __forceinline__ T bcast(T v, int src) const {
+        return __shfl_sync(gmask, v, src, G);
+    }
+};
+
+// A whole CTA (blockDim.x == kCtaThreads) owning one vertex (degree hubs).
+constexpr int kCtaThreads = 256;
+constexpr int kCtaWarps = kCtaThreads / 32;
+
+struct CtaGroup {
+    static constexpr int size = kCtaThreads;
+    unsigned lane;
+    int *s_i;            // kCtaWarps + 1 ints of shared scratch
+    unsigned long long *s_u;  // 2 * kCtaWarps u64 of shared scratch
+    __device__ __forceinline__ CtaGroup(int *si, unsigned long long *su) : lane(threadIdx.x), s_i(si), s_u(su) {}
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ int rank(bool p, int *tot) {
+        unsigned b = __ballot_sync(0xffffffffu, p);
+        int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        if (l == 0) s_i[w] = __popc(b);
+        __syncthreads();
+        int before = 0, all = 0;
+#pragma unroll
+        for (int i = 0; i < kCtaWarps; i++) { int c = s_i[i]; before += (i < w) ? c : 0; all += c; }
+        __syncthreads();
+        *tot = all;
+        return before + __popc(b & ((1u << l) - 1u));
+    }
+    __device__ __forceinline__ long long sum(long long v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) s_u[w] = (unsigned long long)v;
+        __syncthreads();
+        long long a = 0;
+#pragma unroll
+        for (int i = 0; i < kCtaWarps; i++) a += (long long)s_u[i];
+        __syncthreads();
+        return a;
+    }
+    __device__ __forceinline__ int sum(int v) { return (int)sum((long long)v); }
+    __device__ __forceinline__ U128 sum(U128 v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            U128 w{__shfl_xor_sync(0xffffffffu, v.lo, o), __shfl_xor_sync(0xffffffffu, v.hi, o)};
+            v = u128_add(v, w);
+        }
+        int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) { s_u[2 * w] = v.lo; s_u[2 * w + 1] = v.hi; }
+        __syncthreads();
+        U128 a = u128_zero();
+#pragma unroll
+        for (int i = 0; i < kCtaWarps; i++) a = u128_add(a, U128{s_u[2 * i], s_u[2 * i + 1]});
+        __syncthreads();
+        return a;
+    }
+};
+
+__device__ __forceinline__ double atomic_max_nonneg(unsigned long long *addr, double v) {
+    // non-negative IEEE doubles order like their bit patterns
+    return __longlong_as_double((long long)atomicMax(addr, (unsigned long long)__double_as_longlong(v)));
+}
+
+}  // namespace rs

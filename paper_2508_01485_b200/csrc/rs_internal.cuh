@@ -1,0 +1,156 @@
+// Internal declarations of librs (B200 / sm_100a). Not part of the ABI.
+// The oracle (oracle/) shares nothing with this tree: no header, helper,
+// constant or table.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+#include "../../include/rs.h"
+
+#ifdef RS_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace rs {
+
+#ifdef RS_WITH_NCCL
+// NCCL is resolved at run time (dlopen) so that librs uses the libnccl already
+// loaded in the process (e.g. the one torch.distributed brought) instead of
+// linking a second, possibly different, copy.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char *(*GetErrorString)(ncclResult_t);
+};
+const NcclApi *nccl_api(std::string *err);
+#endif
+
+constexpr int kMaxK = 254;        // target columns (uint8 label 0xFF = "other")
+constexpr uint8_t kOther = 0xFF;  // community without its own 8-bit code
+constexpr int kNumBins = 8;       // degree classes (load time)
+// degree class c holds vertices with kBinLo[c] <= d < kBinLo[c+1]
+__host__ __device__ constexpr int64_t bin_lo(int i) {
+    return i <= 0 ? 0 : i == 1 ? 8 : i == 2 ? 16 : i == 3 ? 32 : i == 4 ? 64 : i == 5 ? 128 : i == 6 ? 2048
+         : i == 7 ? 8192 : INT64_MAX;
+}
+
+// 16-byte per-vertex record gathered by the P-list phases (one sector / 2).
+struct __align__(16) VRec {
+    double a_self;     // omega_v(C(v))^(1/3) (unnormalised) if C(v) is a target, else 0
+    int32_t pcnt;      // |P(v)|: inter-community neighbours (G' in-degree)
+    uint8_t lab;       // 8-bit community code (< k: target column)
+    uint8_t head;      // 1 if v can be an RSI head: target community and d(v) >= 2
+    uint16_t pad;
+};
+
+// Per (vertex, column) record read by the Type-II pull (Phase D).
+struct __align__(16) BQ {
+    double B;          // sum_{v in P(w), col(v)=c} a_v(c), exact sum rounded once
+    double Q;          // a_w(c)^2 = omega_w(c)^(2/3)
+};
+
+struct Bins {
+    int64_t count[kNumBins] = {0};
+    int64_t offset[kNumBins + 1] = {0};
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t side[kNumBins] = {nullptr};   // forked streams for concurrent bins
+    cudaEvent_t ev_fork = nullptr, ev_join[kNumBins] = {nullptr};
+    cudaEvent_t ev_phase[8] = {nullptr};
+    std::string err;
+    int64_t launches = 0;
+
+    // multi-GPU
+    int rank = 0, world = 1;
+#ifdef RS_WITH_NCCL
+    ncclComm_t comm = nullptr;
+#endif
+    int64_t head_lo = 0, head_hi = 0;          // owned vertex range [lo, hi)
+    std::vector<int64_t> bounds;               // world+1 range boundaries
+
+    // graph (load time)
+    int64_t n = 0, nnz = 0;
+    int64_t *rowptr = nullptr;   // n+1
+    int32_t *col = nullptr;      // nnz
+    int32_t *binv = nullptr;     // n: vertices grouped by degree class, ascending id within class
+    Bins bins;
+    int64_t d_max = 0;
+    bool loaded = false;
+
+    // communities (set time)
+    int32_t *comm_id = nullptr;  // n
+    uint8_t *lab = nullptr;      // n
+    int32_t *chist = nullptr;    // community sizes, cap entries
+    uint8_t *ccode = nullptr;    // community id -> 8-bit code
+    int64_t ccap = 0;
+    int32_t *targets = nullptr;  // kMaxK
+    int32_t k = 0;
+    int32_t h_targets[kMaxK];
+    bool has_comm = false;
+
+    // score (per rs_score)
+    int32_t *f = nullptr;        // n*k counts
+    double *omega = nullptr;     // n*k weights (unnormalised)
+    VRec *vrec = nullptr;        // n
+    int32_t *pidx = nullptr;     // nnz, P(u) stored at rowptr[u] ...
+    int32_t *pplus = nullptr;    // nnz, P+(u) (orientation) at rowptr[u] ...
+    int32_t *ppcnt = nullptr;    // n
+    BQ *bq = nullptr;            // n*k
+    unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum
+    unsigned long long *n1 = nullptr;    // n Type-I triad counts
+    double *score = nullptr;     // n
+    unsigned long long *scal = nullptr;  // device scalars (see kScal*)
+    int64_t k_alloc = 0;         // k the per-score buffers were sized for
+    bool scored = false;
+
+    // top-k scratch
+    unsigned long long *tk_hist = nullptr;   // 256 * 8
+    unsigned long long *tk_cand = nullptr;   // candidates (key, id) pairs
+    int64_t tk_cap = 0;
+
+    // device scratch for reductions / validation
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+};
+
+// device scalar slots in Ctx::scal
+enum {
+    kScalOmegaMaxBits = 0,   // omega_max as IEEE bits (non-negative => monotone)
+    kScalErr = 1,            // first validation error code (0 = none)
+    kScalErrRow = 2,         // row of the first error
+    kScalCnt0 = 3,           // generic counters
+    kScalNBorder = 4,
+    kScalNPred = 5,
+    kScalNTri = 6,
+    kScalTk = 8,             // top-k state (8 slots)
+    kScalCount = 32
+};
+
+// ---- kernels (launchers). Each returns cudaGetLastError() of the launch. ----
+cudaError_t launch_validate(Ctx &c);
+cudaError_t launch_bins(Ctx &c);
+cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets);
+cudaError_t launch_phase_a(Ctx &c);
+cudaError_t launch_phase_c(Ctx &c);
+cudaError_t launch_phase_e(Ctx &c);
+cudaError_t launch_phase_d(Ctx &c);
+cudaError_t launch_topk(Ctx &c, int64_t K, int32_t *ids_dev, double *scores_dev, int64_t lo, int64_t hi);
+cudaError_t launch_counts_total(Ctx &c, int32_t *total_dev);
+cudaError_t launch_border_list(Ctx &c, int32_t *bv_dev, int64_t *nb_host);
+cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int64_t *nent_host);
+cudaError_t launch_type2_counts(Ctx &c, int64_t *t2_dev);
+cudaError_t launch_type1_export(Ctx &c, int64_t *t1_dev);
+cudaError_t launch_stats(Ctx &c, int64_t out[4]);
+cudaError_t launch_minmax_i32(Ctx &c, const int32_t *a, int64_t n, int64_t *mn, int64_t *mx);
+
+}  // namespace rs

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs -- bit-exact on counts, border sets, G' lists, triad counts
+and top-k ids; fp64 scores within 1e-9 relative (BASELINE north_star)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from rsgpu import assert_scores_close, assert_topk, compare_full, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+rsb = pytest.importorskip("paper_2508_01485_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rsb.load_library()
+
+
+def full(g, k=None, targets=None, K=None, exact_topk=False):
+    K = K or g.n
+    r_or = oracle.run(g, k=k, targets=targets, K=K)
+    r_gpu = run_gpu(g, k=k, targets=r_or.targets, K=K)
+    compare_full(g, r_or, r_gpu, exact_topk=exact_topk)
+    return r_or, r_gpu
+
+
+# ---------------------------------------------------------------- fixtures
+def test_worked_example():
+    g, meta = gen.load_fixture("worked_example")
+    r_or, r_gpu = full(g, targets=[int(x) for x in meta["targets"]], exact_topk=True)
+    assert 0.422 <= r_gpu["R"][0] < 0.423
+    assert (r_gpu["nI"][0], r_gpu["nII"][0]) == (2, 1)
+
+
+@pytest.mark.parametrize("name,k", [("karate", 2), ("karate_greedy3", 3), ("karate_louvain4", 4)])
+def test_karate(name, k):
+    g, meta = gen.load_fixture(name)
+    r_or, r_gpu = full(g, k=k, exact_topk=True)
+    if "expect_tie" in meta:
+        ties = [int(x) for x in meta["expect_tie"]]
+        assert len({r_gpu["R"][t] for t in ties}) == 1          # exact fixed-point ties
+        assert list(r_gpu["top_ids"][:3]) == ties
+
+
+@pytest.mark.parametrize("c,m", [(3, 1), (3, 3), (4, 2), (5, 3), (6, 4), (2, 5)])
+def test_complete_graphs(c, m):
+    n = c * m
+    g = gen.from_adjacency(np.ones((n, n), dtype=bool), [i // m for i in range(n)])
+    full(g, targets=list(range(c)), exact_topk=True)
+
+
+def test_degenerate_cases():
+    # star: centre in one community, leaves in another
+    g = gen.from_edges(9, [(0, i) for i in range(1, 9)], [0] + [1] * 8)
+    r_or, r_gpu = full(g, targets=[0, 1], exact_topk=True)
+    assert np.all(r_gpu["R"] == 0)
+    # triangle over three communities: counted, zero weight
+    g = gen.from_edges(3, [(0, 1), (1, 2), (0, 2)], [0, 1, 2])
+    r_or, r_gpu = full(g, targets=[0, 1, 2], exact_topk=True)
+    assert np.all(r_gpu["nI"] == 2)
+    # isolated vertices and a single edge
+    g = gen.from_edges(6, [(0, 1)], [0, 1, 0, 1, 2, 2])
+    full(g, k=2, exact_topk=True)
+
+
+# ---------------------------------------------------------------- random graphs vs oracle
+PP = [(int(n), int(c), s) for s, (n, c) in enumerate(
+    zip(np.random.default_rng(11).integers(20, 400, 24), np.random.default_rng(12).integers(3, 9, 24)))]
+
+
+@pytest.mark.parametrize("n,c,seed", PP)
+def test_planted_partitions(n, c, seed):
+    rng = np.random.default_rng(seed + 77)
+    g = gen.planted_partition(n, c, float(rng.uniform(0.05, 0.4)), float(rng.uniform(0.01, 0.1)), seed=seed + 500)
+    k = int(min(len(np.unique(g.comm)), rng.integers(2, c + 1)))
+    full(g, k=k)
+
+
+def test_many_columns_smem_path():
+    """k > 8 takes the shared-memory histogram / B-table path."""
+    g = gen.planted_partition(600, 14, 0.12, 0.03, seed=3)
+    full(g, k=12)
+
+
+def test_uncoded_communities_full_id_compare():
+    """More than 255 communities: the smaller ones share the 0xFF code and the
+    border / P-list tests fall back to the full int32 ids."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    g = gen.planted_partition(n, 1, 0.004, 0.004, seed=9)
+    comm = rng.integers(0, 700, size=n).astype(np.int32)
+    comm[: n // 2] = rng.integers(0, 4, size=n // 2)      # four big communities
+    g = gen.Graph(g.rowptr, g.col, comm)
+    full(g, k=4)
+
+
+@pytest.mark.parametrize("name,scale", [("dblp", 0.05), ("lj", 0.004), ("orkut", 0.003), ("orkut", 0.01)])
+def test_rsgen_scaled(name, scale):
+    g = gen.config_graph(name, scale=scale)
+    full(g, k=5, K=200)
+
+
+def test_dblp_full_size():
+    g = gen.config_graph("dblp")
+    full(g, k=5, K=25)
+
+
+@pytest.mark.parametrize("name", ["lj", "orkut"])
+def test_full_size_sampled(name):
+    """BASELINE-size graphs in the bench's launch configuration: every vertex's
+    counts / weights / G' list bit-exact, scores on a sample of heads (random +
+    the GPU's top-25 + the highest-degree heads) against the oracle one by one,
+    and the top-k property on the sample."""
+    g = gen.config_graph(name)
+    r_gpu = run_gpu(g, k=5, K=25, validate=False)
+    t = oracle.select_targets(g.comm, 5)
+    assert np.array_equal(t, r_gpu["targets"])
+    f, T = oracle.counts(g, t)
+    assert np.array_equal(f, r_gpu["f"]) and np.array_equal(T, r_gpu["T"])
+    w = oracle.weights(f)
+    wmax = oracle.omega_max(w)
+    nz = w != 0
+    assert np.array_equal(nz, r_gpu["omega"] != 0)
+    assert np.max(np.abs(r_gpu["omega"][nz] - w[nz]) / w[nz]) <= 1e-10
+    assert np.array_equal(np.nonzero(oracle.border(g))[0].astype(np.int32), r_gpu["border"])
+    rng = np.random.default_rng(1)
+    deg = np.diff(g.rowptr)
+    heads = np.unique(np.concatenate([rng.integers(0, g.n, 400), r_gpu["top_ids"].astype(np.int64),
+                                      np.argsort(deg)[-20:]]))
+    R, nI, nII = oracle.rsi(g, t, w, wmax, heads)
+    assert_scores_close(R, r_gpu["R"][heads])
+    np.testing.assert_array_equal(nI, r_gpu["nI"][heads])
+    np.testing.assert_array_equal(nII, r_gpu["nII"][heads])
+    kth = r_gpu["top_scores"][-1]
+    assert np.all(R[~np.isin(heads, r_gpu["top_ids"])] <= kth * (1 + 1e-9))
+
+
+# ---------------------------------------------------------------- API behaviour
+def test_determinism_and_reuse():
+    g = gen.config_graph("orkut", scale=0.003)
+    s = rsb.Scorer(0)
+    a = run_gpu(g, k=5, scorer=s)
+    b = run_gpu(g, k=5, scorer=s)
+    assert np.array_equal(a["R"].view(np.uint64), b["R"].view(np.uint64))
+    assert np.array_equal(a["top_ids"], b["top_ids"])
+    s.close()
+
+
+def test_topk_edges_and_device_outputs():
+    import torch
+    g, _ = gen.load_fixture("karate_greedy3")
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col, validate=True)
+    s.set_communities(g.comm, 3)
+    s.score()
+    ids, sc = s.topk(1000)                 # K > n clamps
+    assert len(ids) == g.n
+    r_or = oracle.run(g, k=3, K=g.n)
+    assert list(ids) == list(r_or.top_ids)
+    ids1, _ = s.topk(1)
+    assert list(ids1) == [12]
+    d_ids = torch.empty(5, dtype=torch.int32, device="cuda")
+    d_sc = torch.empty(5, dtype=torch.float64, device="cuda")
+    cnt = s.topk(5, d_ids, d_sc)
+    torch.cuda.synchronize()
+    assert cnt == 5 and d_ids.cpu().tolist() == list(r_or.top_ids[:5])
+    # device-resident inputs
+    s2 = rsb.Scorer(0)
+    s2.load_csr(torch.from_numpy(g.rowptr).cuda(), torch.from_numpy(g.col).cuda())
+    s2.set_communities(torch.from_numpy(g.comm).cuda(), 3)
+    out = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    s2.score(scores_out=out)
+    torch.cuda.synchronize()
+    assert_scores_close(r_or.R, out.cpu().numpy())
+    s.close()
+    s2.close()
+
+
+def test_user_targets_and_errors():
+    g, _ = gen.load_fixture("karate_louvain4")
+    r_or = oracle.run(g, targets=[3, 0, 2], K=10)
+    r_gpu = run_gpu(g, targets=[3, 0, 2], K=10)
+    compare_full(g, r_or, r_gpu, exact_topk=True)
+    s = rsb.Scorer(0)
+    with pytest.raises(rsb.RsError) as e:
+        s.score()
+    assert e.value.status == rsb.RS_ESTATE
+    # asymmetric CSR
+    rp = np.array([0, 1, 1], dtype=np.int64)
+    with pytest.raises(rsb.RsError) as e:
+        s.load_csr(rp, np.array([1], dtype=np.int32), validate=True)
+    assert e.value.status == rsb.RS_EINVAL and "symmetric" in str(e.value)
+    # unsorted row
+    rp = np.array([0, 2, 3, 4], dtype=np.int64)
+    with pytest.raises(rsb.RsError) as e:
+        s.load_csr(rp, np.array([2, 1, 0, 0], dtype=np.int32), validate=True)
+    assert "ascending" in str(e.value)
+    s.load_csr(g.rowptr, g.col, validate=True)
+    with pytest.raises(rsb.RsError):
+        s.set_communities(g.comm, 5)           # only 4 communities
+    with pytest.raises(rsb.RsError):
+        s.set_communities(g.comm, 2, targets=[0, 0])
+    with pytest.raises(rsb.RsError):
+        s.set_communities(-g.comm - 1, 2)
+    s.close()
