@@ -51,11 +51,14 @@ typedef struct {
     int64_t m;                /* |E| undirected = nnz / 2                       */
     int64_t n_border;         /* |V_b| over all communities              */
     int64_t n_pred_entries;   /* sum over u of |P(u)| = |E_b|           */
-    int64_t n_triangles;      /* triangles of G' (3 distinct communities)       */
+    int64_t n_triangles;      /* triangles of G' (3 distinct communities) with a
+                                 target among their two lowest-ranked vertices
+                                 (the ones that can carry Type-I terms)         */
     double omega_max;         /* max weight over all cells (C-7)  */
-    float ms_phase[8];        /* [0] targets+labels [1] border/histogram/weight
-                                 [2] B-table + orientation [3] Type-I triangles
-                                 [4] Type-II + finalize  [5..7] reserved        */
+    float ms_phase[8];        /* [0] Phase A border/histogram/weights/G' lists
+                                 [1] Phase C B-table + orientation
+                                 [2] Phase E Type-I triangles
+                                 [3] Phase D Type-II + finalize [4..7] reserved */
 } rs_stats;
 
 /* Flags for rs_load_csr. */

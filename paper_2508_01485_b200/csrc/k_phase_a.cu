@@ -2,30 +2,37 @@
 //   Step 1 border test (Algorithm 1 lines P:254-263),
 //   Step 2a neighbour-community histogram f[u][i] over the k targets,
 //   Step 2b weights omega_u(C_i) = H(L_i) * (L_all - 1) (Eq. 3, Eq. 5, Algorithm 2
-//           P:457-482, closed form of Eq. H_optimal P:417 with exact zeros),
+//           P:457-482, closed form of Eq. H_optimal P:417 with exact zeros) and
+//           their cube roots a_u(C_i) used by every triad term (Eq. 4),
 //   Step 2c omega_max partial maxima,
 //   Step 2d G' predecessor list P(u) = {x in N(u): C(x) != C(u)}, written
-//           in place at col offset rowptr[u] (no scan needed), ascending.
+//           in place at offset rowptr[u] (no scan needed), ascending.
 // Labels are the 8-bit community codes of rs_set_communities; only vertices of
 // two uncoded ("other") communities fall back to comparing full int32 ids.
-// Degree-binned: a group of G lanes (or a whole CTA for hubs) owns a vertex.
+// Degree-binned: a group of G lanes (or a whole CTA for hubs) owns a vertex;
+// each lane keeps kUnroll independent loads in flight (the row walk is
+// latency-bound otherwise).
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
 
 namespace rs {
+
+constexpr int kUnroll = 4;
 
 struct PhaseAArgs {
     const int64_t *__restrict__ rowptr;
     const int32_t *__restrict__ col;
     const int32_t *__restrict__ comm;
     const uint8_t *__restrict__ lab;
-    const int32_t *__restrict__ verts;  // bin slice
+    int64_t vlo;                        // first vertex of the degree-class range
     int64_t nverts;
     int32_t k;
+    double wide_bound;                  // |P|^2 above which a head's Type-I sum needs 3 limbs
     const double *__restrict__ l2t;     // log2 of small integers
     int64_t l2n;
     int32_t *__restrict__ f;
     double *__restrict__ omega;
+    double *__restrict__ amat;
     VRec *__restrict__ vrec;
     int32_t *__restrict__ pidx;
     unsigned long long *scal;
@@ -35,8 +42,30 @@ __device__ __forceinline__ double lg2(const PhaseAArgs &a, int64_t x) {
     return x < a.l2n ? __ldg(a.l2t + x) : log2((double)x);
 }
 
-// k <= 8: per-lane register histogram. Returns the vertex's max weight (group-uniform
-// only on the lanes that computed columns; callers max-reduce per thread anyway).
+// omega for column c of a row with T, L_all, X = sum f log2 f (Algorithm 2)
+__device__ __forceinline__ double weight_of(const PhaseAArgs &a, int fc, int T, int L_all, double X) {
+    const int others = L_all - (fc > 0);   // nonzero columns of L(u, .) besides c
+    if (L_all < 2 || others < 2) return 0.0; // one remaining community: H = 0 exactly
+    const int Y = T - fc;                    // > 0
+    const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
+    const double H = lg2(a, Y) - (X - xc) / (double)Y;
+    const double w = H * (double)(L_all - 1);
+    return w > 0.0 ? w : 0.0;                // canonical +0.0
+}
+
+__device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, double a_self, int pc, uint8_t lu,
+                                           int64_t d) {
+    VRec r;
+    r.a_self = a_self;
+    r.pcnt = pc;
+    r.lab = lu;
+    r.head = (lu < a.k && d >= 2) ? 1 : 0;
+    r.wide = ((double)pc * (double)pc >= a.wide_bound) ? 1 : 0;
+    r.pad = 0;
+    a.vrec[u] = r;
+}
+
+// k <= 8: per-lane register histogram.
 template <class GR>
 __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
     const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
@@ -47,27 +76,33 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
 #pragma unroll
     for (int c = 0; c < 8; c++) cnt[c] = 0;
     int pc = 0;
-    for (int64_t base = beg; base < end; base += GR::size) {
-        const int64_t e = base + g.lane;
-        const bool valid = e < end;
-        int32_t x = 0;
-        uint8_t lx = kOther;
-        if (valid) {
-            x = __ldcs(a.col + e);            // streamed once: evict-first
-            lx = __ldg(a.lab + x);            // 1-byte gather, L2-resident table
-        }
-        bool foreign = valid && (lx != lu);
-        if (valid && lx == kOther && lu == kOther) foreign = __ldg(a.comm + x) != cfull;
+    for (int64_t base = beg; base < end; base += GR::size * kUnroll) {
+        int32_t x[kUnroll];
+        uint8_t lx[kUnroll];
 #pragma unroll
-        for (int c = 0; c < 8; c++) cnt[c] += (c < k && lx == c) ? 1 : 0;
-        int tot;
-        int r = g.rank(foreign, &tot);
-        if (foreign) a.pidx[beg + pc + r] = x;
-        pc += tot;
+        for (int j = 0; j < kUnroll; j++) {
+            const int64_t e = base + j * GR::size + g.lane;
+            x[j] = e < end ? __ldcs(a.col + e) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+            const bool valid = x[j] >= 0;
+            bool foreign = valid && (lx[j] != lu);
+            if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
+#pragma unroll
+            for (int c = 0; c < 8; c++) cnt[c] += (c < k && lx[j] == c) ? 1 : 0;
+            if (base + j * GR::size < end) {          // group-uniform
+                int tot;
+                const int r = g.rank(foreign, &tot);
+                if (foreign) a.pidx[beg + pc + r] = x[j];
+                pc += tot;
+            }
+        }
     }
 #pragma unroll
     for (int c = 0; c < 8; c++) cnt[c] = g.sum(cnt[c]);
-    // row statistics (identical on every lane, fixed order)
     int T = 0, L_all = 0;
     double X = 0.0;
 #pragma unroll
@@ -77,37 +112,21 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
         if (cnt[c] > 1) X += (double)cnt[c] * lg2(a, cnt[c]);
     }
     const int64_t d = end - beg;
-    double wmax = 0.0;
-    double a_self = 0.0;
+    double wmax = 0.0, a_self = 0.0;
     for (int c = g.lane; c < k; c += GR::size) {
         int fc = 0;
 #pragma unroll
         for (int j = 0; j < 8; j++) fc = (j == c) ? cnt[j] : fc;
-        const int others = L_all - (fc > 0);   // nonzero columns of L(u, .) besides c
-        double w = 0.0;
-        if (L_all >= 2 && others >= 2) {
-            const int Y = T - fc;               // > 0
-            const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
-            const double H = lg2(a, Y) - (X - xc) / (double)Y;
-            w = H * (double)(L_all - 1);
-            w = w > 0.0 ? w : 0.0;              // canonical +0.0
-        }
+        const double w = weight_of(a, fc, T, L_all, X);
+        const double ac = w > 0.0 ? cbrt(w) : 0.0;
         a.omega[u * k + c] = w;
+        a.amat[u * k + c] = ac;
         a.f[u * k + c] = fc;
         wmax = w > wmax ? w : wmax;
-        if (c == (int)lu) a_self = cbrt(w);
+        if (c == (int)lu) a_self = ac;
     }
-    // own column lives on lane (lu mod G); the lane holding it writes the record
     const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
-    if ((int)g.lane == owner) {
-        VRec r;
-        r.a_self = a_self;
-        r.pcnt = pc;
-        r.lab = lu;
-        r.head = (lu < k && d >= 2) ? 1 : 0;
-        r.pad = 0;
-        a.vrec[u] = r;
-    }
+    if ((int)g.lane == owner) write_vrec(a, u, a_self, pc, lu, d);
     return wmax;
 }
 
@@ -121,25 +140,35 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     for (int c = g.lane; c < k; c += GR::size) hist[c] = 0;
     g.sync();
     int pc = 0;
-    for (int64_t base = beg; base < end; base += GR::size) {
-        const int64_t e = base + g.lane;
-        const bool valid = e < end;
-        int32_t x = 0;
-        uint8_t lx = kOther;
-        if (valid) { x = __ldcs(a.col + e); lx = __ldg(a.lab + x); }
-        bool foreign = valid && (lx != lu);
-        if (valid && lx == kOther && lu == kOther) foreign = __ldg(a.comm + x) != cfull;
-        if (valid && lx < k) atomicAdd(&hist[lx], 1);
-        int tot;
-        int r = g.rank(foreign, &tot);
-        if (foreign) a.pidx[beg + pc + r] = x;
-        pc += tot;
+    for (int64_t base = beg; base < end; base += GR::size * kUnroll) {
+        int32_t x[kUnroll];
+        uint8_t lx[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+            const int64_t e = base + j * GR::size + g.lane;
+            x[j] = e < end ? __ldcs(a.col + e) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+            const bool valid = x[j] >= 0;
+            bool foreign = valid && (lx[j] != lu);
+            if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
+            if (valid && lx[j] < k) atomicAdd(&hist[lx[j]], 1);
+            if (base + j * GR::size < end) {
+                int tot;
+                const int r = g.rank(foreign, &tot);
+                if (foreign) a.pidx[beg + pc + r] = x[j];
+                pc += tot;
+            }
+        }
     }
     g.sync();
     int T = 0, L_all = 0;
     double X = 0.0;
     for (int c = 0; c < k; c++) {
-        int v = hist[c];
+        const int v = hist[c];
         T += v;
         L_all += v > 0;
         if (v > 1) X += (double)v * lg2(a, v);
@@ -148,27 +177,17 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     double wmax = 0.0;
     for (int c = g.lane; c < k; c += GR::size) {
         const int fc = hist[c];
-        const int others = L_all - (fc > 0);
-        double w = 0.0;
-        if (L_all >= 2 && others >= 2) {
-            const int Y = T - fc;
-            const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
-            w = (lg2(a, Y) - (X - xc) / (double)Y) * (double)(L_all - 1);
-            w = w > 0.0 ? w : 0.0;
-        }
+        const double w = weight_of(a, fc, T, L_all, X);
         a.omega[u * k + c] = w;
+        a.amat[u * k + c] = w > 0.0 ? cbrt(w) : 0.0;
         a.f[u * k + c] = fc;
         wmax = w > wmax ? w : wmax;
     }
     g.sync();
     if (g.lane == 0) {
-        VRec r;
-        r.a_self = lu < k ? cbrt(a.omega[u * k + lu]) : 0.0;
-        r.pcnt = pc;
-        r.lab = lu;
-        r.head = (lu < k && d >= 2) ? 1 : 0;
-        r.pad = 0;
-        a.vrec[u] = r;
+        double as = 0.0;
+        if (lu < k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cbrt(w) : 0.0; }
+        write_vrec(a, u, as, pc, lu, d);
     }
     g.sync();
     return wmax;
@@ -195,7 +214,7 @@ __global__ void __launch_bounds__(256) k_phase_a_warp(PhaseAArgs a) {
     const int64_t ngroups = (int64_t)gridDim.x * groups_per_block;
     double wmax = 0.0;
     for (int64_t i = gid; i < a.nverts; i += ngroups) {
-        const int64_t u = a.verts[i];
+        const int64_t u = (a.vlo + i);
         double w;
         if constexpr (SMEM) w = phase_a_vertex_smem(a, u, g, hist + (threadIdx.x / 32) * 256);
         else w = phase_a_vertex(a, u, g);
@@ -212,7 +231,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_a_cta(PhaseAArgs a) {
     CtaGroup g(s_i, s_u);
     double wmax = 0.0;
     for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) {
-        const int64_t u = a.verts[i];
+        const int64_t u = (a.vlo + i);
         double w;
         if constexpr (SMEM) w = phase_a_vertex_smem(a, u, g, hist);
         else w = phase_a_vertex(a, u, g);
@@ -236,7 +255,7 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
     // class -> group: [0,8):4 [8,16):8 [16,32):16 [32,2048):32 [2048,inf):CTA
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         PhaseAArgs a = base;
-        a.verts = c.binv + c.bins.offset[cls];
+        a.vlo = c.bins.offset[cls];
         a.nverts = c.bins.count[cls];
         if (a.nverts == 0) continue;
         cudaStream_t s = c.side[cls];
@@ -259,8 +278,11 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
 cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
     PhaseAArgs a;
     a.rowptr = c.rowptr; a.col = c.col; a.comm = c.comm_id; a.lab = c.lab;
-    a.verts = nullptr; a.nverts = 0; a.k = c.k; a.l2t = l2t; a.l2n = l2n;
-    a.f = c.f; a.omega = c.omega; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
+    a.vlo = 0; a.nverts = 0; a.k = c.k; a.l2t = l2t; a.l2n = l2n;
+    // unnormalised grouped Type-I terms are < 2 * omega_max_bound; a head needs the
+    // 3-limb accumulator when |P|^2 * that bound could reach 2^31 (fx_red2 contract)
+    a.wide_bound = wide_bound(c.k);
+    a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     if (c.k <= 8) launch_bins_a<false>(c, a);
     else launch_bins_a<true>(c, a);
     return cudaGetLastError();

@@ -44,80 +44,106 @@ __global__ void k_validate(const int64_t *__restrict__ rowptr, const int32_t *__
     }
 }
 
-cudaError_t launch_validate(Ctx &c) {
-    k_validate<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.col, c.n, c.scal);
+cudaError_t launch_validate(Ctx &c, const int64_t *rp, const int32_t *col) {
+    k_validate<<<148 * 8, 256, 0, c.stream>>>(rp, col, c.n, c.scal);
     c.launches++;
     return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- degree classes
-__device__ __forceinline__ int degree_class(int64_t d) {
-    int b = 0;
-#pragma unroll
-    for (int i = 1; i < kNumBins; i++) b += (d >= bin_lo(i));
-    return b;
-}
-
-__global__ void k_bin_flags(const int64_t *__restrict__ rowptr, int64_t n, int cls, int32_t *flags) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
-        flags[u] = degree_class(rowptr[u + 1] - rowptr[u]) == cls;
-}
-
-__global__ void k_bin_scatter(const int32_t *__restrict__ flags, const int32_t *__restrict__ pos, int64_t n,
-                              int64_t base, int32_t *binv) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
-        if (flags[u]) binv[base + pos[u]] = (int32_t)u;
-}
-
-__global__ void k_dmax(const int64_t *__restrict__ rowptr, int64_t n, unsigned long long *out) {
-    unsigned long long m = 0;
+// ---------------------------------------------------------------- internal numbering
+// Vertices are renumbered by degree, descending (ties: ascending original id),
+// once at load time. Every later gather then finds the high-degree vertices --
+// the ones that appear in most adjacency and P lists -- packed at the front of
+// each per-vertex table (L2-friendly), and the degree classes of the binned
+// scheduler become contiguous ranges. Results are mapped back to original ids
+// on output. Exact fixed-point sums make scores independent of the numbering.
+__global__ void k_deg_iota(const int64_t *__restrict__ rp, int64_t n, uint32_t *deg, int32_t *iota) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long d = (unsigned long long)(rowptr[u + 1] - rowptr[u]);
-        m = d > m ? d : m;
+        deg[u] = (uint32_t)(rp[u + 1] - rp[u]);
+        iota[u] = (int32_t)u;
     }
-    for (int o = 16; o > 0; o >>= 1) { unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o); m = x > m ? x : m; }
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+__global__ void k_inv_perm(const int32_t *__restrict__ perm, int64_t n, int32_t *inv, const uint32_t *__restrict__ deg_s,
+                           int64_t *d64) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        inv[perm[r]] = (int32_t)r;
+        d64[r] = deg_s[r];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) d64[n] = 0;
+}
+__global__ void k_relabel_rows(const int64_t *__restrict__ rp_o, const int32_t *__restrict__ col_o,
+                               const int32_t *__restrict__ perm, const int32_t *__restrict__ inv,
+                               const int64_t *__restrict__ rp, int64_t n, int32_t *out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) / 32) {
+        const int64_t src = perm[r], b = rp_o[src], d = rp_o[src + 1] - b, o = rp[r];
+        for (int64_t i = lane; i < d; i += 32) out[o + i] = inv[col_o[b + i]];
+    }
+}
+// number of vertices with degree >= bin_lo(cls), cls = 1..7 (degrees sorted descending)
+__global__ void k_class_bounds(const uint32_t *__restrict__ deg_s, int64_t n, unsigned long long *out) {
+    const int cls = threadIdx.x + 1;
+    if (cls >= kNumBins) return;
+    const int64_t lo_deg = bin_lo(cls);
+    int64_t lo = 0, hi = n;   // first r with deg_s[r] < lo_deg
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)deg_s[mid] >= lo_deg) lo = mid + 1; else hi = mid;
+    }
+    out[cls] = (unsigned long long)lo;
 }
 
-// vertices grouped by degree class, ascending id inside a class (stable)
-cudaError_t launch_bins(Ctx &c) {
-    const int64_t n = c.n;
-    int32_t *flags = (int32_t *)c.scratch;
-    int32_t *pos = flags + n;
-    void *tmp = pos + n;
-    size_t tmp_bytes = c.scratch_bytes - 2 * sizeof(int32_t) * (size_t)n;
-    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    if (blocks < 1) blocks = 1;
-    int64_t base = 0;
+cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o) {
+    const int64_t n = c.n, nnz = c.nnz;
+    uint32_t *deg = nullptr, *deg_s = nullptr;
+    int32_t *iota = nullptr, *tmpcol = nullptr;
+    int64_t *d64 = nullptr;
+    void *tmp = nullptr;
+    cudaError_t e = cudaSuccess;
+    auto done = [&](cudaError_t r) {
+        cudaStreamSynchronize(c.stream);
+        cudaFree(deg); cudaFree(deg_s); cudaFree(iota); cudaFree(tmpcol); cudaFree(d64); cudaFree(tmp);
+        return r;
+    };
+    if ((e = cudaMalloc(&deg, 4 * n)) || (e = cudaMalloc(&deg_s, 4 * n)) || (e = cudaMalloc(&iota, 4 * n)) ||
+        (e = cudaMalloc(&d64, 8 * (n + 1))) || (e = cudaMalloc(&tmpcol, 4 * std::max<int64_t>(nnz, 1))))
+        return done(e);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_deg_iota<<<blocks, 256, 0, c.stream>>>(rp_o, n, deg, iota);
+    size_t need_sort = 0, need_scan = 0, need_seg = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, need_sort, deg, deg_s, iota, c.perm, (int)n, 0, 32, c.stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, need_scan, d64, c.rowptr, (int)(n + 1), c.stream);
+    cub::DeviceSegmentedSort::SortKeys(nullptr, need_seg, tmpcol, c.col, nnz, (int)n, c.rowptr, c.rowptr + 1,
+                                       c.stream);
+    const size_t need = std::max(need_sort, std::max(need_scan, need_seg));
+    if ((e = cudaMalloc(&tmp, need))) return done(e);
+    size_t t1 = need;
+    cub::DeviceRadixSort::SortPairsDescending(tmp, t1, deg, deg_s, iota, c.perm, (int)n, 0, 32, c.stream);
+    k_inv_perm<<<blocks, 256, 0, c.stream>>>(c.perm, n, c.inv, deg_s, d64);
+    t1 = need;
+    cub::DeviceScan::ExclusiveSum(tmp, t1, d64, c.rowptr, (int)(n + 1), c.stream);
+    k_relabel_rows<<<148 * 16, 256, 0, c.stream>>>(rp_o, col_o, c.perm, c.inv, c.rowptr, n, tmpcol);
+    t1 = need;
+    if (nnz) cub::DeviceSegmentedSort::SortKeys(tmp, t1, tmpcol, c.col, nnz, (int)n, c.rowptr, c.rowptr + 1, c.stream);
+    k_class_bounds<<<1, 32, 0, c.stream>>>(deg_s, n, c.scal + kScalTk);
+    c.launches += 8;
+    unsigned long long ge[kNumBins] = {0};
+    uint32_t dmax = 0;
+    cudaMemcpyAsync(ge, c.scal + kScalTk, sizeof(ge), cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(&dmax, deg_s, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream);
+    if ((e = cudaStreamSynchronize(c.stream))) return done(e);
+    if ((e = cudaGetLastError())) return done(e);
+    // ge[cls] = #vertices with degree >= bin_lo(cls); class cls = [ge[cls+1], ge[cls])
+    ge[0] = (unsigned long long)n;
     for (int cls = 0; cls < kNumBins; cls++) {
-        k_bin_flags<<<blocks, 256, 0, c.stream>>>(c.rowptr, n, cls, flags);
-        c.launches++;
-        size_t need = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, need, flags, pos, (int)n, c.stream);
-        if (need > tmp_bytes) return cudaErrorMemoryAllocation;
-        cub::DeviceScan::ExclusiveSum(tmp, need, flags, pos, (int)n, c.stream);
-        c.launches++;
-        k_bin_scatter<<<blocks, 256, 0, c.stream>>>(flags, pos, n, base, c.binv);
-        c.launches++;
-        int32_t last_pos = 0, last_flag = 0;
-        cudaMemcpyAsync(&last_pos, pos + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
-        cudaMemcpyAsync(&last_flag, flags + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
-        cudaError_t e = cudaStreamSynchronize(c.stream);
-        if (e != cudaSuccess) return e;
-        int64_t cnt = (int64_t)last_pos + last_flag;
-        c.bins.count[cls] = cnt;
-        c.bins.offset[cls] = base;
-        base += cnt;
+        const int64_t hi = (int64_t)ge[cls];
+        const int64_t lo = cls + 1 < kNumBins ? (int64_t)ge[cls + 1] : 0;
+        c.bins.offset[cls] = lo;
+        c.bins.count[cls] = hi - lo;
     }
-    c.bins.offset[kNumBins] = base;
-    cudaMemsetAsync(c.scal + kScalCnt0, 0, sizeof(unsigned long long), c.stream);
-    k_dmax<<<blocks, 256, 0, c.stream>>>(c.rowptr, n, c.scal + kScalCnt0);
-    c.launches++;
-    unsigned long long dm = 0;
-    cudaMemcpyAsync(&dm, c.scal + kScalCnt0, sizeof(dm), cudaMemcpyDeviceToHost, c.stream);
-    cudaError_t e = cudaStreamSynchronize(c.stream);
-    c.d_max = (int64_t)dm;
-    return e;
+    c.d_max = dmax;
+    return done(cudaSuccess);
 }
 
 // ---------------------------------------------------------------- log2 table
@@ -272,9 +298,14 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const int32_t *__restric
     }
 }
 
-__global__ void k_labels(const int32_t *__restrict__ comm, const uint8_t *__restrict__ code, int64_t n, uint8_t *lab) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        lab[i] = code[comm[i]];
+// internal vertex r gets the community of original vertex perm[r] and its code
+__global__ void k_labels(const int32_t *__restrict__ comm_in, const int32_t *__restrict__ perm,
+                         const uint8_t *__restrict__ code, int64_t n, int32_t *comm, uint8_t *lab) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t cid = comm_in[perm[r]];
+        comm[r] = cid;
+        lab[r] = code[cid];
+    }
 }
 
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets) {
@@ -282,11 +313,11 @@ cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user
     cudaMemsetAsync(c.chist, 0, sizeof(int32_t) * nbins, c.stream);
     int blocks = (int)std::min<int64_t>((c.n + 255) / 256, 148 * 4);
     if (blocks < 1) blocks = 1;
-    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_id, c.n, c.chist, nbins);
+    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.n, c.chist, nbins);
     c.launches++;
     k_select<<<1, kSelThreads, 0, c.stream>>>(c.chist, nbins, c.k, user_targets, c.targets, c.ccode, c.scal);
     c.launches++;
-    k_labels<<<blocks, 256, 0, c.stream>>>(c.comm_id, c.ccode, c.n, c.lab);
+    k_labels<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.perm, c.ccode, c.n, c.comm_id, c.lab);
     c.launches++;
     return cudaGetLastError();
 }

@@ -20,15 +20,26 @@ __device__ __forceinline__ unsigned long long score_key(double s) {
     return (b == 0x8000000000000000ull) ? 0ull : b;   // -0.0 -> +0.0
 }
 
+struct TkFilter {             // multi-GPU: only original ids whose internal id is owned
+    const int32_t *inv;       // nullptr = no filter
+    int64_t lo, hi;
+    __device__ __forceinline__ bool keep(int64_t v) const {
+        if (!inv) return true;
+        const int64_t u = inv[v];
+        return u >= lo && u < hi;
+    }
+};
+
 __global__ void __launch_bounds__(kTkThreads) k_tk_hist(const double *__restrict__ score, int64_t lo, int64_t hi,
                                                         int pass, const unsigned long long *st,
-                                                        unsigned long long *hist) {
+                                                        unsigned long long *hist, TkFilter flt) {
     __shared__ unsigned int h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long prefix = st[0];
     const int shift = 56 - 8 * pass;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!flt.keep(i)) continue;
         const unsigned long long key = score_key(score[i]);
         const bool match = (pass == 0) || (((key ^ prefix) >> (shift + 8)) == 0ull);
         if (match) atomicAdd(&h[(key >> shift) & 0xFF], 1u);
@@ -59,7 +70,7 @@ __global__ void k_tk_pick(int pass, unsigned long long *st, unsigned long long *
 __global__ void __launch_bounds__(kTkThreads) k_tk_above(const double *__restrict__ score, int64_t lo, int64_t hi,
                                                          const unsigned long long *st, unsigned long long *cand_key,
                                                          int32_t *cand_id, unsigned long long *cursor,
-                                                         unsigned int *tie_cnt, int64_t chunk) {
+                                                         unsigned int *tie_cnt, int64_t chunk, TkFilter flt) {
     __shared__ unsigned int s_ties;
     if (threadIdx.x == 0) s_ties = 0;
     __syncthreads();
@@ -68,6 +79,7 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_above(const double *__restric
     const int64_t b1 = min(hi, b0 + chunk);
     unsigned int ties = 0;
     for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        if (!flt.keep(i)) continue;
         const unsigned long long key = score_key(score[i]);
         if (key > T) {
             const unsigned long long p = atomicAdd(cursor, 1ull);
@@ -86,7 +98,8 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_above(const double *__restric
 // ties in id order: block b takes its ties while their global rank < krem
 __global__ void __launch_bounds__(kTkThreads) k_tk_ties(const double *__restrict__ score, int64_t lo, int64_t hi,
                                                         const unsigned long long *st, unsigned long long *cand_key,
-                                                        int32_t *cand_id, const unsigned int *tie_cnt, int64_t chunk) {
+                                                        int32_t *cand_id, const unsigned int *tie_cnt, int64_t chunk,
+                                                        TkFilter flt) {
     __shared__ unsigned long long s_pre;
     __shared__ int s_w[kTkThreads / 32];
     const unsigned long long T = st[0];
@@ -106,7 +119,7 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_ties(const double *__restrict
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t t0 = b0; t0 < b1 && base < krem; t0 += blockDim.x) {
         const int64_t i = t0 + threadIdx.x;
-        const bool tie = i < b1 && score_key(score[i]) == T;
+        const bool tie = i < b1 && flt.keep(i) && score_key(score[i]) == T;
         const unsigned m = __ballot_sync(0xffffffffu, tie);
         if (lane == 0) s_w[wid] = __popc(m);
         __syncthreads();
@@ -194,7 +207,8 @@ cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t c
 
 // local top-K of score[lo, hi) into (cand_key, cand_id)[0, K') sorted, K' = min(K, hi-lo)
 cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
-                               int32_t *cand_id) {
+                               int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi) {
+    TkFilter flt{own_inv, own_lo, own_hi};
     unsigned long long *st = c.scal + kScalTk;
     unsigned long long *hist = c.tk_hist;
     unsigned long long *cursor = hist + 256;
@@ -206,16 +220,16 @@ cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsign
     int blocks = (int)std::min<int64_t>((range + kTkThreads - 1) / kTkThreads, kTkBlocks);
     if (blocks < 1) blocks = 1;
     for (int pass = 0; pass < 8; pass++) {
-        k_tk_hist<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist);
+        k_tk_hist<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist, flt);
         k_tk_pick<<<1, 32, 0, c.stream>>>(pass, st, hist);
         c.launches += 2;
     }
     const int64_t chunk = (range + kTkBlocks - 1) / kTkBlocks;
     const int cblocks = (int)std::max<int64_t>(1, (range + chunk - 1) / std::max<int64_t>(chunk, 1));
     k_tk_above<<<cblocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, cursor, tie_cnt,
-                                                     std::max<int64_t>(chunk, 1));
+                                                     std::max<int64_t>(chunk, 1), flt);
     k_tk_ties<<<cblocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, tie_cnt,
-                                                    std::max<int64_t>(chunk, 1));
+                                                    std::max<int64_t>(chunk, 1), flt);
     c.launches += 2;
     return cudaGetLastError();
 }

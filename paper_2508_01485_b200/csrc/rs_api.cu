@@ -12,7 +12,7 @@ namespace rs {
 cudaError_t launch_log2_table(Ctx &c, double *t, int64_t len);
 cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n);
 cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
-                               int32_t *cand_id);
+                               int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi);
 cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
                          double *scores_out);
 cudaError_t launch_partition(Ctx &c);
@@ -194,8 +194,8 @@ extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream,
 
 static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
-    dfree(c.rowptr); dfree(c.col); dfree(c.binv); dfree(c.scratch); dfree(ctx->l2t);
-    dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.ppcnt);
+    dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre);
+    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.pc2); dfree(c.amat);
     dfree(c.acc1); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
 }
@@ -248,16 +248,27 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     free_graph(ctx);
     c.n = n;
     c.nnz = nnz;
-    CK(dalloc(&c.rowptr, n + 1));
-    CK(dalloc(&c.col, nnz));
-    CK(cudaMemcpyAsync(c.rowptr, row_offsets, sizeof(int64_t) * (n + 1),
-                       dev_ro ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
-    if (nnz) CK(cudaMemcpyAsync(c.col, col_idx, sizeof(int32_t) * nnz,
-                                dev_ci ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    // the caller's (original-id) CSR on the device: borrowed if already there
+    const int64_t *rp_o = row_offsets;
+    const int32_t *col_o = col_idx;
+    int64_t *rp_tmp = nullptr;
+    int32_t *col_tmp = nullptr;
+    auto free_tmp = [&]() { if (rp_tmp) cudaFree(rp_tmp); if (col_tmp) cudaFree(col_tmp); };
+    if (!dev_ro) {
+        CK(cudaMalloc(&rp_tmp, sizeof(int64_t) * (n + 1)));
+        CK(cudaMemcpyAsync(rp_tmp, row_offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c.stream));
+        rp_o = rp_tmp;
+    }
+    if (!dev_ci) {
+        cudaError_t e = cudaMalloc(&col_tmp, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+        if (e != cudaSuccess) { free_tmp(); CK(e); }
+        if (nnz) CK(cudaMemcpyAsync(col_tmp, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+        col_o = col_tmp;
+    }
     if (flags & RS_VALIDATE) {
         unsigned long long init[3] = {0ull, ~0ull, 0ull};
         CK(cudaMemcpyAsync(c.scal + rs::kScalErr, init, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice, c.stream));
-        CK(rs::launch_validate(c));
+        CK(rs::launch_validate(c, rp_o, col_o));
         unsigned long long er[2];
         CK(cudaMemcpyAsync(er, c.scal + rs::kScalErr, sizeof(er), cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
@@ -267,25 +278,36 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
                                          "graph not symmetric"};
             std::string m = std::string("rs_load_csr: ") + (er[0] < 6 ? what[er[0]] : "invalid") + " at row " +
                             std::to_string((long long)er[1]);
+            free_tmp();
             free_graph(ctx);
             return fail(ctx, RS_EINVAL, m);
         }
+    }
+    // internal degree-descending numbering (k_setup.cu launch_relabel)
+    CK(dalloc(&c.rowptr, n + 1));
+    CK(dalloc(&c.col, nnz));
+    CK(dalloc(&c.perm, n));
+    CK(dalloc(&c.inv, n));
+    {
+        cudaError_t e = rs::launch_relabel(c, rp_o, col_o);
+        free_tmp();
+        CK(e);
     }
     // per-graph buffers (independent of communities)
     size_t scratch = 24 * (size_t)(n + 1) + (64u << 20);
     CK(cudaMalloc(&c.scratch, scratch));
     c.scratch_bytes = scratch;
-    CK(dalloc(&c.binv, n));
-    CK(rs::launch_bins(c));
+    CK(rs::launch_e_items(c));
     ctx->l2n = std::min<int64_t>(c.d_max + 1, 1ll << 20);
     CK(dalloc(&ctx->l2t, ctx->l2n));
     CK(rs::launch_log2_table(c, ctx->l2t, ctx->l2n));
+    CK(dalloc(&c.comm_in, n));
     CK(dalloc(&c.comm_id, n));
     CK(dalloc(&c.lab, n));
     CK(dalloc(&c.vrec, n));
     CK(dalloc(&c.pidx, nnz));
     CK(dalloc(&c.pplus, nnz));
-    CK(dalloc(&c.ppcnt, n));
+    CK(dalloc(&c.pc2, n));
     CK(dalloc(&c.acc1, 3 * n));
     CK(dalloc(&c.n1, n));
     CK(dalloc(&c.score, n));
@@ -307,10 +329,10 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     if (k < 2 || k > rs::kMaxK) return fail(ctx, RS_EINVAL, "rs_set_communities: k must be in [2, 254]");
     c.scored = false;
     c.has_comm = false;
-    CK(cudaMemcpyAsync(c.comm_id, community_of, sizeof(int32_t) * c.n,
+    CK(cudaMemcpyAsync(c.comm_in, community_of, sizeof(int32_t) * c.n,
                        is_device_ptr(community_of) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
     int64_t mn = 0, mx = 0;
-    CK(rs::launch_minmax_i32(c, c.comm_id, c.n, &mn, &mx));
+    CK(rs::launch_minmax_i32(c, c.comm_in, c.n, &mn, &mx));
     if (mn < 0) return fail(ctx, RS_EINVAL, "rs_set_communities: negative community id");
     if (mx >= (1ll << 28)) return fail(ctx, RS_EINVAL, "rs_set_communities: community id >= 2^28");
     if (mx + 1 > c.ccap) {
@@ -323,6 +345,7 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
         CK(dalloc(&c.f, (size_t)c.n * k));
         CK(dalloc(&c.omega, (size_t)c.n * k));
         CK(dalloc(&c.bq, (size_t)c.n * k));
+        CK(dalloc(&c.amat, (size_t)c.n * k));
         c.k_alloc = k;
     }
     c.k = k;
@@ -356,7 +379,6 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     const int64_t n = c.n;
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
-    CK(cudaMemsetAsync(c.n1, 0, sizeof(unsigned long long) * n, c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, sizeof(unsigned long long), c.stream));
     // Phase A: border + histogram + weights + P lists + omega_max partials
@@ -409,6 +431,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(cudaMemcpy(&wb, c.scal + rs::kScalOmegaMaxBits, sizeof(wb), cudaMemcpyDeviceToHost));
         memcpy(&s.omega_max, &wb, sizeof(double));
         for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&s.ms_phase[i], c.ev_phase[i], c.ev_phase[i + 1]));
+        // ms_phase: [0] A (incl. zeroing) [1] C [2] E (Type-I) [3] D (Type-II + finalize)
         *stats_out = s;
     }
     (void)flags;
@@ -452,7 +475,7 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         if (scores_out && !dev_sc) sc_d = ctx->stage_f64;
     }
     if (c.world == 1) {
-        CK(rs::launch_topk_select(c, Kc, 0, c.n, ctx->cand_key, ctx->cand_id));
+        CK(rs::launch_topk_select(c, Kc, 0, c.n, ctx->cand_key, ctx->cand_id, nullptr, 0, 0));
         CK(rs::tk_sort_emit(c, ctx->cand_key, ctx->cand_id, Kc, Kc, ids_d, sc_d));
     } else {
 #ifdef RS_WITH_NCCL
@@ -468,7 +491,8 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         CK(cudaMemsetAsync(lk, 0, sizeof(unsigned long long) * Kc, c.stream));
         CK(cudaMemsetAsync(li, 0x7f, sizeof(int32_t) * Kc, c.stream));
         if (Kl > 0) {
-            CK(rs::launch_topk_select(c, Kl, c.head_lo, c.head_hi, lk, li));
+            // scores are in original order; keep the ids whose internal id is owned
+            CK(rs::launch_topk_select(c, Kl, 0, c.n, lk, li, c.inv, c.head_lo, c.head_hi));
         }
         unsigned long long *gk = (unsigned long long *)c.scratch;
         int32_t *gi = (int32_t *)(gk + Kc * c.world * 3);
@@ -504,13 +528,19 @@ extern "C" rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_o
     Ctx &c = ctx->c;
     cudaSetDevice(c.device);
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_counts: call rs_score first");
-    if (f_out) { rs_status s = out_copy(ctx, f_out, c.f, (size_t)c.n * c.k); if (s) return s; }
-    if (total_out) {
+    int32_t *forig = nullptr;
+    CK(cudaMalloc(&forig, sizeof(int32_t) * (size_t)c.n * c.k));
+    rs_status s = RS_OK;
+    cudaError_t e = rs::launch_permute_i32(c, c.f, c.k, forig);
+    if (e == cudaSuccess && f_out) s = out_copy(ctx, f_out, forig, (size_t)c.n * c.k);
+    if (e == cudaSuccess && s == RS_OK && total_out) {
         int32_t *tmp = (int32_t *)c.scratch;
-        CK(rs::launch_counts_total(c, tmp));
-        return out_copy(ctx, total_out, tmp, (size_t)c.n);
+        e = rs::launch_counts_total(c, forig, tmp);
+        if (e == cudaSuccess) s = out_copy(ctx, total_out, tmp, (size_t)c.n);
     }
-    return RS_OK;
+    cudaFree(forig);
+    CK(e);
+    return s;
 }
 
 extern "C" rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omega_max_out) {
@@ -518,7 +548,15 @@ extern "C" rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omeg
     Ctx &c = ctx->c;
     cudaSetDevice(c.device);
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_weights: call rs_score first");
-    if (omega_out) { rs_status s = out_copy(ctx, omega_out, c.omega, (size_t)c.n * c.k); if (s) return s; }
+    if (omega_out) {
+        double *worig = nullptr;
+        CK(cudaMalloc(&worig, sizeof(double) * (size_t)c.n * c.k));
+        cudaError_t e = rs::launch_permute_f64(c, c.omega, c.k, worig);
+        rs_status s = e == cudaSuccess ? out_copy(ctx, omega_out, worig, (size_t)c.n * c.k) : RS_OK;
+        cudaFree(worig);
+        CK(e);
+        if (s) return s;
+    }
     if (omega_max_out) {
         unsigned long long wb = 0;
         CK(cudaMemcpyAsync(&wb, c.scal + rs::kScalOmegaMaxBits, 8, cudaMemcpyDeviceToHost, c.stream));
@@ -573,6 +611,10 @@ extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_triad_counts: call rs_score first");
     int64_t *tmp = (int64_t *)c.scratch;
     if (type1_out) {
+        // Type-I triads are counted by re-running the triangle pass in COUNT mode
+        // (kept off the timed rs_score path)
+        CK(cudaMemsetAsync(c.n1, 0, sizeof(unsigned long long) * (size_t)c.n, c.stream));
+        CK(rs::launch_triangle_counts(c));
         CK(rs::launch_type1_export(c, tmp));
         rs_status s = out_copy(ctx, type1_out, tmp, (size_t)c.n);
         if (s) return s;

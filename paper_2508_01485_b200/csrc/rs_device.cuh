@@ -77,6 +77,19 @@ __device__ __forceinline__ U128 fx_from3(const unsigned long long *acc3) {
     return u128_add(a, b);
 }
 
+// Two-limb variant for the Type-I scatter: limb0 += bits[0,32), limb1 +=
+// bits[32,96). Exact while a head receives < 2^32 terms and its unnormalised
+// Type-I sum stays below 2^32 (limb1 then never wraps): both hold for any
+// graph with d_max < 2^16 since every grouped term is < 2 * 2^11.
+__device__ __forceinline__ void fx_red2(unsigned long long *acc2, U128 q) {
+    atomicAdd(acc2 + 0, q.lo & 0xFFFFFFFFull);
+    atomicAdd(acc2 + 1, (q.lo >> 32) | (q.hi << 32));
+}
+__device__ __forceinline__ U128 fx_from2(const unsigned long long *acc2) {
+    unsigned long long l0 = acc2[0], l1 = acc2[1];
+    return u128_add(U128{l0, 0ull}, U128{l1 << 32, l1 >> 32});
+}
+
 // ---------------------------------------------------------------------------
 // Vertex groups. A group of G lanes (G in {4, 8, 16, 32}) owns one vertex and
 // walks its adjacency G entries per step; 32/G groups share a warp. Lanes of

@@ -35,7 +35,9 @@ const NcclApi *nccl_api(std::string *err);
 constexpr int kMaxK = 254;        // target columns (uint8 label 0xFF = "other")
 constexpr uint8_t kOther = 0xFF;  // community without its own 8-bit code
 constexpr int kNumBins = 8;       // degree classes (load time)
-// degree class c holds vertices with kBinLo[c] <= d < kBinLo[c+1]
+// degree class c holds vertices with bin_lo(c) <= d < bin_lo(c+1); in the
+// internal (degree-descending) numbering class c is the range
+// [bins.offset[c], bins.offset[c] + bins.count[c]), class 7 first
 __host__ __device__ constexpr int64_t bin_lo(int i) {
     return i <= 0 ? 0 : i == 1 ? 8 : i == 2 ? 16 : i == 3 ? 32 : i == 4 ? 64 : i == 5 ? 128 : i == 6 ? 2048
          : i == 7 ? 8192 : INT64_MAX;
@@ -47,7 +49,8 @@ struct __align__(16) VRec {
     int32_t pcnt;      // |P(v)|: inter-community neighbours (G' in-degree)
     uint8_t lab;       // 8-bit community code (< k: target column)
     uint8_t head;      // 1 if v can be an RSI head: target community and d(v) >= 2
-    uint16_t pad;
+    uint8_t wide;      // Type-I sum of this head needs the 3-limb accumulator
+    uint8_t pad;
 };
 
 // Per (vertex, column) record read by the Type-II pull (Phase D).
@@ -82,13 +85,17 @@ struct Ctx {
     int64_t n = 0, nnz = 0;
     int64_t *rowptr = nullptr;   // n+1
     int32_t *col = nullptr;      // nnz
-    int32_t *binv = nullptr;     // n: vertices grouped by degree class, ascending id within class
+    int32_t *perm = nullptr;     // n: original id of internal vertex r (degree-descending order)
+    int32_t *inv = nullptr;      // n: internal id of original vertex v
     Bins bins;
     int64_t d_max = 0;
+    int64_t *e_pre = nullptr;    // Phase E work items: prefix of extra chunks of the e_nbig largest rows
+    int64_t e_nbig = 0, e_extra = 0;
     bool loaded = false;
 
     // communities (set time)
-    int32_t *comm_id = nullptr;  // n
+    int32_t *comm_in = nullptr;  // n: communities as given (original order)
+    int32_t *comm_id = nullptr;  // n: communities in internal order
     uint8_t *lab = nullptr;      // n
     int32_t *chist = nullptr;    // community sizes, cap entries
     uint8_t *ccode = nullptr;    // community id -> 8-bit code
@@ -104,11 +111,12 @@ struct Ctx {
     VRec *vrec = nullptr;        // n
     int32_t *pidx = nullptr;     // nnz, P(u) stored at rowptr[u] ...
     int32_t *pplus = nullptr;    // nnz, P+(u) (orientation) at rowptr[u] ...
-    int32_t *ppcnt = nullptr;    // n
+    int2 *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|}
+    double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQ *bq = nullptr;            // n*k
-    unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum
+    unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)
     unsigned long long *n1 = nullptr;    // n Type-I triad counts
-    double *score = nullptr;     // n
+    double *score = nullptr;     // n, ORIGINAL vertex order
     unsigned long long *scal = nullptr;  // device scalars (see kScal*)
     int64_t k_alloc = 0;         // k the per-score buffers were sized for
     bool scored = false;
@@ -136,16 +144,29 @@ enum {
     kScalCount = 32
 };
 
+// |P(h)|^2 at or above which head h's unnormalised Type-I sum could reach 2^31
+// (grouped terms are < 2 * omega_max <= 2 (k-1) log2(k-1)): such heads use the
+// 3-limb accumulator (fx_red3) instead of fx_red2.
+inline double wide_bound(int k) {
+    const double km1 = (double)(k - 1);
+    const double wb = km1 > 1.0 ? km1 * __builtin_log2(km1) : 1.0;
+    return 2147483648.0 / (2.0 * wb);
+}
+
 // ---- kernels (launchers). Each returns cudaGetLastError() of the launch. ----
-cudaError_t launch_validate(Ctx &c);
-cudaError_t launch_bins(Ctx &c);
+cudaError_t launch_validate(Ctx &c, const int64_t *rp, const int32_t *col);
+cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o);
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets);
 cudaError_t launch_phase_a(Ctx &c);
 cudaError_t launch_phase_c(Ctx &c);
 cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
+cudaError_t launch_triangle_counts(Ctx &c);
+cudaError_t launch_e_items(Ctx &c);
 cudaError_t launch_topk(Ctx &c, int64_t K, int32_t *ids_dev, double *scores_dev, int64_t lo, int64_t hi);
-cudaError_t launch_counts_total(Ctx &c, int32_t *total_dev);
+cudaError_t launch_counts_total(Ctx &c, const int32_t *f_orig, int32_t *total_dev);
+cudaError_t launch_permute_i32(Ctx &c, const int32_t *in, int k, int32_t *out);
+cudaError_t launch_permute_f64(Ctx &c, const double *in, int k, double *out);
 cudaError_t launch_border_list(Ctx &c, int32_t *bv_dev, int64_t *nb_host);
 cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int64_t *nent_host);
 cudaError_t launch_type2_counts(Ctx &c, int64_t *t2_dev);

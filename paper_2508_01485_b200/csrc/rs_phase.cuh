@@ -1,0 +1,41 @@
+// Shared argument block of the P-list phases (C, D, E).
+#pragma once
+#include "rs_internal.cuh"
+#include "rs_device.cuh"
+
+namespace rs {
+
+struct CdeArgs {
+    const int64_t *__restrict__ rowptr;
+    int64_t vlo;                        // first vertex of the range
+    int64_t nverts;
+    int64_t n;
+    int32_t k;
+    const double *__restrict__ amat;    // n*k cube roots a_v(c), row-major
+    const VRec *__restrict__ vrec;
+    const int32_t *__restrict__ pidx;   // P(u) at rowptr[u]
+    int32_t *__restrict__ pplus;        // P+(u) at rowptr[u]
+    int2 *__restrict__ pc2;             // {|P+(u)|, |P(u)|}
+    BQ *__restrict__ bq;                // column-major: bq[c*n + w]
+    unsigned long long *__restrict__ acc1;  // 3 limbs per vertex (Type-I)
+    unsigned long long *__restrict__ n1;    // Type-I triad counts (COUNT mode)
+    double *__restrict__ score;         // original vertex order
+    const int32_t *__restrict__ perm;   // internal -> original id
+    const uint8_t *__restrict__ lab;    // 8-bit community codes
+    unsigned long long *scal;
+    int64_t head_lo, head_hi;           // owned head range (multi-GPU); [0, n) on one GPU
+    bool any_wide;                      // some head may need the 3-limb Type-I accumulator
+};
+
+inline CdeArgs cde_args(Ctx &c) {
+    CdeArgs a;
+    a.rowptr = c.rowptr; a.vlo = 0; a.nverts = 0; a.n = c.n; a.k = c.k;
+    a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pplus = c.pplus; a.pc2 = c.pc2;
+    a.bq = c.bq; a.acc1 = c.acc1; a.n1 = c.n1; a.score = c.score; a.scal = c.scal;
+    a.perm = c.perm; a.lab = c.lab;
+    a.any_wide = (double)c.d_max * (double)c.d_max >= wide_bound(c.k);
+    a.head_lo = c.head_lo; a.head_hi = c.head_hi;
+    return a;
+}
+
+}  // namespace rs
