@@ -35,6 +35,9 @@ sys.path.insert(0, REPO)
 import gen  # noqa: E402
 
 METRIC = "RSI-scored edges/sec (GTEPS)"
+# DRAM bytes per launch of the dominant phase from the committed ncu captures
+# (profiles/); filled per round, None when not captured for that config
+TRAFFIC_NCU = {}
 UNIT = "GTEPS"
 
 
@@ -62,28 +65,36 @@ def load_graph(name, alloc=None):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    5 ms during the timed region (nvidia-smi is too slow for a 100 ms region)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index=0):
+    def __init__(self, index=0, period_s=0.005):
         self.index = index
+        self.period = period_s
         self.rows = []
+        self.maxclk = None
         self._stop = threading.Event()
         self._t = None
+        self.err = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.maxclk = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap,
+                    "hw_power_brake": N.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+            while not self._stop.is_set():
+                clk = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((clk, [k for k, v in bits.items() if rs & v]))
+                self._stop.wait(self.period)
+        except Exception as e:  # NVML unavailable: report it
+            self.err = repr(e)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -96,22 +107,22 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.maxclk, "reasons": [self.err or "no samples"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[1]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.maxclk, "reasons": reasons,
+                "samples": len(self.rows), "source": "NVML, 5 ms period, timed region only"}
 
 
 # ------------------------------------------------------------------ algorithmic bytes
 def phase_bytes(n, D, Db, k, ntri, nb):
-    """Bytes each phase must move at least once."""
-    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 12 * k * n + 16 * n
-    C = 8 * n + 16 * n + 4 * Db + 16 * Db + 8 * k * n + 16 * k * nb + 2 * Db + 4 * n
+    """Algorithmic DRAM bytes of each phase: what it must read or write at least
+    once (per-unit figures x units)."""
+    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 20 * k * n + 16 * n
+    C = 8 * n + 16 * n + 4 * Db + 16 * Db + 8 * k * n + 16 * k * nb + 2 * Db + 8 * n
+    E = 4 * Db + 2 * Db + 17 * n + 8 * k * n + 32 * ntri
     D_ = 8 * n + 16 * n + 4 * Db + 16 * Db + 24 * n + 8 * n
-    return {"A": A, "C": C, "D": D_}
+    return {"A": A, "C": C, "E": E, "D": D_}
 
 
 def main():
@@ -219,16 +230,22 @@ def main():
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    # dominant HBM-bound phase (A, C or D; E is reported separately)
-    cand = {"A_border_hist_weights": (ph[0], pb["A"]), "C_btable_orient": (ph[1], pb["C"]),
-            "D_type2_finalize": (ph[3], pb["D"])}
-    dom = max(cand, key=lambda x: cand[x][0])
-    dms, dbytes = cand[dom]
-    achieved = dbytes / (dms * 1e-3) / 1e9 if dms > 0 else 0.0
-    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(achieved / hbm_peak, 4), "traffic": None,
-            "phase_ms": {nm: round(float(x), 4) for nm, x in zip(names, ph)},
-            "phase_bytes": pb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"}
+    # every phase against the HBM roof (phase time = CUDA events on the library
+    # stream around the phase's launches); the dominant one is the headline
+    keys = {"A_border_hist_weights": "A", "C_btable_orient": "C", "E_type1_triangles": "E", "D_type2_finalize": "D"}
+    phases = {}
+    for nm, ms in zip(names, ph):
+        by = pb[keys[nm]]
+        gbs = by / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        phases[nm] = {"ms": round(float(ms), 4), "alg_bytes": int(by), "GBps": round(gbs, 1),
+                      "frac": round(gbs / hbm_peak, 4)}
+    dom = max(phases, key=lambda x: phases[x]["ms"])
+    traffic = TRAFFIC_NCU.get(a.config, {}).get(dom)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["GBps"], "peak": hbm_peak, "unit": "GB/s",
+            "frac": phases[dom]["frac"], "traffic": traffic,
+            "traffic_source": "profiles/ ncu --set full dram__bytes_read.sum+dram__bytes_write.sum per launch"
+            if traffic else None,
+            "phases": phases, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"}
 
     e2e = None
     if not a.no_e2e:

@@ -10,14 +10,13 @@
 // Labels are the 8-bit community codes of rs_set_communities; only vertices of
 // two uncoded ("other") communities fall back to comparing full int32 ids.
 // Degree-binned: a group of G lanes (or a whole CTA for hubs) owns a vertex;
-// each lane keeps kUnroll independent loads in flight (the row walk is
+// each lane keeps U independent loads in flight (the row walk is
 // latency-bound otherwise).
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
 
 namespace rs {
 
-constexpr int kUnroll = 4;
 
 struct PhaseAArgs {
     const int64_t *__restrict__ rowptr;
@@ -66,33 +65,38 @@ __device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, doubl
 }
 
 // k <= 8: per-lane register histogram.
-template <class GR>
+template <int U, class GR>
 __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
     const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
     const uint8_t lu = a.lab[u];
     const int32_t cfull = (lu == kOther) ? a.comm[u] : 0;
     const int k = a.k;
-    int cnt[8];
-#pragma unroll
-    for (int c = 0; c < 8; c++) cnt[c] = 0;
+    // per-lane histogram as 16-bit counters packed in two words (columns 0-3,
+    // 4-7): one shift and one add per neighbour. A lane sees at most
+    // ceil(d / G) neighbours < 2^16 (launch_phase_a_impl falls back to the
+    // shared-memory histogram when d_max >= 2^22).
+    unsigned long long h0 = 0ull, h1 = 0ull;
     int pc = 0;
-    for (int64_t base = beg; base < end; base += GR::size * kUnroll) {
-        int32_t x[kUnroll];
-        uint8_t lx[kUnroll];
+    for (int64_t base = beg; base < end; base += GR::size * U) {
+        int32_t x[U];
+        uint8_t lx[U];
 #pragma unroll
-        for (int j = 0; j < kUnroll; j++) {
+        for (int j = 0; j < U; j++) {
             const int64_t e = base + j * GR::size + g.lane;
             x[j] = e < end ? __ldcs(a.col + e) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < kUnroll; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
+        for (int j = 0; j < U; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
 #pragma unroll
-        for (int j = 0; j < kUnroll; j++) {
+        for (int j = 0; j < U; j++) {
             const bool valid = x[j] >= 0;
             bool foreign = valid && (lx[j] != lu);
             if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
-#pragma unroll
-            for (int c = 0; c < 8; c++) cnt[c] += (c < k && lx[j] == c) ? 1 : 0;
+            const unsigned l = lx[j];
+            if (l < (unsigned)k) {
+                const unsigned long long inc = 1ull << ((l & 3u) * 16u);
+                if (l < 4u) h0 += inc; else h1 += inc;
+            }
             if (base + j * GR::size < end) {          // group-uniform
                 int tot;
                 const int r = g.rank(foreign, &tot);
@@ -101,8 +105,22 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
             }
         }
     }
+    int cnt[8];
+    if (end - beg < 65536) {          // group totals still fit the 16-bit fields
+        h0 = g.sum(h0);
+        h1 = g.sum(h1);
 #pragma unroll
-    for (int c = 0; c < 8; c++) cnt[c] = g.sum(cnt[c]);
+        for (int c = 0; c < 4; c++) {
+            cnt[c] = (int)((h0 >> (16 * c)) & 0xFFFFull);
+            cnt[c + 4] = (int)((h1 >> (16 * c)) & 0xFFFFull);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            cnt[c] = g.sum((int)((h0 >> (16 * c)) & 0xFFFFull));
+            cnt[c + 4] = g.sum((int)((h1 >> (16 * c)) & 0xFFFFull));
+        }
+    }
     int T = 0, L_all = 0;
     double X = 0.0;
 #pragma unroll
@@ -131,7 +149,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
 }
 
 // k > 8: histogram in shared memory (one warp or one CTA per vertex)
-template <class GR>
+template <int U, class GR>
 __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64_t u, GR &g, int *hist) {
     const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
     const uint8_t lu = a.lab[u];
@@ -140,18 +158,18 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     for (int c = g.lane; c < k; c += GR::size) hist[c] = 0;
     g.sync();
     int pc = 0;
-    for (int64_t base = beg; base < end; base += GR::size * kUnroll) {
-        int32_t x[kUnroll];
-        uint8_t lx[kUnroll];
+    for (int64_t base = beg; base < end; base += GR::size * U) {
+        int32_t x[U];
+        uint8_t lx[U];
 #pragma unroll
-        for (int j = 0; j < kUnroll; j++) {
+        for (int j = 0; j < U; j++) {
             const int64_t e = base + j * GR::size + g.lane;
             x[j] = e < end ? __ldcs(a.col + e) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < kUnroll; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
+        for (int j = 0; j < U; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
 #pragma unroll
-        for (int j = 0; j < kUnroll; j++) {
+        for (int j = 0; j < U; j++) {
             const bool valid = x[j] >= 0;
             bool foreign = valid && (lx[j] != lu);
             if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
@@ -205,7 +223,7 @@ __device__ __forceinline__ void block_max_to_scal(double v, unsigned long long *
     }
 }
 
-template <int G, bool SMEM>
+template <int G, int U, bool SMEM>
 __global__ void __launch_bounds__(256) k_phase_a_warp(PhaseAArgs a) {
     __shared__ int hist[SMEM ? 8 * 256 : 1];
     WarpGroup<G> g;
@@ -216,8 +234,8 @@ __global__ void __launch_bounds__(256) k_phase_a_warp(PhaseAArgs a) {
     for (int64_t i = gid; i < a.nverts; i += ngroups) {
         const int64_t u = (a.vlo + i);
         double w;
-        if constexpr (SMEM) w = phase_a_vertex_smem(a, u, g, hist + (threadIdx.x / 32) * 256);
-        else w = phase_a_vertex(a, u, g);
+        if constexpr (SMEM) w = phase_a_vertex_smem<U>(a, u, g, hist + (threadIdx.x / 32) * 256);
+        else w = phase_a_vertex<U>(a, u, g);
         wmax = w > wmax ? w : wmax;
     }
     block_max_to_scal(wmax, a.scal);
@@ -233,26 +251,27 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_a_cta(PhaseAArgs a) {
     for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) {
         const int64_t u = (a.vlo + i);
         double w;
-        if constexpr (SMEM) w = phase_a_vertex_smem(a, u, g, hist);
-        else w = phase_a_vertex(a, u, g);
+        if constexpr (SMEM) w = phase_a_vertex_smem<4>(a, u, g, hist);
+        else w = phase_a_vertex<4>(a, u, g);
         wmax = w > wmax ? w : wmax;
     }
     block_max_to_scal(wmax, a.scal);
 }
 
-template <int G, bool SMEM>
+template <int G, int U, bool SMEM>
 static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
     const int64_t gpb = 256 / G;
     int64_t blocks = (a.nverts + gpb - 1) / gpb;
     blocks = std::min<int64_t>(blocks, 148 * 16);
     if (blocks < 1) return;
-    k_phase_a_warp<G, SMEM><<<(unsigned)blocks, 256, 0, s>>>(a);
+    k_phase_a_warp<G, U, SMEM><<<(unsigned)blocks, 256, 0, s>>>(a);
     c.launches++;
 }
 
 template <bool SMEM>
 static void launch_bins_a(Ctx &c, PhaseAArgs base) {
-    // class -> group: [0,8):4 [8,16):8 [16,32):16 [32,2048):32 [2048,inf):CTA
+    // class -> (lanes per vertex, loads in flight per lane), G*U about the row length:
+    // [0,8):4x2 [8,16):4x4 [16,32):8x4 [32,64):16x4 [64,2048):32x4 [2048,inf):CTAx4
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         PhaseAArgs a = base;
         a.vlo = c.bins.offset[cls];
@@ -263,14 +282,16 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
             int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
             k_phase_a_cta<SMEM><<<(unsigned)blocks, kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (SMEM || cls >= 3) {
-            launch_warp_bin<32, SMEM>(c, a, s);
+        } else if (SMEM || cls >= 4) {
+            launch_warp_bin<32, 4, SMEM>(c, a, s);
+        } else if (cls == 3) {
+            launch_warp_bin<16, 4, SMEM>(c, a, s);
         } else if (cls == 2) {
-            launch_warp_bin<16, SMEM>(c, a, s);
+            launch_warp_bin<8, 4, SMEM>(c, a, s);
         } else if (cls == 1) {
-            launch_warp_bin<8, SMEM>(c, a, s);
+            launch_warp_bin<4, 4, SMEM>(c, a, s);
         } else {
-            launch_warp_bin<4, SMEM>(c, a, s);
+            launch_warp_bin<4, 2, SMEM>(c, a, s);
         }
     }
 }
@@ -283,7 +304,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
     // 3-limb accumulator when |P|^2 * that bound could reach 2^31 (fx_red2 contract)
     a.wide_bound = wide_bound(c.k);
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
-    if (c.k <= 8) launch_bins_a<false>(c, a);
+    if (c.k <= 8 && c.d_max < (1ll << 22)) launch_bins_a<false>(c, a);
     else launch_bins_a<true>(c, a);
     return cudaGetLastError();
 }

@@ -16,13 +16,12 @@
 
 namespace rs {
 
-constexpr int kUnrollP = 4;
 
 // ============================================================================
 // Phase C: B_w[c] for every column, Q_w[c] = a_w(c)^2, and the degree
 // orientation of G' (P+(w): neighbours of larger (|P|, id)) for Phase E.
 // ============================================================================
-template <class GR>
+template <int U, class GR>
 __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &g) {
     const VRec rw = a.vrec[w];
     const int pc = rw.pcnt;
@@ -32,21 +31,21 @@ __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &
 #pragma unroll
     for (int c = 0; c < 8; c++) B[c] = u128_zero();
     int ppc = 0;
-    for (int base = 0; base < pc; base += GR::size * kUnrollP) {
-        int32_t v[kUnrollP];
-        VRec rv[kUnrollP];
+    for (int base = 0; base < pc; base += GR::size * U) {
+        int32_t v[U];
+        VRec rv[U];
 #pragma unroll
-        for (int j = 0; j < kUnrollP; j++) {
+        for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
             v[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < kUnrollP; j++) {
+        for (int j = 0; j < U; j++) {
             if (v[j] >= 0) rv[j] = a.vrec[v[j]];
             else { rv[j].lab = kOther; rv[j].pcnt = 0; rv[j].a_self = 0.0; }
         }
 #pragma unroll
-        for (int j = 0; j < kUnrollP; j++) {
+        for (int j = 0; j < U; j++) {
             const U128 q = fx_quantize(rv[j].a_self);
 #pragma unroll
             for (int c = 0; c < 8; c++)
@@ -114,14 +113,14 @@ __device__ __forceinline__ void phase_c_vertex_smem(const CdeArgs &a, int64_t w,
     g.sync();
 }
 
-template <int G, bool SMEM>
+template <int G, int U, bool SMEM>
 __global__ void __launch_bounds__(256) k_phase_c_warp(CdeArgs a) {
     __shared__ unsigned long long sB[SMEM ? 8 * 3 * kMaxK : 1];
     WarpGroup<G> g;
     const int64_t gpb = blockDim.x / G;
     for (int64_t i = blockIdx.x * gpb + threadIdx.x / G; i < a.nverts; i += (int64_t)gridDim.x * gpb) {
         if constexpr (SMEM) phase_c_vertex_smem(a, a.vlo + i, g, sB + (threadIdx.x / 32) * 3 * kMaxK);
-        else phase_c_vertex(a, a.vlo + i, g);
+        else phase_c_vertex<U>(a, a.vlo + i, g);
     }
 }
 
@@ -133,14 +132,14 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_c_cta(CdeArgs a) {
     CtaGroup g(s_i, s_u);
     for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) {
         if constexpr (SMEM) phase_c_vertex_smem(a, a.vlo + i, g, sB);
-        else phase_c_vertex(a, a.vlo + i, g);
+        else phase_c_vertex<4>(a, a.vlo + i, g);
     }
 }
 
 // ============================================================================
 // Phase D: Type-II pull for every head + Type-I limbs + finalize.
 // ============================================================================
-template <class GR>
+template <int U, class GR>
 __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &g, double wmax) {
     const VRec ru = a.vrec[u];
     if (!ru.head || u < a.head_lo || u >= a.head_hi) {
@@ -153,19 +152,19 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const int64_t beg = a.rowptr[u];
     const int64_t d = a.rowptr[u + 1] - beg;
     U128 S = u128_zero();
-    for (int base = 0; base < pc; base += GR::size * kUnrollP) {
-        int32_t w[kUnrollP];
-        BQ r[kUnrollP];
+    for (int base = 0; base < pc; base += GR::size * U) {
+        int32_t w[U];
+        BQ r[U];
 #pragma unroll
-        for (int j = 0; j < kUnrollP; j++) {
+        for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
             w[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < kUnrollP; j++)
+        for (int j = 0; j < U; j++)
             if (w[j] >= 0) r[j] = a.bq[(int64_t)cu * a.n + w[j]];
 #pragma unroll
-        for (int j = 0; j < kUnrollP; j++) {
+        for (int j = 0; j < U; j++) {
             if (w[j] >= 0) {
                 // B_w[c_u] includes a_u exactly, so the difference is >= 0 and exactly 0
                 // when u is w's only neighbour in C(u) (Type-II needs v != u)
@@ -184,13 +183,13 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     }
 }
 
-template <int G>
+template <int G, int U>
 __global__ void __launch_bounds__(256) k_phase_d_warp(CdeArgs a) {
     WarpGroup<G> g;
     const double wmax = __longlong_as_double((long long)a.scal[kScalOmegaMaxBits]);
     const int64_t gpb = blockDim.x / G;
     for (int64_t i = blockIdx.x * gpb + threadIdx.x / G; i < a.nverts; i += (int64_t)gridDim.x * gpb)
-        phase_d_vertex(a, a.vlo + i, g, wmax);
+        phase_d_vertex<U>(a, a.vlo + i, g, wmax);
 }
 
 __global__ void __launch_bounds__(kCtaThreads) k_phase_d_cta(CdeArgs a) {
@@ -198,7 +197,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_d_cta(CdeArgs a) {
     __shared__ unsigned long long s_u[2 * kCtaWarps];
     CtaGroup g(s_i, s_u);
     const double wmax = __longlong_as_double((long long)a.scal[kScalOmegaMaxBits]);
-    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) phase_d_vertex(a, a.vlo + i, g, wmax);
+    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) phase_d_vertex<4>(a, a.vlo + i, g, wmax);
 }
 
 // ============================================================================
@@ -214,7 +213,8 @@ static void launch_grid(Ctx &c, K kern, int64_t groups, int gpb, cudaStream_t s,
 }
 
 // P-list phases: |P| is about a quarter of d, so a class uses a smaller group
-// than in Phase A: [0,16):4 [16,64):8 [64,128):16 [128,2048):32 [2048,inf):CTA
+// than in Phase A (lanes x loads per lane): [0,32):4x2 [32,64):4x4 [64,128):8x4
+// [128,2048):32x4 [2048,inf):CTAx4
 template <bool SMEM>
 static void launch_c_bins(Ctx &c) {
     CdeArgs base = cde_args(c);
@@ -227,10 +227,10 @@ static void launch_c_bins(Ctx &c) {
         if (cls >= 6) {
             k_phase_c_cta<SMEM><<<(unsigned)std::min<int64_t>(a.nverts, 148 * 8), kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (SMEM || cls == 5) launch_grid(c, k_phase_c_warp<32, SMEM>, a.nverts, 8, s, a);
-        else if (cls == 4) launch_grid(c, k_phase_c_warp<16, SMEM>, a.nverts, 16, s, a);
-        else if (cls >= 2) launch_grid(c, k_phase_c_warp<8, SMEM>, a.nverts, 32, s, a);
-        else launch_grid(c, k_phase_c_warp<4, SMEM>, a.nverts, 64, s, a);
+        } else if (SMEM || cls == 5) launch_grid(c, k_phase_c_warp<32, 4, SMEM>, a.nverts, 8, s, a);
+        else if (cls == 4) launch_grid(c, k_phase_c_warp<8, 4, SMEM>, a.nverts, 32, s, a);
+        else if (cls == 3) launch_grid(c, k_phase_c_warp<4, 4, SMEM>, a.nverts, 64, s, a);
+        else launch_grid(c, k_phase_c_warp<4, 2, SMEM>, a.nverts, 64, s, a);
     }
 }
 
@@ -251,10 +251,10 @@ cudaError_t launch_phase_d(Ctx &c) {
         if (cls >= 6) {
             k_phase_d_cta<<<(unsigned)std::min<int64_t>(a.nverts, 148 * 8), kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (cls == 5) launch_grid(c, k_phase_d_warp<32>, a.nverts, 8, s, a);
-        else if (cls == 4) launch_grid(c, k_phase_d_warp<16>, a.nverts, 16, s, a);
-        else if (cls >= 2) launch_grid(c, k_phase_d_warp<8>, a.nverts, 32, s, a);
-        else launch_grid(c, k_phase_d_warp<4>, a.nverts, 64, s, a);
+        } else if (cls == 5) launch_grid(c, k_phase_d_warp<32, 4>, a.nverts, 8, s, a);
+        else if (cls == 4) launch_grid(c, k_phase_d_warp<8, 4>, a.nverts, 32, s, a);
+        else if (cls == 3) launch_grid(c, k_phase_d_warp<4, 4>, a.nverts, 64, s, a);
+        else launch_grid(c, k_phase_d_warp<4, 2>, a.nverts, 64, s, a);
     }
     return cudaGetLastError();
 }

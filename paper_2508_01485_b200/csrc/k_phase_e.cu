@@ -33,7 +33,7 @@ namespace rs {
 constexpr int kChunkE = 128;     // positions of P(y) per work item
 constexpr int kTabE = 1024;      // hash slots per warp (P+(y) up to kTabE/4 hashed, load <= 1/4)
 constexpr int kBmWords = 128;    // 4096-bit membership filter of P+(y) per warp
-constexpr int kQCapE = 160;      // hit queue per warp (31 + 4*32 < 160)
+constexpr int kQCapE = 160;      // candidate queue per warp (31 + 4*32 < 160)
 constexpr int kUnrollE = 4;
 constexpr int kWarpsE = 8;
 
@@ -45,6 +45,16 @@ __device__ __forceinline__ uint32_t bm_bit(int32_t z) {
 // Fibonacci hashing: the top log2(size) bits of z * 2^32/phi
 __device__ __forceinline__ uint32_t hslot(int32_t z, uint32_t shift) {
     return ((uint32_t)z * 2654435769u) >> shift;
+}
+
+// z in the sorted list p[0, len)
+__device__ __forceinline__ bool in_sorted(const int32_t *p, int len, int32_t z) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(p + mid) < z) lo = mid + 1; else hi = mid;
+    }
+    return lo < len && __ldg(p + lo) == z;
 }
 
 __device__ __forceinline__ double amat_at(const CdeArgs &a, int32_t v, int c) {
@@ -90,8 +100,8 @@ __device__ __forceinline__ U128 tri_terms(const CdeArgs &a, int32_t x, int32_t y
 }
 
 struct EItems {
-    const int64_t *epre;   // exclusive prefix of extra chunks over vertices [0, nbig)
-    int64_t nbig, n_extra, total;
+    const int2 *items;     // {y, chunk} work items of the heavy middle vertices, heaviest first
+    const int32_t *total;  // number of items (device scalar, written by the item scan)
 };
 
 __host__ __device__ constexpr int e_stride_bytes(int k) {
@@ -110,26 +120,16 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
     longlong2 *XL = (longlong2 *)(base + kTabE * 4 + kBmWords * 4 + kQCapE * 8);   // {P+(x) base - offset, (x << 32) | end}
     double *Ay = (double *)(base + kTabE * 4 + kBmWords * 4 + kQCapE * 8 + kChunkE * 16);
     unsigned long long ntri = 0;
+    const unsigned long long n_items = (unsigned long long)*it.total;
 
     for (;;) {
         unsigned long long q = 0;
         if (lane == 0) q = atomicAdd(queue_ctr, 1ull);
         q = __shfl_sync(0xffffffffu, q, 0);
-        if ((int64_t)q >= it.total) break;
-        int32_t y;
-        int chunk;
-        if ((int64_t)q < it.n_extra) {           // extra chunks of high-degree vertices first
-            int64_t lo = 0, hi = it.nbig;        // last y with epre[y] <= q
-            while (hi - lo > 1) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (it.epre[mid] <= (int64_t)q) lo = mid; else hi = mid;
-            }
-            y = (int32_t)lo;
-            chunk = 1 + (int)((int64_t)q - it.epre[lo]);
-        } else {
-            y = (int32_t)((int64_t)q - it.n_extra);
-            chunk = 0;
-        }
+        if (q >= n_items) break;
+        const int2 itm = it.items[q];
+        const int32_t y = itm.x;
+        const int chunk = itm.y;
         const int2 pcy = a.pc2[y];
         const int py = pcy.x, pc = pcy.y;
         const int start = chunk * kChunkE;
@@ -164,13 +164,30 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
         U128 accy = u128_zero();
         unsigned long long cnty = 0;
         int qn = 0;
+        // queued candidates (x, z) passed the bitmap filter; verify z in P+(y)
+        // exactly, then evaluate the triangle -- 32 at a time, all lanes busy
         auto drain = [&](int upto) {
             while (qn >= upto && qn > 0) {
                 const int take = qn < 32 ? qn : 32;
                 const int b = qn - take;
                 if (lane < take) {
                     const int2 e = Q[b + lane];
-                    accy = u128_add(accy, tri_terms<COUNT>(a, e.x, y, ly, Ay, e.y, cnty));
+                    bool hit;
+                    if (hashed) {
+                        uint32_t h = hslot(e.y, shift);
+                        for (;;) {
+                            const int32_t sv = T[h];
+                            if (sv == e.y) { hit = true; break; }
+                            if (sv == -1) { hit = false; break; }
+                            h = (h + 1) & mask;
+                        }
+                    } else {
+                        hit = in_sorted(a.pplus + by, py, e.y);
+                    }
+                    if (hit) {
+                        ntri++;
+                        accy = u128_add(accy, tri_terms<COUNT>(a, e.x, y, ly, Ay, e.y, cnty));
+                    }
                 }
                 __syncwarp();
                 qn = b;
@@ -214,68 +231,62 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
         // every lane walks one contiguous segment of the probe sequence
         const int seg = (total + 31) >> 5;
         const int t_beg = min(total, lane * seg), t_end = min(total, t_beg + seg);
-        int xi = 0;
-        {
+        // the lane's current list: P+(xcur) covers probe positions [.., xe), at base + t
+        int xi = 0, xe = 0;
+        int64_t xbase = 0;
+        int32_t xcur = 0;
+        if (t_beg < t_end) {
             int lo = 0, hi = nx;            // first list whose end > t_beg
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
                 if ((int)(XL[mid].y & 0xffffffff) <= t_beg) lo = mid + 1; else hi = mid;
             }
             xi = lo;
+            const longlong2 e = XL[xi];
+            xbase = e.x;
+            xe = (int)(e.y & 0xffffffff);
+            xcur = (int32_t)(e.y >> 32);
         }
+        int t = t_beg;
         for (int s0 = 0; s0 < seg; s0 += kUnrollE) {
             {
                 int32_t z[kUnrollE], xj[kUnrollE];
 #pragma unroll
                 for (int u = 0; u < kUnrollE; u++) {
-                    const int t = t_beg + s0 + u;
                     z[u] = -1;
-                    xj[u] = 0;
+                    xj[u] = xcur;
                     if (t < t_end) {
-                        while ((int)(XL[xi].y & 0xffffffff) <= t) xi++;
-                        const longlong2 e = XL[xi];
-                        xj[u] = (int32_t)(e.y >> 32);
-                        z[u] = __ldg(a.pplus + e.x + t);
-                    }
-                }
-                bool hit[kUnrollE];
-#pragma unroll
-                for (int u = 0; u < kUnrollE; u++) {
-                    hit[u] = false;
-                    bool maybe = false;
-                    if (z[u] >= 0) {
-                        const uint32_t b = bm_bit(z[u]);
-                        maybe = (BM[b >> 5] >> (b & 31)) & 1u;
-                    }
-                    if (maybe) {
-                        if (hashed) {
-                            uint32_t h = hslot(z[u], shift);
-                            for (;;) {
-                                const int32_t s = T[h];
-                                if (s == z[u]) { hit[u] = true; break; }
-                                if (s == -1) break;
-                                h = (h + 1) & mask;
-                            }
-                        } else {
-                            int64_t lo = by, hi = by + py;
-                            while (lo < hi) {
-                                const int64_t mid = (lo + hi) >> 1;
-                                if (__ldg(a.pplus + mid) < z[u]) lo = mid + 1; else hi = mid;
-                            }
-                            hit[u] = lo < by + py && __ldg(a.pplus + lo) == z[u];
+                        if (t >= xe) {           // lists are non-empty: one step crosses at most one end
+                            const longlong2 e = XL[++xi];
+                            xbase = e.x;
+                            xe = (int)(e.y & 0xffffffff);
+                            xcur = (int32_t)(e.y >> 32);
+                            xj[u] = xcur;
                         }
+                        z[u] = __ldg(a.pplus + xbase + t);
                     }
+                    t++;
                 }
+                // bitmap filter; the lanes' candidates are packed with one warp scan
+                int npos = 0;
+                bool pos[kUnrollE];
 #pragma unroll
                 for (int u = 0; u < kUnrollE; u++) {
-                    const unsigned hb = __ballot_sync(0xffffffffu, hit[u]);
-                    if (hb) {
-                        const int r = __popc(hb & ((1u << lane) - 1u));
-                        if (hit[u]) Q[qn + r] = make_int2(xj[u], z[u]);
-                        qn += __popc(hb);
-                        if (lane == 0) ntri += __popc(hb);
-                    }
+                    const uint32_t b = bm_bit(z[u]);
+                    pos[u] = z[u] >= 0 && ((BM[b >> 5] >> (b & 31)) & 1u);
+                    npos += pos[u];
                 }
+                int incl = npos;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                int w = qn + incl - npos;
+#pragma unroll
+                for (int u = 0; u < kUnrollE; u++)
+                    if (pos[u]) Q[w++] = make_int2(xj[u], z[u]);
+                qn += __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
                 drain(32);
             }
@@ -295,48 +306,65 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
         }
         __syncwarp();
     }
+    for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
     if (lane == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
 }
 
-// ---------------------------------------------------------------- work items (load time)
-__global__ void k_e_nbig(const int64_t *__restrict__ rowptr, int64_t n, unsigned long long *out) {
-    if (threadIdx.x || blockIdx.x) return;
-    int64_t lo = 0, hi = n;    // first r with d(r) <= kChunkE (degrees descending)
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (rowptr[mid + 1] - rowptr[mid] > kChunkE) lo = mid + 1; else hi = mid;
+// ---------------------------------------------------------------- work items (per step)
+// Heavy middle vertices (degree >= 128) are cut into chunks of kChunkE
+// positions of P(y); the chunk counts depend on the communities, so the item
+// list is rebuilt every step (count, scan, scatter), heaviest vertices first.
+__global__ void k_e_count(const int2 *__restrict__ pc2, int64_t n_heavy, int32_t *cnt) {
+    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
+        int c = 0;
+        if (y < n_heavy) {
+            const int2 p = pc2[y];
+            if (p.x > 0 && p.y > p.x) c = (p.y + kChunkE - 1) / kChunkE;
+        }
+        cnt[y] = c;
     }
-    *out = (unsigned long long)lo;
 }
-__global__ void k_e_extra(const int64_t *__restrict__ rowptr, int64_t nbig, int64_t *e) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nbig; r += (int64_t)gridDim.x * blockDim.x)
-        e[r] = r < nbig ? (rowptr[r + 1] - rowptr[r] + kChunkE - 1) / kChunkE - 1 : 0;
+__global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off, int64_t n_heavy,
+                            int2 *items) {
+    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
+        const int c = cnt[y], o = off[y];
+        for (int j = 0; j < c; j++) items[o + j] = make_int2((int)y, j);
+    }
 }
 
+// load time: buffers sized for any community assignment
 cudaError_t launch_e_items(Ctx &c) {
     cudaError_t e;
-    k_e_nbig<<<1, 32, 0, c.stream>>>(c.rowptr, c.n, c.scal + kScalTk);
-    unsigned long long nb = 0;
-    cudaMemcpyAsync(&nb, c.scal + kScalTk, sizeof(nb), cudaMemcpyDeviceToHost, c.stream);
-    if ((e = cudaStreamSynchronize(c.stream))) return e;
-    c.e_nbig = (int64_t)nb;
+    const int64_t nh = c.bins.offset[4];          // degree classes 5-7
+    c.e_nbig = nh;
+    c.e_extra = nh + c.nnz / kChunkE + 1;         // item capacity
+    // layout: cnt[nh+1] | off[nh+1] | items[cap] (int2); grow-only
+    const size_t bytes = sizeof(int32_t) * 2 * (size_t)(nh + 1) + sizeof(int2) * (size_t)c.e_extra + 16;
+    if (bytes <= c.e_bytes) return cudaSuccess;
     if (c.e_pre) cudaFree(c.e_pre);
     c.e_pre = nullptr;
-    if ((e = cudaMalloc(&c.e_pre, sizeof(int64_t) * (c.e_nbig + 1)))) return e;
-    int64_t *tmp = (int64_t *)c.scratch;
-    k_e_extra<<<148, 256, 0, c.stream>>>(c.rowptr, c.e_nbig, tmp);
+    c.e_bytes = 0;
+    if ((e = cudaMalloc(&c.e_pre, bytes))) return e;
+    c.e_bytes = bytes;
+    return cudaSuccess;
+}
+
+static cudaError_t build_e_items(Ctx &c, EItems &it) {
+    const int64_t nh = c.e_nbig;
+    int32_t *cnt = (int32_t *)c.e_pre;
+    int32_t *off = cnt + (nh + 1);
+    int2 *items = (int2 *)(((uintptr_t)(off + (nh + 1)) + 15) & ~(uintptr_t)15);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nh + 256) / 256, 148 * 4));
+    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, cnt);
     size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, tmp, c.e_pre, (int)(c.e_nbig + 1), c.stream);
-    void *t2 = nullptr;
-    if ((e = cudaMalloc(&t2, std::max<size_t>(need, 1)))) return e;
-    cub::DeviceScan::ExclusiveSum(t2, need, tmp, c.e_pre, (int)(c.e_nbig + 1), c.stream);
-    int64_t tot = 0;
-    cudaMemcpyAsync(&tot, c.e_pre + c.e_nbig, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
-    e = cudaStreamSynchronize(c.stream);
-    cudaFree(t2);
-    c.e_extra = tot;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
+    if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
+    cub::DeviceScan::ExclusiveSum(c.scratch, need, cnt, off, (int)(nh + 1), c.stream);
+    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, nh, items);
     c.launches += 3;
-    return e;
+    it.items = items;
+    it.total = off + nh;
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- light middle vertices
@@ -347,14 +375,6 @@ constexpr int kGL = 8;                         // lanes per light vertex
 constexpr int kXLL = 32;                       // P(y) positions per x-list pass
 constexpr int kQL = kGL * kUnrollE + kGL;      // hit queue per group
 
-__device__ __forceinline__ bool in_sorted(const int32_t *p, int len, int32_t z) {
-    int lo = 0, hi = len;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(p + mid) < z) lo = mid + 1; else hi = mid;
-    }
-    return lo < len && __ldg(p + lo) == z;
-}
 
 template <bool COUNT>
 __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
@@ -434,20 +454,33 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                     const int mid = (lo + hi) >> 1;
                     if ((int)(XL[mid].y & 0xffffffff) <= t_beg) lo = mid + 1; else hi = mid;
                 }
-                int xi = lo;
+                int xi = lo, xe = 0;
+                int64_t xbase = 0;
+                int32_t xcur = 0;
+                if (t_beg < t_end) {
+                    const longlong2 e = XL[xi];
+                    xbase = e.x;
+                    xe = (int)(e.y & 0xffffffff);
+                    xcur = (int32_t)(e.y >> 32);
+                }
+                int t = t_beg;
                 for (int s0 = 0; s0 < seg; s0 += kUnrollE) {
                     int32_t z[kUnrollE], xj[kUnrollE];
 #pragma unroll
                     for (int u = 0; u < kUnrollE; u++) {
-                        const int t = t_beg + s0 + u;
                         z[u] = -1;
-                        xj[u] = 0;
+                        xj[u] = xcur;
                         if (t < t_end) {
-                            while ((int)(XL[xi].y & 0xffffffff) <= t) xi++;
-                            const longlong2 e = XL[xi];
-                            xj[u] = (int32_t)(e.y >> 32);
-                            z[u] = __ldg(a.pplus + e.x + t);
+                            if (t >= xe) {
+                                const longlong2 e = XL[++xi];
+                                xbase = e.x;
+                                xe = (int)(e.y & 0xffffffff);
+                                xcur = (int32_t)(e.y >> 32);
+                                xj[u] = xcur;
+                            }
+                            z[u] = __ldg(a.pplus + xbase + t);
                         }
+                        t++;
                     }
 #pragma unroll
                     for (int u = 0; u < kUnrollE; u++) {
@@ -496,7 +529,11 @@ static cudaError_t launch_e(Ctx &c) {
         c.launches++;
     }
     cudaEventRecord(c.ev_join[0], c.side[0]);
-    EItems it{c.e_pre, c.e_nbig, c.e_extra, c.e_extra + n_heavy};
+    EItems it{nullptr, nullptr};
+    if (n_heavy > 0) {
+        cudaError_t e = build_e_items(c, it);
+        if (e != cudaSuccess) return e;
+    }
     const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.k);
     static bool attr_set[2] = {false, false};
     if (!attr_set[COUNT]) {
@@ -508,7 +545,7 @@ static cudaError_t launch_e(Ctx &c) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     const int grid = std::max(1, per_sm) * sms;
-    if (it.total > 0) {
+    if (n_heavy > 0) {
         k_phase_e<COUNT><<<grid, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
         c.launches++;
     }

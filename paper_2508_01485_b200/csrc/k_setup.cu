@@ -94,30 +94,34 @@ __global__ void k_class_bounds(const uint32_t *__restrict__ deg_s, int64_t n, un
     out[cls] = (unsigned long long)lo;
 }
 
-cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o) {
+// temporaries of launch_relabel, carved from the caller's arena
+size_t relabel_arena_bytes(int64_t n, int64_t nnz) {
+    size_t need_sort = 0, need_scan = 0, need_seg = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, need_sort, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                              (int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, 32);
+    cub::DeviceScan::ExclusiveSum(nullptr, need_scan, (int64_t *)nullptr, (int64_t *)nullptr, (int)(n + 1));
+    cub::DeviceSegmentedSort::SortKeys(nullptr, need_seg, (int32_t *)nullptr, (int32_t *)nullptr, nnz, (int)n,
+                                       (int64_t *)nullptr, (int64_t *)nullptr);
+    const size_t cub_b = std::max(need_sort, std::max(need_scan, need_seg));
+    return 3 * (4 * (size_t)n + 256) + (8 * (size_t)(n + 1) + 256) + (4 * (size_t)std::max<int64_t>(nnz, 1) + 256) +
+           cub_b + 256;
+}
+
+cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, void *arena, size_t arena_bytes) {
     const int64_t n = c.n, nnz = c.nnz;
-    uint32_t *deg = nullptr, *deg_s = nullptr;
-    int32_t *iota = nullptr, *tmpcol = nullptr;
-    int64_t *d64 = nullptr;
-    void *tmp = nullptr;
+    char *ap = (char *)arena;
+    auto carve = [&](size_t b) { void *p = ap; ap += (b + 255) & ~(size_t)255; return p; };
+    uint32_t *deg = (uint32_t *)carve(4 * (size_t)n);
+    uint32_t *deg_s = (uint32_t *)carve(4 * (size_t)n);
+    int32_t *iota = (int32_t *)carve(4 * (size_t)n);
+    int64_t *d64 = (int64_t *)carve(8 * (size_t)(n + 1));
+    int32_t *tmpcol = (int32_t *)carve(4 * (size_t)std::max<int64_t>(nnz, 1));
+    void *tmp = ap;
+    if ((size_t)(ap - (char *)arena) > arena_bytes) return cudaErrorMemoryAllocation;
+    const size_t need = arena_bytes - (size_t)(ap - (char *)arena);
     cudaError_t e = cudaSuccess;
-    auto done = [&](cudaError_t r) {
-        cudaStreamSynchronize(c.stream);
-        cudaFree(deg); cudaFree(deg_s); cudaFree(iota); cudaFree(tmpcol); cudaFree(d64); cudaFree(tmp);
-        return r;
-    };
-    if ((e = cudaMalloc(&deg, 4 * n)) || (e = cudaMalloc(&deg_s, 4 * n)) || (e = cudaMalloc(&iota, 4 * n)) ||
-        (e = cudaMalloc(&d64, 8 * (n + 1))) || (e = cudaMalloc(&tmpcol, 4 * std::max<int64_t>(nnz, 1))))
-        return done(e);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
     k_deg_iota<<<blocks, 256, 0, c.stream>>>(rp_o, n, deg, iota);
-    size_t need_sort = 0, need_scan = 0, need_seg = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, need_sort, deg, deg_s, iota, c.perm, (int)n, 0, 32, c.stream);
-    cub::DeviceScan::ExclusiveSum(nullptr, need_scan, d64, c.rowptr, (int)(n + 1), c.stream);
-    cub::DeviceSegmentedSort::SortKeys(nullptr, need_seg, tmpcol, c.col, nnz, (int)n, c.rowptr, c.rowptr + 1,
-                                       c.stream);
-    const size_t need = std::max(need_sort, std::max(need_scan, need_seg));
-    if ((e = cudaMalloc(&tmp, need))) return done(e);
     size_t t1 = need;
     cub::DeviceRadixSort::SortPairsDescending(tmp, t1, deg, deg_s, iota, c.perm, (int)n, 0, 32, c.stream);
     k_inv_perm<<<blocks, 256, 0, c.stream>>>(c.perm, n, c.inv, deg_s, d64);
@@ -132,8 +136,8 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o) {
     uint32_t dmax = 0;
     cudaMemcpyAsync(ge, c.scal + kScalTk, sizeof(ge), cudaMemcpyDeviceToHost, c.stream);
     cudaMemcpyAsync(&dmax, deg_s, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream);
-    if ((e = cudaStreamSynchronize(c.stream))) return done(e);
-    if ((e = cudaGetLastError())) return done(e);
+    if ((e = cudaStreamSynchronize(c.stream))) return e;
+    if ((e = cudaGetLastError())) return e;
     // ge[cls] = #vertices with degree >= bin_lo(cls); class cls = [ge[cls+1], ge[cls])
     ge[0] = (unsigned long long)n;
     for (int cls = 0; cls < kNumBins; cls++) {
@@ -143,7 +147,7 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o) {
         c.bins.count[cls] = hi - lo;
     }
     c.d_max = dmax;
-    return done(cudaSuccess);
+    return cudaSuccess;
 }
 
 // ---------------------------------------------------------------- log2 table

@@ -194,10 +194,12 @@ extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream,
 
 static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
-    dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre);
+    dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
     dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.pc2); dfree(c.amat);
     dfree(c.acc1); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
+    c.cap_n = c.cap_nnz = 0;
+    ctx->l2n = 0;
 }
 
 extern "C" void rs_destroy(rs_ctx *ctx) {
@@ -206,7 +208,7 @@ extern "C" void rs_destroy(rs_ctx *ctx) {
     cudaSetDevice(c.device);
     if (c.stream) cudaStreamSynchronize(c.stream);
     free_graph(ctx);
-    dfree(c.chist); dfree(c.ccode); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist);
+    dfree(c.chist); dfree(c.ccode); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist); dfree(c.arena);
     dfree(ctx->utargets); dfree(ctx->stage_i32); dfree(ctx->stage_f64); dfree(ctx->cand_key); dfree(ctx->cand_id);
     for (int i = 0; i < rs::kNumBins; i++) {
         if (c.side[i]) cudaStreamDestroy(c.side[i]);
@@ -245,23 +247,34 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     }
     if (first != 0) return fail(ctx, RS_EINVAL, "rs_load_csr: row_offsets[0] != 0");
     if (nnz < 0) return fail(ctx, RS_EINVAL, "rs_load_csr: row_offsets[n] < 0");
-    free_graph(ctx);
+    // buffers are reused when the new graph fits their capacity (no free/alloc per load)
+    const bool fits = c.cap_n >= n && c.cap_nnz >= nnz;
+    if (!fits) free_graph(ctx);
+    c.loaded = c.has_comm = c.scored = false;
     c.n = n;
     c.nnz = nnz;
+    // arena: host-input staging + relabel temporaries (grow-only)
+    const size_t stage_b = (dev_ro ? 0 : 8 * (size_t)(n + 1) + 256) + (dev_ci ? 0 : 4 * (size_t)std::max<int64_t>(nnz, 1) + 256);
+    const size_t arena_need = stage_b + rs::relabel_arena_bytes(n, nnz);
+    if (arena_need > c.arena_bytes) {
+        dfree(c.arena);
+        c.arena_bytes = 0;
+        CK(cudaMalloc(&c.arena, arena_need));
+        c.arena_bytes = arena_need;
+    }
+    char *ap = (char *)c.arena;
     // the caller's (original-id) CSR on the device: borrowed if already there
     const int64_t *rp_o = row_offsets;
     const int32_t *col_o = col_idx;
-    int64_t *rp_tmp = nullptr;
-    int32_t *col_tmp = nullptr;
-    auto free_tmp = [&]() { if (rp_tmp) cudaFree(rp_tmp); if (col_tmp) cudaFree(col_tmp); };
     if (!dev_ro) {
-        CK(cudaMalloc(&rp_tmp, sizeof(int64_t) * (n + 1)));
+        int64_t *rp_tmp = (int64_t *)ap;
+        ap += (8 * (size_t)(n + 1) + 255) & ~(size_t)255;
         CK(cudaMemcpyAsync(rp_tmp, row_offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c.stream));
         rp_o = rp_tmp;
     }
     if (!dev_ci) {
-        cudaError_t e = cudaMalloc(&col_tmp, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-        if (e != cudaSuccess) { free_tmp(); CK(e); }
+        int32_t *col_tmp = (int32_t *)ap;
+        ap += (4 * (size_t)std::max<int64_t>(nnz, 1) + 255) & ~(size_t)255;
         if (nnz) CK(cudaMemcpyAsync(col_tmp, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
         col_o = col_tmp;
     }
@@ -278,39 +291,39 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
                                          "graph not symmetric"};
             std::string m = std::string("rs_load_csr: ") + (er[0] < 6 ? what[er[0]] : "invalid") + " at row " +
                             std::to_string((long long)er[1]);
-            free_tmp();
-            free_graph(ctx);
             return fail(ctx, RS_EINVAL, m);
         }
     }
-    // internal degree-descending numbering (k_setup.cu launch_relabel)
-    CK(dalloc(&c.rowptr, n + 1));
-    CK(dalloc(&c.col, nnz));
-    CK(dalloc(&c.perm, n));
-    CK(dalloc(&c.inv, n));
-    {
-        cudaError_t e = rs::launch_relabel(c, rp_o, col_o);
-        free_tmp();
-        CK(e);
+    if (!fits) {
+        CK(dalloc(&c.rowptr, n + 1));
+        CK(dalloc(&c.col, nnz));
+        CK(dalloc(&c.perm, n));
+        CK(dalloc(&c.inv, n));
+        const size_t scratch = 24 * (size_t)(n + 1) + (64u << 20);
+        CK(cudaMalloc(&c.scratch, scratch));
+        c.scratch_bytes = scratch;
+        CK(dalloc(&c.comm_in, n));
+        CK(dalloc(&c.comm_id, n));
+        CK(dalloc(&c.lab, n));
+        CK(dalloc(&c.vrec, n));
+        CK(dalloc(&c.pidx, nnz));
+        CK(dalloc(&c.pplus, nnz));
+        CK(dalloc(&c.pc2, n));
+        CK(dalloc(&c.acc1, 3 * n));
+        CK(dalloc(&c.n1, n));
+        CK(dalloc(&c.score, n));
+        c.cap_n = n;
+        c.cap_nnz = nnz;
     }
-    // per-graph buffers (independent of communities)
-    size_t scratch = 24 * (size_t)(n + 1) + (64u << 20);
-    CK(cudaMalloc(&c.scratch, scratch));
-    c.scratch_bytes = scratch;
+    // internal degree-descending numbering (k_setup.cu launch_relabel)
+    CK(rs::launch_relabel(c, rp_o, col_o, ap, c.arena_bytes - (size_t)(ap - (char *)c.arena)));
     CK(rs::launch_e_items(c));
-    ctx->l2n = std::min<int64_t>(c.d_max + 1, 1ll << 20);
-    CK(dalloc(&ctx->l2t, ctx->l2n));
-    CK(rs::launch_log2_table(c, ctx->l2t, ctx->l2n));
-    CK(dalloc(&c.comm_in, n));
-    CK(dalloc(&c.comm_id, n));
-    CK(dalloc(&c.lab, n));
-    CK(dalloc(&c.vrec, n));
-    CK(dalloc(&c.pidx, nnz));
-    CK(dalloc(&c.pplus, nnz));
-    CK(dalloc(&c.pc2, n));
-    CK(dalloc(&c.acc1, 3 * n));
-    CK(dalloc(&c.n1, n));
-    CK(dalloc(&c.score, n));
+    const int64_t l2n = std::min<int64_t>(c.d_max + 1, 1ll << 20);
+    if (l2n > ctx->l2n) {
+        CK(dalloc(&ctx->l2t, l2n));
+        ctx->l2n = l2n;
+        CK(rs::launch_log2_table(c, ctx->l2t, ctx->l2n));
+    }
     c.head_lo = 0;
     c.head_hi = n;
     if (c.world > 1) CK(rs::launch_partition(c));
@@ -341,12 +354,13 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
         CK(dalloc(&c.ccode, cap));
         c.ccap = cap;
     }
-    if (c.k_alloc != k) {
+    if (c.k_alloc != k || c.kn_alloc != c.n) {
         CK(dalloc(&c.f, (size_t)c.n * k));
         CK(dalloc(&c.omega, (size_t)c.n * k));
         CK(dalloc(&c.bq, (size_t)c.n * k));
         CK(dalloc(&c.amat, (size_t)c.n * k));
         c.k_alloc = k;
+        c.kn_alloc = c.n;
     }
     c.k = k;
     const int32_t *ut = nullptr;

@@ -172,6 +172,9 @@ struct CtaGroup {
         return a;
     }
     __device__ __forceinline__ int sum(int v) { return (int)sum((long long)v); }
+    __device__ __forceinline__ unsigned long long sum(unsigned long long v) {
+        return (unsigned long long)sum((long long)v);
+    }
     __device__ __forceinline__ U128 sum(U128 v) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {

@@ -91,6 +91,7 @@ struct Ctx {
     int64_t d_max = 0;
     int64_t *e_pre = nullptr;    // Phase E work items: prefix of extra chunks of the e_nbig largest rows
     int64_t e_nbig = 0, e_extra = 0;
+    size_t e_bytes = 0;
     bool loaded = false;
 
     // communities (set time)
@@ -119,6 +120,7 @@ struct Ctx {
     double *score = nullptr;     // n, ORIGINAL vertex order
     unsigned long long *scal = nullptr;  // device scalars (see kScal*)
     int64_t k_alloc = 0;         // k the per-score buffers were sized for
+    int64_t kn_alloc = 0;        // ... and n
     bool scored = false;
 
     // top-k scratch
@@ -129,6 +131,10 @@ struct Ctx {
     // device scratch for reductions / validation
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
+    // grow-only arena for load-time staging and relabel temporaries; buffer capacities
+    void *arena = nullptr;
+    size_t arena_bytes = 0;
+    int64_t cap_n = 0, cap_nnz = 0;
 };
 
 // device scalar slots in Ctx::scal
@@ -155,7 +161,8 @@ inline double wide_bound(int k) {
 
 // ---- kernels (launchers). Each returns cudaGetLastError() of the launch. ----
 cudaError_t launch_validate(Ctx &c, const int64_t *rp, const int32_t *col);
-cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o);
+size_t relabel_arena_bytes(int64_t n, int64_t nnz);
+cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, void *arena, size_t arena_bytes);
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets);
 cudaError_t launch_phase_a(Ctx &c);
 cudaError_t launch_phase_c(Ctx &c);
