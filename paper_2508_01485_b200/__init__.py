@@ -66,10 +66,12 @@ SIGNATURES = [
 ]
 
 
-def load_library(path: str = LIB_PATH):
-    """Load librs.so (build it first with paper_2508_01485_b200.build). Raises if absent."""
+def load_library(path: str | None = None):
+    """Load librs.so (build it first with paper_2508_01485_b200.build). Raises if absent.
+    ``RS_LIBRARY`` overrides the path (experiment builds)."""
     global _lib
     if _lib is None:
+        path = path or os.environ.get("RS_LIBRARY") or LIB_PATH
         if not os.path.exists(path):
             raise ImportError(f"librs.so not built at {path}; run `python -m paper_2508_01485_b200.build`")
         lib = ctypes.CDLL(path)

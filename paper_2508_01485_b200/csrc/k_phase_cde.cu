@@ -30,14 +30,18 @@ __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &
     U128 B[8];
 #pragma unroll
     for (int c = 0; c < 8; c++) B[c] = u128_zero();
-    int ppc = 0;
+    // w's own cube-root row: a_w(c_v) for every P+ entry v goes beside v (wps)
+    double arow[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) arow[c] = c < k ? __ldg(a.amat + w * k + c) : 0.0;
+    int ppc = 0, pmc = 0;
     for (int base = 0; base < pc; base += GR::size * U) {
         int32_t v[U];
         VRec rv[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
-            v[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
+            v[j] = i < pc ? a.pidx[beg + i] : -1;     // plain load: this kernel rewrites P lists
         }
 #pragma unroll
         for (int j = 0; j < U; j++) {
@@ -54,14 +58,26 @@ __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &
                 const bool plus = v[j] >= 0 && (rv[j].pcnt > pc || (rv[j].pcnt == pc && v[j] > (int32_t)w));
                 int tot;
                 const int r = g.rank(plus, &tot);
-                if (plus) a.pplus[beg + ppc + r] = v[j];
+                if (plus) {
+                    double wv = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 8; c++) wv = (rv[j].lab == c) ? arow[c] : wv;
+                    a.pplus[beg + ppc + r] = v[j];
+                    a.wps[beg + ppc + r] = wv;
+                }
+                // P-(w) compacted in place to the front of w's P list (every position
+                // written has been read: the count of minus entries trails the reads)
+                int totm;
+                const int rm = g.rank(v[j] >= 0 && !plus, &totm);
+                if (v[j] >= 0 && !plus) a.pidx[beg + pmc + rm] = v[j];
                 ppc += tot;
+                pmc += totm;
             }
         }
     }
 #pragma unroll
     for (int c = 0; c < 8; c++) B[c] = g.sum(B[c]);
-    if (g.lane == 0) a.pc2[w] = make_int2(ppc, pc);
+    if (g.lane == 0) { PRec r; r.x = ppc; r.y = pc; r.start = beg; a.pc2[w] = r; }
     if (pc == 0) return;   // w is in no P(u): its B/Q row is never read
     for (int c = g.lane; c < k; c += GR::size) {
         U128 Bc = u128_zero();
@@ -84,23 +100,30 @@ __device__ __forceinline__ void phase_c_vertex_smem(const CdeArgs &a, int64_t w,
     const int k = a.k;
     for (int c = g.lane; c < 3 * k; c += GR::size) sB[c] = 0ull;
     g.sync();
-    int ppc = 0;
+    int ppc = 0, pmc = 0;
     for (int base = 0; base < pc; base += GR::size) {
         const int i = base + (int)g.lane;
         const bool valid = i < pc;
         int32_t v = 0;
         VRec rv;
         rv.lab = kOther; rv.pcnt = 0; rv.a_self = 0.0;
-        if (valid) { v = __ldg(a.pidx + beg + i); rv = a.vrec[v]; }
+        if (valid) { v = a.pidx[beg + i]; rv = a.vrec[v]; }
         if (valid && rv.lab < k) fx_red3(sB + 3 * rv.lab, fx_quantize(rv.a_self));
         const bool plus = valid && (rv.pcnt > pc || (rv.pcnt == pc && v > (int32_t)w));
         int tot;
         const int r = g.rank(plus, &tot);
-        if (plus) a.pplus[beg + ppc + r] = v;
+        if (plus) {
+            a.pplus[beg + ppc + r] = v;
+            a.wps[beg + ppc + r] = rv.lab < k ? __ldg(a.amat + w * k + rv.lab) : 0.0;
+        }
+        int totm;
+        const int rm = g.rank(valid && !plus, &totm);
+        if (valid && !plus) a.pidx[beg + pmc + rm] = v;
         ppc += tot;
+        pmc += totm;
     }
     g.sync();
-    if (g.lane == 0) a.pc2[w] = make_int2(ppc, pc);
+    if (g.lane == 0) { PRec r; r.x = ppc; r.y = pc; r.start = beg; a.pc2[w] = r; }
     if (pc > 0) {
         for (int c = g.lane; c < k; c += GR::size) {
             const double aw = a.amat[w * k + c];
@@ -149,6 +172,7 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const int cu = ru.lab;
     const double au = ru.a_self;
     const int pc = ru.pcnt;
+    const int pm = pc - a.pc2[u].x;            // P(u) = P-(u) (front of pidx) + P+(u) (pplus)
     const int64_t beg = a.rowptr[u];
     const int64_t d = a.rowptr[u + 1] - beg;
     U128 S = u128_zero();
@@ -158,7 +182,7 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
-            w[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
+            w[j] = i < pm ? __ldg(a.pidx + beg + i) : (i < pc ? __ldg(a.pplus + beg + i - pm) : -1);
         }
 #pragma unroll
         for (int j = 0; j < U; j++)

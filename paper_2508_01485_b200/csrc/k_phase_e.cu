@@ -7,96 +7,97 @@
 // by rank (|P|, id) (Phase C's P+ lists), each triangle x < y < z is found
 // exactly once from its middle vertex y, as z in P+(x) ∩ P+(y) for x in
 // P-(y), the lower-ranked part of P(y) (the paper's "common predecessor"
-// search, with hash probes instead of a merge).
+// search, with bitmap/binary-search probes instead of a merge).
 //
-// Work items are (y, chunk of 128 positions of P(y)); a warp takes an item
-// from a global queue (the heaviest vertices first: internal ids are
-// degree-descending), hashes P+(y) into shared memory, lists the item's
-// predecessors x with their P+(x) in shared memory, and lets every lane walk
-// one contiguous segment of the concatenated P+(x) lists, kUnrollE probes at
-// a time (independent loads of one cache line in flight, no shuffles). Hits are queued in shared memory and
-// evaluated 32 at a time with every lane busy; each triangle adds the grouped
-// terms of its (up to) three heads:
+// Each triangle adds the grouped terms of its (up to) three heads
 //   head x: a_y(c_x) a_z(c_x) (a_z(c_y) + a_y(c_z))
 //   head y: a_x(c_y) a_z(c_y) (a_z(c_x) + a_x(c_z))
 //   head z: a_x(c_z) a_y(c_z) (a_y(c_x) + a_x(c_y))
-// (a_v(c) = 0 for a non-target column c: a non-target mid has no term; each
-// expression is symmetric in the two other vertices, so the numbering does not
-// change any bit of the result). Head y accumulates in registers (one RED per
-// item); x and z use exact fixed-point RED. COUNT mode (parity getter) counts
+// with a_v(c) = 0 for a non-target column c -- so a non-target head or mid
+// contributes exactly 0 without a test -- and each expression symmetric in
+// the two other vertices (the numbering changes no bit of the result).
+// a_x(c_z) comes from the weight Phase C stored beside z in P+(x) (read at the
+// probe's own index). Sums are exact fixed point (C-12).
+//
+// Heavy middle vertices (degree >= 128): work items (y, 64 positions of
+// P(y)), a warp per item from a global queue, heaviest first. The warp puts a
+// 4096-bit filter and a sorted copy of P+(y) in shared memory, lists the
+// item's predecessors x, and cuts every P+(x) into pieces of kPiece entries:
+// a lane probes one piece per round (independent loads in flight), filter
+// candidates are packed with one warp scan and verified 32 at a time by binary
+// search in the shared copy. Head terms accumulate per item in shared memory
+// (x per list slot, z per P+(y) position, y in registers) and are flushed with
+// one RED per touched head. Light middle vertices: one thread per y, two-
+// pointer merge of the short sorted lists. COUNT mode (parity getter) counts
 // the ordered (head, mid) target pairs instead.
 #include "rs_phase.cuh"
 #include <cub/cub.cuh>
 
 namespace rs {
 
-constexpr int kChunkE = 128;     // positions of P(y) per work item
-constexpr int kTabE = 1024;      // hash slots per warp (P+(y) up to kTabE/4 hashed, load <= 1/4)
-constexpr int kBmWords = 128;    // 4096-bit membership filter of P+(y) per warp
-constexpr int kQCapE = 160;      // candidate queue per warp (31 + 4*32 < 160)
-constexpr int kUnrollE = 4;
+constexpr int kChunkE = 64;      // positions of P(y) per work item
+constexpr int kPyCap = 256;      // P+(y) kept in shared memory (sorted copy + labels)
+constexpr int kBmWords = 128;    // 4096-bit membership filter of P+(y)
+constexpr int kPiece = 4;        // consecutive P+(x) entries one lane probes per round
+constexpr int kQCapE = 160;      // candidate queue (31 + 32 * kPiece < 160)
+constexpr int kPieceMap = 512;   // piece -> slot map capacity (else binary search)
+constexpr int kSlotMaxHits = 4096;   // smem limbs of an x slot take at most this many terms
 constexpr int kWarpsE = 8;
 
-// membership filter bit of z (top 12 bits of a second multiplicative hash)
+// membership filter bit of z (top 12 bits of a multiplicative hash)
 __device__ __forceinline__ uint32_t bm_bit(int32_t z) {
     return ((uint32_t)z * 0x85EBCA6Bu) >> 20;
 }
 
-// Fibonacci hashing: the top log2(size) bits of z * 2^32/phi
-__device__ __forceinline__ uint32_t hslot(int32_t z, uint32_t shift) {
-    return ((uint32_t)z * 2654435769u) >> shift;
+// position of z in the sorted list p[0, len), or -1
+__device__ __forceinline__ int find_sorted(const int32_t *p, int len, int32_t z) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (p[mid] < z) lo = mid + 1; else hi = mid;
+    }
+    return (lo < len && p[lo] == z) ? lo : -1;
 }
-
-// z in the sorted list p[0, len)
-__device__ __forceinline__ bool in_sorted(const int32_t *p, int len, int32_t z) {
+__device__ __forceinline__ int find_sorted_g(const int32_t *p, int len, int32_t z) {
     int lo = 0, hi = len;
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (__ldg(p + mid) < z) lo = mid + 1; else hi = mid;
     }
-    return lo < len && __ldg(p + lo) == z;
+    return (lo < len && __ldg(p + lo) == z) ? lo : -1;
 }
 
 __device__ __forceinline__ double amat_at(const CdeArgs &a, int32_t v, int c) {
-    return __ldg(a.amat + (int64_t)v * a.k + c);
+    return c < a.k ? __ldg(a.amat + (int64_t)v * a.k + c) : 0.0;
 }
 
+__device__ __forceinline__ bool owned(const CdeArgs &a, int64_t h) { return h >= a.head_lo && h < a.head_hi; }
+
+// global exact accumulation of a head's (partial) Type-I sum
 __device__ __forceinline__ void acc_add(const CdeArgs &a, int32_t h, const U128 &q) {
     unsigned long long *acc = a.acc1 + 3 * (int64_t)h;
     if (a.any_wide && a.vrec[h].wide) fx_red3(acc, q);
     else fx_red2(acc, q);
 }
 
-// one queued triangle (x, y, z) on this lane; returns head-y's term
-template <bool COUNT>
-__device__ __forceinline__ U128 tri_terms(const CdeArgs &a, int32_t x, int32_t y, int ly, const double *Ay,
-                                          int32_t z, unsigned long long &cnt_y) {
-    const int k = a.k;
-    const int lx = __ldg(a.lab + x), lz = __ldg(a.lab + z);
-    const bool tx = lx < k, ty = ly < k, tz = lz < k;
-    if constexpr (COUNT) {
-        if (tx && x >= a.head_lo && x < a.head_hi && (ty + tz)) atomicAdd(a.n1 + x, (unsigned long long)(ty + tz));
-        if (tz && z >= a.head_lo && z < a.head_hi && (tx + ty)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
-        cnt_y += ty ? (unsigned long long)(tx + tz) : 0ull;
-        return u128_zero();
-    } else {
-        const double Axly = ty ? amat_at(a, x, ly) : 0.0;
-        const double Axlz = tz ? amat_at(a, x, lz) : 0.0;
-        const double Azlx = tx ? amat_at(a, z, lx) : 0.0;
-        const double Azly = ty ? amat_at(a, z, ly) : 0.0;
-        const double Aylx = tx ? Ay[lx] : 0.0;
-        const double Aylz = tz ? Ay[lz] : 0.0;
-        if (tx && x >= a.head_lo && x < a.head_hi) {
-            const double t = Aylx * Azlx * (Azly + Aylz);
-            if (t > 0.0) acc_add(a, x, fx_quantize(t));
-        }
-        if (tz && z >= a.head_lo && z < a.head_hi) {
-            const double t = Axlz * Aylz * (Aylx + Axly);
-            if (t > 0.0) acc_add(a, z, fx_quantize(t));
-        }
-        if (ty) return fx_quantize(Axly * Azly * (Azlx + Axlz));
-        return u128_zero();
-    }
+// shared-memory per-item accumulator: four 20-bit limbs of q (< 2^80) added with
+// native 32-bit shared atomics (64-bit shared atomics are CAS loops); exact
+// while a slot receives fewer than 2^12 terms per item (x slots with longer
+// P+(x) and z positions beyond kPyCap go straight to the global limbs).
+__device__ __forceinline__ void smem_red4(uint32_t *acc4, const U128 &q) {
+    const uint32_t l0 = (uint32_t)(q.lo & 0xFFFFFull), l1 = (uint32_t)((q.lo >> 20) & 0xFFFFFull);
+    const uint32_t l2 = (uint32_t)((q.lo >> 40) & 0xFFFFFull), l3 = (uint32_t)((q.lo >> 60) | (q.hi << 4));
+    if (l0) atomicAdd(acc4 + 0, l0);
+    if (l1) atomicAdd(acc4 + 1, l1);
+    if (l2) atomicAdd(acc4 + 2, l2);
+    if (l3) atomicAdd(acc4 + 3, l3);
+}
+__device__ __forceinline__ U128 from4(const uint32_t *acc4) {
+    U128 s = U128{(unsigned long long)acc4[0], 0ull};
+    s = u128_add(s, U128{(unsigned long long)acc4[1] << 20, 0ull});
+    s = u128_add(s, U128{(unsigned long long)acc4[2] << 40, (unsigned long long)acc4[2] >> 24});
+    s = u128_add(s, U128{(unsigned long long)acc4[3] << 60, (unsigned long long)acc4[3] >> 4});
+    return s;
 }
 
 struct EItems {
@@ -104,8 +105,20 @@ struct EItems {
     const int32_t *total;  // number of items (device scalar, written by the item scan)
 };
 
-__host__ __device__ constexpr int e_stride_bytes(int k) {
-    return kTabE * 4 + kBmWords * 4 + kQCapE * 8 + kChunkE * 16 + ((8 * k + 15) / 16) * 16;
+struct ESmem {             // one warp's shared memory
+    uint32_t bm[kBmWords];
+    int32_t py[kPyCap];
+    longlong2 xl[kChunkE];  // {P+(x) start, (x << 32) | (lab(x) << 24) | |P+(x)|}
+    double2 xw[kChunkE];    // {a_x(c_y), a_y(c_x)}
+    uint32_t xa[4 * kChunkE];
+    int32_t pe[kChunkE];    // end of each list's pieces
+    int2 q[kQCapE];         // candidates {x slot, offset in P+(x)}
+    uint8_t pslot[kPieceMap];   // piece -> x slot (items with at most kPieceMap pieces)
+    uint8_t zl[kPyCap];         // label of z in P+(y)
+};
+
+__host__ __device__ constexpr size_t e_stride_bytes(int k) {
+    return ((sizeof(ESmem) + 15) / 16) * 16 + ((8 * (size_t)k + 15) / 16) * 16;
 }
 
 template <bool COUNT>
@@ -114,105 +127,60 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k;
     unsigned char *base = e_smem + (size_t)wid * e_stride_bytes(k);
-    int32_t *T = (int32_t *)base;
-    uint32_t *BM = (uint32_t *)(base + kTabE * 4);
-    int2 *Q = (int2 *)(base + kTabE * 4 + kBmWords * 4);
-    longlong2 *XL = (longlong2 *)(base + kTabE * 4 + kBmWords * 4 + kQCapE * 8);   // {P+(x) base - offset, (x << 32) | end}
-    double *Ay = (double *)(base + kTabE * 4 + kBmWords * 4 + kQCapE * 8 + kChunkE * 16);
+    ESmem &S = *reinterpret_cast<ESmem *>(base);
+    double *Ay = (double *)(base + ((sizeof(ESmem) + 15) / 16) * 16);
     unsigned long long ntri = 0;
     const unsigned long long n_items = (unsigned long long)*it.total;
 
     for (;;) {
-        unsigned long long q = 0;
-        if (lane == 0) q = atomicAdd(queue_ctr, 1ull);
-        q = __shfl_sync(0xffffffffu, q, 0);
-        if (q >= n_items) break;
-        const int2 itm = it.items[q];
+        unsigned long long qi = 0;
+        if (lane == 0) qi = atomicAdd(queue_ctr, 1ull);
+        qi = __shfl_sync(0xffffffffu, qi, 0);
+        if (qi >= n_items) break;
+        const int2 itm = it.items[qi];
         const int32_t y = itm.x;
-        const int chunk = itm.y;
-        const int2 pcy = a.pc2[y];
-        const int py = pcy.x, pc = pcy.y;
-        const int start = chunk * kChunkE;
-        if (py == 0 || start >= pc) continue;    // no z above y, or an empty chunk
-        const int end = min(pc, start + kChunkE);
+        const PRec pcy = a.pc2[y];
+        const int py = pcy.x, pm = pcy.y - pcy.x;   // |P+(y)|, |P-(y)| (P-(y) = front of pidx)
+        const int start = itm.y * kChunkE;
+        if (py == 0 || start >= pm) continue;       // no z above y, or an empty chunk
+        const int end = min(pm, start + kChunkE);
         const int ly = a.lab[y];
-        const int64_t by = a.rowptr[y];
-        const bool hashed = py <= kTabE / 4;
-        uint32_t mask = 0, shift = 0;
-        for (int w = lane; w < kBmWords; w += 32) BM[w] = 0u;
+        const int64_t by = pcy.start;
+        const bool local = py <= kPyCap;            // P+(y) copy + accumulators in smem
+        for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
+        for (int c = lane; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
         __syncwarp();
         for (int i = lane; i < py; i += 32) {
-            const uint32_t b = bm_bit(__ldg(a.pplus + by + i));
-            atomicOr(&BM[b >> 5], 1u << (b & 31));
-        }
-        if (hashed) {
-            uint32_t size = 32;
-            while (size < 4u * (uint32_t)py) size <<= 1;
-            mask = size - 1;
-            shift = 32 - __ffs(size) + 1;
-            for (uint32_t s = lane; s < size; s += 32) T[s] = -1;
-            __syncwarp();
-            for (int i = lane; i < py; i += 32) {
-                const int32_t z = __ldg(a.pplus + by + i);
-                uint32_t h = hslot(z, shift);
-                while (atomicCAS(&T[h], -1, z) != -1) h = (h + 1) & mask;
+            const int32_t z = __ldg(a.pplus + by + i);
+            const uint32_t b = bm_bit(z);
+            atomicOr(&S.bm[b >> 5], 1u << (b & 31));
+            if (local) {
+                S.py[i] = z;
+                const int lzi = __ldg(a.lab + z);
+                S.zl[i] = (uint8_t)lzi;
             }
         }
-        for (int c = lane; c < k; c += 32) Ay[c] = amat_at(a, y, c);
-        __syncwarp();
-
-        U128 accy = u128_zero();
-        unsigned long long cnty = 0;
-        int qn = 0;
-        // queued candidates (x, z) passed the bitmap filter; verify z in P+(y)
-        // exactly, then evaluate the triangle -- 32 at a time, all lanes busy
-        auto drain = [&](int upto) {
-            while (qn >= upto && qn > 0) {
-                const int take = qn < 32 ? qn : 32;
-                const int b = qn - take;
-                if (lane < take) {
-                    const int2 e = Q[b + lane];
-                    bool hit;
-                    if (hashed) {
-                        uint32_t h = hslot(e.y, shift);
-                        for (;;) {
-                            const int32_t sv = T[h];
-                            if (sv == e.y) { hit = true; break; }
-                            if (sv == -1) { hit = false; break; }
-                            h = (h + 1) & mask;
-                        }
-                    } else {
-                        hit = in_sorted(a.pplus + by, py, e.y);
-                    }
-                    if (hit) {
-                        ntri++;
-                        accy = u128_add(accy, tri_terms<COUNT>(a, e.x, y, ly, Ay, e.y, cnty));
-                    }
-                }
-                __syncwarp();
-                qn = b;
-            }
-        };
-
         // the item's predecessors x (lower rank, non-empty P+(x), a target among
-        // x and y) -> a compact list in shared memory: P+(x) occupies the
-        // positions [end - |P+(x)|, end) of the concatenated probe sequence
-        int nx = 0, total = 0;
+        // x and y), each P+(x) cut into pieces numbered across the list
+        int nx = 0, npieces = 0;
         for (int i0 = start; i0 < end; i0 += 32) {
             const int i = i0 + lane;
             int32_t x = 0;
             int64_t bx = 0;
-            int lenx = 0;
+            int lenx = 0, lx = kOther;
             if (i < end) {
-                x = __ldg(a.pidx + by + i);
-                const int2 pcx = a.pc2[x];
-                const bool lower = pcx.y < pc || (pcx.y == pc && x < y);
-                if (lower && pcx.x > 0 && (__ldg(a.lab + x) < k || ly < k)) {
-                    lenx = pcx.x;
-                    bx = a.rowptr[x];
+                x = __ldg(a.pidx + by + i);              // x in P-(y): lower rank than y
+                const PRec pcx = a.pc2[x];
+                if (pcx.x > 0) {
+                    lx = __ldg(a.lab + x);
+                    if (lx < k || ly < k) {
+                        lenx = pcx.x;
+                        bx = pcx.start;
+                    }
                 }
             }
-            int incl = lenx;
+            const int pieces = (lenx + kPiece - 1) / kPiece;
+            int incl = pieces;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -221,78 +189,138 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
             const unsigned has = __ballot_sync(0xffffffffu, lenx > 0);
             if (lenx > 0) {
                 const int slot = nx + __popc(has & ((1u << lane) - 1u));
-                const int e_end = total + incl;
-                XL[slot] = make_longlong2(bx - (e_end - lenx), ((long long)x << 32) | (unsigned)e_end);
+                S.xl[slot] = make_longlong2(bx, ((long long)x << 32) | ((long long)(lx & 0xFF) << 24) | lenx);
+                S.xw[slot] = make_double2(ly < k ? __ldg(a.amat + (int64_t)x * k + ly) : 0.0, lx < k ? Ay[lx] : 0.0);
+                S.xa[4 * slot] = 0u;
+                S.xa[4 * slot + 1] = 0u;
+                S.xa[4 * slot + 2] = 0u;
+                S.xa[4 * slot + 3] = 0u;
+                S.pe[slot] = npieces + incl;
             }
             nx += __popc(has);
-            total += __shfl_sync(0xffffffffu, incl, 31);
+            npieces += __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncwarp();
-        // every lane walks one contiguous segment of the probe sequence
-        const int seg = (total + 31) >> 5;
-        const int t_beg = min(total, lane * seg), t_end = min(total, t_beg + seg);
-        // the lane's current list: P+(xcur) covers probe positions [.., xe), at base + t
-        int xi = 0, xe = 0;
-        int64_t xbase = 0;
-        int32_t xcur = 0;
-        if (t_beg < t_end) {
-            int lo = 0, hi = nx;            // first list whose end > t_beg
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if ((int)(XL[mid].y & 0xffffffff) <= t_beg) lo = mid + 1; else hi = mid;
-            }
-            xi = lo;
-            const longlong2 e = XL[xi];
-            xbase = e.x;
-            xe = (int)(e.y & 0xffffffff);
-            xcur = (int32_t)(e.y >> 32);
+        if (npieces == 0) continue;
+#ifdef RS_EXP_SETUP_ONLY
+        if (npieces >= 0) continue;
+#endif
+        const bool mapped = npieces <= kPieceMap;
+        if (mapped) {
+            for (int s = lane; s < nx; s += 32)
+                for (int p = s ? S.pe[s - 1] : 0; p < S.pe[s]; p++) S.pslot[p] = (uint8_t)s;
+            __syncwarp();
         }
-        int t = t_beg;
-        for (int s0 = 0; s0 < seg; s0 += kUnrollE) {
-            {
-                int32_t z[kUnrollE], xj[kUnrollE];
-#pragma unroll
-                for (int u = 0; u < kUnrollE; u++) {
-                    z[u] = -1;
-                    xj[u] = xcur;
-                    if (t < t_end) {
-                        if (t >= xe) {           // lists are non-empty: one step crosses at most one end
-                            const longlong2 e = XL[++xi];
-                            xbase = e.x;
-                            xe = (int)(e.y & 0xffffffff);
-                            xcur = (int32_t)(e.y >> 32);
-                            xj[u] = xcur;
+
+        U128 accy = u128_zero();
+        unsigned long long cnty = 0;
+        int qn = 0;
+        // verify candidates (x slot, offset) 32 at a time and add the triangle's terms
+        auto drain = [&](int upto) {
+            while (qn >= upto && qn > 0) {
+                const int take = qn < 32 ? qn : 32;
+                const int b0 = qn - take;
+                if (lane < take) {
+                    const int2 e = S.q[b0 + lane];
+                    const longlong2 xe = S.xl[e.x];
+                    const int32_t z = __ldg(a.pplus + xe.x + e.y);
+                    const int iz = local ? find_sorted(S.py, py, z) : find_sorted_g(a.pplus + by, py, z);
+                    if (iz >= 0) {
+                        ntri++;
+                        const int32_t x = (int32_t)(xe.y >> 32);
+                        const int lx = (int)((xe.y >> 24) & 0xFF);
+                        const int lz = local ? (int)S.zl[iz] : (int)__ldg(a.lab + z);
+                        if constexpr (COUNT) {
+                            const bool tx = lx < k, ty = ly < k, tz = lz < k;
+                            if (tx && (ty + tz) && owned(a, x)) atomicAdd(a.n1 + x, (unsigned long long)(ty + tz));
+                            if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
+                            cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
+                        } else {
+                            const double2 w = S.xw[e.x];
+                            const double Axly = w.x, Aylx = w.y;
+                            const double Axlz = __ldg(a.wps + xe.x + e.y);   // a_x(c_z), stored by Phase C
+                            const double Aylz = lz < k ? Ay[lz] : 0.0;
+                            const double Azlx = amat_at(a, z, lx);
+                            const double Azly = amat_at(a, z, ly);
+                            const double tx = Aylx * Azlx * (Azly + Aylz);
+                            const double tz = Axlz * Aylz * (Aylx + Axly);
+                            accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
+                            if (tx > 0.0) {
+                                if ((int)(xe.y & 0xFFFFFF) <= kSlotMaxHits) smem_red4(S.xa + 4 * e.x, fx_quantize(tx));
+                                else if (owned(a, x)) acc_add(a, x, fx_quantize(tx));
+                            }
+                            if (tz > 0.0) {
+                                if (owned(a, z)) acc_add(a, z, fx_quantize(tz));   // z: hub-ish, hot in L2
+                            }
                         }
-                        z[u] = __ldg(a.pplus + xbase + t);
                     }
-                    t++;
                 }
-                // bitmap filter; the lanes' candidates are packed with one warp scan
-                int npos = 0;
-                bool pos[kUnrollE];
-#pragma unroll
-                for (int u = 0; u < kUnrollE; u++) {
-                    const uint32_t b = bm_bit(z[u]);
-                    pos[u] = z[u] >= 0 && ((BM[b >> 5] >> (b & 31)) & 1u);
-                    npos += pos[u];
-                }
-                int incl = npos;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                int w = qn + incl - npos;
-#pragma unroll
-                for (int u = 0; u < kUnrollE; u++)
-                    if (pos[u]) Q[w++] = make_int2(xj[u], z[u]);
-                qn += __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
-                drain(32);
+                qn = b0;
             }
+        };
+
+        // one piece per lane per round; the round's filter candidates packed by one scan
+        for (int p0 = 0; p0 < npieces; p0 += 32) {
+            const int p = p0 + lane;
+            int slot = 0, off = 0, cnt = 0;
+            int64_t pb = 0;
+            if (p < npieces) {
+                int lo;                                // list holding piece p
+                if (mapped) {
+                    lo = S.pslot[p];
+                } else {
+                    lo = 0;
+                    int hi = nx;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (S.pe[mid] <= p) lo = mid + 1; else hi = mid;
+                    }
+                }
+                slot = lo;
+                const longlong2 xe = S.xl[lo];
+                off = (p - (lo ? S.pe[lo - 1] : 0)) * kPiece;
+                cnt = min(kPiece, (int)(xe.y & 0xFFFFFF) - off);
+                pb = xe.x + off;
+            }
+            int32_t z[kPiece];
+#pragma unroll
+            for (int j = 0; j < kPiece; j++) z[j] = j < cnt ? __ldg(a.pplus + pb + j) : -1;
+            unsigned m = 0;
+#pragma unroll
+            for (int j = 0; j < kPiece; j++) {
+                const uint32_t b = bm_bit(z[j]);
+                if (z[j] >= 0 && ((S.bm[b >> 5] >> (b & 31)) & 1u)) m |= 1u << j;
+            }
+            const int npos = __popc(m);
+            int incl = npos;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int w = qn + incl - npos;
+#pragma unroll
+            for (int j = 0; j < kPiece; j++)
+                if ((m >> j) & 1u) S.q[w++] = make_int2(slot, off + j);
+            qn += __shfl_sync(0xffffffffu, incl, 31);
+#ifdef RS_EXP_NO_DRAIN
+            qn = 0;
+#endif
+            __syncwarp();
+            drain(32);
         }
         drain(1);
-        if (ly < k && y >= a.head_lo && y < a.head_hi) {
+        __syncwarp();
+        // flush the item's per-head partial sums: one RED per touched head
+        if constexpr (!COUNT) {
+            for (int s = lane; s < nx; s += 32) {
+                const uint32_t *l = S.xa + 4 * s;
+                const int32_t x = (int32_t)(S.xl[s].y >> 32);
+                if ((l[0] | l[1] | l[2] | l[3]) && owned(a, x)) acc_add(a, x, from4(l));
+            }
+        }
+        if (ly < k && owned(a, y)) {
             if constexpr (COUNT) {
                 for (int o = 16; o > 0; o >>= 1) cnty += __shfl_xor_sync(0xffffffffu, cnty, o);
                 if (lane == 0 && cnty) atomicAdd(a.n1 + y, cnty);
@@ -310,16 +338,100 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
     if (lane == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
 }
 
+// ---------------------------------------------------------------- light middle vertices
+// Vertices of degree < 128 (most of them, ~5% of the probe work): one thread
+// per y; P(y), P+(y) and the P+(x) are short and sorted, so each x in P-(y)
+// is intersected with P+(y) by a two-pointer merge in L1. x's terms gather in
+// a register while its list is merged (one RED per x).
+template <bool COUNT>
+__global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
+    const int k = a.k;
+    unsigned long long ntri = 0;
+    for (int64_t y64 = ylo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y64 < a.n;
+         y64 += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t y = (int32_t)y64;
+        const PRec pcy = a.pc2[y];
+        const int py = pcy.x, pm = pcy.y - pcy.x;
+        if (py == 0 || pm == 0) continue;
+        const int ly = a.lab[y];
+        const int64_t by = pcy.start;
+        const int32_t *Py = a.pplus + by;
+        const double *Wy = a.wps + by;              // a_y(c_z) beside z in P+(y)
+        U128 accy = u128_zero();
+        unsigned long long cnty = 0;
+        for (int i = 0; i < pm; i++) {
+            const int32_t x = __ldg(a.pidx + by + i);   // P-(y): lower rank than y
+            const PRec pcx = a.pc2[x];
+            if (pcx.x == 0) continue;
+            const int lx = __ldg(a.lab + x);
+            if (lx >= k && ly >= k) continue;
+            const int64_t bx = pcx.start;
+            const int32_t *Px = a.pplus + bx;
+            const double Axly = amat_at(a, x, ly), Aylx = amat_at(a, y, lx);
+            U128 accx = u128_zero();
+            unsigned long long cntx = 0;
+            int ix = 0, iy = 0;
+            int32_t zx = __ldg(Px), zy = __ldg(Py);
+            while (true) {
+                if (zx == zy) {
+                    ntri++;
+                    const int32_t z = zx;
+                    const int lz = __ldg(a.lab + z);
+                    if constexpr (COUNT) {
+                        const bool tx = lx < k, ty = ly < k, tz = lz < k;
+                        cntx += tx ? (unsigned long long)(ty + tz) : 0ull;
+                        if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
+                        cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
+                    } else {
+                        const double Axlz = __ldg(a.wps + bx + ix), Aylz = __ldg(Wy + iy);
+                        const double Azlx = amat_at(a, z, lx), Azly = amat_at(a, z, ly);
+                        const double tx = Aylx * Azlx * (Azly + Aylz);
+                        const double tz = Axlz * Aylz * (Aylx + Axly);
+                        accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
+                        if (tx > 0.0) accx = u128_add(accx, fx_quantize(tx));
+                        if (tz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(tz));
+                    }
+                    if (++ix >= pcx.x || ++iy >= py) break;
+                    zx = __ldg(Px + ix);
+                    zy = __ldg(Py + iy);
+                } else if (zx < zy) {
+                    if (++ix >= pcx.x) break;
+                    zx = __ldg(Px + ix);
+                } else {
+                    if (++iy >= py) break;
+                    zy = __ldg(Py + iy);
+                }
+            }
+            if (owned(a, x)) {
+                if constexpr (COUNT) {
+                    if (cntx) atomicAdd(a.n1 + x, cntx);
+                } else {
+                    if (accx.lo | accx.hi) acc_add(a, x, accx);
+                }
+            }
+        }
+        if (ly < k && owned(a, y)) {
+            if constexpr (COUNT) {
+                if (cnty) atomicAdd(a.n1 + y, cnty);
+            } else {
+                if (accy.lo | accy.hi) acc_add(a, y, accy);
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
+    if ((threadIdx.x & 31) == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
+}
+
 // ---------------------------------------------------------------- work items (per step)
 // Heavy middle vertices (degree >= 128) are cut into chunks of kChunkE
 // positions of P(y); the chunk counts depend on the communities, so the item
 // list is rebuilt every step (count, scan, scatter), heaviest vertices first.
-__global__ void k_e_count(const int2 *__restrict__ pc2, int64_t n_heavy, int32_t *cnt) {
+__global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int32_t *cnt) {
     for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
         int c = 0;
         if (y < n_heavy) {
-            const int2 p = pc2[y];
-            if (p.x > 0 && p.y > p.x) c = (p.y + kChunkE - 1) / kChunkE;
+            const PRec p = pc2[y];
+            if (p.x > 0 && p.y > p.x) c = (p.y - p.x + kChunkE - 1) / kChunkE;   // chunks of P-(y)
         }
         cnt[y] = c;
     }
@@ -332,13 +444,13 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
     }
 }
 
-// load time: buffers sized for any community assignment
+// load time: buffers sized for any community assignment (grow-only)
 cudaError_t launch_e_items(Ctx &c) {
     cudaError_t e;
     const int64_t nh = c.bins.offset[4];          // degree classes 5-7
     c.e_nbig = nh;
     c.e_extra = nh + c.nnz / kChunkE + 1;         // item capacity
-    // layout: cnt[nh+1] | off[nh+1] | items[cap] (int2); grow-only
+    // layout: cnt[nh+1] | off[nh+1] | items[cap] (int2)
     const size_t bytes = sizeof(int32_t) * 2 * (size_t)(nh + 1) + sizeof(int2) * (size_t)c.e_extra + 16;
     if (bytes <= c.e_bytes) return cudaSuccess;
     if (c.e_pre) cudaFree(c.e_pre);
@@ -367,168 +479,12 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- light middle vertices
-// Vertices of degree < 128 (most of them, but a few percent of the probe
-// work): a group of kGL lanes per y, no hash table -- P+(y) is short and
-// sorted, so membership is a binary search that stays in L1.
-constexpr int kGL = 8;                         // lanes per light vertex
-constexpr int kXLL = 32;                       // P(y) positions per x-list pass
-constexpr int kQL = kGL * kUnrollE + kGL;      // hit queue per group
-
-
-template <bool COUNT>
-__global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
-    __shared__ longlong2 XLs[256 / kGL][kXLL];
-    __shared__ int2 Qs[256 / kGL][kQL];
-    WarpGroup<kGL> g;
-    const int gi = threadIdx.x / kGL;
-    const int lane = (int)g.lane;
-    longlong2 *XL = XLs[gi];
-    int2 *Q = Qs[gi];
-    const int k = a.k;
-    unsigned long long ntri = 0;
-    const int64_t gpb = blockDim.x / kGL;
-    const int64_t ngroups = (int64_t)gridDim.x * gpb;
-    for (int64_t y64 = ylo + blockIdx.x * gpb + gi; y64 < a.n; y64 += ngroups) {
-        const int32_t y = (int32_t)y64;
-        const int2 pcy = a.pc2[y];
-        const int py = pcy.x, pc = pcy.y;
-        if (py == 0 || pc == py) continue;
-        const int ly = a.lab[y];
-        const int64_t by = a.rowptr[y];
-        const int32_t *Py = a.pplus + by;
-        const double *Ay = a.amat + (int64_t)y * k;
-        U128 accy = u128_zero();
-        unsigned long long cnty = 0;
-        int qn = 0;
-        auto drain = [&](int upto) {
-            while (qn >= upto && qn > 0) {
-                const int take = qn < kGL ? qn : kGL;
-                const int b = qn - take;
-                if (lane < take) {
-                    const int2 e = Q[b + lane];
-                    accy = u128_add(accy, tri_terms<COUNT>(a, e.x, y, ly, Ay, e.y, cnty));
-                }
-                g.sync();
-                qn = b;
-            }
-        };
-        for (int i0 = 0; i0 < pc; i0 += kXLL) {
-            const int iend = min(pc, i0 + kXLL);
-            int nx = 0, total = 0;
-            for (int j0 = i0; j0 < iend; j0 += kGL) {
-                const int i = j0 + lane;
-                int32_t x = 0;
-                int64_t bx = 0;
-                int lenx = 0;
-                if (i < iend) {
-                    x = __ldg(a.pidx + by + i);
-                    const int2 pcx = a.pc2[x];
-                    const bool lower = pcx.y < pc || (pcx.y == pc && x < y);
-                    if (lower && pcx.x > 0 && (__ldg(a.lab + x) < k || ly < k)) {
-                        lenx = pcx.x;
-                        bx = a.rowptr[x];
-                    }
-                }
-                int incl = lenx;
-#pragma unroll
-                for (int o = 1; o < kGL; o <<= 1) {
-                    const int t = __shfl_up_sync(g.gmask, incl, o, kGL);
-                    if (lane >= o) incl += t;
-                }
-                int cnt;
-                const int r = g.rank(lenx > 0, &cnt);
-                if (lenx > 0) {
-                    const int e_end = total + incl;
-                    XL[nx + r] = make_longlong2(bx - (e_end - lenx), ((long long)x << 32) | (unsigned)e_end);
-                }
-                nx += cnt;
-                total += g.bcast(incl, kGL - 1);
-            }
-            g.sync();
-            if (total > 0) {
-                const int seg = (total + kGL - 1) / kGL;
-                const int t_beg = min(total, lane * seg), t_end = min(total, t_beg + seg);
-                int lo = 0, hi = nx;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if ((int)(XL[mid].y & 0xffffffff) <= t_beg) lo = mid + 1; else hi = mid;
-                }
-                int xi = lo, xe = 0;
-                int64_t xbase = 0;
-                int32_t xcur = 0;
-                if (t_beg < t_end) {
-                    const longlong2 e = XL[xi];
-                    xbase = e.x;
-                    xe = (int)(e.y & 0xffffffff);
-                    xcur = (int32_t)(e.y >> 32);
-                }
-                int t = t_beg;
-                for (int s0 = 0; s0 < seg; s0 += kUnrollE) {
-                    int32_t z[kUnrollE], xj[kUnrollE];
-#pragma unroll
-                    for (int u = 0; u < kUnrollE; u++) {
-                        z[u] = -1;
-                        xj[u] = xcur;
-                        if (t < t_end) {
-                            if (t >= xe) {
-                                const longlong2 e = XL[++xi];
-                                xbase = e.x;
-                                xe = (int)(e.y & 0xffffffff);
-                                xcur = (int32_t)(e.y >> 32);
-                                xj[u] = xcur;
-                            }
-                            z[u] = __ldg(a.pplus + xbase + t);
-                        }
-                        t++;
-                    }
-#pragma unroll
-                    for (int u = 0; u < kUnrollE; u++) {
-                        const bool hit = z[u] >= 0 && in_sorted(Py, py, z[u]);
-                        int cnt;
-                        const int r = g.rank(hit, &cnt);
-                        if (hit) Q[qn + r] = make_int2(xj[u], z[u]);
-                        qn += cnt;
-                        if (lane == 0) ntri += cnt;
-                    }
-                    g.sync();
-                    drain(kGL);
-                }
-            }
-            g.sync();
-        }
-        drain(1);
-        if (ly < k && y >= a.head_lo && y < a.head_hi) {
-            if constexpr (COUNT) {
-                cnty = g.sum(cnty);
-                if (lane == 0 && cnty) atomicAdd(a.n1 + y, cnty);
-            } else {
-                accy = g.sum(accy);
-                if (lane == 0 && (accy.lo | accy.hi)) acc_add(a, y, accy);
-            }
-        }
-        g.sync();
-    }
-    for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
-    if ((threadIdx.x & 31) == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
-}
-
 template <bool COUNT>
 static cudaError_t launch_e(Ctx &c) {
     CdeArgs a = cde_args(c);
     unsigned long long *ctr = c.scal + kScalCnt0;
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
-    const int64_t n_heavy = c.bins.offset[4];          // degree classes 5-7 (d >= 128)
-    // light middle vertices on a side stream, concurrently with the heavy ones
-    cudaEventRecord(c.ev_fork, c.stream);
-    cudaStreamWaitEvent(c.side[0], c.ev_fork, 0);
-    if (n_heavy < c.n) {
-        const int64_t groups = c.n - n_heavy;
-        const int64_t blocks = std::min<int64_t>((groups + 31) / 32, 148 * 8);
-        k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, c.side[0]>>>(a, n_heavy);
-        c.launches++;
-    }
-    cudaEventRecord(c.ev_join[0], c.side[0]);
+    const int64_t n_heavy = c.e_nbig;                 // degree classes 5-7 (d >= 128)
     EItems it{nullptr, nullptr};
     if (n_heavy > 0) {
         cudaError_t e = build_e_items(c, it);
@@ -544,12 +500,16 @@ static cudaError_t launch_e(Ctx &c) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase_e<COUNT>, kWarpsE * 32, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    const int grid = std::max(1, per_sm) * sms;
     if (n_heavy > 0) {
-        k_phase_e<COUNT><<<grid, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
+        k_phase_e<COUNT><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
         c.launches++;
     }
-    cudaStreamWaitEvent(c.stream, c.ev_join[0], 0);
+    if (n_heavy < c.n) {
+        const int64_t threads = c.n - n_heavy;
+        const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
+        k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, c.stream>>>(a, n_heavy);
+        c.launches++;
+    }
     return cudaGetLastError();
 }
 

@@ -53,6 +53,14 @@ struct __align__(16) VRec {
     uint8_t pad;
 };
 
+// Per-vertex G' record written by Phase C, gathered once per predecessor x by
+// Phase E: where P+(x) starts and how long P+(x) and P(x) are (one sector).
+struct __align__(16) PRec {
+    int x;             // |P+(u)| (orientation out-degree)
+    int y;             // |P(u)|
+    long long start;   // rowptr[u]: P(u) and P+(u) live at this offset
+};
+
 // Per (vertex, column) record read by the Type-II pull (Phase D).
 struct __align__(16) BQ {
     double B;          // sum_{v in P(w), col(v)=c} a_v(c), exact sum rounded once
@@ -112,7 +120,8 @@ struct Ctx {
     VRec *vrec = nullptr;        // n
     int32_t *pidx = nullptr;     // nnz, P(u) stored at rowptr[u] ...
     int32_t *pplus = nullptr;    // nnz, P+(u) (orientation) at rowptr[u] ...
-    int2 *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|}
+    double *wps = nullptr;       // nnz, a_u(c_z) for each z of P+(u), same positions
+    PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, rowptr[u]}
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQ *bq = nullptr;            // n*k
     unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)

@@ -13,9 +13,10 @@ struct CdeArgs {
     int32_t k;
     const double *__restrict__ amat;    // n*k cube roots a_v(c), row-major
     const VRec *__restrict__ vrec;
-    const int32_t *__restrict__ pidx;   // P(u) at rowptr[u]
+    int32_t *__restrict__ pidx;         // P(u) at rowptr[u]; after Phase C: P-(u) at its front
     int32_t *__restrict__ pplus;        // P+(u) at rowptr[u]
-    int2 *__restrict__ pc2;             // {|P+(u)|, |P(u)|}
+    double *__restrict__ wps;           // a_u(c_z) beside each z of P+(u)
+    PRec *__restrict__ pc2;             // {|P+(u)|, |P(u)|, rowptr[u]}
     BQ *__restrict__ bq;                // column-major: bq[c*n + w]
     unsigned long long *__restrict__ acc1;  // 3 limbs per vertex (Type-I)
     unsigned long long *__restrict__ n1;    // Type-I triad counts (COUNT mode)
@@ -30,7 +31,7 @@ struct CdeArgs {
 inline CdeArgs cde_args(Ctx &c) {
     CdeArgs a;
     a.rowptr = c.rowptr; a.vlo = 0; a.nverts = 0; a.n = c.n; a.k = c.k;
-    a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pplus = c.pplus; a.pc2 = c.pc2;
+    a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2;
     a.bq = c.bq; a.acc1 = c.acc1; a.n1 = c.n1; a.score = c.score; a.scal = c.scal;
     a.perm = c.perm; a.lab = c.lab;
     a.any_wide = (double)c.d_max * (double)c.d_max >= wide_bound(c.k);
