@@ -51,9 +51,10 @@ typedef struct {
     int64_t m;                /* |E| undirected = nnz / 2                       */
     int64_t n_border;         /* |V_b| over all communities              */
     int64_t n_pred_entries;   /* sum over u of |P(u)| = |E_b|           */
-    int64_t n_triangles;      /* triangles of G' (3 distinct communities) with a
-                                 target among their two lowest-ranked vertices
-                                 (the ones that can carry Type-I terms)         */
+    int64_t n_triangles;      /* triangles of G' (3 distinct communities) with at
+                                 least two target vertices: the ones that carry
+                                 Type-I terms (a term needs a target head and a
+                                 target column among the other two)             */
     double omega_max;         /* max weight over all cells (C-7)  */
     float ms_phase[8];        /* [0] Phase A border/histogram/weights/G' lists
                                  [1] Phase C B-table + orientation

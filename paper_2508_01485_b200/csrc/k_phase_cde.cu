@@ -17,6 +17,18 @@
 namespace rs {
 
 
+// -1 padding of the two runs of P+(w) to multiples of 4 (aligned probes)
+__device__ __forceinline__ void dense_pads(const CdeArgs &a, int64_t dw, int cap, int t, int no, int lane, int gs) {
+    for (int i = lane; i < 8; i += gs) {
+        const int64_t at = i < 4 ? (t + i < ceil4(t) ? dw + t + i : -1)
+                                 : (no + (i - 4) < ceil4(no) ? dw + cap - 1 - (no + (i - 4)) : -1);
+        if (at >= 0) {
+            a.pd[at] = -1;
+            a.wd[at] = 0.0;
+        }
+    }
+}
+
 // ============================================================================
 // Phase C: B_w[c] for every column, Q_w[c] = a_w(c)^2, and the degree
 // orientation of G' (P+(w): neighbours of larger (|P|, id)) for Phase E.
@@ -30,11 +42,13 @@ __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &
     U128 B[8];
 #pragma unroll
     for (int c = 0; c < 8; c++) B[c] = u128_zero();
-    // w's own cube-root row: a_w(c_v) for every P+ entry v goes beside v (wps)
+    // w's own cube-root row: a_w(c_v) for every P+ entry v goes beside v (wd)
+    const int64_t dw = a.dpos[w];
+    const int cap = dcap(pc);
     double arow[8];
 #pragma unroll
     for (int c = 0; c < 8; c++) arow[c] = c < k ? __ldg(a.amat + w * k + c) : 0.0;
-    int ppc = 0, pmc = 0;
+    int ppc = 0, ppn = 0, pmc = 0;   // |P+_T|, |P+ \ P+_T|, |P-| so far
     for (int base = 0; base < pc; base += GR::size * U) {
         int32_t v[U];
         VRec rv[U];
@@ -56,14 +70,18 @@ __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &
                 if (rv[j].lab == c) B[c] = u128_add(B[c], q);
             if (base + j * GR::size < pc) {
                 const bool plus = v[j] >= 0 && (rv[j].pcnt > pc || (rv[j].pcnt == pc && v[j] > (int32_t)w));
-                int tot;
-                const int r = g.rank(plus, &tot);
+                const bool tgt = rv[j].lab < k;
+                int tot, totn;
+                const int r = g.rank(plus && tgt, &tot);
+                const int rn = g.rank(plus && !tgt, &totn);
                 if (plus) {
                     double wv = 0.0;
 #pragma unroll
                     for (int c = 0; c < 8; c++) wv = (rv[j].lab == c) ? arow[c] : wv;
-                    a.pplus[beg + ppc + r] = v[j];
-                    a.wps[beg + ppc + r] = wv;
+                    // target run ascending from the front, the rest descending from the back
+                    const int64_t at = tgt ? dw + ppc + r : dw + cap - 1 - (ppn + rn);
+                    a.pd[at] = v[j];
+                    a.wd[at] = rv[j].wide ? -wv : wv;   // sign bit: v needs 3 limbs
                 }
                 // P-(w) compacted in place to the front of w's P list (every position
                 // written has been read: the count of minus entries trails the reads)
@@ -71,14 +89,16 @@ __device__ __forceinline__ void phase_c_vertex(const CdeArgs &a, int64_t w, GR &
                 const int rm = g.rank(v[j] >= 0 && !plus, &totm);
                 if (v[j] >= 0 && !plus) a.pidx[beg + pmc + rm] = v[j];
                 ppc += tot;
+                ppn += totn;
                 pmc += totm;
             }
         }
     }
 #pragma unroll
     for (int c = 0; c < 8; c++) B[c] = g.sum(B[c]);
-    if (g.lane == 0) { PRec r; r.x = ppc; r.y = pc; r.start = beg; a.pc2[w] = r; }
+    if (g.lane == 0) { PRec r; r.x = ppc + ppn; r.y = pc; r.start = dw | ((long long)ppc << kPrShift); a.pc2[w] = r; }
     if (pc == 0) return;   // w is in no P(u): its B/Q row is never read
+    dense_pads(a, dw, cap, ppc, ppn, (int)g.lane, GR::size);
     for (int c = g.lane; c < k; c += GR::size) {
         U128 Bc = u128_zero();
 #pragma unroll
@@ -98,9 +118,11 @@ __device__ __forceinline__ void phase_c_vertex_smem(const CdeArgs &a, int64_t w,
     const int pc = rw.pcnt;
     const int64_t beg = a.rowptr[w];
     const int k = a.k;
+    const int64_t dw = a.dpos[w];
+    const int cap = dcap(pc);
     for (int c = g.lane; c < 3 * k; c += GR::size) sB[c] = 0ull;
     g.sync();
-    int ppc = 0, pmc = 0;
+    int ppc = 0, ppn = 0, pmc = 0;
     for (int base = 0; base < pc; base += GR::size) {
         const int i = base + (int)g.lane;
         const bool valid = i < pc;
@@ -110,21 +132,27 @@ __device__ __forceinline__ void phase_c_vertex_smem(const CdeArgs &a, int64_t w,
         if (valid) { v = a.pidx[beg + i]; rv = a.vrec[v]; }
         if (valid && rv.lab < k) fx_red3(sB + 3 * rv.lab, fx_quantize(rv.a_self));
         const bool plus = valid && (rv.pcnt > pc || (rv.pcnt == pc && v > (int32_t)w));
-        int tot;
-        const int r = g.rank(plus, &tot);
+        const bool tgt = rv.lab < k;
+        int tot, totn;
+        const int r = g.rank(plus && tgt, &tot);
+        const int rn = g.rank(plus && !tgt, &totn);
         if (plus) {
-            a.pplus[beg + ppc + r] = v;
-            a.wps[beg + ppc + r] = rv.lab < k ? __ldg(a.amat + w * k + rv.lab) : 0.0;
+            const int64_t at = tgt ? dw + ppc + r : dw + cap - 1 - (ppn + rn);
+            const double wv = tgt ? __ldg(a.amat + w * k + rv.lab) : 0.0;
+            a.pd[at] = v;
+            a.wd[at] = rv.wide ? -wv : wv;
         }
         int totm;
         const int rm = g.rank(valid && !plus, &totm);
         if (valid && !plus) a.pidx[beg + pmc + rm] = v;
         ppc += tot;
+        ppn += totn;
         pmc += totm;
     }
     g.sync();
-    if (g.lane == 0) { PRec r; r.x = ppc; r.y = pc; r.start = beg; a.pc2[w] = r; }
+    if (g.lane == 0) { PRec r; r.x = ppc + ppn; r.y = pc; r.start = dw | ((long long)ppc << kPrShift); a.pc2[w] = r; }
     if (pc > 0) {
+        dense_pads(a, dw, cap, ppc, ppn, (int)g.lane, GR::size);
         for (int c = g.lane; c < k; c += GR::size) {
             const double aw = a.amat[w * k + c];
             BQ r;
@@ -172,7 +200,10 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const int cu = ru.lab;
     const double au = ru.a_self;
     const int pc = ru.pcnt;
-    const int pm = pc - a.pc2[u].x;            // P(u) = P-(u) (front of pidx) + P+(u) (pplus)
+    const PRec pr = a.pc2[u];
+    const int pm = pc - pr.x;                  // P(u) = P-(u) (front of pidx) + P+(u) (pplus, two runs)
+    const int pt = pm + pr_plus_t(pr);         // [pm, pt): target run; [pt, pc): the other run
+    const int64_t dw = pr_start(pr), de = dw + dcap(pc) - 1 + pt;   // the other run: de - i, descending
     const int64_t beg = a.rowptr[u];
     const int64_t d = a.rowptr[u + 1] - beg;
     U128 S = u128_zero();
@@ -182,7 +213,8 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
-            w[j] = i < pm ? __ldg(a.pidx + beg + i) : (i < pc ? __ldg(a.pplus + beg + i - pm) : -1);
+            w[j] = i < pm ? __ldg(a.pidx + beg + i)
+                          : (i < pt ? __ldg(a.pd + dw + i - pm) : (i < pc ? __ldg(a.pd + de - i) : -1));
         }
 #pragma unroll
         for (int j = 0; j < U; j++)

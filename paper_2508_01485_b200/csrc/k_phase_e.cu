@@ -40,7 +40,7 @@ constexpr int kPyCap = 256;      // P+(y) kept in shared memory (sorted copy + l
 constexpr int kBmWords = 128;    // 4096-bit membership filter of P+(y)
 constexpr int kPiece = 4;        // consecutive P+(x) entries one lane probes per round
 constexpr int kQCapE = 160;      // candidate queue (31 + 32 * kPiece < 160)
-constexpr int kPieceMap = 512;   // piece -> slot map capacity (else binary search)
+constexpr int kPsWords = 128;    // piece-start bitmap: items of at most 4096 pieces (else binary search)
 constexpr int kSlotMaxHits = 4096;   // smem limbs of an x slot take at most this many terms
 constexpr int kWarpsE = 8;
 
@@ -73,17 +73,28 @@ __device__ __forceinline__ double amat_at(const CdeArgs &a, int32_t v, int c) {
 
 __device__ __forceinline__ bool owned(const CdeArgs &a, int64_t h) { return h >= a.head_lo && h < a.head_hi; }
 
-// global exact accumulation of a head's (partial) Type-I sum
-__device__ __forceinline__ void acc_add(const CdeArgs &a, int32_t h, const U128 &q) {
+// global exact accumulation of a head's (partial) Type-I sum; `wide` is the
+// head's 3-limb flag (VRec::wide), carried with the head's record
+__device__ __forceinline__ void acc_add(const CdeArgs &a, int32_t h, const U128 &q, bool wide) {
     unsigned long long *acc = a.acc1 + 3 * (int64_t)h;
-    if (a.any_wide && a.vrec[h].wide) fx_red3(acc, q);
+    if (wide) fx_red3(acc, q);
     else fx_red2(acc, q);
+}
+
+// position of z in the DESCENDING list p[0, len), or -1
+__device__ __forceinline__ int find_desc_g(const int32_t *p, int len, int32_t z) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(p + mid) > z) lo = mid + 1; else hi = mid;
+    }
+    return (lo < len && __ldg(p + lo) == z) ? lo : -1;
 }
 
 // shared-memory per-item accumulator: four 20-bit limbs of q (< 2^80) added with
 // native 32-bit shared atomics (64-bit shared atomics are CAS loops); exact
 // while a slot receives fewer than 2^12 terms per item (x slots with longer
-// P+(x) and z positions beyond kPyCap go straight to the global limbs).
+// P+(x) go straight to the global limbs).
 __device__ __forceinline__ void smem_red4(uint32_t *acc4, const U128 &q) {
     const uint32_t l0 = (uint32_t)(q.lo & 0xFFFFFull), l1 = (uint32_t)((q.lo >> 20) & 0xFFFFFull);
     const uint32_t l2 = (uint32_t)((q.lo >> 40) & 0xFFFFFull), l3 = (uint32_t)((q.lo >> 60) | (q.hi << 4));
@@ -100,21 +111,30 @@ __device__ __forceinline__ U128 from4(const uint32_t *acc4) {
     return s;
 }
 
+// a work item: positions [64 chunk, 64 chunk + 64) of P-(y), with y's record
+struct __align__(16) EItem {
+    int64_t by;            // start of y's slot (rowptr[y]): P-(y) in pidx
+    int64_t dy;            // y's P+ region | |P+_T(y)| << 40
+    int32_t y, chunk;
+    int32_t pyl;           // |P+(y)| | lab(y) << 24
+    int32_t pm;            // |P-(y)|
+};
 struct EItems {
-    const int2 *items;     // {y, chunk} work items of the heavy middle vertices, heaviest first
+    const EItem *items;    // work items of the heavy middle vertices, heaviest first
     const int32_t *total;  // number of items (device scalar, written by the item scan)
 };
 
 struct ESmem {             // one warp's shared memory
     uint32_t bm[kBmWords];
-    int32_t py[kPyCap];
-    longlong2 xl[kChunkE];  // {P+(x) start, (x << 32) | (lab(x) << 24) | |P+(x)|}
-    double2 xw[kChunkE];    // {a_x(c_y), a_y(c_x)}
+    int32_t py[kPyCap];     // P+(y): target run, then the other run, each ascending
+    longlong2 xl[kChunkE];  // {x's region start, (wide << 63) | (x << 32) | (lab(x) << 24) | |P+_T(x)|}
+    int2 xn[kChunkE];       // {offset of the padded other run of P+(x), its probed length}
+    double axy[kChunkE];    // a_x(c_y)
     uint32_t xa[4 * kChunkE];
     int32_t pe[kChunkE];    // end of each list's pieces
-    int2 q[kQCapE];         // candidates {x slot, offset in P+(x)}
-    uint8_t pslot[kPieceMap];   // piece -> x slot (items with at most kPieceMap pieces)
-    uint8_t zl[kPyCap];         // label of z in P+(y)
+    int2 q[kQCapE];         // candidates {(offset of z in x's lists << 6) | x slot, z}
+    uint32_t ps[kPsWords];  // bit p: piece p is the first piece of a list
+    uint8_t zl[kPyCap];     // label of z in the target run of P+(y)
 };
 
 __host__ __device__ constexpr size_t e_stride_bytes(int k) {
@@ -122,7 +142,7 @@ __host__ __device__ constexpr size_t e_stride_bytes(int k) {
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, unsigned long long *queue_ctr) {
+__global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems it, unsigned long long *queue_ctr) {
     extern __shared__ __align__(16) unsigned char e_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k;
@@ -132,65 +152,86 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
     unsigned long long ntri = 0;
     const unsigned long long n_items = (unsigned long long)*it.total;
 
+    unsigned long long qnext = 0;
+    if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);
     for (;;) {
-        unsigned long long qi = 0;
-        if (lane == 0) qi = atomicAdd(queue_ctr, 1ull);
-        qi = __shfl_sync(0xffffffffu, qi, 0);
+        const unsigned long long qi = __shfl_sync(0xffffffffu, qnext, 0);
         if (qi >= n_items) break;
-        const int2 itm = it.items[qi];
-        const int32_t y = itm.x;
-        const PRec pcy = a.pc2[y];
-        const int py = pcy.x, pm = pcy.y - pcy.x;   // |P+(y)|, |P-(y)| (P-(y) = front of pidx)
-        const int start = itm.y * kChunkE;
-        if (py == 0 || start >= pm) continue;       // no z above y, or an empty chunk
-        const int end = min(pm, start + kChunkE);
-        const int ly = a.lab[y];
-        const int64_t by = pcy.start;
-        const bool local = py <= kPyCap;            // P+(y) copy + accumulators in smem
+        if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);   // next item, consumed at the loop top
+        const EItem itm = it.items[qi];
+        const int32_t y = itm.y;
+        const int py = itm.pyl & 0xFFFFFF, ly = (int)((uint32_t)itm.pyl >> 24);
+        const int pyt = (int)(itm.dy >> kPrShift);
+        const int64_t dy = itm.dy & ((1ll << kPrShift) - 1);
+        const int pcy = py + itm.pm;                // |P(y)|
+        const int start = itm.chunk * kChunkE, end = min(itm.pm, start + kChunkE);
+        const int64_t by = itm.by;
+        const bool ty = ly < k;
+        const bool local = py <= kPyCap;            // sorted copy of P+(y) in smem
+        // setup: the loads of P-(y) (x list), P+(y) (filter) and y's weights are
+        // independent and issued together; then the x records, lab(z), a_x(c_y)
+        int32_t xv[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int i = start + 32 * h + lane;
+            xv[h] = i < end ? __ldg(a.pidx + by + i) : -1;   // x in P-(y): lower rank than y
+        }
+        // i-th entry of P+(y) in ascending order within its run (the other run is
+        // stored descending at the end of y's region)
+        const int64_t dye = dy + dcap(pcy) - 1;
+        auto py_at = [&](int i) -> int64_t { return i < pyt ? dy + i : dye - (i - pyt); };
+        const int32_t z0 = lane < py ? __ldg(a.pd + py_at(lane)) : -1;
+        const double ay0 = lane < k ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
+        PRec pcx[2];
+        int lxv[2];
+        double axy[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            pcx[h] = xv[h] >= 0 ? a.pc2[xv[h]] : PRec{0, 0, 0};
+            lxv[h] = xv[h] >= 0 ? (int)__ldg(a.lab + xv[h]) : kOther;
+            axy[h] = (xv[h] >= 0 && ty) ? __ldg(a.amat + (int64_t)xv[h] * k + ly) : 0.0;
+        }
+        const int lz0 = (z0 >= 0 && local && lane < pyt) ? (int)__ldg(a.lab + z0) : kOther;
         for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
-        for (int c = lane; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
+        if (lane < k) Ay[lane] = ay0;
+        for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
         __syncwarp();
         for (int i = lane; i < py; i += 32) {
-            const int32_t z = __ldg(a.pplus + by + i);
+            const int32_t z = i == lane ? z0 : __ldg(a.pd + py_at(i));
             const uint32_t b = bm_bit(z);
             atomicOr(&S.bm[b >> 5], 1u << (b & 31));
             if (local) {
                 S.py[i] = z;
-                const int lzi = __ldg(a.lab + z);
-                S.zl[i] = (uint8_t)lzi;
+                if (i < pyt) S.zl[i] = (uint8_t)(i == lane ? lz0 : __ldg(a.lab + z));
             }
         }
-        // the item's predecessors x (lower rank, non-empty P+(x), a target among
-        // x and y), each P+(x) cut into pieces numbered across the list
+        // the item's predecessors x. A triangle carries a term only if two of its
+        // vertices are targets: with both x and y targets every z of P+(x) is
+        // probed, with one of them only the target run of P+(x), with neither
+        // nothing. Each probed list is cut into pieces numbered across the item.
         int nx = 0, npieces = 0;
-        for (int i0 = start; i0 < end; i0 += 32) {
-            const int i = i0 + lane;
-            int32_t x = 0;
-            int64_t bx = 0;
-            int lenx = 0, lx = kOther;
-            if (i < end) {
-                x = __ldg(a.pidx + by + i);              // x in P-(y): lower rank than y
-                const PRec pcx = a.pc2[x];
-                if (pcx.x > 0) {
-                    lx = __ldg(a.lab + x);
-                    if (lx < k || ly < k) {
-                        lenx = pcx.x;
-                        bx = pcx.start;
-                    }
-                }
-            }
-            const int pieces = (lenx + kPiece - 1) / kPiece;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int lx = lxv[h];
+            const bool tx = lx < k;
+            const int t = (tx || ty) ? pr_plus_t(pcx[h]) : 0;
+            const int lenn = (tx && ty) ? pcx[h].x - pr_plus_t(pcx[h]) : 0;
+            const bool use = t + lenn > 0;
+            const int pieces = ceil4(t) / kPiece + ceil4(lenn) / kPiece;
             int incl = pieces;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
             }
-            const unsigned has = __ballot_sync(0xffffffffu, lenx > 0);
-            if (lenx > 0) {
+            const unsigned has = __ballot_sync(0xffffffffu, use);
+            if (use) {
                 const int slot = nx + __popc(has & ((1u << lane) - 1u));
-                S.xl[slot] = make_longlong2(bx, ((long long)x << 32) | ((long long)(lx & 0xFF) << 24) | lenx);
-                S.xw[slot] = make_double2(ly < k ? __ldg(a.amat + (int64_t)x * k + ly) : 0.0, lx < k ? Ay[lx] : 0.0);
+                const long long wide = is_wide(a, pcx[h].y) ? (1ll << 63) : 0ll;
+                S.xl[slot] = make_longlong2(pr_start(pcx[h]),
+                                            wide | ((long long)xv[h] << 32) | ((long long)(lx & 0xFF) << 24) | t);
+                S.xn[slot] = make_int2(dcap(pcx[h].y) - ceil4(lenn), lenn);
+                S.axy[slot] = axy[h];
                 S.xa[4 * slot] = 0u;
                 S.xa[4 * slot + 1] = 0u;
                 S.xa[4 * slot + 2] = 0u;
@@ -205,40 +246,84 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
 #ifdef RS_EXP_SETUP_ONLY
         if (npieces >= 0) continue;
 #endif
-        const bool mapped = npieces <= kPieceMap;
+        // piece -> list: bit p of S.ps marks the first piece of a list, so the list
+        // of piece p0 + lane is (lists started before p0) + popc(word & lanes <= lane) - 1
+        const bool mapped = npieces <= 32 * kPsWords;
         if (mapped) {
-            for (int s = lane; s < nx; s += 32)
-                for (int p = s ? S.pe[s - 1] : 0; p < S.pe[s]; p++) S.pslot[p] = (uint8_t)s;
+            for (int w = lane; w < ((npieces + 31) >> 5); w += 32) S.ps[w] = 0u;
+            __syncwarp();
+            for (int s = lane; s < nx; s += 32) {
+                const int st = s ? S.pe[s - 1] : 0;
+                atomicOr(&S.ps[st >> 5], 1u << (st & 31));
+            }
             __syncwarp();
         }
+        int lists_before = 0;
+        auto fetch = [&](int p0, int32_t (&z)[kPiece], int &tag) {
+            const int p = p0 + lane;
+            int slot;
+            if (mapped) {
+                const uint32_t wd = S.ps[p0 >> 5];
+                slot = lists_before + __popc(wd & (0xFFFFFFFFu >> (31 - lane))) - 1;
+                lists_before += __popc(wd);
+            } else {
+                int lo = 0, hi = nx;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.pe[mid] <= p) lo = mid + 1; else hi = mid;
+                }
+                slot = lo;
+            }
+            int off = 0;
+            if (p < npieces) {
+                const longlong2 xe = S.xl[slot];
+                const int t = (int)(xe.y & 0xFFFFFF);
+                const int q = p - (slot ? S.pe[slot - 1] : 0);   // piece within the list
+                const int qt = ceil4(t) / kPiece;
+                off = q < qt ? q * kPiece : S.xn[slot].x + (q - qt) * kPiece;
+                // one aligned 16-byte load; padding entries are -1
+                const int4 v = __ldg(reinterpret_cast<const int4 *>(a.pd + xe.x + off));
+                z[0] = v.x; z[1] = v.y; z[2] = v.z; z[3] = v.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < kPiece; j++) z[j] = -1;
+            }
+            tag = (off << 6) | (slot & 63);
+        };
 
         U128 accy = u128_zero();
         unsigned long long cnty = 0;
         int qn = 0;
-        // verify candidates (x slot, offset) 32 at a time and add the triangle's terms
+        // verify candidates 32 at a time and add the triangle's terms
         auto drain = [&](int upto) {
             while (qn >= upto && qn > 0) {
                 const int take = qn < 32 ? qn : 32;
                 const int b0 = qn - take;
                 if (lane < take) {
                     const int2 e = S.q[b0 + lane];
-                    const longlong2 xe = S.xl[e.x];
-                    const int32_t z = __ldg(a.pplus + xe.x + e.y);
-                    const int iz = local ? find_sorted(S.py, py, z) : find_sorted_g(a.pplus + by, py, z);
+                    const int slot = e.x & 63, off = e.x >> 6;
+                    const int32_t z = e.y;
+                    const longlong2 xe = S.xl[slot];
+                    const bool zt = off < (int)(xe.y & 0xFFFFFF);   // z from the target run of P+(x)
+                    int iz;
+                    if (local) iz = zt ? find_sorted(S.py, pyt, z) : find_sorted(S.py + pyt, py - pyt, z);
+                    else iz = zt ? find_sorted_g(a.pd + dy, pyt, z) : find_desc_g(a.pd + dye + 1 - (py - pyt), py - pyt, z);
                     if (iz >= 0) {
                         ntri++;
-                        const int32_t x = (int32_t)(xe.y >> 32);
+                        const int32_t x = (int32_t)((xe.y >> 32) & 0x7FFFFFFF);
                         const int lx = (int)((xe.y >> 24) & 0xFF);
-                        const int lz = local ? (int)S.zl[iz] : (int)__ldg(a.lab + z);
+                        const int lz = zt ? (local ? (int)S.zl[iz] : (int)__ldg(a.lab + z)) : (int)kOther;
                         if constexpr (COUNT) {
-                            const bool tx = lx < k, ty = ly < k, tz = lz < k;
+                            const bool tx = lx < k, tz = lz < k;
                             if (tx && (ty + tz) && owned(a, x)) atomicAdd(a.n1 + x, (unsigned long long)(ty + tz));
                             if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
                             cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
                         } else {
-                            const double2 w = S.xw[e.x];
-                            const double Axly = w.x, Aylx = w.y;
-                            const double Axlz = __ldg(a.wps + xe.x + e.y);   // a_x(c_z), stored by Phase C
+                            const double wr = __ldg(a.wd + xe.x + off);     // a_x(c_z), stored by Phase C
+                            const bool zwide = __double_as_longlong(wr) < 0;  // its sign: z's 3-limb flag
+                            const double Axlz = fabs(wr);
+                            const double Axly = S.axy[slot];
+                            const double Aylx = lx < k ? Ay[lx] : 0.0;
                             const double Aylz = lz < k ? Ay[lz] : 0.0;
                             const double Azlx = amat_at(a, z, lx);
                             const double Azly = amat_at(a, z, ly);
@@ -246,12 +331,11 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
                             const double tz = Axlz * Aylz * (Aylx + Axly);
                             accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
                             if (tx > 0.0) {
-                                if ((int)(xe.y & 0xFFFFFF) <= kSlotMaxHits) smem_red4(S.xa + 4 * e.x, fx_quantize(tx));
-                                else if (owned(a, x)) acc_add(a, x, fx_quantize(tx));
+                                const int lenx = ceil4((int)(xe.y & 0xFFFFFF)) + S.xn[slot].y;
+                                if (lenx <= kSlotMaxHits) smem_red4(S.xa + 4 * slot, fx_quantize(tx));
+                                else if (owned(a, x)) acc_add(a, x, fx_quantize(tx), xe.y < 0);
                             }
-                            if (tz > 0.0) {
-                                if (owned(a, z)) acc_add(a, z, fx_quantize(tz));   // z: hub-ish, hot in L2
-                            }
+                            if (tz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(tz), zwide);
                         }
                     }
                 }
@@ -260,37 +344,25 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
             }
         };
 
-        // one piece per lane per round; the round's filter candidates packed by one scan
+        // one piece per lane per round, the next round's loads in flight while this
+        // round is filtered; filter candidates packed by one warp scan
+        int32_t zc[kPiece];
+        int tagc;
+        fetch(0, zc, tagc);
         for (int p0 = 0; p0 < npieces; p0 += 32) {
-            const int p = p0 + lane;
-            int slot = 0, off = 0, cnt = 0;
-            int64_t pb = 0;
-            if (p < npieces) {
-                int lo;                                // list holding piece p
-                if (mapped) {
-                    lo = S.pslot[p];
-                } else {
-                    lo = 0;
-                    int hi = nx;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (S.pe[mid] <= p) lo = mid + 1; else hi = mid;
-                    }
-                }
-                slot = lo;
-                const longlong2 xe = S.xl[lo];
-                off = (p - (lo ? S.pe[lo - 1] : 0)) * kPiece;
-                cnt = min(kPiece, (int)(xe.y & 0xFFFFFF) - off);
-                pb = xe.x + off;
-            }
-            int32_t z[kPiece];
+            int32_t zn[kPiece];
+            int tagn = 0;
+            if (p0 + 32 < npieces) {
+                fetch(p0 + 32, zn, tagn);
+            } else {
 #pragma unroll
-            for (int j = 0; j < kPiece; j++) z[j] = j < cnt ? __ldg(a.pplus + pb + j) : -1;
+                for (int j = 0; j < kPiece; j++) zn[j] = -1;
+            }
             unsigned m = 0;
 #pragma unroll
             for (int j = 0; j < kPiece; j++) {
-                const uint32_t b = bm_bit(z[j]);
-                if (z[j] >= 0 && ((S.bm[b >> 5] >> (b & 31)) & 1u)) m |= 1u << j;
+                const uint32_t b = bm_bit(zc[j]);
+                if (zc[j] >= 0 && ((S.bm[b >> 5] >> (b & 31)) & 1u)) m |= 1u << j;
             }
             const int npos = __popc(m);
             int incl = npos;
@@ -302,13 +374,16 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
             int w = qn + incl - npos;
 #pragma unroll
             for (int j = 0; j < kPiece; j++)
-                if ((m >> j) & 1u) S.q[w++] = make_int2(slot, off + j);
+                if ((m >> j) & 1u) S.q[w++] = make_int2(tagc + (j << 6), zc[j]);
             qn += __shfl_sync(0xffffffffu, incl, 31);
 #ifdef RS_EXP_NO_DRAIN
             qn = 0;
 #endif
             __syncwarp();
             drain(32);
+#pragma unroll
+            for (int j = 0; j < kPiece; j++) zc[j] = zn[j];
+            tagc = tagn;
         }
         drain(1);
         __syncwarp();
@@ -316,11 +391,12 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
         if constexpr (!COUNT) {
             for (int s = lane; s < nx; s += 32) {
                 const uint32_t *l = S.xa + 4 * s;
-                const int32_t x = (int32_t)(S.xl[s].y >> 32);
-                if ((l[0] | l[1] | l[2] | l[3]) && owned(a, x)) acc_add(a, x, from4(l));
+                const longlong2 xe = S.xl[s];
+                const int32_t x = (int32_t)((xe.y >> 32) & 0x7FFFFFFF);
+                if ((l[0] | l[1] | l[2] | l[3]) && owned(a, x)) acc_add(a, x, from4(l), xe.y < 0);
             }
         }
-        if (ly < k && owned(a, y)) {
+        if (ty && owned(a, y)) {
             if constexpr (COUNT) {
                 for (int o = 16; o > 0; o >>= 1) cnty += __shfl_xor_sync(0xffffffffu, cnty, o);
                 if (lane == 0 && cnty) atomicAdd(a.n1 + y, cnty);
@@ -329,7 +405,7 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
                     const U128 w{__shfl_xor_sync(0xffffffffu, accy.lo, o), __shfl_xor_sync(0xffffffffu, accy.hi, o)};
                     accy = u128_add(accy, w);
                 }
-                if (lane == 0 && (accy.lo | accy.hi)) acc_add(a, y, accy);
+                if (lane == 0 && (accy.lo | accy.hi)) acc_add(a, y, accy, is_wide(a, pcy));
             }
         }
         __syncwarp();
@@ -339,87 +415,121 @@ __global__ void __launch_bounds__(kWarpsE * 32) k_phase_e(CdeArgs a, EItems it, 
 }
 
 // ---------------------------------------------------------------- light middle vertices
-// Vertices of degree < 128 (most of them, ~5% of the probe work): one thread
-// per y; P(y), P+(y) and the P+(x) are short and sorted, so each x in P-(y)
-// is intersected with P+(y) by a two-pointer merge in L1. x's terms gather in
-// a register while its list is merged (one RED per x).
+// Vertices of degree < 128 (most of them, ~5% of the probe work). A warp takes
+// 32 consecutive y; their (y, x in P-(y)) pairs are numbered by one warp scan
+// and dealt to the lanes, so a lane's work is one pair, not one vertex. The
+// runs of P+(x) and P+(y) are short and sorted: two-pointer merges in L1 (the
+// target runs; the other runs too when x and y are both targets). Each pair
+// adds its x and y terms with one RED each (z terms per triangle).
 template <bool COUNT>
 __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
     const int k = a.k;
+    const int lane = threadIdx.x & 31;
     unsigned long long ntri = 0;
-    for (int64_t y64 = ylo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y64 < a.n;
-         y64 += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t y = (int32_t)y64;
-        const PRec pcy = a.pc2[y];
-        const int py = pcy.x, pm = pcy.y - pcy.x;
-        if (py == 0 || pm == 0) continue;
-        const int ly = a.lab[y];
-        const int64_t by = pcy.start;
-        const int32_t *Py = a.pplus + by;
-        const double *Wy = a.wps + by;              // a_y(c_z) beside z in P+(y)
-        U128 accy = u128_zero();
-        unsigned long long cnty = 0;
-        for (int i = 0; i < pm; i++) {
-            const int32_t x = __ldg(a.pidx + by + i);   // P-(y): lower rank than y
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t y0 = ylo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; y0 < a.n;
+         y0 += nwarps * 32) {
+        const int64_t yl = y0 + lane;
+        PRec pcl{0, 0, 0};
+        int64_t rpl = 0;
+        if (yl < a.n) {
+            pcl = a.pc2[yl];
+            rpl = a.rowptr[yl];
+        }
+        const int cnt = pcl.x > 0 ? pcl.y - pcl.x : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int q0 = 0; q0 < total; q0 += 32) {
+            const int q = q0 + lane;
+            // owner lane j of pair q: the first lane whose inclusive count exceeds q
+            int j = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, j + s - 1);
+                if (v <= q) j += s;
+            }
+            const int inc_j = __shfl_sync(0xffffffffu, incl, j);
+            const int cnt_j = __shfl_sync(0xffffffffu, cnt, j);
+            PRec pcy;
+            pcy.x = __shfl_sync(0xffffffffu, pcl.x, j);
+            pcy.y = __shfl_sync(0xffffffffu, pcl.y, j);
+            pcy.start = __shfl_sync(0xffffffffu, pcl.start, j);
+            const int64_t by = __shfl_sync(0xffffffffu, rpl, j);
+            if (q >= total) continue;
+            const int i = q - (inc_j - cnt_j);
+            const int32_t y = (int32_t)(y0 + j);
+            const int32_t x = __ldg(a.pidx + by + i);    // P-(y): lower rank than y
             const PRec pcx = a.pc2[x];
             if (pcx.x == 0) continue;
-            const int lx = __ldg(a.lab + x);
-            if (lx >= k && ly >= k) continue;
-            const int64_t bx = pcx.start;
-            const int32_t *Px = a.pplus + bx;
+            const int lx = __ldg(a.lab + x), ly = __ldg(a.lab + y);
+            const bool tx = lx < k, ty = ly < k;
+            if (!tx && !ty) continue;
+            const int64_t bx = pr_start(pcx), dy = pr_start(pcy);
             const double Axly = amat_at(a, x, ly), Aylx = amat_at(a, y, lx);
-            U128 accx = u128_zero();
-            unsigned long long cntx = 0;
-            int ix = 0, iy = 0;
-            int32_t zx = __ldg(Px), zy = __ldg(Py);
-            while (true) {
-                if (zx == zy) {
-                    ntri++;
-                    const int32_t z = zx;
-                    const int lz = __ldg(a.lab + z);
-                    if constexpr (COUNT) {
-                        const bool tx = lx < k, ty = ly < k, tz = lz < k;
-                        cntx += tx ? (unsigned long long)(ty + tz) : 0ull;
-                        if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
-                        cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
+            U128 accx = u128_zero(), accy = u128_zero();
+            unsigned long long cntx = 0, cnty = 0;
+            // merge of two runs walked with step s (ids ascending)
+            auto merge = [&](int64_t ix, int nxr, int64_t iy, int nyr, int s, bool run_t) {
+                if (nxr == 0 || nyr == 0) return;
+                const int64_t ex = ix + (int64_t)s * nxr, ey = iy + (int64_t)s * nyr;
+                int32_t zx = __ldg(a.pd + ix), zy = __ldg(a.pd + iy);
+                while (true) {
+                    if (zx == zy) {
+                        ntri++;
+                        const int32_t z = zx;
+                        const int lz = run_t ? (int)__ldg(a.lab + z) : (int)kOther;
+                        if constexpr (COUNT) {
+                            const bool tz = lz < k;
+                            cntx += tx ? (unsigned long long)(ty + tz) : 0ull;
+                            if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
+                            cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
+                        } else {
+                            const double wr = __ldg(a.wd + ix);
+                            const bool zwide = __double_as_longlong(wr) < 0;
+                            const double Axlz = fabs(wr), Aylz = fabs(__ldg(a.wd + iy));
+                            const double Azlx = amat_at(a, z, lx), Azly = amat_at(a, z, ly);
+                            const double ttx = Aylx * Azlx * (Azly + Aylz);
+                            const double ttz = Axlz * Aylz * (Aylx + Axly);
+                            accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
+                            if (ttx > 0.0) accx = u128_add(accx, fx_quantize(ttx));
+                            if (ttz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(ttz), zwide);
+                        }
+                        ix += s;
+                        iy += s;
+                        if (ix == ex || iy == ey) break;
+                        zx = __ldg(a.pd + ix);
+                        zy = __ldg(a.pd + iy);
+                    } else if (zx < zy) {
+                        ix += s;
+                        if (ix == ex) break;
+                        zx = __ldg(a.pd + ix);
                     } else {
-                        const double Axlz = __ldg(a.wps + bx + ix), Aylz = __ldg(Wy + iy);
-                        const double Azlx = amat_at(a, z, lx), Azly = amat_at(a, z, ly);
-                        const double tx = Aylx * Azlx * (Azly + Aylz);
-                        const double tz = Axlz * Aylz * (Aylx + Axly);
-                        accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
-                        if (tx > 0.0) accx = u128_add(accx, fx_quantize(tx));
-                        if (tz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(tz));
+                        iy += s;
+                        if (iy == ey) break;
+                        zy = __ldg(a.pd + iy);
                     }
-                    if (++ix >= pcx.x || ++iy >= py) break;
-                    zx = __ldg(Px + ix);
-                    zy = __ldg(Py + iy);
-                } else if (zx < zy) {
-                    if (++ix >= pcx.x) break;
-                    zx = __ldg(Px + ix);
-                } else {
-                    if (++iy >= py) break;
-                    zy = __ldg(Py + iy);
                 }
-            }
-            if (owned(a, x)) {
-                if constexpr (COUNT) {
-                    if (cntx) atomicAdd(a.n1 + x, cntx);
-                } else {
-                    if (accx.lo | accx.hi) acc_add(a, x, accx);
-                }
-            }
-        }
-        if (ly < k && owned(a, y)) {
+            };
+            const int txn = pr_plus_t(pcx), tyn = pr_plus_t(pcy);
+            merge(bx, txn, dy, tyn, 1, true);                                    // target runs
+            if (tx && ty)                                                        // the other runs
+                merge(bx + dcap(pcx.y) - 1, pcx.x - txn, dy + dcap(pcy.y) - 1, pcy.x - tyn, -1, false);
             if constexpr (COUNT) {
-                if (cnty) atomicAdd(a.n1 + y, cnty);
+                if (cntx && owned(a, x)) atomicAdd(a.n1 + x, cntx);
+                if (cnty && ty && owned(a, y)) atomicAdd(a.n1 + y, cnty);
             } else {
-                if (accy.lo | accy.hi) acc_add(a, y, accy);
+                if ((accx.lo | accx.hi) && owned(a, x)) acc_add(a, x, accx, is_wide(a, pcx.y));
+                if ((accy.lo | accy.hi) && ty && owned(a, y)) acc_add(a, y, accy, is_wide(a, pcy.y));
             }
         }
     }
     for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
-    if ((threadIdx.x & 31) == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
+    if (lane == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
 }
 
 // ---------------------------------------------------------------- work items (per step)
@@ -436,12 +546,45 @@ __global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int32_t
         cnt[y] = c;
     }
 }
-__global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off, int64_t n_heavy,
-                            int2 *items) {
+__global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
+                            const PRec *__restrict__ pc2, const int64_t *__restrict__ rowptr,
+                            const uint8_t *__restrict__ lab, int64_t n_heavy,
+                            EItem *items) {
     for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
         const int c = cnt[y], o = off[y];
-        for (int j = 0; j < c; j++) items[o + j] = make_int2((int)y, j);
+        if (c == 0) continue;
+        const PRec p = pc2[y];
+        EItem e;
+        e.by = rowptr[y];
+        e.dy = p.start;                 // region start | |P+_T(y)| << 40
+        e.y = (int32_t)y;
+        e.pyl = p.x | ((int32_t)lab[y] << 24);
+        e.pm = p.y - p.x;
+        for (int j = 0; j < c; j++) {
+            e.chunk = j;
+            items[o + j] = e;
+        }
     }
+}
+
+// ---------------------------------------------------------------- P+ regions (per step)
+// Region of u in pd/wd: dcap(|P(u)|) entries at dpos[u] (scan), written by Phase C.
+__global__ void k_dense_cap(const VRec *__restrict__ vrec, int64_t n, int64_t *sz) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u <= n; u += (int64_t)gridDim.x * blockDim.x)
+        sz[u] = u < n ? dcap(vrec[u].pcnt) : 0;
+}
+cudaError_t launch_dense_pos(Ctx &c) {
+    const int64_t n = c.n;
+    int64_t *sz = (int64_t *)c.scratch;
+    void *tmp = sz + (n + 1);
+    const size_t tmp_bytes = c.scratch_bytes - sizeof(int64_t) * (size_t)(n + 1);
+    k_dense_cap<<<148 * 8, 256, 0, c.stream>>>(c.vrec, n, sz);
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, sz, c.dpos, (int)(n + 1), c.stream);
+    if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+    cub::DeviceScan::ExclusiveSum(tmp, need, sz, c.dpos, (int)(n + 1), c.stream);
+    c.launches += 2;
+    return cudaGetLastError();
 }
 
 // load time: buffers sized for any community assignment (grow-only)
@@ -450,8 +593,8 @@ cudaError_t launch_e_items(Ctx &c) {
     const int64_t nh = c.bins.offset[4];          // degree classes 5-7
     c.e_nbig = nh;
     c.e_extra = nh + c.nnz / kChunkE + 1;         // item capacity
-    // layout: cnt[nh+1] | off[nh+1] | items[cap] (int2)
-    const size_t bytes = sizeof(int32_t) * 2 * (size_t)(nh + 1) + sizeof(int2) * (size_t)c.e_extra + 16;
+    // layout: cnt[nh+1] | off[nh+1] | items[cap] (EItem)
+    const size_t bytes = sizeof(int32_t) * 2 * (size_t)(nh + 1) + sizeof(EItem) * (size_t)c.e_extra + 16;
     if (bytes <= c.e_bytes) return cudaSuccess;
     if (c.e_pre) cudaFree(c.e_pre);
     c.e_pre = nullptr;
@@ -465,14 +608,14 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     const int64_t nh = c.e_nbig;
     int32_t *cnt = (int32_t *)c.e_pre;
     int32_t *off = cnt + (nh + 1);
-    int2 *items = (int2 *)(((uintptr_t)(off + (nh + 1)) + 15) & ~(uintptr_t)15);
+    EItem *items = (EItem *)(((uintptr_t)(off + (nh + 1)) + 15) & ~(uintptr_t)15);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nh + 256) / 256, 148 * 4));
     k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, cnt);
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
     if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
     cub::DeviceScan::ExclusiveSum(c.scratch, need, cnt, off, (int)(nh + 1), c.stream);
-    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, nh, items);
+    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, c.pc2, c.rowptr, c.lab, nh, items);
     c.launches += 3;
     it.items = items;
     it.total = off + nh;
@@ -505,7 +648,7 @@ static cudaError_t launch_e(Ctx &c) {
         c.launches++;
     }
     if (n_heavy < c.n) {
-        const int64_t threads = c.n - n_heavy;
+        const int64_t threads = c.n - n_heavy;            // a warp per 32 vertices
         const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
         k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, c.stream>>>(a, n_heavy);
         c.launches++;

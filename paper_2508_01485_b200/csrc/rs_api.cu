@@ -195,7 +195,7 @@ extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream,
 static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
-    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.wps); dfree(c.pc2); dfree(c.amat);
+    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pd); dfree(c.wd); dfree(c.dpos); c.cap_d = 0; dfree(c.pc2); dfree(c.amat);
     dfree(c.acc1); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
@@ -307,8 +307,10 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         CK(dalloc(&c.lab, n));
         CK(dalloc(&c.vrec, n));
         CK(dalloc(&c.pidx, nnz));
-        CK(dalloc(&c.pplus, nnz));
-        CK(dalloc(&c.wps, nnz));
+        c.cap_d = nnz + 12 * n + 16;  // sum of dcap(|P(u)|) <= nnz + 11 n
+        CK(dalloc(&c.pd, c.cap_d));
+        CK(dalloc(&c.wd, c.cap_d));
+        CK(dalloc(&c.dpos, n + 1));
         CK(dalloc(&c.pc2, n));
         CK(dalloc(&c.acc1, 3 * n));
         CK(dalloc(&c.n1, n));
@@ -402,6 +404,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     join(c);
     CK(cudaEventRecord(c.ev_phase[1], c.stream));
     // Phase C: B table + orientation
+    CK(rs::launch_dense_pos(c));
     fork(c);
     CK(rs::launch_phase_c(c));
     join(c);

@@ -55,11 +55,23 @@ struct __align__(16) VRec {
 
 // Per-vertex G' record written by Phase C, gathered once per predecessor x by
 // Phase E: where P+(x) starts and how long P+(x) and P(x) are (one sector).
+// P+(u) lives in the dense array pd, in a region of dcap(|P(u)|) entries at
+// `start` (dpos[u], a scan over the capacities): the entries in a target
+// community ascending at [0, t) padded with -1 to ceil4(t), the others in
+// DESCENDING order at the end [cap - (|P+| - t), cap), padded with -1 down to
+// cap - ceil4(|P+| - t) (Phase C writes both runs in one pass). wd holds
+// a_u(c_z) beside each entry. t = |P+_T(u)| is packed above bit 40 of `start`
+// (offsets < 2^40; |P+| <= sqrt(2 |E'|) < 2^24 by the orientation).
 struct __align__(16) PRec {
     int x;             // |P+(u)| (orientation out-degree)
     int y;             // |P(u)|
-    long long start;   // rowptr[u]: P(u) and P+(u) live at this offset
+    long long start;   // rowptr[u] | (|P+_T(u)| << 40)
 };
+constexpr int kPrShift = 40;
+__host__ __device__ __forceinline__ int ceil4(int v) { return (v + 3) & ~3; }
+__host__ __device__ __forceinline__ int dcap(int p) { return p > 0 ? ceil4(p) + 8 : 0; }
+__host__ __device__ __forceinline__ long long pr_start(const PRec &r) { return r.start & ((1ll << kPrShift) - 1); }
+__host__ __device__ __forceinline__ int pr_plus_t(const PRec &r) { return (int)(r.start >> kPrShift); }
 
 // Per (vertex, column) record read by the Type-II pull (Phase D).
 struct __align__(16) BQ {
@@ -119,9 +131,11 @@ struct Ctx {
     double *omega = nullptr;     // n*k weights (unnormalised)
     VRec *vrec = nullptr;        // n
     int32_t *pidx = nullptr;     // nnz, P(u) stored at rowptr[u] ...
-    int32_t *pplus = nullptr;    // nnz, P+(u) (orientation) at rowptr[u] ...
-    double *wps = nullptr;       // nnz, a_u(c_z) for each z of P+(u), same positions
-    PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, rowptr[u]}
+    int32_t *pd = nullptr;       // P+(u) (orientation), two runs in a region of dcap(|P(u)|) (see PRec)
+    double *wd = nullptr;        // a_u(c_z) beside each z of P+(u); sign bit: z needs 3 limbs
+    int64_t *dpos = nullptr;     // n+1: start of u's region (scan of dcap(|P(u)|))
+    int64_t cap_d = 0;           // capacity of pd / wd
+    PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, start | |P+_T(u)| << 40}
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQ *bq = nullptr;            // n*k
     unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)
@@ -175,6 +189,7 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, vo
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets);
 cudaError_t launch_phase_a(Ctx &c);
 cudaError_t launch_phase_c(Ctx &c);
+cudaError_t launch_dense_pos(Ctx &c);
 cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
 cudaError_t launch_triangle_counts(Ctx &c);
