@@ -231,8 +231,14 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     }
     S = g.sum(S);
     if (g.lane == 0) {
+        const bool wide = a.any_wide && ru.wide;
         const unsigned long long *acc = a.acc1 + 3 * u;
-        S = u128_add(S, (a.any_wide && ru.wide) ? fx_from3(acc) : fx_from2(acc));
+        S = u128_add(S, wide ? fx_from3(acc) : fx_from2(acc));
+        if (u < a.n_hub)
+            for (int s = 0; s < kHubStripes; s++) {
+                const unsigned long long *h = a.acc_hub + 3 * ((int64_t)s * a.n_hub + u);
+                S = u128_add(S, wide ? fx_from3(h) : fx_from2(h));
+            }
         double R = 0.0;
         if (wmax > 0.0) R = fx_to_double(S) / wmax / ((double)d * (double)(d - 1));
         a.score[a.perm[u]] = R;

@@ -77,6 +77,10 @@ __device__ __forceinline__ bool owned(const CdeArgs &a, int64_t h) { return h >=
 // head's 3-limb flag (VRec::wide), carried with the head's record
 __device__ __forceinline__ void acc_add(const CdeArgs &a, int32_t h, const U128 &q, bool wide) {
     unsigned long long *acc = a.acc1 + 3 * (int64_t)h;
+    if (h < a.n_hub) {
+        const int stripe = (int)(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) & (kHubStripes - 1));
+        acc = a.acc_hub + 3 * ((int64_t)stripe * a.n_hub + h);
+    }
     if (wide) fx_red3(acc, q);
     else fx_red2(acc, q);
 }
@@ -308,7 +312,12 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                     int iz;
                     if (local) iz = zt ? find_sorted(S.py, pyt, z) : find_sorted(S.py + pyt, py - pyt, z);
                     else iz = zt ? find_sorted_g(a.pd + dy, pyt, z) : find_desc_g(a.pd + dye + 1 - (py - pyt), py - pyt, z);
+#ifdef RS_EXP_NO_TERMS
+                    if (iz >= 0) ntri++;
+                    if (iz >= 0 && z == -7) {
+#else
                     if (iz >= 0) {
+#endif
                         ntri++;
                         const int32_t x = (int32_t)((xe.y >> 32) & 0x7FFFFFFF);
                         const int lx = (int)((xe.y >> 24) & 0xFF);
@@ -330,12 +339,16 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                             const double tx = Aylx * Azlx * (Azly + Aylz);
                             const double tz = Axlz * Aylz * (Aylx + Axly);
                             accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
+#ifndef RS_EXP_NO_XRED
                             if (tx > 0.0) {
                                 const int lenx = ceil4((int)(xe.y & 0xFFFFFF)) + S.xn[slot].y;
                                 if (lenx <= kSlotMaxHits) smem_red4(S.xa + 4 * slot, fx_quantize(tx));
                                 else if (owned(a, x)) acc_add(a, x, fx_quantize(tx), xe.y < 0);
                             }
+#endif
+#ifndef RS_EXP_NO_ZRED
                             if (tz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(tz), zwide);
+#endif
                         }
                     }
                 }

@@ -196,7 +196,7 @@ static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
     dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pd); dfree(c.wd); dfree(c.dpos); c.cap_d = 0; dfree(c.pc2); dfree(c.amat);
-    dfree(c.acc1); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
+    dfree(c.acc1); dfree(c.acc_hub); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
     ctx->l2n = 0;
@@ -313,6 +313,8 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         CK(dalloc(&c.dpos, n + 1));
         CK(dalloc(&c.pc2, n));
         CK(dalloc(&c.acc1, 3 * n));
+        c.n_hub = std::min<int64_t>(n, rs::kHubMax);
+        CK(dalloc(&c.acc_hub, 3 * rs::kHubStripes * c.n_hub));
         CK(dalloc(&c.n1, n));
         CK(dalloc(&c.score, n));
         c.cap_n = n;
@@ -396,6 +398,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     const int64_t n = c.n;
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
+    CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, sizeof(unsigned long long), c.stream));
     // Phase A: border + histogram + weights + P lists + omega_max partials

@@ -68,6 +68,11 @@ struct __align__(16) PRec {
     long long start;   // rowptr[u] | (|P+_T(u)| << 40)
 };
 constexpr int kPrShift = 40;
+// Type-I accumulation of the n_hub highest-degree heads is striped over
+// kHubStripes copies (a RED picks its copy by warp): a hub closes up to
+// millions of triangles, and same-address atomics serialise in the L2.
+constexpr int kHubStripes = 16;
+constexpr int64_t kHubMax = 1 << 16;
 __host__ __device__ __forceinline__ int ceil4(int v) { return (v + 3) & ~3; }
 __host__ __device__ __forceinline__ int dcap(int p) { return p > 0 ? ceil4(p) + 8 : 0; }
 __host__ __device__ __forceinline__ long long pr_start(const PRec &r) { return r.start & ((1ll << kPrShift) - 1); }
@@ -139,6 +144,8 @@ struct Ctx {
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQ *bq = nullptr;            // n*k
     unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)
+    unsigned long long *acc_hub = nullptr;  // kHubStripes copies of the limbs of the first n_hub vertices
+    int64_t n_hub = 0;                   //   (the highest degrees: contended heads), summed by Phase D
     unsigned long long *n1 = nullptr;    // n Type-I triad counts
     double *score = nullptr;     // n, ORIGINAL vertex order
     unsigned long long *scal = nullptr;  // device scalars (see kScal*)
