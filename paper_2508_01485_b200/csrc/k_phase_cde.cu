@@ -165,7 +165,7 @@ __device__ __forceinline__ void phase_c_vertex_smem(const CdeArgs &a, int64_t w,
 }
 
 template <int G, int U, bool SMEM>
-__global__ void __launch_bounds__(256) k_phase_c_warp(CdeArgs a) {
+__global__ void __launch_bounds__(256, 4) k_phase_c_warp(CdeArgs a) {
     __shared__ unsigned long long sB[SMEM ? 8 * 3 * kMaxK : 1];
     WarpGroup<G> g;
     const int64_t gpb = blockDim.x / G;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) k_phase_c_warp(CdeArgs a) {
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(kCtaThreads) k_phase_c_cta(CdeArgs a) {
+__global__ void __launch_bounds__(kCtaThreads, 4) k_phase_c_cta(CdeArgs a) {
     __shared__ int s_i[kCtaWarps + 1];
     __shared__ unsigned long long s_u[2 * kCtaWarps];
     __shared__ unsigned long long sB[SMEM ? 3 * kMaxK : 1];

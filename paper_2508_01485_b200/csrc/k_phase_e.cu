@@ -603,7 +603,10 @@ cudaError_t launch_dense_pos(Ctx &c) {
 // load time: buffers sized for any community assignment (grow-only)
 cudaError_t launch_e_items(Ctx &c) {
     cudaError_t e;
-    const int64_t nh = c.bins.offset[4];          // degree classes 5-7
+#ifndef RS_EXP_HEAVY_CLS
+#define RS_EXP_HEAVY_CLS 4
+#endif
+    const int64_t nh = c.bins.offset[RS_EXP_HEAVY_CLS];   // degree classes 5-7
     c.e_nbig = nh;
     c.e_extra = nh + c.nnz / kChunkE + 1;         // item capacity
     // layout: cnt[nh+1] | off[nh+1] | items[cap] (EItem)
