@@ -429,25 +429,38 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 
 // ---------------------------------------------------------------- light middle vertices
 // Vertices of degree < 128 (most of them, ~5% of the probe work). A warp takes
-// 32 consecutive y; their (y, x in P-(y)) pairs are numbered by one warp scan
-// and dealt to the lanes, so a lane's work is one pair, not one vertex. The
-// runs of P+(x) and P+(y) are short and sorted: two-pointer merges in L1 (the
-// target runs; the other runs too when x and y are both targets). Each pair
-// adds its x and y terms with one RED each (z terms per triangle).
+// 32 consecutive y; their pairs (y, x in P-(y)) are dealt to the lanes 32 at a
+// time (one warp scan), and the probes of those 32 pairs -- the entries of the
+// probed runs of P+(x) -- are flattened by a second scan: a lane probes one z
+// per round and looks it up by binary search in the matching run of P+(y)
+// (short, L1-resident), so the work per lane is uniform whatever the list
+// lengths. Terms go to the heads with one RED each.
 template <bool COUNT>
 __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
     const int k = a.k;
     const int lane = threadIdx.x & 31;
     unsigned long long ntri = 0;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    auto owner = [&](int incl, int q) {          // first lane whose inclusive count exceeds q
+        int j = 0;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, j + s - 1);
+            if (v <= q) j += s;
+        }
+        return j;
+    };
     for (int64_t y0 = ylo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; y0 < a.n;
          y0 += nwarps * 32) {
+        // ---- y level: lane j holds y0 + j
         const int64_t yl = y0 + lane;
         PRec pcl{0, 0, 0};
         int64_t rpl = 0;
+        int lyl = kOther;
         if (yl < a.n) {
             pcl = a.pc2[yl];
             rpl = a.rowptr[yl];
+            lyl = a.lab[yl];
         }
         const int cnt = pcl.x > 0 ? pcl.y - pcl.x : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
         int incl = cnt;
@@ -458,86 +471,89 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         for (int q0 = 0; q0 < total; q0 += 32) {
+            // ---- pair level: lane holds pair q0 + lane
             const int q = q0 + lane;
-            // owner lane j of pair q: the first lane whose inclusive count exceeds q
-            int j = 0;
-#pragma unroll
-            for (int s = 16; s > 0; s >>= 1) {
-                const int v = __shfl_sync(0xffffffffu, incl, j + s - 1);
-                if (v <= q) j += s;
-            }
+            const int j = owner(incl, q);
             const int inc_j = __shfl_sync(0xffffffffu, incl, j);
             const int cnt_j = __shfl_sync(0xffffffffu, cnt, j);
-            PRec pcy;
-            pcy.x = __shfl_sync(0xffffffffu, pcl.x, j);
-            pcy.y = __shfl_sync(0xffffffffu, pcl.y, j);
-            pcy.start = __shfl_sync(0xffffffffu, pcl.start, j);
-            const int64_t by = __shfl_sync(0xffffffffu, rpl, j);
-            if (q >= total) continue;
-            const int i = q - (inc_j - cnt_j);
-            const int32_t y = (int32_t)(y0 + j);
-            const int32_t x = __ldg(a.pidx + by + i);    // P-(y): lower rank than y
-            const PRec pcx = a.pc2[x];
-            if (pcx.x == 0) continue;
-            const int lx = __ldg(a.lab + x), ly = __ldg(a.lab + y);
+            const long long by = __shfl_sync(0xffffffffu, rpl, j);
+            const int ly = __shfl_sync(0xffffffffu, lyl, j);
+            int32_t x = -1;
+            if (q < total) x = __ldg(a.pidx + by + (q - (inc_j - cnt_j)));   // P-(y): lower rank than y
+            PRec pcx{0, 0, 0};
+            int lx = kOther;
+            double Axly = 0.0;
+            if (x >= 0) {
+                pcx = a.pc2[x];
+                lx = __ldg(a.lab + x);
+                Axly = amat_at(a, x, ly);
+            }
             const bool tx = lx < k, ty = ly < k;
-            if (!tx && !ty) continue;
-            const int64_t bx = pr_start(pcx), dy = pr_start(pcy);
-            const double Axly = amat_at(a, x, ly), Aylx = amat_at(a, y, lx);
-            U128 accx = u128_zero(), accy = u128_zero();
-            unsigned long long cntx = 0, cnty = 0;
-            // merge of two runs walked with step s (ids ascending)
-            auto merge = [&](int64_t ix, int nxr, int64_t iy, int nyr, int s, bool run_t) {
-                if (nxr == 0 || nyr == 0) return;
-                const int64_t ex = ix + (int64_t)s * nxr, ey = iy + (int64_t)s * nyr;
-                int32_t zx = __ldg(a.pd + ix), zy = __ldg(a.pd + iy);
-                while (true) {
-                    if (zx == zy) {
-                        ntri++;
-                        const int32_t z = zx;
-                        const int lz = run_t ? (int)__ldg(a.lab + z) : (int)kOther;
-                        if constexpr (COUNT) {
-                            const bool tz = lz < k;
-                            cntx += tx ? (unsigned long long)(ty + tz) : 0ull;
-                            if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
-                            cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
-                        } else {
-                            const double wr = __ldg(a.wd + ix);
-                            const bool zwide = __double_as_longlong(wr) < 0;
-                            const double Axlz = fabs(wr), Aylz = fabs(__ldg(a.wd + iy));
-                            const double Azlx = amat_at(a, z, lx), Azly = amat_at(a, z, ly);
-                            const double ttx = Aylx * Azlx * (Azly + Aylz);
-                            const double ttz = Axlz * Aylz * (Aylx + Axly);
-                            accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
-                            if (ttx > 0.0) accx = u128_add(accx, fx_quantize(ttx));
-                            if (ttz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(ttz), zwide);
-                        }
-                        ix += s;
-                        iy += s;
-                        if (ix == ex || iy == ey) break;
-                        zx = __ldg(a.pd + ix);
-                        zy = __ldg(a.pd + iy);
-                    } else if (zx < zy) {
-                        ix += s;
-                        if (ix == ex) break;
-                        zx = __ldg(a.pd + ix);
-                    } else {
-                        iy += s;
-                        if (iy == ey) break;
-                        zy = __ldg(a.pd + iy);
-                    }
+            const int t = (tx || ty) ? pr_plus_t(pcx) : 0;               // probed: the target run,
+            const int np = t + ((tx && ty) ? pcx.x - pr_plus_t(pcx) : 0); // and the other if both
+            const double Aylx = (x >= 0 && tx) ? __ldg(a.amat + (y0 + j) * k + lx) : 0.0;
+            int incl2 = np;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl2, o);
+                if (lane >= o) incl2 += v;
+            }
+            const int total2 = __shfl_sync(0xffffffffu, incl2, 31);
+            for (int r0 = 0; r0 < total2; r0 += 32) {
+                // ---- probe level: lane probes entry o of pair p's runs
+                const int r = r0 + lane;
+                const int p = owner(incl2, r);
+                const int o = r - (__shfl_sync(0xffffffffu, incl2, p) - __shfl_sync(0xffffffffu, np, p));
+                const int32_t xp = __shfl_sync(0xffffffffu, x, p);
+                const long long bx = __shfl_sync(0xffffffffu, pr_start(pcx), p);
+                const int pxy = __shfl_sync(0xffffffffu, pcx.y, p);          // |P(x)|
+                const int capx = dcap(pxy);
+                const int tp = __shfl_sync(0xffffffffu, t, p);
+                const int lxp = __shfl_sync(0xffffffffu, lx, p);
+                const double Axlyp = __shfl_sync(0xffffffffu, Axly, p);
+                const double Aylxp = __shfl_sync(0xffffffffu, Aylx, p);
+                const int jp = __shfl_sync(0xffffffffu, j, p);               // y's lane
+                const PRec pcy{__shfl_sync(0xffffffffu, pcl.x, jp), __shfl_sync(0xffffffffu, pcl.y, jp),
+                               __shfl_sync(0xffffffffu, pcl.start, jp)};
+                const int lyp = __shfl_sync(0xffffffffu, lyl, jp);
+                if (r >= total2) continue;
+                const int32_t y = (int32_t)(y0 + jp);
+                const bool zt = o < tp;                                     // z from the target run
+                const int64_t pos = zt ? bx + o : bx + capx - 1 - (o - tp);
+                const int32_t z = __ldg(a.pd + pos);
+                const int64_t dy = pr_start(pcy);
+                const int tyn = pr_plus_t(pcy), nyn = pcy.x - tyn;
+                int iz;
+                int64_t ypos;
+                if (zt) {
+                    iz = find_sorted_g(a.pd + dy, tyn, z);
+                    ypos = dy + iz;
+                } else {
+                    const int64_t nb = dy + dcap(pcy.y) - nyn;                // the other run, descending
+                    iz = find_desc_g(a.pd + nb, nyn, z);
+                    ypos = nb + iz;
                 }
-            };
-            const int txn = pr_plus_t(pcx), tyn = pr_plus_t(pcy);
-            merge(bx, txn, dy, tyn, 1, true);                                    // target runs
-            if (tx && ty)                                                        // the other runs
-                merge(bx + dcap(pcx.y) - 1, pcx.x - txn, dy + dcap(pcy.y) - 1, pcy.x - tyn, -1, false);
-            if constexpr (COUNT) {
-                if (cntx && owned(a, x)) atomicAdd(a.n1 + x, cntx);
-                if (cnty && ty && owned(a, y)) atomicAdd(a.n1 + y, cnty);
-            } else {
-                if ((accx.lo | accx.hi) && owned(a, x)) acc_add(a, x, accx, is_wide(a, pcx.y));
-                if ((accy.lo | accy.hi) && ty && owned(a, y)) acc_add(a, y, accy, is_wide(a, pcy.y));
+                if (iz < 0) continue;
+                ntri++;
+                const bool txp = lxp < k, typ = lyp < k;
+                const int lz = zt ? (int)__ldg(a.lab + z) : (int)kOther;
+                if constexpr (COUNT) {
+                    const bool tz = lz < k;
+                    if (txp && (typ + tz) && owned(a, xp)) atomicAdd(a.n1 + xp, (unsigned long long)(typ + tz));
+                    if (tz && (txp + typ) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(txp + typ));
+                    if (typ && (txp + tz) && owned(a, y)) atomicAdd(a.n1 + y, (unsigned long long)(txp + tz));
+                } else {
+                    const double wr = __ldg(a.wd + pos);
+                    const bool zwide = __double_as_longlong(wr) < 0;
+                    const double Axlz = fabs(wr), Aylz = fabs(__ldg(a.wd + ypos));
+                    const double Azlx = amat_at(a, z, lxp), Azly = amat_at(a, z, lyp);
+                    const double ttx = Aylxp * Azlx * (Azly + Aylz);
+                    const double tty = Axlyp * Azly * (Azlx + Axlz);
+                    const double ttz = Axlz * Aylz * (Aylxp + Axlyp);
+                    if (ttx > 0.0 && owned(a, xp)) acc_add(a, xp, fx_quantize(ttx), is_wide(a, pxy));
+                    if (tty > 0.0 && owned(a, y)) acc_add(a, y, fx_quantize(tty), is_wide(a, pcy.y));
+                    if (ttz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(ttz), zwide);
+                }
             }
         }
     }
