@@ -1,7 +1,7 @@
 // Step 4 (Algorithm 1, optional): top-K vertices by R, ties by ascending
 // vertex id (C-14). Radix select over the IEEE bit patterns of the
 // non-negative scores (monotone as unsigned integers once -0.0 is folded into
-// +0.0), 8 digit passes of 8 bits; ties at the threshold are resolved by an
+// +0.0), 6 digit passes of 11 bits; ties at the threshold are resolved by an
 // id-ordered block scan; the K survivors are sorted (key desc, id asc).
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
@@ -30,40 +30,80 @@ struct TkFilter {             // multi-GPU: only original ids whose internal id 
     }
 };
 
-__global__ void __launch_bounds__(kTkThreads) k_tk_hist(const double *__restrict__ score, int64_t lo, int64_t hi,
-                                                        int pass, const unsigned long long *st,
-                                                        unsigned long long *hist, TkFilter flt) {
-    __shared__ unsigned int h[256];
-    h[threadIdx.x] = 0;
+// digit pass: 11-bit digits from the top (6 passes: 11 x 5 + 9). Blocks count
+// the digits of the keys still matching the prefix into a shared histogram and
+// add it to the global one; the last block to finish (ticket) picks the digit
+// with a block scan from the top, updates the state and clears the histogram.
+constexpr int kTkBits = 11, kTkBins = 1 << kTkBits, kTkPasses = 6;
+__device__ __forceinline__ void tk_digit(int pass, int &shift, int &width) {
+    const int hi = 64 - kTkBits * pass;
+    width = hi < kTkBits ? hi : kTkBits;
+    shift = hi - width;
+}
+
+__global__ void __launch_bounds__(kTkThreads) k_tk_pass(const double *__restrict__ score, int64_t lo, int64_t hi,
+                                                        int pass, unsigned long long *st, unsigned int *hist,
+                                                        unsigned int *ticket, TkFilter flt) {
+    __shared__ unsigned int h[kTkBins];
+    __shared__ unsigned long long s_sum[kTkThreads];
+    __shared__ bool s_last;
+    for (int i = threadIdx.x; i < kTkBins; i += blockDim.x) h[i] = 0;
     __syncthreads();
+    int shift, width;
+    tk_digit(pass, shift, width);
     const unsigned long long prefix = st[0];
-    const int shift = 56 - 8 * pass;
+    const int top = shift + width;      // bits above the digit must match the prefix
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
         if (!flt.keep(i)) continue;
         const unsigned long long key = score_key(score[i]);
-        const bool match = (pass == 0) || (((key ^ prefix) >> (shift + 8)) == 0ull);
-        if (match) atomicAdd(&h[(key >> shift) & 0xFF], 1u);
+        const bool match = top >= 64 || ((key ^ prefix) >> top) == 0ull;
+        if (match) atomicAdd(&h[(key >> shift) & (kTkBins - 1)], 1u);
     }
     __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
-}
-
-// one warp: choose the digit of this pass
-__global__ void k_tk_pick(int pass, unsigned long long *st, unsigned long long *hist) {
-    if (threadIdx.x != 0) return;
-    const int shift = 56 - 8 * pass;
-    unsigned long long krem = st[1];
-    unsigned long long above = 0;
-    int t = 0;
-    for (int dgt = 255; dgt >= 0; dgt--) {
-        const unsigned long long h = hist[dgt];
-        if (above + h >= krem) { t = dgt; break; }
-        above += h;
+    for (int i = threadIdx.x; i < kTkBins; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    // last block: thread t owns the 8 digits [kTkBins - 8 (t + 1), kTkBins - 8 t), scanned from the top
+    constexpr int per = kTkBins / kTkThreads;
+    const int t = threadIdx.x;
+    unsigned int c[per];
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int j = 0; j < per; j++) {
+        c[j] = __ldcg(hist + kTkBins - 1 - (per * t + j));   // descending digit order
+        mine += c[j];
     }
-    st[0] |= ((unsigned long long)t) << shift;
-    st[1] = krem - above;
-    st[2] += above;
-    for (int i = 0; i < 256; i++) hist[i] = 0;   // ready for the next pass
+    s_sum[t] = mine;
+    __syncthreads();
+    for (int o = 1; o < kTkThreads; o <<= 1) {   // inclusive scan (Hillis-Steele)
+        const unsigned long long v = t >= o ? s_sum[t - o] : 0ull;
+        __syncthreads();
+        s_sum[t] += v;
+        __syncthreads();
+    }
+    const unsigned long long krem = st[1];
+    const unsigned long long before = t ? s_sum[t - 1] : 0ull;   // keys in higher digits
+    // the crossing is in my digits (or there is none: fewer keys than krem, the
+    // lowest thread takes digit 0 with every key above, as a full scan would)
+    if ((before < krem && s_sum[t] >= krem) || (t == kTkThreads - 1 && s_sum[t] < krem)) {
+        unsigned long long above = before;
+        int dgt = 0;
+#pragma unroll
+        for (int j = 0; j < per; j++) {
+            const int d = kTkBins - 1 - (per * t + j);
+            if (above + c[j] >= krem) { dgt = d; break; }
+            above += c[j];
+        }
+        st[0] = prefix | ((unsigned long long)dgt << shift);
+        st[1] = krem - above;
+        st[2] += above;
+    }
+    for (int i = threadIdx.x; i < kTkBins; i += blockDim.x) hist[i] = 0;   // ready for the next pass
+    if (threadIdx.x == 0) *ticket = 0;
 }
 
 // keys above the threshold -> cand[0, count_gt) (any order); ties counted per block
@@ -210,19 +250,20 @@ cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsign
                                int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi) {
     TkFilter flt{own_inv, own_lo, own_hi};
     unsigned long long *st = c.scal + kScalTk;
-    unsigned long long *hist = c.tk_hist;
-    unsigned long long *cursor = hist + 256;
-    unsigned int *tie_cnt = (unsigned int *)(hist + 512);
+    // tk_hist (2048 u64): digit histogram u32[kTkBins] | ticket | cursor | per-block tie counts
+    unsigned int *hist = (unsigned int *)c.tk_hist;
+    unsigned int *ticket = (unsigned int *)(c.tk_hist + kTkBins / 2);
+    unsigned long long *cursor = c.tk_hist + kTkBins / 2 + 1;
+    unsigned int *tie_cnt = (unsigned int *)(c.tk_hist + kTkBins / 2 + 8);
     const int64_t range = hi - lo;
     unsigned long long init[3] = {0ull, (unsigned long long)K, 0ull};
     cudaMemcpyAsync(st, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
-    cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 257, c.stream);
+    cudaMemsetAsync(c.tk_hist, 0, sizeof(unsigned long long) * (kTkBins / 2 + 2), c.stream);
     int blocks = (int)std::min<int64_t>((range + kTkThreads - 1) / kTkThreads, kTkBlocks);
     if (blocks < 1) blocks = 1;
-    for (int pass = 0; pass < 8; pass++) {
-        k_tk_hist<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist, flt);
-        k_tk_pick<<<1, 32, 0, c.stream>>>(pass, st, hist);
-        c.launches += 2;
+    for (int pass = 0; pass < kTkPasses; pass++) {
+        k_tk_pass<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist, ticket, flt);
+        c.launches++;
     }
     const int64_t chunk = (range + kTkBlocks - 1) / kTkBlocks;
     const int cblocks = (int)std::max<int64_t>(1, (range + chunk - 1) / std::max<int64_t>(chunk, 1));
