@@ -115,12 +115,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def phase_bytes(n, D, Db, k, ntri, nb):
+def phase_bytes(n, D, Db, k, ntri, nb, nprobe):
     """Algorithmic DRAM bytes of each phase: what it must read or write at least
-    once (per-unit figures x units)."""
+    once (per-unit figures x units). Phase E: its intersection
+    volume (4 B per probed P+ entry), 20 B per G' edge (the P-
+    entry and the predecessor's record), 32 B per Type-I triangle (weights and
+    head updates) and y's weight rows."""
     A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 20 * k * n + 16 * n
     C = 8 * n + 16 * n + 4 * Db + 16 * Db + 8 * k * n + 16 * k * nb + 2 * Db + 8 * n
-    E = 4 * Db + 2 * Db + 17 * n + 8 * k * n + 32 * ntri
+    E = 4 * nprobe + 20 * (Db // 2) + 32 * ntri + 8 * k * n
     D_ = 8 * n + 16 * n + 4 * Db + 16 * Db + 24 * n + 8 * n
     return {"A": A, "C": C, "E": E, "D": D_}
 
@@ -225,8 +228,8 @@ def main():
         ph.append(s["ms_phase"][:4])
     ph = np.median(np.array(ph), axis=0)
     names = ["A_border_hist_weights", "C_btable_orient", "E_type1_triangles", "D_type2_finalize"]
-    Db, nb, ntri = st["n_pred_entries"], st["n_border"], st["n_triangles"]
-    pb = phase_bytes(n, D, Db, a.k, ntri, nb)
+    Db, nb, ntri, nprobe = st["n_pred_entries"], st["n_border"], st["n_triangles"], st["n_probes"]
+    pb = phase_bytes(n, D, Db, a.k, ntri, nb, nprobe)
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -263,7 +266,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{a.config}-shape DC-SBM (SURVEY §8(d))", "n": n, "m": m, "nnz": D,
                        "k_targets": a.k, "K": a.K, "seed": gen.CONFIGS.get(a.config, {}).get("seed"),
-                       "n_border": nb, "pred_entries": Db, "triangles": ntri, "omega_max": st["omega_max"],
+                       "n_border": nb, "pred_entries": Db, "triangles": ntri, "probes": nprobe, "omega_max": st["omega_max"],
                        "l2": "flushed between timed steps (512 MiB write)", "gen_s": round(gen_s, 1),
                        "parallelism": f"head-range x{world}" if world > 1 else "single GPU"},
             "roofline": roof,

@@ -55,6 +55,8 @@ typedef struct {
                                  least two target vertices: the ones that carry
                                  Type-I terms (a term needs a target head and a
                                  target column among the other two)             */
+    int64_t n_probes;         /* Phase E: P+ list entries probed (the Type-I
+                                 intersection volume, bench roofline)           */
     double omega_max;         /* max weight over all cells (C-7)  */
     float ms_phase[8];        /* [0] Phase A border/histogram/weights/G' lists
                                  [1] Phase C B-table + orientation

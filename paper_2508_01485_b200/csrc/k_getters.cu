@@ -188,12 +188,10 @@ cudaError_t launch_stats(Ctx &c, int64_t out[4]) {
     cudaMemsetAsync(c.scal + kScalNBorder, 0, 2 * sizeof(unsigned long long), c.stream);
     k_stats<<<148 * 2, 256, 0, c.stream>>>(c.vrec, c.n, c.scal);
     c.launches++;
-    unsigned long long v[3];
+    unsigned long long v[4];
     cudaMemcpyAsync(v, c.scal + kScalNBorder, sizeof(v), cudaMemcpyDeviceToHost, c.stream);
     cudaError_t e = cudaStreamSynchronize(c.stream);
-    out[0] = (int64_t)v[0];
-    out[1] = (int64_t)v[1];
-    out[2] = (int64_t)v[2];
+    for (int i = 0; i < 4; i++) out[i] = (int64_t)v[i];
     return e;
 }
 

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
     unsigned char *base = e_smem + (size_t)wid * e_stride_bytes(k);
     ESmem &S = *reinterpret_cast<ESmem *>(base);
     double *Ay = (double *)(base + ((sizeof(ESmem) + 15) / 16) * 16);
-    unsigned long long ntri = 0;
+    unsigned long long ntri = 0, nprobe = 0;
     const unsigned long long n_items = (unsigned long long)*it.total;
 
     unsigned long long qnext = 0;
@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             const int t = (tx || ty) ? pr_plus_t(pcx[h]) : 0;
             const int lenn = (tx && ty) ? pcx[h].x - pr_plus_t(pcx[h]) : 0;
             const bool use = t + lenn > 0;
+            nprobe += (unsigned)(t + lenn);
             const int pieces = ceil4(t) / kPiece + ceil4(lenn) / kPiece;
             int incl = pieces;
 #pragma unroll
@@ -423,8 +424,12 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         }
         __syncwarp();
     }
-    for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
+        nprobe += __shfl_xor_sync(0xffffffffu, nprobe, o);
+    }
     if (lane == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
+    if (lane == 0 && nprobe) atomicAdd(&a.scal[kScalNProbe], nprobe);
 }
 
 // ---------------------------------------------------------------- light middle vertices
@@ -439,7 +444,7 @@ template <bool COUNT>
 __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
     const int k = a.k;
     const int lane = threadIdx.x & 31;
-    unsigned long long ntri = 0;
+    unsigned long long ntri = 0, nprobe = 0;   // nprobe: warp-uniform
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     auto owner = [&](int incl, int q) {          // first lane whose inclusive count exceeds q
         int j = 0;
@@ -499,6 +504,7 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 if (lane >= o) incl2 += v;
             }
             const int total2 = __shfl_sync(0xffffffffu, incl2, 31);
+            nprobe += (unsigned)total2;
             for (int r0 = 0; r0 < total2; r0 += 32) {
                 // ---- probe level: lane probes entry o of pair p's runs
                 const int r = r0 + lane;
@@ -559,6 +565,7 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
     }
     for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
     if (lane == 0 && ntri) atomicAdd(&a.scal[kScalNTri], ntri);
+    if (lane == 0 && nprobe) atomicAdd(&a.scal[kScalNProbe], nprobe);
 }
 
 // ---------------------------------------------------------------- work items (per step)

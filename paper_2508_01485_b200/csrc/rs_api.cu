@@ -400,7 +400,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
     CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
-    CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, sizeof(unsigned long long), c.stream));
+    CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, 2 * sizeof(unsigned long long), c.stream));   // NTri, NProbe
     // Phase A: border + histogram + weights + P lists + omega_max partials
     fork(c);
     CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n));
@@ -439,7 +439,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         if (!dev) CK(cudaStreamSynchronize(c.stream));
     }
     if (stats_out) {
-        int64_t st[3];
+        int64_t st[4];
         CK(rs::launch_stats(c, st));
         rs_stats s;
         memset(&s, 0, sizeof(s));
@@ -448,6 +448,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         s.n_border = st[0];
         s.n_pred_entries = st[1];
         s.n_triangles = st[2];
+        s.n_probes = st[3];
         unsigned long long wb = 0;
         CK(cudaMemcpy(&wb, c.scal + rs::kScalOmegaMaxBits, sizeof(wb), cudaMemcpyDeviceToHost));
         memcpy(&s.omega_max, &wb, sizeof(double));

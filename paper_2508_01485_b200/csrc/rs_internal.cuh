@@ -176,6 +176,7 @@ enum {
     kScalNBorder = 4,
     kScalNPred = 5,
     kScalNTri = 6,
+    kScalNProbe = 7,         // Phase E: entries of P+ lists probed
     kScalTk = 8,             // top-k state (8 slots)
     kScalCount = 32
 };
