@@ -185,6 +185,29 @@ rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out);
 /* Number of librs kernels launched on ctx since creation (bench accounting). */
 int64_t rs_kernel_launches(const rs_ctx *ctx);
 
+/* ---- Multi-GPU host protocol. Pure host functions on host
+ * arrays, no context, no device work; rs_create_dist / rs_topk call them, and
+ * they are exported so that the protocol can be exercised without GPUs. ---- */
+
+/* Contiguous vertex ranges balanced by work: work_incl int64[n] is the
+ * inclusive prefix sum of a non-negative per-vertex work estimate (librs uses
+ * d(u) + 1 in its internal numbering). bounds_out int64[world+1]: rank r owns
+ * [bounds[r], bounds[r+1]); bounds[0] = 0, bounds[world] = n, non-decreasing;
+ * boundary r is the first vertex after the prefix reaches ceil(total r / world).
+ * RS_EINVAL if n < 0, world < 1 or a pointer is NULL (work_incl may be NULL
+ * when n == 0). */
+rs_status rs_split_ranges(int64_t n, const int64_t *work_incl, int32_t world, int64_t *bounds_out);
+
+/* Step 4 merge of the per-rank top-K candidate lists gathered from all
+ * ranks: keys uint64[count] are the IEEE-754 bits of the non-negative scores
+ * (-0.0 folded to +0.0: monotone as integers), ids int32[count] the original
+ * vertex ids; padding entries are (0, INT32_MAX). Writes the first
+ * min(K, count) by (key descending, id ascending) to ids_out int32[K] and, if
+ * not NULL, their scores to scores_out double[K]; *count_out receives the
+ * number written. Deterministic: every rank computes the same result. */
+rs_status rs_merge_candidates(int64_t count, const uint64_t *keys, const int32_t *ids, int64_t K,
+                              int32_t *ids_out, double *scores_out, int64_t *count_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,9 @@ SIGNATURES = [
     ("rs_get_triad_counts", ctypes.c_int, [_P, _P, _P]),
     ("rs_get_targets", ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int32)]),
     ("rs_kernel_launches", ctypes.c_int64, [_P]),
+    ("rs_split_ranges", ctypes.c_int, [ctypes.c_int64, _P, ctypes.c_int32, _P]),
+    ("rs_merge_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P,
+                                           ctypes.POINTER(ctypes.c_int64)]),
 ]
 
 
@@ -220,6 +223,39 @@ def rs_get_targets(ctx):
 
 def rs_kernel_launches(ctx) -> int:
     return int(load_library().rs_kernel_launches(ctx))
+
+
+# ------------------------------------------------------------------ multi-GPU host protocol
+def rs_split_ranges(work_incl, world: int) -> np.ndarray:
+    """bounds int64[world+1] of the balanced contiguous split (include/rs.h)."""
+    w = np.ascontiguousarray(work_incl, dtype=np.int64)
+    b = np.empty(world + 1, dtype=np.int64)
+    st = load_library().rs_split_ranges(int(w.shape[0]), _ptr(w) if w.size else None, int(world), _ptr(b))
+    if st != RS_OK:
+        raise RsError(st, "rs_split_ranges: invalid arguments")
+    return b
+
+
+def rs_merge_candidates(keys, ids, K: int):
+    """(ids, scores) of the merged top-K of gathered (key, id) candidates."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    i = np.ascontiguousarray(ids, dtype=np.int32)
+    out_i = np.empty(max(K, 1), dtype=np.int32)
+    out_s = np.empty(max(K, 1), dtype=np.float64)
+    cnt = ctypes.c_int64(0)
+    st = load_library().rs_merge_candidates(int(k.shape[0]), _ptr(k) if k.size else None,
+                                            _ptr(i) if i.size else None, int(K), _ptr(out_i), _ptr(out_s),
+                                            ctypes.byref(cnt))
+    if st != RS_OK:
+        raise RsError(st, "rs_merge_candidates: invalid arguments")
+    return out_i[:cnt.value].copy(), out_s[:cnt.value].copy()
+
+
+def score_keys(scores) -> np.ndarray:
+    """The Step 4 order key of non-negative scores: IEEE bits, -0.0 folded to +0.0."""
+    b = np.ascontiguousarray(scores, dtype=np.float64).view(np.uint64).copy()
+    b[b == np.uint64(0x8000000000000000)] = 0
+    return b
 
 
 # ------------------------------------------------------------------ object wrapper

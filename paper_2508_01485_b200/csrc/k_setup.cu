@@ -2,6 +2,7 @@
 //  - CSR contract check (C-17), degree classes for binned scheduling,
 //  - community-size histogram, target selection (C-15), 8-bit labels.
 #include "rs_internal.cuh"
+#include "rs_protocol.h"
 #include "rs_device.cuh"
 #include <cub/cub.cuh>
 
@@ -336,19 +337,10 @@ __global__ void k_work(const int64_t *__restrict__ rowptr, int64_t n, int64_t *w
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
         w[u] = rowptr[u + 1] - rowptr[u] + 1;
 }
+// boundaries of the head ranges (rs_protocol.h split_point, = rs_split_ranges)
 __global__ void k_split(const int64_t *__restrict__ incl, int64_t n, int world, int64_t *bounds) {
     const int r = threadIdx.x;
-    if (r > world) return;
-    if (r == 0) { bounds[0] = 0; return; }
-    if (r == world) { bounds[world] = n; return; }
-    const int64_t total = incl[n - 1];
-    const int64_t target = (total * r + world - 1) / world;
-    int64_t lo = 0, hi = n;   // first u with incl[u] >= target -> boundary u+1
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (incl[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    bounds[r] = lo + 1 < n ? lo + 1 : n;
+    if (r <= world) bounds[r] = split_point(incl, n, world, r);
 }
 cudaError_t launch_partition(Ctx &c) {
     const int64_t n = c.n;

@@ -2,6 +2,8 @@
 // call-order state machine, stream fork/join for the degree bins, phase
 // timing and the NCCL exchange steps of the multi-GPU path.
 #include "rs_internal.cuh"
+#include <vector>
+#include "rs_protocol.h"
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -522,7 +524,19 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         NK(NCCL.AllGather(lk, gk, (size_t)Kc, ncclUint64, c.comm, c.stream));
         NK(NCCL.AllGather(li, gi, (size_t)Kc, ncclInt32, c.comm, c.stream));
         NK(NCCL.GroupEnd());
-        CK(rs::tk_sort_emit(c, gk, gi, Kc * c.world, Kc, ids_d, sc_d));
+        // world * K candidates: merged on the host by the exported protocol function
+        const int64_t cnt = Kc * c.world;
+        std::vector<uint64_t> hk(cnt);
+        std::vector<int32_t> hi(cnt), hid(Kc);
+        std::vector<double> hs(Kc);
+        CK(cudaMemcpyAsync(hk.data(), gk, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(hi.data(), gi, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        int64_t got = 0;
+        rs_merge_candidates(cnt, hk.data(), hi.data(), Kc, hid.data(), hs.data(), &got);
+        CK(cudaMemcpyAsync(ids_d, hid.data(), sizeof(int32_t) * Kc, cudaMemcpyHostToDevice, c.stream));
+        if (sc_d) CK(cudaMemcpyAsync(sc_d, hs.data(), sizeof(double) * Kc, cudaMemcpyHostToDevice, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
 #else
         return fail(ctx, RS_ENCCL, "librs built without NCCL");
 #endif
@@ -532,6 +546,34 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         CK(cudaMemcpyAsync(scores_out, sc_d, sizeof(double) * Kc, cudaMemcpyDeviceToHost, c.stream));
     if (!dev_ids || !dev_sc) CK(cudaStreamSynchronize(c.stream));
     if (count_out) *count_out = Kc;
+    return RS_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU host protocol
+extern "C" rs_status rs_split_ranges(int64_t n, const int64_t *work_incl, int32_t world, int64_t *bounds_out) {
+    if (n < 0 || world < 1 || !bounds_out || (n > 0 && !work_incl)) return RS_EINVAL;
+    for (int r = 0; r <= world; r++) bounds_out[r] = rs::split_point(work_incl, n, world, r);
+    return RS_OK;
+}
+
+extern "C" rs_status rs_merge_candidates(int64_t count, const uint64_t *keys, const int32_t *ids, int64_t K,
+                                         int32_t *ids_out, double *scores_out, int64_t *count_out) {
+    if (count < 0 || K < 0 || (count > 0 && (!keys || !ids)) || (K > 0 && !ids_out)) return RS_EINVAL;
+    std::vector<int64_t> ord(count);
+    for (int64_t i = 0; i < count; i++) ord[i] = i;
+    const int64_t out = std::min(K, count);
+    std::partial_sort(ord.begin(), ord.begin() + out, ord.end(), [&](int64_t a, int64_t b) {
+        return rs::cand_before(keys[a], ids[a], keys[b], ids[b]);
+    });
+    for (int64_t i = 0; i < out; i++) {
+        ids_out[i] = ids[ord[i]];
+        if (scores_out) {
+            double d;
+            memcpy(&d, &keys[ord[i]], sizeof(d));
+            scores_out[i] = d;
+        }
+    }
+    if (count_out) *count_out = out;
     return RS_OK;
 }
 
