@@ -154,7 +154,10 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
     ESmem &S = *reinterpret_cast<ESmem *>(base);
     double *Ay = (double *)(base + ((sizeof(ESmem) + 15) / 16) * 16);
     unsigned long long ntri = 0, nprobe = 0;
-    const unsigned long long n_items = (unsigned long long)*it.total;
+    // multi-GPU: rank r takes items r, r + world, ... (heaviest first on every rank)
+    const unsigned long long n_all = (unsigned long long)*it.total;
+    const unsigned long long n_items = n_all > (unsigned long long)a.e_rank
+                                           ? (n_all - a.e_rank + a.e_world - 1) / a.e_world : 0ull;
 
     unsigned long long qnext = 0;
     if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         const unsigned long long qi = __shfl_sync(0xffffffffu, qnext, 0);
         if (qi >= n_items) break;
         if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);   // next item, consumed at the loop top
-        const EItem itm = it.items[qi];
+        const EItem itm = it.items[qi * a.e_world + a.e_rank];
         const int32_t y = itm.y;
         const int py = itm.pyl & 0xFFFFFF, ly = (int)((uint32_t)itm.pyl >> 24);
         const int pyt = (int)(itm.dy >> kPrShift);
@@ -455,8 +458,10 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
         }
         return j;
     };
-    for (int64_t y0 = ylo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; y0 < a.n;
-         y0 += nwarps * 32) {
+    // warp task t covers y in [ylo + 32 t, +32); multi-GPU: rank r takes t = r mod world
+    for (int64_t t = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * a.e_world + a.e_rank;
+         ylo + 32 * t < a.n; t += nwarps * a.e_world) {
+        const int64_t y0 = ylo + 32 * t;
         // ---- y level: lane j holds y0 + j
         const int64_t yl = y0 + lane;
         PRec pcl{0, 0, 0};
@@ -664,6 +669,14 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
 template <bool COUNT>
 static cudaError_t launch_e(Ctx &c) {
     CdeArgs a = cde_args(c);
+    if (c.world > 1) {
+        // the middle vertices are shared out; every head's terms are accumulated
+        // here and summed over the ranks afterwards (exact integer limbs)
+        a.head_lo = 0;
+        a.head_hi = c.n;
+        a.e_rank = c.rank;
+        a.e_world = c.world;
+    }
     unsigned long long *ctr = c.scal + kScalCnt0;
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
     const int64_t n_heavy = c.e_nbig;                 // degree classes 5-7 (d >= 128)

@@ -416,7 +416,21 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(cudaEventRecord(c.ev_phase[2], c.stream));
     // Phase E: Type-I triangles
     CK(rs::launch_phase_e(c));
+#ifdef RS_WITH_NCCL
+    if (c.world > 1) {
+        // Phase E is split by middle vertex: sum every head's Type-I limbs (and the
+        // triangle/probe counters) over the ranks; integer sums, exact in any order
+        NK(NCCL.GroupStart());
+        NK(NCCL.AllReduce(c.acc1, c.acc1, (size_t)(3 * n), ncclUint64, ncclSum, c.comm, c.stream));
+        NK(NCCL.AllReduce(c.acc_hub, c.acc_hub, (size_t)(3 * rs::kHubStripes * c.n_hub), ncclUint64, ncclSum,
+                          c.comm, c.stream));
+        NK(NCCL.AllReduce(c.scal + rs::kScalNTri, c.scal + rs::kScalNTri, 2, ncclUint64, ncclSum, c.comm, c.stream));
+        NK(NCCL.GroupEnd());
+    }
+#endif
     CK(cudaEventRecord(c.ev_phase[3], c.stream));
+    // multi-GPU: a rank writes only its heads' scores (scattered in original order)
+    if (c.world > 1) CK(cudaMemsetAsync(c.score, 0, sizeof(double) * n, c.stream));
     // Phase D: Type-II + finalize
     fork(c);
     CK(rs::launch_phase_d(c));
@@ -424,12 +438,10 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(cudaEventRecord(c.ev_phase[4], c.stream));
 #ifdef RS_WITH_NCCL
     if (c.world > 1 && (flags & RS_GATHER_SCORES)) {
-        // owned ranges are contiguous and of different sizes: one broadcast per rank
+        // owned heads are a contiguous internal range, scattered in original order;
+        // every other entry is +0.0 on a rank, so a sum gathers the scores exactly
         NK(NCCL.GroupStart());
-        for (int r = 0; r < c.world; r++) {
-            const int64_t lo = c.bounds[r], hi = c.bounds[r + 1];
-            if (hi > lo) NK(NCCL.Broadcast(c.score + lo, c.score + lo, (size_t)(hi - lo), ncclFloat64, r, c.comm, c.stream));
-        }
+        NK(NCCL.AllReduce(c.score, c.score, (size_t)n, ncclFloat64, ncclSum, c.comm, c.stream));
         NK(NCCL.GroupEnd());
     }
 #endif
@@ -679,6 +691,10 @@ extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_
         // (kept off the timed rs_score path)
         CK(cudaMemsetAsync(c.n1, 0, sizeof(unsigned long long) * (size_t)c.n, c.stream));
         CK(rs::launch_triangle_counts(c));
+#ifdef RS_WITH_NCCL
+        if (c.world > 1)
+            NK(NCCL.AllReduce(c.n1, c.n1, (size_t)c.n, ncclUint64, ncclSum, c.comm, c.stream));
+#endif
         CK(rs::launch_type1_export(c, tmp));
         rs_status s = out_copy(ctx, type1_out, tmp, (size_t)c.n);
         if (s) return s;

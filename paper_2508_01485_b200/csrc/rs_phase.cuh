@@ -28,6 +28,7 @@ struct CdeArgs {
     const uint8_t *__restrict__ lab;    // 8-bit community codes
     unsigned long long *scal;
     int64_t head_lo, head_hi;           // owned head range (multi-GPU); [0, n) on one GPU
+    int32_t e_rank, e_world;            // Phase E: this rank's share of the middle vertices
     bool any_wide;                      // some head may need the 3-limb Type-I accumulator
     double wide_bound;                  // |P(h)|^2 >= wide_bound: head h is wide (VRec::wide)
 };
@@ -47,6 +48,7 @@ inline CdeArgs cde_args(Ctx &c) {
     a.any_wide = (double)c.d_max * (double)c.d_max >= wide_bound(c.k);
     a.wide_bound = wide_bound(c.k);
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
+    a.e_rank = 0; a.e_world = 1;
     return a;
 }
 
