@@ -69,6 +69,10 @@ typedef struct {
 
 /* Flags for rs_score. */
 #define RS_GATHER_SCORES 1u /* multi-GPU: make scores_out complete on every rank */
+/* Test hook: run Phase E (Type-I) as s sequential shares of the multi-GPU
+ * split by middle vertex (s = 2..255) on one GPU; results must not change. */
+#define RS_E_SHARES(s)    (((uint32_t)(s) & 0xFFu) << 8)
+#define RS_E_SHARES_OF(f) (((f) >> 8) & 0xFFu)
 
 /* Create a context on CUDA device `device`. `cuda_stream` is a cudaStream_t
  * (NULL = the legacy default stream) on which all work is issued; the caller

@@ -22,6 +22,11 @@ LIB_PATH = os.path.join(_HERE, "librs.so")
 RS_OK, RS_EINVAL, RS_ESTATE, RS_ENOMEM, RS_ECUDA, RS_ENCCL = 0, -1, -2, -3, -4, -5
 RS_VALIDATE = 1
 RS_GATHER_SCORES = 1
+
+
+def RS_E_SHARES(s: int) -> int:
+    """rs_score test hook: Phase E as s sequential shares of the multi-GPU split."""
+    return (int(s) & 0xFF) << 8
 _STATUS = {0: "RS_OK", -1: "RS_EINVAL", -2: "RS_ESTATE", -3: "RS_ENOMEM", -4: "RS_ECUDA", -5: "RS_ENCCL"}
 
 

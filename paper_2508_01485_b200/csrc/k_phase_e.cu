@@ -677,8 +677,9 @@ static cudaError_t launch_e(Ctx &c) {
         a.e_rank = c.rank;
         a.e_world = c.world;
     }
+    // test hook (RS_E_SHARES): the rank split run as sequential shares on one GPU
+    const int shares = c.world > 1 ? 1 : std::max(1, c.e_shares);
     unsigned long long *ctr = c.scal + kScalCnt0;
-    cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
     const int64_t n_heavy = c.e_nbig;                 // degree classes 5-7 (d >= 128)
     EItems it{nullptr, nullptr};
     if (n_heavy > 0) {
@@ -695,15 +696,22 @@ static cudaError_t launch_e(Ctx &c) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase_e<COUNT>, kWarpsE * 32, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    if (n_heavy > 0) {
-        k_phase_e<COUNT><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
-        c.launches++;
-    }
-    if (n_heavy < c.n) {
-        const int64_t threads = c.n - n_heavy;            // a warp per 32 vertices
-        const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
-        k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, c.stream>>>(a, n_heavy);
-        c.launches++;
+    for (int s = 0; s < shares; s++) {
+        if (shares > 1) {
+            a.e_rank = s;
+            a.e_world = shares;
+        }
+        cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
+        if (n_heavy > 0) {
+            k_phase_e<COUNT><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
+            c.launches++;
+        }
+        if (n_heavy < c.n) {
+            const int64_t threads = c.n - n_heavy;        // a warp per 32 vertices
+            const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
+            k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, c.stream>>>(a, n_heavy);
+            c.launches++;
+        }
     }
     return cudaGetLastError();
 }

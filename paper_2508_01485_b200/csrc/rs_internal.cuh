@@ -152,6 +152,7 @@ struct Ctx {
     int64_t k_alloc = 0;         // k the per-score buffers were sized for
     int64_t kn_alloc = 0;        // ... and n
     bool scored = false;
+    int e_shares = 1;            // test hook: Phase E run as this many rank shares (rs_score flags)
 
     // top-k scratch
     unsigned long long *tk_hist = nullptr;   // 256 * 8
