@@ -83,16 +83,89 @@ __global__ void k_relabel_rows(const int64_t *__restrict__ rp_o, const int32_t *
     }
 }
 // number of vertices with degree >= bin_lo(cls), cls = 1..7 (degrees sorted descending)
+// (out[kNumBins]: degree >= 512, a split point of the row sorts)
 __global__ void k_class_bounds(const uint32_t *__restrict__ deg_s, int64_t n, unsigned long long *out) {
     const int cls = threadIdx.x + 1;
-    if (cls >= kNumBins) return;
-    const int64_t lo_deg = bin_lo(cls);
+    if (cls > kNumBins) return;
+    const int64_t lo_deg = cls == kNumBins ? 512 : bin_lo(cls);
     int64_t lo = 0, hi = n;   // first r with deg_s[r] < lo_deg
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if ((int64_t)deg_s[mid] >= lo_deg) lo = mid + 1; else hi = mid;
     }
     out[cls] = (unsigned long long)lo;
+}
+
+// rows of length in [lo, cap] sorted by one CTA each (cub::BlockRadixSort in
+// shared memory, keys < 2^bits; padding keys 2^bits - 1 sort last)
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) k_row_sort(const int64_t *__restrict__ rowptr, int64_t r0, int64_t r1,
+                                                      const int32_t *__restrict__ in, int32_t *out, int bits) {
+    using BRS = cub::BlockRadixSort<uint32_t, THREADS, ITEMS>;
+    __shared__ typename BRS::TempStorage ts;
+    const uint32_t pad = bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u;
+    for (int64_t r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const int64_t b = rowptr[r];
+        const int d = (int)(rowptr[r + 1] - b);
+        uint32_t keys[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const int idx = threadIdx.x * ITEMS + i;
+            keys[i] = idx < d ? (uint32_t)in[b + idx] : pad;
+        }
+        BRS(ts).Sort(keys, 0, bits);
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const int idx = threadIdx.x * ITEMS + i;
+            if (idx < d) out[b + idx] = (int32_t)keys[i];
+        }
+        __syncthreads();
+    }
+}
+
+// rows of at most 32 J entries: a warp per row, bitonic sort in registers
+// (element i = 32 j + lane; partners across lanes by shuffle, within a lane by
+// register swap), padding keys 0xFFFFFFFF sort last
+template <int J>
+__global__ void __launch_bounds__(256) k_row_sort_warp(const int64_t *__restrict__ rowptr, int64_t r0, int64_t r1,
+                                                       const int32_t *__restrict__ in, int32_t *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < r1; r += nw) {
+        const int64_t b = rowptr[r];
+        const int d = (int)(rowptr[r + 1] - b);
+        uint32_t v[J];
+#pragma unroll
+        for (int j = 0; j < J; j++) v[j] = 32 * j + lane < d ? (uint32_t)in[b + 32 * j + lane] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 2; k <= 32 * J; k <<= 1) {
+#pragma unroll
+            for (int s = k >> 1; s > 0; s >>= 1) {
+                if (s >= 32) {
+#pragma unroll
+                    for (int j = 0; j < J; j++) {
+                        const int pj = j ^ (s >> 5);
+                        if (pj > j) {
+                            const bool up = ((32 * j + lane) & k) == 0;
+                            const uint32_t a = v[j], c = v[pj];
+                            if ((a > c) == up) { v[j] = c; v[pj] = a; }
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < J; j++) {
+                        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[j], s);
+                        const bool up = ((32 * j + lane) & k) == 0;
+                        const bool low = (lane & s) == 0;
+                        v[j] = (low == up) ? min(v[j], o) : max(v[j], o);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < J; j++)
+            if (32 * j + lane < d) out[b + 32 * j + lane] = (int32_t)v[j];
+    }
 }
 
 // temporaries of launch_relabel, carved from the caller's arena
@@ -103,7 +176,10 @@ size_t relabel_arena_bytes(int64_t n, int64_t nnz) {
     cub::DeviceScan::ExclusiveSum(nullptr, need_scan, (int64_t *)nullptr, (int64_t *)nullptr, (int)(n + 1));
     cub::DeviceSegmentedSort::SortKeys(nullptr, need_seg, (int32_t *)nullptr, (int32_t *)nullptr, nnz, (int)n,
                                        (int64_t *)nullptr, (int64_t *)nullptr);
-    const size_t cub_b = std::max(need_sort, std::max(need_scan, need_seg));
+    size_t need_rad = 0;
+    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, need_rad, (int32_t *)nullptr, (int32_t *)nullptr, nnz, (int)n,
+                                            (int64_t *)nullptr, (int64_t *)nullptr, 0, 32);
+    const size_t cub_b = std::max(std::max(need_sort, need_scan), std::max(need_seg, need_rad));
     return 3 * (4 * (size_t)n + 256) + (8 * (size_t)(n + 1) + 256) + (4 * (size_t)std::max<int64_t>(nnz, 1) + 256) +
            cub_b + 256;
 }
@@ -129,16 +205,39 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, vo
     t1 = need;
     cub::DeviceScan::ExclusiveSum(tmp, t1, d64, c.rowptr, (int)(n + 1), c.stream);
     k_relabel_rows<<<148 * 16, 256, 0, c.stream>>>(rp_o, col_o, c.perm, c.inv, c.rowptr, n, tmpcol);
-    t1 = need;
-    if (nnz) cub::DeviceSegmentedSort::SortKeys(tmp, t1, tmpcol, c.col, nnz, (int)n, c.rowptr, c.rowptr + 1, c.stream);
     k_class_bounds<<<1, 32, 0, c.stream>>>(deg_s, n, c.scal + kScalTk);
-    c.launches += 8;
-    unsigned long long ge[kNumBins] = {0};
+    c.launches += 6;
+    unsigned long long ge[kNumBins + 1] = {0};
     uint32_t dmax = 0;
     cudaMemcpyAsync(ge, c.scal + kScalTk, sizeof(ge), cudaMemcpyDeviceToHost, c.stream);
     cudaMemcpyAsync(&dmax, deg_s, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream);
     if ((e = cudaStreamSynchronize(c.stream))) return e;
     if ((e = cudaGetLastError())) return e;
+    // every row sorted by internal id. Rows are in degree-descending order, so
+    // each length class is a contiguous range: rows >= 8192 with CUB's segmented
+    // radix sort, [512, 8192) one CTA per row (block radix sort sized to the
+    // class), < 512 a warp per row (register bitonic). Keys need log2(n) bits.
+    if (nnz) {
+        int bits = 1;
+        while (bits < 31 && (1ll << bits) < n) bits++;
+        const int64_t r8192 = (int64_t)ge[7], r2048 = (int64_t)ge[6], r512 = (int64_t)ge[kNumBins];
+        const int64_t r128 = (int64_t)ge[5], r32 = (int64_t)ge[3];
+        if (r8192 > 0) {
+            int64_t e8 = 0;
+            if ((e = cudaMemcpy(&e8, c.rowptr + r8192, sizeof(int64_t), cudaMemcpyDeviceToHost))) return e;
+            t1 = need;
+            cub::DeviceSegmentedRadixSort::SortKeys(tmp, t1, tmpcol, c.col, e8, (int)r8192, c.rowptr, c.rowptr + 1, 0,
+                                                    bits, c.stream);
+            c.launches++;
+        }
+        auto wgrid = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 7) / 8, 148 * 16)); };
+        auto rows = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(hi - lo, 148 * 32)); };
+        if (r2048 > r8192) { k_row_sort<256, 32><<<rows(r8192, r2048), 256, 0, c.stream>>>(c.rowptr, r8192, r2048, tmpcol, c.col, bits); c.launches++; }
+        if (r512 > r2048) { k_row_sort<256, 8><<<rows(r2048, r512), 256, 0, c.stream>>>(c.rowptr, r2048, r512, tmpcol, c.col, bits); c.launches++; }
+        if (r128 > r512) { k_row_sort_warp<16><<<wgrid(r512, r128), 256, 0, c.stream>>>(c.rowptr, r512, r128, tmpcol, c.col); c.launches++; }
+        if (r32 > r128) { k_row_sort_warp<4><<<wgrid(r128, r32), 256, 0, c.stream>>>(c.rowptr, r128, r32, tmpcol, c.col); c.launches++; }
+        if (n > r32) { k_row_sort_warp<1><<<wgrid(r32, n), 256, 0, c.stream>>>(c.rowptr, r32, n, tmpcol, c.col); c.launches++; }
+    }
     // ge[cls] = #vertices with degree >= bin_lo(cls); class cls = [ge[cls+1], ge[cls])
     ge[0] = (unsigned long long)n;
     for (int cls = 0; cls < kNumBins; cls++) {
