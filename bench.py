@@ -37,7 +37,10 @@ import gen  # noqa: E402
 METRIC = "RSI-scored edges/sec (GTEPS)"
 # DRAM bytes per launch of the dominant phase from the committed ncu captures
 # (profiles/); filled per round, None when not captured for that config
-TRAFFIC_NCU = {}
+# ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per step of the
+# dominant phase (profiles/r01_full_phaseE_summary.txt: heavy 5.767 + 0.126 GB,
+# light 1.586 + 0.017 GB; ncu flushes the L2 before each kernel)
+TRAFFIC_NCU = {"orkut": {"E_type1_triangles": 7.496e9}}
 UNIT = "GTEPS"
 
 

@@ -1,10 +1,12 @@
-"""Summarise an ncu --csv launch list: per-kernel count, time, DRAM bytes."""
+"""Summarise an ncu --csv launch list: per-kernel launch count, total time over
+the capture, mean time per launch, DRAM bytes (if captured), share of the total.
+usage: launches.py list.csv [top]"""
 import collections
 import csv
 import sys
 
 
-def summarise(path, runs=1, top=30):
+def summarise(path, top=40):
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
@@ -28,10 +30,10 @@ def summarise(path, runs=1, top=30):
     tot = sum(a[1] for a in agg.values())
     out = []
     for k, (c, t, r, w) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-        out.append(f"{k:70s} n={c:4d} t/run={t / 1e6 / runs:8.3f}ms rd/run={r / 1e9 / runs:7.3f}GB "
-                   f"wr/run={w / 1e9 / runs:6.3f}GB {100 * t / tot:5.1f}%")
+        out.append(f"{k:70s} n={c:4d} total={t / 1e6:8.3f}ms mean={t / 1e6 / max(c, 1):7.3f}ms "
+                   f"rd={r / 1e9:7.3f}GB wr={w / 1e9:6.3f}GB {100 * t / tot:5.1f}%")
     return "\n".join(out)
 
 
 if __name__ == "__main__":
-    print(summarise(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 1))
+    print(summarise(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40))
