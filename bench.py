@@ -38,9 +38,11 @@ METRIC = "RSI-scored edges/sec (GTEPS)"
 # DRAM bytes per launch of the dominant phase from the committed ncu captures
 # (profiles/); filled per round, None when not captured for that config
 # ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per step of the
-# dominant phase (profiles/r01_full_phaseE_summary.txt: heavy 5.767 + 0.126 GB,
-# light 1.586 + 0.017 GB; ncu flushes the L2 before each kernel)
-TRAFFIC_NCU = {"orkut": {"E_type1_triangles": 7.496e9}}
+# dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 5.767 +
+# 0.126 GB, light 1.586 + 0.017 GB) + the Phase D launches of
+# profiles/r01_full_phaseACD_summary.txt (2.056 + 0.091 GB); ncu flushes the L2
+# before each kernel, so this bounds the in-step traffic from above
+TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 9.643e9}}
 UNIT = "GTEPS"
 
 
@@ -127,8 +129,9 @@ def phase_bytes(n, D, Db, k, ntri, nb, nprobe):
     A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 20 * k * n + 16 * n
     C = 8 * n + 16 * n + 4 * Db + 16 * Db + 8 * k * n + 16 * k * nb + 2 * Db + 8 * n
     E = 4 * nprobe + 20 * (Db // 2) + 32 * ntri + 8 * k * n
-    D_ = 8 * n + 16 * n + 4 * Db + 16 * Db + 24 * n + 8 * n
-    return {"A": A, "C": C, "E": E, "D": D_}
+    D_ = 8 * n + 16 * n + 4 * Db + 16 * Db + 16 * n          # Type-II pull (concurrent with E)
+    F = 16 * n + 24 * n + 16 * n + 8 * n + 4 * n + 8 * n      # finalize: sums, vrec, rowptr, perm, score
+    return {"A": A, "C": C, "ED": E + D_, "F": F}
 
 
 def main():
@@ -230,7 +233,7 @@ def main():
         s = sc.score(stats=True)
         ph.append(s["ms_phase"][:4])
     ph = np.median(np.array(ph), axis=0)
-    names = ["A_border_hist_weights", "C_btable_orient", "E_type1_triangles", "D_type2_finalize"]
+    names = ["A_border_hist_weights", "C_btable_orient", "ED_type1_type2", "F_finalize"]
     Db, nb, ntri, nprobe = st["n_pred_entries"], st["n_border"], st["n_triangles"], st["n_probes"]
     pb = phase_bytes(n, D, Db, a.k, ntri, nb, nprobe)
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -238,7 +241,7 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     # every phase against the HBM roof (phase time = CUDA events on the library
     # stream around the phase's launches); the dominant one is the headline
-    keys = {"A_border_hist_weights": "A", "C_btable_orient": "C", "E_type1_triangles": "E", "D_type2_finalize": "D"}
+    keys = {"A_border_hist_weights": "A", "C_btable_orient": "C", "ED_type1_type2": "ED", "F_finalize": "F"}
     phases = {}
     for nm, ms in zip(names, ph):
         by = pb[keys[nm]]

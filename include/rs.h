@@ -60,8 +60,9 @@ typedef struct {
     double omega_max;         /* max weight over all cells (C-7)  */
     float ms_phase[8];        /* [0] Phase A border/histogram/weights/G' lists
                                  [1] Phase C B-table + orientation
-                                 [2] Phase E Type-I triangles
-                                 [3] Phase D Type-II + finalize [4..7] reserved */
+                                 [2] Phase E Type-I triangles, concurrent with
+                                     Phase D Type-II pull
+                                 [3] finalize (sum, normalise) [4..7] reserved */
 } rs_stats;
 
 /* Flags for rs_load_csr. */

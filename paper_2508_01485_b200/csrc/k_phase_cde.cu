@@ -188,15 +188,14 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_phase_c_cta(CdeArgs a) {
 }
 
 // ============================================================================
-// Phase D: Type-II pull for every head + Type-I limbs + finalize.
+// Phase D: Type-II pull for every head (concurrent with Phase E: it needs only
+// Phase C's B table), then the finalize pass adds the Type-I limbs and
+// normalises.
 // ============================================================================
 template <int U, class GR>
-__device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &g, double wmax) {
+__device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &g) {
     const VRec ru = a.vrec[u];
-    if (!ru.head || u < a.head_lo || u >= a.head_hi) {
-        if (g.lane == 0 && u >= a.head_lo && u < a.head_hi) a.score[a.perm[u]] = 0.0;
-        return;
-    }
+    if (!ru.head || u < a.head_lo || u >= a.head_hi) return;   // finalize writes R = 0
     const int cu = ru.lab;
     const double au = ru.a_self;
     const int pc = ru.pcnt;
@@ -205,7 +204,6 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const int pt = pm + pr_plus_t(pr);         // [pm, pt): target run; [pt, pc): the other run
     const int64_t dw = pr_start(pr), de = dw + dcap(pc) - 1 + pt;   // the other run: de - i, descending
     const int64_t beg = a.rowptr[u];
-    const int64_t d = a.rowptr[u + 1] - beg;
     U128 S = u128_zero();
     for (int base = 0; base < pc; base += GR::size * U) {
         int32_t w[U];
@@ -230,17 +228,31 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
         }
     }
     S = g.sum(S);
-    if (g.lane == 0) {
-        const bool wide = a.any_wide && ru.wide;
-        const unsigned long long *acc = a.acc1 + 3 * u;
-        S = u128_add(S, wide ? fx_from3(acc) : fx_from2(acc));
-        if (u < a.n_hub)
-            for (int s = 0; s < kHubStripes; s++) {
-                const unsigned long long *h = a.acc_hub + 3 * ((int64_t)s * a.n_hub + u);
-                S = u128_add(S, wide ? fx_from3(h) : fx_from2(h));
-            }
+    if (g.lane == 0) a.t2[u] = make_ulonglong2(S.lo, S.hi);   // the exact Type-II sum
+}
+
+// R(u) = (Type-II + Type-I) / omega_max / (d(d-1)) for every owned vertex, in
+// original order (0 for non-heads, C-22)
+__global__ void __launch_bounds__(256) k_finalize(CdeArgs a) {
+    const double wmax = __longlong_as_double((long long)a.scal[kScalOmegaMaxBits]);
+    for (int64_t u = a.head_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.head_hi;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const VRec ru = a.vrec[u];
         double R = 0.0;
-        if (wmax > 0.0) R = fx_to_double(S) / wmax / ((double)d * (double)(d - 1));
+        if (ru.head) {
+            const ulonglong2 t = a.t2[u];
+            U128 S{t.x, t.y};
+            const bool wide = a.any_wide && ru.wide;
+            const unsigned long long *acc = a.acc1 + 3 * u;
+            S = u128_add(S, wide ? fx_from3(acc) : fx_from2(acc));
+            if (u < a.n_hub)
+                for (int s = 0; s < kHubStripes; s++) {
+                    const unsigned long long *h = a.acc_hub + 3 * ((int64_t)s * a.n_hub + u);
+                    S = u128_add(S, wide ? fx_from3(h) : fx_from2(h));
+                }
+            const double d = (double)(a.rowptr[u + 1] - a.rowptr[u]);
+            if (wmax > 0.0) R = fx_to_double(S) / wmax / (d * (d - 1.0));
+        }
         a.score[a.perm[u]] = R;
     }
 }
@@ -248,18 +260,16 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
 template <int G, int U>
 __global__ void __launch_bounds__(256) k_phase_d_warp(CdeArgs a) {
     WarpGroup<G> g;
-    const double wmax = __longlong_as_double((long long)a.scal[kScalOmegaMaxBits]);
     const int64_t gpb = blockDim.x / G;
     for (int64_t i = blockIdx.x * gpb + threadIdx.x / G; i < a.nverts; i += (int64_t)gridDim.x * gpb)
-        phase_d_vertex<U>(a, a.vlo + i, g, wmax);
+        phase_d_vertex<U>(a, a.vlo + i, g);
 }
 
 __global__ void __launch_bounds__(kCtaThreads) k_phase_d_cta(CdeArgs a) {
     __shared__ int s_i[kCtaWarps + 1];
     __shared__ unsigned long long s_u[2 * kCtaWarps];
     CtaGroup g(s_i, s_u);
-    const double wmax = __longlong_as_double((long long)a.scal[kScalOmegaMaxBits]);
-    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) phase_d_vertex<4>(a, a.vlo + i, g, wmax);
+    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) phase_d_vertex<4>(a, a.vlo + i, g);
 }
 
 // ============================================================================
@@ -318,6 +328,15 @@ cudaError_t launch_phase_d(Ctx &c) {
         else if (cls == 3) launch_grid(c, k_phase_d_warp<4, 4>, a.nverts, 64, s, a);
         else launch_grid(c, k_phase_d_warp<4, 2>, a.nverts, 64, s, a);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(Ctx &c) {
+    CdeArgs a = cde_args(c);
+    const int64_t m = c.head_hi - c.head_lo;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 8));
+    k_finalize<<<(unsigned)blocks, 256, 0, c.stream>>>(a);
+    c.launches++;
     return cudaGetLastError();
 }
 

@@ -667,7 +667,7 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
 }
 
 template <bool COUNT>
-static cudaError_t launch_e(Ctx &c) {
+static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     CdeArgs a = cde_args(c);
     if (c.world > 1) {
         // the middle vertices are shared out; every head's terms are accumulated
@@ -702,21 +702,23 @@ static cudaError_t launch_e(Ctx &c) {
             a.e_world = shares;
         }
         cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
-        if (n_heavy > 0) {
-            k_phase_e<COUNT><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
-            c.launches++;
-        }
-        if (n_heavy < c.n) {
+        if (n_heavy < c.n) {                              // light first (see rs_score)
             const int64_t threads = c.n - n_heavy;        // a warp per 32 vertices
             const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
-            k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, c.stream>>>(a, n_heavy);
+            k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, light>>>(a, n_heavy);
+            c.launches++;
+        }
+        if (n_heavy > 0) {
+            k_phase_e<COUNT><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
             c.launches++;
         }
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_phase_e(Ctx &c) { return launch_e<false>(c); }
-cudaError_t launch_triangle_counts(Ctx &c) { return launch_e<true>(c); }
+cudaError_t launch_phase_e(Ctx &c) { return launch_e<false>(c, c.stream); }
+// light kernel on `light` (forked from c.stream by the caller)
+cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light) { return launch_e<false>(c, light); }
+cudaError_t launch_triangle_counts(Ctx &c) { return launch_e<true>(c, c.stream); }
 
 }  // namespace rs

@@ -113,10 +113,10 @@ static void dfree(T *&p) {
 
 static void fork(Ctx &c) {
     cudaEventRecord(c.ev_fork, c.stream);
-    for (int i = 0; i < rs::kNumBins; i++) cudaStreamWaitEvent(c.side[i], c.ev_fork, 0);
+    for (int i = 0; i < rs::kNumBins + 1; i++) cudaStreamWaitEvent(c.side[i], c.ev_fork, 0);
 }
 static void join(Ctx &c) {
-    for (int i = 0; i < rs::kNumBins; i++) {
+    for (int i = 0; i < rs::kNumBins + 1; i++) {
         cudaEventRecord(c.ev_join[i], c.side[i]);
         cudaStreamWaitEvent(c.stream, c.ev_join[i], 0);
     }
@@ -136,7 +136,7 @@ static rs_status create_common(rs_ctx **out, int device, void *cuda_stream) {
     Ctx &c = ctx->c;
     c.device = device;
     c.stream = (cudaStream_t)cuda_stream;
-    for (int i = 0; i < rs::kNumBins; i++) {
+    for (int i = 0; i < rs::kNumBins + 1; i++) {
         CK(cudaStreamCreateWithFlags(&c.side[i], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
@@ -198,7 +198,7 @@ static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
     dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pd); dfree(c.wd); dfree(c.dpos); c.cap_d = 0; dfree(c.pc2); dfree(c.amat);
-    dfree(c.acc1); dfree(c.acc_hub); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
+    dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
     ctx->l2n = 0;
@@ -212,7 +212,7 @@ extern "C" void rs_destroy(rs_ctx *ctx) {
     free_graph(ctx);
     dfree(c.chist); dfree(c.ccode); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist); dfree(c.arena);
     dfree(ctx->utargets); dfree(ctx->stage_i32); dfree(ctx->stage_f64); dfree(ctx->cand_key); dfree(ctx->cand_id);
-    for (int i = 0; i < rs::kNumBins; i++) {
+    for (int i = 0; i < rs::kNumBins + 1; i++) {
         if (c.side[i]) cudaStreamDestroy(c.side[i]);
         if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
     }
@@ -318,6 +318,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         c.n_hub = std::min<int64_t>(n, rs::kHubMax);
         CK(dalloc(&c.acc_hub, 3 * rs::kHubStripes * c.n_hub));
         CK(dalloc(&c.n1, n));
+        CK(dalloc(&c.t2, n));
         CK(dalloc(&c.score, n));
         c.cap_n = n;
         c.cap_nnz = nnz;
@@ -415,8 +416,13 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(rs::launch_phase_c(c));
     join(c);
     CK(cudaEventRecord(c.ev_phase[2], c.stream));
-    // Phase E: Type-I triangles
-    CK(rs::launch_phase_e(c));
+    // Phase E (Type-I triangles) and Phase D (Type-II pull, which needs only
+    // Phase C's B table) run concurrently: E heavy on the library stream, E light
+    // and the D bins on the forked streams
+    fork(c);
+    CK(rs::launch_phase_d(c));                           // first: their blocks are queued ahead of
+    CK(rs::launch_phase_e_on(c, c.side[rs::kNumBins]));  // the persistent heavy Phase E grid
+    join(c);
 #ifdef RS_WITH_NCCL
     if (c.world > 1) {
         // Phase E is split by middle vertex: sum every head's Type-I limbs (and the
@@ -432,10 +438,8 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(cudaEventRecord(c.ev_phase[3], c.stream));
     // multi-GPU: a rank writes only its heads' scores (scattered in original order)
     if (c.world > 1) CK(cudaMemsetAsync(c.score, 0, sizeof(double) * n, c.stream));
-    // Phase D: Type-II + finalize
-    fork(c);
-    CK(rs::launch_phase_d(c));
-    join(c);
+    // finalize: Type-II + Type-I sums, / omega_max / d(d-1), original order
+    CK(rs::launch_finalize(c));
     CK(cudaEventRecord(c.ev_phase[4], c.stream));
 #ifdef RS_WITH_NCCL
     if (c.world > 1 && (flags & RS_GATHER_SCORES)) {
@@ -468,7 +472,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(cudaMemcpy(&wb, c.scal + rs::kScalOmegaMaxBits, sizeof(wb), cudaMemcpyDeviceToHost));
         memcpy(&s.omega_max, &wb, sizeof(double));
         for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&s.ms_phase[i], c.ev_phase[i], c.ev_phase[i + 1]));
-        // ms_phase: [0] A (incl. zeroing) [1] C [2] E (Type-I) [3] D (Type-II + finalize)
+        // ms_phase: [0] A (incl. zeroing) [1] C [2] E (Type-I) || D (Type-II) [3] finalize
         *stats_out = s;
     }
     (void)flags;

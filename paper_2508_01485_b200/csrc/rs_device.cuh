@@ -58,7 +58,7 @@ __device__ __forceinline__ double fx_to_double(U128 v) {
     else { top = (v.hi << lz) | (v.lo >> (64 - lz)); rest = v.lo << lz; }
     if (rest) top |= 1ull;                        // sticky bit below the rounding point
     // v = top * 2^(64 - lz) (up to the sticky bit), times 2^-64
-    return __ull2double_rn(top) * exp2((double)(-lz));
+    return __ull2double_rn(top) * __longlong_as_double((long long)(1023 - lz) << 52);   // * 2^-lz, exact
 }
 
 // Type-I accumulators are three 64-bit limbs per head updated with

@@ -92,8 +92,8 @@ struct Bins {
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t side[kNumBins] = {nullptr};   // forked streams for concurrent bins
-    cudaEvent_t ev_fork = nullptr, ev_join[kNumBins] = {nullptr};
+    cudaStream_t side[kNumBins + 1] = {nullptr};   // forked streams: concurrent bins (+ light Phase E)
+    cudaEvent_t ev_fork = nullptr, ev_join[kNumBins + 1] = {nullptr};
     cudaEvent_t ev_phase[8] = {nullptr};
     std::string err;
     int64_t launches = 0;
@@ -147,6 +147,7 @@ struct Ctx {
     unsigned long long *acc_hub = nullptr;  // kHubStripes copies of the limbs of the first n_hub vertices
     int64_t n_hub = 0;                   //   (the highest degrees: contended heads), summed by Phase D
     unsigned long long *n1 = nullptr;    // n Type-I triad counts
+    ulonglong2 *t2 = nullptr;            // n exact Type-II sums (Phase D, read by the finalize pass)
     double *score = nullptr;     // n, ORIGINAL vertex order
     unsigned long long *scal = nullptr;  // device scalars (see kScal*)
     int64_t k_alloc = 0;         // k the per-score buffers were sized for
@@ -201,6 +202,8 @@ cudaError_t launch_phase_c(Ctx &c);
 cudaError_t launch_dense_pos(Ctx &c);
 cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
+cudaError_t launch_finalize(Ctx &c);
+cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light);
 cudaError_t launch_triangle_counts(Ctx &c);
 cudaError_t launch_e_items(Ctx &c);
 cudaError_t launch_topk(Ctx &c, int64_t K, int32_t *ids_dev, double *scores_dev, int64_t lo, int64_t hi);

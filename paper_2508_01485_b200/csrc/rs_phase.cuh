@@ -23,6 +23,7 @@ struct CdeArgs {
     unsigned long long *__restrict__ acc_hub;  // striped limbs of vertices < n_hub
     int64_t n_hub;
     unsigned long long *__restrict__ n1;    // Type-I triad counts (COUNT mode)
+    ulonglong2 *__restrict__ t2;            // exact Type-II sum per head (Phase D)
     double *__restrict__ score;         // original vertex order
     const int32_t *__restrict__ perm;   // internal -> original id
     const uint8_t *__restrict__ lab;    // 8-bit community codes
@@ -43,7 +44,7 @@ inline CdeArgs cde_args(Ctx &c) {
     a.rowptr = c.rowptr; a.vlo = 0; a.nverts = 0; a.n = c.n; a.k = c.k;
     a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pc2 = c.pc2;
     a.pd = c.pd; a.wd = c.wd; a.dpos = c.dpos;
-    a.bq = c.bq; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.score = c.score; a.scal = c.scal;
+    a.bq = c.bq; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.t2 = c.t2; a.score = c.score; a.scal = c.scal;
     a.perm = c.perm; a.lab = c.lab;
     a.any_wide = (double)c.d_max * (double)c.d_max >= wide_bound(c.k);
     a.wide_bound = wide_bound(c.k);
