@@ -126,12 +126,13 @@ def phase_bytes(n, D, Db, k, ntri, nb, nprobe):
     volume (4 B per probed P+ entry), 20 B per G' edge (the P-
     entry and the predecessor's record), 32 B per Type-I triangle (weights and
     head updates) and y's weight rows."""
-    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 20 * k * n + 16 * n
-    C = 8 * n + 16 * n + 4 * Db + 16 * Db + 8 * k * n + 16 * k * nb + 2 * Db + 8 * n
+    # A: row, labels, P(u) writes, weights, vrec; then P(u) re-read, the P+ runs
+    # with their weights (half of P), the B pushes (16 B per P entry), PRec
+    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 28 * k * n + 16 * n + 4 * Db + 6 * Db + 16 * Db + 16 * n
     E = 4 * nprobe + 20 * (Db // 2) + 32 * ntri + 8 * k * n
-    D_ = 8 * n + 16 * n + 4 * Db + 16 * Db + 16 * n          # Type-II pull (concurrent with E)
+    D_ = 4 * Db + 32 * Db + 16 * n + 16 * n                   # Type-II pull (concurrent with E)
     F = 16 * n + 24 * n + 16 * n + 8 * n + 4 * n + 8 * n      # finalize: sums, vrec, rowptr, perm, score
-    return {"A": A, "C": C, "ED": E + D_, "F": F}
+    return {"A": A, "ED": E + D_, "F": F}
 
 
 def main():
@@ -231,9 +232,9 @@ def main():
             flush.fill_(7)
         sc.set_communities(comm_d, a.k)
         s = sc.score(stats=True)
-        ph.append(s["ms_phase"][:4])
+        ph.append([s["ms_phase"][0], s["ms_phase"][2], s["ms_phase"][3]])
     ph = np.median(np.array(ph), axis=0)
-    names = ["A_border_hist_weights", "C_btable_orient", "ED_type1_type2", "F_finalize"]
+    names = ["A_hist_weights_lists", "ED_type1_type2", "F_finalize"]
     Db, nb, ntri, nprobe = st["n_pred_entries"], st["n_border"], st["n_triangles"], st["n_probes"]
     pb = phase_bytes(n, D, Db, a.k, ntri, nb, nprobe)
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -241,7 +242,7 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     # every phase against the HBM roof (phase time = CUDA events on the library
     # stream around the phase's launches); the dominant one is the headline
-    keys = {"A_border_hist_weights": "A", "C_btable_orient": "C", "ED_type1_type2": "ED", "F_finalize": "F"}
+    keys = {"A_hist_weights_lists": "A", "ED_type1_type2": "ED", "F_finalize": "F"}
     phases = {}
     for nm, ms in zip(names, ph):
         by = pb[keys[nm]]

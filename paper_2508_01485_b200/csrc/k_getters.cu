@@ -81,24 +81,20 @@ __global__ void k_pcnt64(const VRec *__restrict__ vrec, const int32_t *__restric
         out[v] = vrec[inv[v]].pcnt;
 }
 // original row v <- internal P list of inv[v], mapped to original ids (unsorted)
-// P(u) after Phase C = P-(u) at the front of pidx + the two runs of P+(u) in pd
-__device__ __forceinline__ int32_t p_entry(const int64_t *rowptr, const int32_t *pidx, const int32_t *pd,
-                                           const PRec &pr, int64_t u, int i) {
-    const int pm = pr.y - pr.x, pt = pm + pr_plus_t(pr);
-    const int64_t dw = pr_start(pr);
-    return i < pm ? pidx[rowptr[u] + i] : (i < pt ? pd[dw + i - pm] : pd[dw + dcap(pr.y) - 1 - (i - pt)]);
+// P(u): ascending at rowptr[u] in pidx (Phase A)
+__device__ __forceinline__ int32_t p_entry(const int64_t *rowptr, const int32_t *pidx, int64_t u, int i) {
+    return pidx[rowptr[u] + i];
 }
 
 __global__ void k_pred_copy(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ pidx,
-                            const int32_t *__restrict__ pd, const PRec *__restrict__ pc2,
-                            const int32_t *__restrict__ inv, const int32_t *__restrict__ perm,
+                            const PRec *__restrict__ pc2, const int32_t *__restrict__ inv, const int32_t *__restrict__ perm,
                             const int64_t *__restrict__ off, int64_t n, int32_t *out) {
     const int lane = threadIdx.x & 31;
     for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; v < n;
          v += ((int64_t)gridDim.x * blockDim.x) / 32) {
         const int32_t u = inv[v];
         const PRec pr = pc2[u];
-        for (int i = lane; i < pr.y; i += 32) out[off[v] + i] = perm[p_entry(rowptr, pidx, pd, pr, u, i)];
+        for (int i = lane; i < pr.y; i += 32) out[off[v] + i] = perm[p_entry(rowptr, pidx, u, i)];
     }
 }
 
@@ -125,7 +121,7 @@ cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int6
         int32_t *unsorted = nullptr;
         void *stmp = nullptr;
         if ((e = cudaMalloc(&unsorted, sizeof(int32_t) * tot))) return e;
-        k_pred_copy<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.pidx, c.pd, c.pc2, c.inv, c.perm, off, n, unsorted);
+        k_pred_copy<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.pidx, c.pc2, c.inv, c.perm, off, n, unsorted);
         size_t sneed = 0;
         cub::DeviceSegmentedSort::SortKeys(nullptr, sneed, unsorted, pred_dev, tot, (int)n, off, off + 1, c.stream);
         if ((e = cudaMalloc(&stmp, std::max<size_t>(sneed, 1)))) { cudaFree(unsorted); return e; }
@@ -142,8 +138,7 @@ cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int6
 // (all such v are foreign to w) closes a Type-II triad (u, w, v).
 // Written at out[perm[u]] (original order).
 __global__ void k_type2_counts(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ pidx,
-                               const int32_t *__restrict__ pd, const PRec *__restrict__ pc2,
-                               const VRec *__restrict__ vrec, const int32_t *__restrict__ f,
+                               const PRec *__restrict__ pc2, const VRec *__restrict__ vrec, const int32_t *__restrict__ f,
                                const int32_t *__restrict__ perm, int64_t n, int k, int64_t lo, int64_t hi,
                                int64_t *out) {
     const int lane = threadIdx.x & 31;
@@ -154,13 +149,13 @@ __global__ void k_type2_counts(const int64_t *__restrict__ rowptr, const int32_t
         long long s = 0;
         if (r.head && u >= lo && u < hi)
             for (int i = lane; i < r.pcnt; i += 32)
-                s += (long long)f[(int64_t)p_entry(rowptr, pidx, pd, pr, u, i) * k + r.lab] - 1;
+                s += (long long)f[(int64_t)p_entry(rowptr, pidx, u, i) * k + r.lab] - 1;
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) out[perm[u]] = s;
     }
 }
 cudaError_t launch_type2_counts(Ctx &c, int64_t *t2_dev) {
-    k_type2_counts<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.pidx, c.pd, c.pc2, c.vrec, c.f, c.perm, c.n, c.k,
+    k_type2_counts<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.pidx, c.pc2, c.vrec, c.f, c.perm, c.n, c.k,
                                                   c.head_lo, c.head_hi, t2_dev);
     c.launches++;
     return cudaGetLastError();

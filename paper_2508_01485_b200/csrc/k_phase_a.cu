@@ -6,7 +6,11 @@
 //           their cube roots a_u(C_i) used by every triad term (Eq. 4),
 //   Step 2c omega_max partial maxima,
 //   Step 2d G' predecessor list P(u) = {x in N(u): C(x) != C(u)}, written
-//           in place at offset rowptr[u] (no scan needed), ascending.
+//           in place at offset rowptr[u] (no scan needed), ascending,
+// and, once u's weights are known, the inputs of Step 3: the orientation of G'
+// by internal id (P+(u) = the prefix of P(u) below u, split into its target run
+// and the rest, with a_u(c_z) beside each z) and u's pushes of a_u(c_u) into
+// B_w[c_u] for every w in P(u) (v in P(w) iff w in P(v)), exact 2-limb REDs.
 // Labels are the 8-bit community codes of rs_set_communities; only vertices of
 // two uncoded ("other") communities fall back to comparing full int32 ids.
 // Degree-binned: a group of G lanes (or a whole CTA for hubs) owns a vertex;
@@ -26,7 +30,12 @@ struct PhaseAArgs {
     int64_t vlo;                        // first vertex of the degree-class range
     int64_t nverts;
     int32_t k;
-    double wide_bound;                  // |P|^2 above which a head's Type-I sum needs 3 limbs
+    double wide_bound;                  // d^2 above which a head's Type-I sum needs 3 limbs
+    int64_t n;
+    int32_t *__restrict__ pplus;
+    double *__restrict__ wps;
+    PRec *__restrict__ pc2;
+    BQL *__restrict__ bql;
     const double *__restrict__ l2t;     // log2 of small integers
     int64_t l2n;
     int32_t *__restrict__ f;
@@ -59,9 +68,63 @@ __device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, doubl
     r.pcnt = pc;
     r.lab = lu;
     r.head = (lu < a.k && d >= 2) ? 1 : 0;
-    r.wide = ((double)pc * (double)pc >= a.wide_bound) ? 1 : 0;
+    r.wide = ((double)d * (double)d >= a.wide_bound) ? 1 : 0;   // = (u < n_wide), degree-descending ids
     r.pad = 0;
     a.vrec[u] = r;
+}
+
+// Step 3 inputs of u (after its weights and amat row are written and the group
+// synchronised): B pushes, the P+ runs with a_u(c_z), the PRec record.
+template <int U, class GR>
+__device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR &g, int64_t beg, int pc, int pp,
+                                              int lu) {
+    const int k = a.k;
+    const double *arow = a.amat + u * k;           // this group's writes, plain loads
+    const bool push = lu < k;
+    const U128 qs = push ? fx_quantize(arow[lu]) : u128_zero();
+    BQL *bcol = a.bql + (int64_t)(push ? lu : 0) * a.n;
+    int ct = 0, cn = 0;
+    for (int base = 0; base < pc; base += GR::size * U) {
+        int32_t v[U];
+        int lv[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            v[j] = i < pc ? a.pidx[beg + i] : -1;  // plain load: written by this group
+        }
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            lv[j] = (v[j] >= 0 && i < pp) ? (int)__ldg(a.lab + v[j]) : (int)kOther;
+        }
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            if (push && v[j] >= 0) fx_red2(&bcol[v[j]].b0, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
+            if (base + j * GR::size < pp) {                      // group-uniform
+                const bool inp = v[j] >= 0 && i < pp;
+                const bool tgt = inp && lv[j] < k;
+                int tt, tn;
+                const int rt = g.rank(tgt, &tt);
+                const int rn = g.rank(inp && !tgt, &tn);
+                if (inp) {
+                    // target run ascending from the front, the rest descending from |P+|
+                    const int64_t at = tgt ? beg + ct + rt : beg + pp - 1 - (cn + rn);
+                    a.pplus[at] = v[j];
+                    a.wps[at] = tgt ? arow[lv[j]] : 0.0;
+                }
+                ct += tt;
+                cn += tn;
+            }
+        }
+    }
+    if (g.lane == 0) {
+        PRec r;
+        r.x = pp;
+        r.y = pc;
+        r.start = beg | ((long long)ct << kPrShift);
+        a.pc2[u] = r;
+    }
 }
 
 // k <= 8: per-lane register histogram.
@@ -76,7 +139,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
     // ceil(d / G) neighbours < 2^16 (launch_phase_a_impl falls back to the
     // shared-memory histogram when d_max >= 2^22).
     unsigned long long h0 = 0ull, h1 = 0ull;
-    int pc = 0;
+    int pc = 0, pp = 0;   // |P(u)|, |P+(u)| (foreign neighbours below u)
     for (int64_t base = beg; base < end; base += GR::size * U) {
         int32_t x[U];
         uint8_t lx[U];
@@ -98,10 +161,12 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
                 if (l < 4u) h0 += inc; else h1 += inc;
             }
             if (base + j * GR::size < end) {          // group-uniform
-                int tot;
+                int tot, totp;
                 const int r = g.rank(foreign, &tot);
+                g.rank(foreign && x[j] < (int32_t)u, &totp);
                 if (foreign) a.pidx[beg + pc + r] = x[j];
                 pc += tot;
+                pp += totp;
             }
         }
     }
@@ -140,11 +205,14 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
         a.omega[u * k + c] = w;
         a.amat[u * k + c] = ac;
         a.f[u * k + c] = fc;
+        a.bql[(int64_t)c * a.n + u].Q = ac * ac;
         wmax = w > wmax ? w : wmax;
         if (c == (int)lu) a_self = ac;
     }
     const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
     if ((int)g.lane == owner) write_vrec(a, u, a_self, pc, lu, d);
+    g.sync();
+    phase_a_lists<U>(a, u, g, beg, pc, pp, lu);
     return wmax;
 }
 
@@ -157,7 +225,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     const int k = a.k;
     for (int c = g.lane; c < k; c += GR::size) hist[c] = 0;
     g.sync();
-    int pc = 0;
+    int pc = 0, pp = 0;
     for (int64_t base = beg; base < end; base += GR::size * U) {
         int32_t x[U];
         uint8_t lx[U];
@@ -175,10 +243,12 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
             if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
             if (valid && lx[j] < k) atomicAdd(&hist[lx[j]], 1);
             if (base + j * GR::size < end) {
-                int tot;
+                int tot, totp;
                 const int r = g.rank(foreign, &tot);
+                g.rank(foreign && x[j] < (int32_t)u, &totp);
                 if (foreign) a.pidx[beg + pc + r] = x[j];
                 pc += tot;
+                pp += totp;
             }
         }
     }
@@ -196,9 +266,11 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     for (int c = g.lane; c < k; c += GR::size) {
         const int fc = hist[c];
         const double w = weight_of(a, fc, T, L_all, X);
+        const double ac = w > 0.0 ? cbrt(w) : 0.0;
         a.omega[u * k + c] = w;
-        a.amat[u * k + c] = w > 0.0 ? cbrt(w) : 0.0;
+        a.amat[u * k + c] = ac;
         a.f[u * k + c] = fc;
+        a.bql[(int64_t)c * a.n + u].Q = ac * ac;
         wmax = w > wmax ? w : wmax;
     }
     g.sync();
@@ -207,6 +279,8 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
         if (lu < k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cbrt(w) : 0.0; }
         write_vrec(a, u, as, pc, lu, d);
     }
+    g.sync();
+    phase_a_lists<U>(a, u, g, beg, pc, pp, lu);
     g.sync();
     return wmax;
 }
@@ -301,9 +375,10 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
     a.rowptr = c.rowptr; a.col = c.col; a.comm = c.comm_id; a.lab = c.lab;
     a.vlo = 0; a.nverts = 0; a.k = c.k; a.l2t = l2t; a.l2n = l2n;
     // unnormalised grouped Type-I terms are < 2 * omega_max_bound; a head needs the
-    // 3-limb accumulator when |P|^2 * that bound could reach 2^31 (fx_red2 contract)
+    // 3-limb accumulator when d^2 >= |P|^2 times that bound could reach 2^31 (fx_red2)
     a.wide_bound = wide_bound(c.k);
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
+    a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8 && c.d_max < (1ll << 22)) launch_bins_a<false>(c, a);
     else launch_bins_a<true>(c, a);
     return cudaGetLastError();

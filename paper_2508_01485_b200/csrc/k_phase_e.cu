@@ -3,33 +3,36 @@
 //
 // G' has an edge between u and w iff they are adjacent in G and C(u) != C(w)
 // (P:493), so the three communities of a G' triangle are pairwise distinct:
-// every Type-I triad is a (head, mid) ordering of a G' triangle. Orienting G'
-// by rank (|P|, id) (Phase C's P+ lists), each triangle x < y < z is found
-// exactly once from its middle vertex y, as z in P+(x) ∩ P+(y) for x in
-// P-(y), the lower-ranked part of P(y) (the paper's "common predecessor"
-// search, with bitmap/binary-search probes instead of a merge).
+// every Type-I triad is a (head, mid) ordering of a G' triangle. G' is
+// oriented by internal id (degree-descending: z is above u iff z < u; P+(u)
+// is the prefix of P(u)), and each triangle z < y < x is found exactly once
+// from its middle vertex y, as z in P+(x) ∩ P+(y) for x in P-(y) (the paper's
+// "common predecessor" search, with filter/binary-search probes
+// instead of a merge). Only triangles with two target vertices can carry a
+// term (reading C-27): a pair (x, y) of targets probes all of P+(x), a pair
+// with one target only the target run of P+(x), a pair without none.
 //
 // Each triangle adds the grouped terms of its (up to) three heads
 //   head x: a_y(c_x) a_z(c_x) (a_z(c_y) + a_y(c_z))
 //   head y: a_x(c_y) a_z(c_y) (a_z(c_x) + a_x(c_z))
 //   head z: a_x(c_z) a_y(c_z) (a_y(c_x) + a_x(c_y))
-// with a_v(c) = 0 for a non-target column c -- so a non-target head or mid
-// contributes exactly 0 without a test -- and each expression symmetric in
-// the two other vertices (the numbering changes no bit of the result).
-// a_x(c_z) comes from the weight Phase C stored beside z in P+(x) (read at the
-// probe's own index). Sums are exact fixed point (C-12).
+// with a_v(c) = 0 for a non-target column c, each expression symmetric in the
+// two other vertices (the numbering changes no bit of the result). a_x(c_z)
+// comes from the weight Phase A stored beside z in P+(x) (read at the probe's
+// own index). Sums are exact fixed point (C-12); the highest-degree heads are
+// striped over kHubStripes accumulators (same-address atomics serialise).
 //
 // Heavy middle vertices (degree >= 128): work items (y, 64 positions of
-// P(y)), a warp per item from a global queue, heaviest first. The warp puts a
+// P-(y)), a warp per item from a global queue, heaviest first. The warp puts a
 // 4096-bit filter and a sorted copy of P+(y) in shared memory, lists the
-// item's predecessors x, and cuts every P+(x) into pieces of kPiece entries:
-// a lane probes one piece per round (independent loads in flight), filter
-// candidates are packed with one warp scan and verified 32 at a time by binary
-// search in the shared copy. Head terms accumulate per item in shared memory
-// (x per list slot, z per P+(y) position, y in registers) and are flushed with
-// one RED per touched head. Light middle vertices: one thread per y, two-
-// pointer merge of the short sorted lists. COUNT mode (parity getter) counts
-// the ordered (head, mid) target pairs instead.
+// item's predecessors x, and cuts every probed prefix of P+(x) into aligned
+// 16-byte pieces: a lane probes one piece per round (the next round's load in
+// flight), filter candidates are packed with one warp scan and verified 32 at a
+// time by binary search in the run of P+(y) they can belong to. Head terms:
+// y's in registers, x's in shared 20-bit limbs, z's by RED. Light middle
+// vertices: a warp per 32 consecutive y, pairs and then probes flattened over
+// the lanes. COUNT mode (parity getter) counts the ordered (head, mid) target
+// pairs instead.
 #include "rs_phase.cuh"
 #include <cub/cub.cuh>
 
@@ -73,9 +76,10 @@ __device__ __forceinline__ double amat_at(const CdeArgs &a, int32_t v, int c) {
 
 __device__ __forceinline__ bool owned(const CdeArgs &a, int64_t h) { return h >= a.head_lo && h < a.head_hi; }
 
-// global exact accumulation of a head's (partial) Type-I sum; `wide` is the
-// head's 3-limb flag (VRec::wide), carried with the head's record
-__device__ __forceinline__ void acc_add(const CdeArgs &a, int32_t h, const U128 &q, bool wide) {
+// global exact accumulation of a head's (partial) Type-I sum (3 limbs for the
+// wide heads, VRec::wide = h < n_wide)
+__device__ __forceinline__ void acc_add(const CdeArgs &a, int32_t h, const U128 &q) {
+    const bool wide = is_wide(a, h);
     unsigned long long *acc = a.acc1 + 3 * (int64_t)h;
     if (h < a.n_hub) {
         const int stripe = (int)(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) & (kHubStripes - 1));
@@ -117,11 +121,11 @@ __device__ __forceinline__ U128 from4(const uint32_t *acc4) {
 
 // a work item: positions [64 chunk, 64 chunk + 64) of P-(y), with y's record
 struct __align__(16) EItem {
-    int64_t by;            // start of y's slot (rowptr[y]): P-(y) in pidx
-    int64_t dy;            // y's P+ region | |P+_T(y)| << 40
+    int64_t by;            // start of y's slot (rowptr[y]): P(y) in pidx, P+(y) runs in pplus
     int32_t y, chunk;
     int32_t pyl;           // |P+(y)| | lab(y) << 24
     int32_t pm;            // |P-(y)|
+    int32_t pyt, pad;      // |P+_T(y)|
 };
 struct EItems {
     const EItem *items;    // work items of the heavy middle vertices, heaviest first
@@ -131,12 +135,12 @@ struct EItems {
 struct ESmem {             // one warp's shared memory
     uint32_t bm[kBmWords];
     int32_t py[kPyCap];     // P+(y): target run, then the other run, each ascending
-    longlong2 xl[kChunkE];  // {x's region start, (wide << 63) | (x << 32) | (lab(x) << 24) | |P+_T(x)|}
-    int2 xn[kChunkE];       // {offset of the padded other run of P+(x), its probed length}
+    longlong2 xl[kChunkE];  // {x's slot start, (x << 32) | (lab(x) << 24) | |P+_T(x)|}
+    int2 xn[kChunkE];       // {probed length of P+(x) (its target run, or all of it), -}
     double axy[kChunkE];    // a_x(c_y)
     uint32_t xa[4 * kChunkE];
     int32_t pe[kChunkE];    // end of each list's pieces
-    int2 q[kQCapE];         // candidates {(offset of z in x's lists << 6) | x slot, z}
+    int2 q[kQCapE];         // candidates {((offset of z in P+(x)) + 4) << 6 | x slot, z}
     uint32_t ps[kPsWords];  // bit p: piece p is the first piece of a list
     uint8_t zl[kPyCap];     // label of z in the target run of P+(y)
 };
@@ -168,9 +172,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         const EItem itm = it.items[qi * a.e_world + a.e_rank];
         const int32_t y = itm.y;
         const int py = itm.pyl & 0xFFFFFF, ly = (int)((uint32_t)itm.pyl >> 24);
-        const int pyt = (int)(itm.dy >> kPrShift);
-        const int64_t dy = itm.dy & ((1ll << kPrShift) - 1);
-        const int pcy = py + itm.pm;                // |P(y)|
+        const int pyt = itm.pyt;
         const int start = itm.chunk * kChunkE, end = min(itm.pm, start + kChunkE);
         const int64_t by = itm.by;
         const bool ty = ly < k;
@@ -181,13 +183,12 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int i = start + 32 * h + lane;
-            xv[h] = i < end ? __ldg(a.pidx + by + i) : -1;   // x in P-(y): lower rank than y
+            xv[h] = i < end ? __ldg(a.pidx + by + py + i) : -1;   // x in P-(y) (suffix of P(y)): x > y
         }
         // i-th entry of P+(y) in ascending order within its run (the other run is
-        // stored descending at the end of y's region)
-        const int64_t dye = dy + dcap(pcy) - 1;
-        auto py_at = [&](int i) -> int64_t { return i < pyt ? dy + i : dye - (i - pyt); };
-        const int32_t z0 = lane < py ? __ldg(a.pd + py_at(lane)) : -1;
+        // stored descending after the target run)
+        auto py_at = [&](int i) -> int64_t { return i < pyt ? by + i : by + py - 1 - (i - pyt); };
+        const int32_t z0 = lane < py ? __ldg(a.pplus + py_at(lane)) : -1;
         const double ay0 = lane < k ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
         PRec pcx[2];
         int lxv[2];
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
         __syncwarp();
         for (int i = lane; i < py; i += 32) {
-            const int32_t z = i == lane ? z0 : __ldg(a.pd + py_at(i));
+            const int32_t z = i == lane ? z0 : __ldg(a.pplus + py_at(i));
             const uint32_t b = bm_bit(z);
             atomicOr(&S.bm[b >> 5], 1u << (b & 31));
             if (local) {
@@ -221,11 +222,13 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         for (int h = 0; h < 2; h++) {
             const int lx = lxv[h];
             const bool tx = lx < k;
-            const int t = (tx || ty) ? pr_plus_t(pcx[h]) : 0;
-            const int lenn = (tx && ty) ? pcx[h].x - pr_plus_t(pcx[h]) : 0;
-            const bool use = t + lenn > 0;
-            nprobe += (unsigned)(t + lenn);
-            const int pieces = ceil4(t) / kPiece + ceil4(lenn) / kPiece;
+            const int t = pr_plus_t(pcx[h]);
+            const int lenx = (tx && ty) ? pcx[h].x : ((tx || ty) ? t : 0);   // probed prefix of P+(x)
+            const bool use = lenx > 0;
+            nprobe += (unsigned)lenx;
+            const int64_t bx = pr_start(pcx[h]);
+            // aligned 16-byte pieces covering [bx, bx + lenx)
+            const int pieces = use ? (int)(((bx + lenx - 1) >> 2) - (bx >> 2) + 1) : 0;
             int incl = pieces;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -235,10 +238,8 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             const unsigned has = __ballot_sync(0xffffffffu, use);
             if (use) {
                 const int slot = nx + __popc(has & ((1u << lane) - 1u));
-                const long long wide = is_wide(a, pcx[h].y) ? (1ll << 63) : 0ll;
-                S.xl[slot] = make_longlong2(pr_start(pcx[h]),
-                                            wide | ((long long)xv[h] << 32) | ((long long)(lx & 0xFF) << 24) | t);
-                S.xn[slot] = make_int2(dcap(pcx[h].y) - ceil4(lenn), lenn);
+                S.xl[slot] = make_longlong2(bx, ((long long)xv[h] << 32) | ((long long)(lx & 0xFF) << 24) | t);
+                S.xn[slot] = make_int2(lenx, 0);
                 S.axy[slot] = axy[h];
                 S.xa[4 * slot] = 0u;
                 S.xa[4 * slot + 1] = 0u;
@@ -282,21 +283,24 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                 }
                 slot = lo;
             }
-            int off = 0;
+            int off = 0;   // offset in P+(x) of the piece's first entry (-3..-1 for a head piece)
             if (p < npieces) {
-                const longlong2 xe = S.xl[slot];
-                const int t = (int)(xe.y & 0xFFFFFF);
+                const int64_t bx = S.xl[slot].x;
+                const int lenx = S.xn[slot].x;
                 const int q = p - (slot ? S.pe[slot - 1] : 0);   // piece within the list
-                const int qt = ceil4(t) / kPiece;
-                off = q < qt ? q * kPiece : S.xn[slot].x + (q - qt) * kPiece;
-                // one aligned 16-byte load; padding entries are -1
-                const int4 v = __ldg(reinterpret_cast<const int4 *>(a.pd + xe.x + off));
-                z[0] = v.x; z[1] = v.y; z[2] = v.z; z[3] = v.w;
+                const int64_t blk = (bx >> 2) + q;
+                off = (int)(4 * blk - bx);
+                // one aligned 16-byte load; entries outside [0, lenx) are masked
+                const int4 v = __ldg(reinterpret_cast<const int4 *>(a.pplus + 4 * blk));
+                z[0] = (off >= 0 && off < lenx) ? v.x : -1;
+                z[1] = (off + 1 >= 0 && off + 1 < lenx) ? v.y : -1;
+                z[2] = (off + 2 >= 0 && off + 2 < lenx) ? v.z : -1;
+                z[3] = (off + 3 < lenx) ? v.w : -1;
             } else {
 #pragma unroll
                 for (int j = 0; j < kPiece; j++) z[j] = -1;
             }
-            tag = (off << 6) | (slot & 63);
+            tag = ((off + 4) << 6) | (slot & 63);
         };
 
         U128 accy = u128_zero();
@@ -309,13 +313,13 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                 const int b0 = qn - take;
                 if (lane < take) {
                     const int2 e = S.q[b0 + lane];
-                    const int slot = e.x & 63, off = e.x >> 6;
+                    const int slot = e.x & 63, off = (e.x >> 6) - 4;
                     const int32_t z = e.y;
                     const longlong2 xe = S.xl[slot];
                     const bool zt = off < (int)(xe.y & 0xFFFFFF);   // z from the target run of P+(x)
                     int iz;
                     if (local) iz = zt ? find_sorted(S.py, pyt, z) : find_sorted(S.py + pyt, py - pyt, z);
-                    else iz = zt ? find_sorted_g(a.pd + dy, pyt, z) : find_desc_g(a.pd + dye + 1 - (py - pyt), py - pyt, z);
+                    else iz = zt ? find_sorted_g(a.pplus + by, pyt, z) : find_desc_g(a.pplus + by + pyt, py - pyt, z);
 #ifdef RS_EXP_NO_TERMS
                     if (iz >= 0) ntri++;
                     if (iz >= 0 && z == -7) {
@@ -332,9 +336,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                             if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
                             cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
                         } else {
-                            const double wr = __ldg(a.wd + xe.x + off);     // a_x(c_z), stored by Phase C
-                            const bool zwide = __double_as_longlong(wr) < 0;  // its sign: z's 3-limb flag
-                            const double Axlz = fabs(wr);
+                            const double Axlz = __ldg(a.wps + xe.x + off);  // a_x(c_z), stored by Phase A
                             const double Axly = S.axy[slot];
                             const double Aylx = lx < k ? Ay[lx] : 0.0;
                             const double Aylz = lz < k ? Ay[lz] : 0.0;
@@ -345,13 +347,13 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                             accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
 #ifndef RS_EXP_NO_XRED
                             if (tx > 0.0) {
-                                const int lenx = ceil4((int)(xe.y & 0xFFFFFF)) + S.xn[slot].y;
+                                const int lenx = S.xn[slot].x;
                                 if (lenx <= kSlotMaxHits) smem_red4(S.xa + 4 * slot, fx_quantize(tx));
-                                else if (owned(a, x)) acc_add(a, x, fx_quantize(tx), xe.y < 0);
+                                else if (owned(a, x)) acc_add(a, x, fx_quantize(tx));
                             }
 #endif
 #ifndef RS_EXP_NO_ZRED
-                            if (tz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(tz), zwide);
+                            if (tz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(tz));
 #endif
                         }
                     }
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                 const uint32_t *l = S.xa + 4 * s;
                 const longlong2 xe = S.xl[s];
                 const int32_t x = (int32_t)((xe.y >> 32) & 0x7FFFFFFF);
-                if ((l[0] | l[1] | l[2] | l[3]) && owned(a, x)) acc_add(a, x, from4(l), xe.y < 0);
+                if ((l[0] | l[1] | l[2] | l[3]) && owned(a, x)) acc_add(a, x, from4(l));
             }
         }
         if (ty && owned(a, y)) {
@@ -422,7 +424,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                     const U128 w{__shfl_xor_sync(0xffffffffu, accy.lo, o), __shfl_xor_sync(0xffffffffu, accy.hi, o)};
                     accy = u128_add(accy, w);
                 }
-                if (lane == 0 && (accy.lo | accy.hi)) acc_add(a, y, accy, is_wide(a, pcy));
+                if (lane == 0 && (accy.lo | accy.hi)) acc_add(a, y, accy);
             }
         }
         __syncwarp();
@@ -465,13 +467,12 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
         // ---- y level: lane j holds y0 + j
         const int64_t yl = y0 + lane;
         PRec pcl{0, 0, 0};
-        int64_t rpl = 0;
         int lyl = kOther;
         if (yl < a.n) {
             pcl = a.pc2[yl];
-            rpl = a.rowptr[yl];
             lyl = a.lab[yl];
         }
+        const int64_t rpl = pr_start(pcl);                 // rowptr[y]
         const int cnt = pcl.x > 0 ? pcl.y - pcl.x : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
         int incl = cnt;
 #pragma unroll
@@ -487,9 +488,10 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
             const int inc_j = __shfl_sync(0xffffffffu, incl, j);
             const int cnt_j = __shfl_sync(0xffffffffu, cnt, j);
             const long long by = __shfl_sync(0xffffffffu, rpl, j);
+            const int ppj = __shfl_sync(0xffffffffu, pcl.x, j);            // |P+(y)|
             const int ly = __shfl_sync(0xffffffffu, lyl, j);
             int32_t x = -1;
-            if (q < total) x = __ldg(a.pidx + by + (q - (inc_j - cnt_j)));   // P-(y): lower rank than y
+            if (q < total) x = __ldg(a.pidx + by + ppj + (q - (inc_j - cnt_j)));   // P-(y): the suffix, x > y
             PRec pcx{0, 0, 0};
             int lx = kOther;
             double Axly = 0.0;
@@ -517,8 +519,6 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 const int o = r - (__shfl_sync(0xffffffffu, incl2, p) - __shfl_sync(0xffffffffu, np, p));
                 const int32_t xp = __shfl_sync(0xffffffffu, x, p);
                 const long long bx = __shfl_sync(0xffffffffu, pr_start(pcx), p);
-                const int pxy = __shfl_sync(0xffffffffu, pcx.y, p);          // |P(x)|
-                const int capx = dcap(pxy);
                 const int tp = __shfl_sync(0xffffffffu, t, p);
                 const int lxp = __shfl_sync(0xffffffffu, lx, p);
                 const double Axlyp = __shfl_sync(0xffffffffu, Axly, p);
@@ -530,18 +530,18 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 if (r >= total2) continue;
                 const int32_t y = (int32_t)(y0 + jp);
                 const bool zt = o < tp;                                     // z from the target run
-                const int64_t pos = zt ? bx + o : bx + capx - 1 - (o - tp);
-                const int32_t z = __ldg(a.pd + pos);
+                const int64_t pos = bx + o;                                 // the probed prefix of P+(x)
+                const int32_t z = __ldg(a.pplus + pos);
                 const int64_t dy = pr_start(pcy);
                 const int tyn = pr_plus_t(pcy), nyn = pcy.x - tyn;
                 int iz;
                 int64_t ypos;
                 if (zt) {
-                    iz = find_sorted_g(a.pd + dy, tyn, z);
+                    iz = find_sorted_g(a.pplus + dy, tyn, z);
                     ypos = dy + iz;
                 } else {
-                    const int64_t nb = dy + dcap(pcy.y) - nyn;                // the other run, descending
-                    iz = find_desc_g(a.pd + nb, nyn, z);
+                    const int64_t nb = dy + tyn;                              // the other run, descending
+                    iz = find_desc_g(a.pplus + nb, nyn, z);
                     ypos = nb + iz;
                 }
                 if (iz < 0) continue;
@@ -554,16 +554,14 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                     if (tz && (txp + typ) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(txp + typ));
                     if (typ && (txp + tz) && owned(a, y)) atomicAdd(a.n1 + y, (unsigned long long)(txp + tz));
                 } else {
-                    const double wr = __ldg(a.wd + pos);
-                    const bool zwide = __double_as_longlong(wr) < 0;
-                    const double Axlz = fabs(wr), Aylz = fabs(__ldg(a.wd + ypos));
+                    const double Axlz = __ldg(a.wps + pos), Aylz = __ldg(a.wps + ypos);
                     const double Azlx = amat_at(a, z, lxp), Azly = amat_at(a, z, lyp);
                     const double ttx = Aylxp * Azlx * (Azly + Aylz);
                     const double tty = Axlyp * Azly * (Azlx + Axlz);
                     const double ttz = Axlz * Aylz * (Aylxp + Axlyp);
-                    if (ttx > 0.0 && owned(a, xp)) acc_add(a, xp, fx_quantize(ttx), is_wide(a, pxy));
-                    if (tty > 0.0 && owned(a, y)) acc_add(a, y, fx_quantize(tty), is_wide(a, pcy.y));
-                    if (ttz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(ttz), zwide);
+                    if (ttx > 0.0 && owned(a, xp)) acc_add(a, xp, fx_quantize(ttx));
+                    if (tty > 0.0 && owned(a, y)) acc_add(a, y, fx_quantize(tty));
+                    if (ttz > 0.0 && owned(a, z)) acc_add(a, z, fx_quantize(ttz));
                 }
             }
         }
@@ -597,35 +595,16 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         const PRec p = pc2[y];
         EItem e;
         e.by = rowptr[y];
-        e.dy = p.start;                 // region start | |P+_T(y)| << 40
         e.y = (int32_t)y;
         e.pyl = p.x | ((int32_t)lab[y] << 24);
         e.pm = p.y - p.x;
+        e.pyt = pr_plus_t(p);
+        e.pad = 0;
         for (int j = 0; j < c; j++) {
             e.chunk = j;
             items[o + j] = e;
         }
     }
-}
-
-// ---------------------------------------------------------------- P+ regions (per step)
-// Region of u in pd/wd: dcap(|P(u)|) entries at dpos[u] (scan), written by Phase C.
-__global__ void k_dense_cap(const VRec *__restrict__ vrec, int64_t n, int64_t *sz) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u <= n; u += (int64_t)gridDim.x * blockDim.x)
-        sz[u] = u < n ? dcap(vrec[u].pcnt) : 0;
-}
-cudaError_t launch_dense_pos(Ctx &c) {
-    const int64_t n = c.n;
-    int64_t *sz = (int64_t *)c.scratch;
-    void *tmp = sz + (n + 1);
-    const size_t tmp_bytes = c.scratch_bytes - sizeof(int64_t) * (size_t)(n + 1);
-    k_dense_cap<<<148 * 8, 256, 0, c.stream>>>(c.vrec, n, sz);
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, sz, c.dpos, (int)(n + 1), c.stream);
-    if (need > tmp_bytes) return cudaErrorMemoryAllocation;
-    cub::DeviceScan::ExclusiveSum(tmp, need, sz, c.dpos, (int)(n + 1), c.stream);
-    c.launches += 2;
-    return cudaGetLastError();
 }
 
 // load time: buffers sized for any community assignment (grow-only)

@@ -412,6 +412,18 @@ __global__ void k_labels(const int32_t *__restrict__ comm_in, const int32_t *__r
     }
 }
 
+// n_wide: the vertices with d^2 >= wide_bound(k) (VRec::wide), a prefix of the
+// degree-descending numbering
+__global__ void k_nwide(const int64_t *__restrict__ rowptr, int64_t n, double bound, unsigned long long *out) {
+    int64_t lo = 0, hi = n;   // first u with d(u)^2 < bound
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const double d = (double)(rowptr[mid + 1] - rowptr[mid]);
+        if (d * d >= bound) lo = mid + 1; else hi = mid;
+    }
+    *out = (unsigned long long)lo;
+}
+
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets) {
     const int64_t nbins = max_comm + 1;
     cudaMemsetAsync(c.chist, 0, sizeof(int32_t) * nbins, c.stream);
@@ -422,7 +434,8 @@ cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user
     k_select<<<1, kSelThreads, 0, c.stream>>>(c.chist, nbins, c.k, user_targets, c.targets, c.ccode, c.scal);
     c.launches++;
     k_labels<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.perm, c.ccode, c.n, c.comm_id, c.lab);
-    c.launches++;
+    k_nwide<<<1, 1, 0, c.stream>>>(c.rowptr, c.n, wide_bound(c.k), c.scal + kScalNWide);
+    c.launches += 2;
     return cudaGetLastError();
 }
 

@@ -197,8 +197,8 @@ extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream,
 static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
-    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pd); dfree(c.wd); dfree(c.dpos); c.cap_d = 0; dfree(c.pc2); dfree(c.amat);
-    dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bq);
+    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.wps); dfree(c.pc2); dfree(c.amat);
+    dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bql);
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
     ctx->l2n = 0;
@@ -309,10 +309,8 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         CK(dalloc(&c.lab, n));
         CK(dalloc(&c.vrec, n));
         CK(dalloc(&c.pidx, nnz));
-        c.cap_d = nnz + 12 * n + 16;  // sum of dcap(|P(u)|) <= nnz + 11 n
-        CK(dalloc(&c.pd, c.cap_d));
-        CK(dalloc(&c.wd, c.cap_d));
-        CK(dalloc(&c.dpos, n + 1));
+        CK(dalloc(&c.pplus, nnz + 4));   // + 4: aligned 16-byte probes may read past the end
+        CK(dalloc(&c.wps, nnz));
         CK(dalloc(&c.pc2, n));
         CK(dalloc(&c.acc1, 3 * n));
         c.n_hub = std::min<int64_t>(n, rs::kHubMax);
@@ -365,7 +363,7 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     if (c.k_alloc != k || c.kn_alloc != c.n) {
         CK(dalloc(&c.f, (size_t)c.n * k));
         CK(dalloc(&c.omega, (size_t)c.n * k));
-        CK(dalloc(&c.bq, (size_t)c.n * k));
+        CK(dalloc(&c.bql, (size_t)c.n * k));
         CK(dalloc(&c.amat, (size_t)c.n * k));
         c.k_alloc = k;
         c.kn_alloc = c.n;
@@ -383,7 +381,10 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     CK(cudaMemcpyAsync(&er, c.scal + rs::kScalErr, sizeof(er), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaMemcpyAsync(&ndist, c.scal + rs::kScalCnt0, sizeof(ndist), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaMemcpyAsync(c.h_targets, c.targets, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c.stream));
+    unsigned long long nw = 0;
+    CK(cudaMemcpyAsync(&nw, c.scal + rs::kScalNWide, sizeof(nw), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    c.n_wide = (int64_t)nw;
     if (er == 10)
         return fail(ctx, RS_EINVAL, "rs_set_communities: k = " + std::to_string(k) + " exceeds the " +
                                         std::to_string((long long)ndist) + " distinct communities");
@@ -405,19 +406,16 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, 2 * sizeof(unsigned long long), c.stream));   // NTri, NProbe
-    // Phase A: border + histogram + weights + P lists + omega_max partials
+    CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs (Q rewritten)
+    // Phase A: border + histogram + weights + P lists + omega_max partials, the
+    // orientation of G' and the B-table pushes
     fork(c);
     CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n));
     join(c);
     CK(cudaEventRecord(c.ev_phase[1], c.stream));
-    // Phase C: B table + orientation
-    CK(rs::launch_dense_pos(c));
-    fork(c);
-    CK(rs::launch_phase_c(c));
-    join(c);
-    CK(cudaEventRecord(c.ev_phase[2], c.stream));
+    CK(cudaEventRecord(c.ev_phase[2], c.stream));   // (Phase C folded into A: ms_phase[1] = 0)
     // Phase E (Type-I triangles) and Phase D (Type-II pull, which needs only
-    // Phase C's B table) run concurrently: E heavy on the library stream, E light
+    // Phase A's B table) run concurrently: E heavy on the library stream, E light
     // and the D bins on the forked streams
     fork(c);
     CK(rs::launch_phase_d(c));                           // first: their blocks are queued ahead of
@@ -472,7 +470,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(cudaMemcpy(&wb, c.scal + rs::kScalOmegaMaxBits, sizeof(wb), cudaMemcpyDeviceToHost));
         memcpy(&s.omega_max, &wb, sizeof(double));
         for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&s.ms_phase[i], c.ev_phase[i], c.ev_phase[i + 1]));
-        // ms_phase: [0] A (incl. zeroing) [1] C [2] E (Type-I) || D (Type-II) [3] finalize
+        // ms_phase: [0] A (incl. zeroing) [1] - (no Phase C) [2] E (Type-I) || D (Type-II) [3] finalize
         *stats_out = s;
     }
     (void)flags;

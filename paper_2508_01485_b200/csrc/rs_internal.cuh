@@ -49,19 +49,18 @@ struct __align__(16) VRec {
     int32_t pcnt;      // |P(v)|: inter-community neighbours (G' in-degree)
     uint8_t lab;       // 8-bit community code (< k: target column)
     uint8_t head;      // 1 if v can be an RSI head: target community and d(v) >= 2
-    uint8_t wide;      // Type-I sum of this head needs the 3-limb accumulator
+    uint8_t wide;      // Type-I sum of this head needs the 3-limb accumulator (d(v)^2 >= wide_bound)
     uint8_t pad;
 };
 
-// Per-vertex G' record written by Phase C, gathered once per predecessor x by
-// Phase E: where P+(x) starts and how long P+(x) and P(x) are (one sector).
-// P+(u) lives in the dense array pd, in a region of dcap(|P(u)|) entries at
-// `start` (dpos[u], a scan over the capacities): the entries in a target
-// community ascending at [0, t) padded with -1 to ceil4(t), the others in
-// DESCENDING order at the end [cap - (|P+| - t), cap), padded with -1 down to
-// cap - ceil4(|P+| - t) (Phase C writes both runs in one pass). wd holds
-// a_u(c_z) beside each entry. t = |P+_T(u)| is packed above bit 40 of `start`
-// (offsets < 2^40; |P+| <= sqrt(2 |E'|) < 2^24 by the orientation).
+// Per-vertex G' record written by Phase A, gathered once per predecessor x by
+// Phase E. G' is oriented by internal id: z is above u iff z < u, i.e. iff z
+// has the higher degree (the numbering is degree-descending), so P+(u) is the
+// prefix of the ascending list P(u) = pidx[rowptr[u], +|P|) and P-(u) its
+// suffix. Phase A also copies P+(u) to pplus at the same offset as two runs:
+// the entries in a target community ascending at [0, t), the others in
+// DESCENDING order at [t, |P+|); wps holds a_u(c_z) beside each entry.
+// t = |P+_T(u)| is packed above bit 40 of `start` (offsets < 2^40).
 struct __align__(16) PRec {
     int x;             // |P+(u)| (orientation out-degree)
     int y;             // |P(u)|
@@ -74,14 +73,16 @@ constexpr int kPrShift = 40;
 constexpr int kHubStripes = 16;
 constexpr int64_t kHubMax = 1 << 16;
 __host__ __device__ __forceinline__ int ceil4(int v) { return (v + 3) & ~3; }
-__host__ __device__ __forceinline__ int dcap(int p) { return p > 0 ? ceil4(p) + 8 : 0; }
 __host__ __device__ __forceinline__ long long pr_start(const PRec &r) { return r.start & ((1ll << kPrShift) - 1); }
 __host__ __device__ __forceinline__ int pr_plus_t(const PRec &r) { return (int)(r.start >> kPrShift); }
 
-// Per (vertex, column) record read by the Type-II pull (Phase D).
-struct __align__(16) BQ {
-    double B;          // sum_{v in P(w), col(v)=c} a_v(c), exact sum rounded once
-    double Q;          // a_w(c)^2 = omega_w(c)^(2/3)
+// Per (vertex, column) record read by the Type-II pull (Phase D), one sector.
+// B_w[c] = sum_{v in P(w), col(v)=c} a_v(c) is pushed by every such v during
+// Phase A (v is in P(w) iff w is in P(v)) as exact 2-limb REDs (fx_red2).
+struct __align__(32) BQL {
+    unsigned long long b0, b1;   // fx_red2 limbs of B_w[c]
+    double Q;                    // a_w(c)^2 = omega_w(c)^(2/3), written by w
+    double pad;
 };
 
 struct Bins {
@@ -135,14 +136,13 @@ struct Ctx {
     int32_t *f = nullptr;        // n*k counts
     double *omega = nullptr;     // n*k weights (unnormalised)
     VRec *vrec = nullptr;        // n
-    int32_t *pidx = nullptr;     // nnz, P(u) stored at rowptr[u] ...
-    int32_t *pd = nullptr;       // P+(u) (orientation), two runs in a region of dcap(|P(u)|) (see PRec)
-    double *wd = nullptr;        // a_u(c_z) beside each z of P+(u); sign bit: z needs 3 limbs
-    int64_t *dpos = nullptr;     // n+1: start of u's region (scan of dcap(|P(u)|))
-    int64_t cap_d = 0;           // capacity of pd / wd
-    PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, start | |P+_T(u)| << 40}
+    int32_t *pidx = nullptr;     // nnz, P(u) ascending at rowptr[u] (P+(u) its prefix, see PRec)
+    int32_t *pplus = nullptr;    // nnz, P+(u) at rowptr[u] as a target run and the other run
+    double *wps = nullptr;       // nnz, a_u(c_z) beside each z of P+(u)
+    PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, rowptr[u] | |P+_T(u)| << 40}
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
-    BQ *bq = nullptr;            // n*k
+    BQL *bql = nullptr;          // k*n, column-major: bql[c*n + w]
+    int64_t n_wide = 0;          // vertices [0, n_wide) (degree^2 >= wide_bound) use 3 Type-I limbs
     unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)
     unsigned long long *acc_hub = nullptr;  // kHubStripes copies of the limbs of the first n_hub vertices
     int64_t n_hub = 0;                   //   (the highest degrees: contended heads), summed by Phase D
@@ -179,7 +179,8 @@ enum {
     kScalNPred = 5,
     kScalNTri = 6,
     kScalNProbe = 7,         // Phase E: entries of P+ lists probed
-    kScalTk = 8,             // top-k state (8 slots)
+    kScalTk = 8,             // top-k state (8 slots; load time: degree class bounds, 9 slots)
+    kScalNWide = 17,         // n_wide (rs_set_communities)
     kScalCount = 32
 };
 
@@ -198,8 +199,6 @@ size_t relabel_arena_bytes(int64_t n, int64_t nnz);
 cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, void *arena, size_t arena_bytes);
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets);
 cudaError_t launch_phase_a(Ctx &c);
-cudaError_t launch_phase_c(Ctx &c);
-cudaError_t launch_dense_pos(Ctx &c);
 cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
 cudaError_t launch_finalize(Ctx &c);

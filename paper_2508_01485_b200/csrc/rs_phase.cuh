@@ -1,4 +1,4 @@
-// Shared argument block of the P-list phases (C, D, E).
+// Shared argument block of the P-list phases (D, E) and the finalize pass.
 #pragma once
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
@@ -13,12 +13,11 @@ struct CdeArgs {
     int32_t k;
     const double *__restrict__ amat;    // n*k cube roots a_v(c), row-major
     const VRec *__restrict__ vrec;
-    int32_t *__restrict__ pidx;         // P(u) at rowptr[u]; after Phase C: P-(u) at its front
-    int32_t *__restrict__ pd;           // P+(u): two runs in u's region (see PRec)
-    double *__restrict__ wd;            // a_u(c_z) beside each z of P+(u); sign bit: z is wide
-    const int64_t *__restrict__ dpos;   // start of u's region
-    PRec *__restrict__ pc2;             // {|P+(u)|, |P(u)|, start | |P+_T(u)| << 40}
-    BQ *__restrict__ bq;                // column-major: bq[c*n + w]
+    const int32_t *__restrict__ pidx;   // P(u) ascending at rowptr[u]: P+(u) prefix, P-(u) suffix
+    const int32_t *__restrict__ pplus;  // P+(u) at rowptr[u]: target run + other run (see PRec)
+    const double *__restrict__ wps;     // a_u(c_z) beside each z of P+(u)
+    const PRec *__restrict__ pc2;       // {|P+(u)|, |P(u)|, rowptr[u] | |P+_T(u)| << 40}
+    const BQL *__restrict__ bql;        // column-major: bql[c*n + w]
     unsigned long long *__restrict__ acc1;  // 3 limbs per vertex (Type-I)
     unsigned long long *__restrict__ acc_hub;  // striped limbs of vertices < n_hub
     int64_t n_hub;
@@ -30,24 +29,20 @@ struct CdeArgs {
     unsigned long long *scal;
     int64_t head_lo, head_hi;           // owned head range (multi-GPU); [0, n) on one GPU
     int32_t e_rank, e_world;            // Phase E: this rank's share of the middle vertices
-    bool any_wide;                      // some head may need the 3-limb Type-I accumulator
-    double wide_bound;                  // |P(h)|^2 >= wide_bound: head h is wide (VRec::wide)
+    int64_t n_wide;                     // heads [0, n_wide) use the 3-limb Type-I accumulator
 };
 
-// the 3-limb rule of VRec::wide from |P(h)| alone
-__device__ __forceinline__ bool is_wide(const CdeArgs &a, int p) {
-    return a.any_wide && (double)p * (double)p >= a.wide_bound;
-}
+// VRec::wide by internal id: d(h)^2 >= wide_bound, d non-increasing in h
+__device__ __forceinline__ bool is_wide(const CdeArgs &a, int64_t h) { return h < a.n_wide; }
 
 inline CdeArgs cde_args(Ctx &c) {
     CdeArgs a;
     a.rowptr = c.rowptr; a.vlo = 0; a.nverts = 0; a.n = c.n; a.k = c.k;
     a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pc2 = c.pc2;
-    a.pd = c.pd; a.wd = c.wd; a.dpos = c.dpos;
-    a.bq = c.bq; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.t2 = c.t2; a.score = c.score; a.scal = c.scal;
+    a.pplus = c.pplus; a.wps = c.wps;
+    a.bql = c.bql; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.t2 = c.t2; a.score = c.score; a.scal = c.scal;
     a.perm = c.perm; a.lab = c.lab;
-    a.any_wide = (double)c.d_max * (double)c.d_max >= wide_bound(c.k);
-    a.wide_bound = wide_bound(c.k);
+    a.n_wide = c.n_wide;
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
     a.e_rank = 0; a.e_world = 1;
     return a;
