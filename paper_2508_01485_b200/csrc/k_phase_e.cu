@@ -163,18 +163,26 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
     const unsigned long long n_items = n_all > (unsigned long long)a.e_rank
                                            ? (n_all - a.e_rank + a.e_world - 1) / a.e_world : 0ull;
 
+    // the next item's index and its 32-byte record (word `lane` of it in lanes
+    // 0-7) are fetched while the current item is processed
+    const int32_t *items_w = reinterpret_cast<const int32_t *>(it.items);
     unsigned long long qnext = 0;
     if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);
+    unsigned long long qi = __shfl_sync(0xffffffffu, qnext, 0);
+    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
     for (;;) {
-        const unsigned long long qi = __shfl_sync(0xffffffffu, qnext, 0);
         if (qi >= n_items) break;
-        if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);   // next item, consumed at the loop top
-        const EItem itm = it.items[qi * a.e_world + a.e_rank];
-        const int32_t y = itm.y;
-        const int py = itm.pyl & 0xFFFFFF, ly = (int)((uint32_t)itm.pyl >> 24);
-        const int pyt = itm.pyt;
-        const int start = itm.chunk * kChunkE, end = min(itm.pm, start + kChunkE);
-        const int64_t by = itm.by;
+        if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);   // next item
+        // EItem words: by (0, 1), y (2), chunk (3), pyl (4), pm (5), pyt (6)
+        const int64_t by = (int64_t)(uint32_t)__shfl_sync(0xffffffffu, rec, 0) |
+                           ((int64_t)__shfl_sync(0xffffffffu, rec, 1) << 32);
+        const int32_t y = __shfl_sync(0xffffffffu, rec, 2);
+        const int chunk = __shfl_sync(0xffffffffu, rec, 3);
+        const int pyl = __shfl_sync(0xffffffffu, rec, 4);
+        const int ipm = __shfl_sync(0xffffffffu, rec, 5);
+        const int pyt = __shfl_sync(0xffffffffu, rec, 6);
+        const int py = pyl & 0xFFFFFF, ly = (int)((uint32_t)pyl >> 24);
+        const int start = chunk * kChunkE, end = min(ipm, start + kChunkE);
         const bool ty = ly < k;
         const bool local = py <= kPyCap;            // sorted copy of P+(y) in smem
         // setup: the loads of P-(y) (x list), P+(y) (filter) and y's weights are
@@ -213,6 +221,9 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                 if (i < pyt) S.zl[i] = (uint8_t)(i == lane ? lz0 : __ldg(a.lab + z));
             }
         }
+        // the next item's record, in flight during this item
+        qi = __shfl_sync(0xffffffffu, qnext, 0);
+        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
         // the item's predecessors x. A triangle carries a term only if two of its
         // vertices are targets: with both x and y targets every z of P+(x) is
         // probed, with one of them only the target run of P+(x), with neither

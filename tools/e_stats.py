@@ -93,3 +93,33 @@ def py_buckets(name="orkut", scale=1.0, k=5):
     for lo, hi in [(0, 32), (32, 64), (64, 128), (128, 256), (256, 1 << 30)]:
         m = (pyv >= lo) & (pyv < hi)
         print(f"|P+(y)| in [{lo},{hi}): probe share {probes[m].sum() / probes.sum():.3f}")
+
+
+def orientation_compare(name="orkut", scale=1.0, k=5):
+    """probe volume (with target-run pruning) for the rank (|P|, id) orientation
+    vs the rank (degree, id) orientation"""
+    g = gen.config_graph(name, scale)
+    n, rp, col, comm = g.n, g.rowptr, g.col, g.comm
+    deg = np.diff(rp)
+    row = np.repeat(np.arange(n, dtype=np.int32), deg)
+    foreign = comm[col] != comm[row]
+    pcnt = np.bincount(row[foreign], minlength=n)
+    sizes = np.bincount(comm)
+    order = np.lexsort((np.arange(sizes.size), -sizes))
+    is_t = np.zeros(sizes.size, bool)
+    is_t[order[:k]] = True
+    tv = is_t[comm]
+    r_src, r_dst = row[foreign], col[foreign]
+    del row, foreign
+    for label, key in [("|P|", pcnt), ("degree", deg)]:
+        up = (key[r_dst] > key[r_src]) | ((key[r_dst] == key[r_src]) & (r_dst > r_src))
+        pplus = np.bincount(r_src[up], minlength=n)
+        pplus_t = np.bincount(r_src[up & tv[r_dst]], minlength=n)
+        dn = ~up
+        ys, xs = r_src[dn], r_dst[dn]
+        keep = (pplus[xs] > 0) & (pplus[ys] > 0) & (tv[xs] | tv[ys])
+        ys, xs = ys[keep], xs[keep]
+        both = tv[xs] & tv[ys]
+        probes_t = np.where(both, pplus[xs], pplus_t[xs]).astype(np.int64)
+        print(f"orientation by {label}: probes {probes_t.sum():.4e}, max |P+| {pplus.max()}, "
+              f"pairs {ys.size:.3e}")
