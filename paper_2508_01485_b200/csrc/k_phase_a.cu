@@ -100,7 +100,9 @@ __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
+#ifndef RS_EXP_NO_BPUSH
             if (push && v[j] >= 0) fx_red2(&bcol[v[j]].b0, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
+#endif
             if (base + j * GR::size < pp) {                      // group-uniform
                 const bool inp = v[j] >= 0 && i < pp;
                 const bool tgt = inp && lv[j] < k;
