@@ -123,3 +123,40 @@ def orientation_compare(name="orkut", scale=1.0, k=5):
         probes_t = np.where(both, pplus[xs], pplus_t[xs]).astype(np.int64)
         print(f"orientation by {label}: probes {probes_t.sum():.4e}, max |P+| {pplus.max()}, "
               f"pairs {ys.size:.3e}")
+
+
+def direction_stats(name="orkut", scale=1.0, k=5):
+    """probe volume if each (x, y) pair probed its shorter side (id orientation,
+    target-run pruning): sum of |P+(x)| vs sum of min(|P+(x)|, c |P+(y)| log2 |P+(x)|)"""
+    g = gen.config_graph(name, scale)
+    n, rp, col, comm = g.n, g.rowptr, g.col, g.comm
+    deg = np.diff(rp)
+    # internal order: degree descending, stable
+    order = np.argsort(-deg, kind="stable")
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    row = np.repeat(np.arange(n, dtype=np.int32), deg)
+    foreign = comm[col] != comm[row]
+    sizes = np.bincount(comm)
+    corder = np.lexsort((np.arange(sizes.size), -sizes))
+    is_t = np.zeros(sizes.size, bool)
+    is_t[corder[:k]] = True
+    tv = is_t[comm]
+    r_src, r_dst = row[foreign], col[foreign]
+    del row, foreign
+    up = rank[r_dst] < rank[r_src]              # dst above src
+    pplus = np.bincount(r_src[up], minlength=n)
+    pplus_t = np.bincount(r_src[up & tv[r_dst]], minlength=n)
+    dn = ~up
+    ys, xs = r_src[dn], r_dst[dn]
+    keep = (pplus[xs] > 0) & (pplus[ys] > 0) & (tv[xs] | tv[ys])
+    ys, xs = ys[keep], xs[keep]
+    both = tv[xs] & tv[ys]
+    px = np.where(both, pplus[xs], pplus_t[xs]).astype(np.float64)
+    py = np.where(both, pplus[ys], pplus_t[ys]).astype(np.float64)
+    print(f"forward probes {px.sum():.4e}")
+    for c in [1, 2, 4]:
+        cost = np.minimum(px, c * py * np.log2(np.maximum(px, 2)))
+        rev = px > c * py * np.log2(np.maximum(px, 2))
+        print(f"c={c}: hybrid cost {cost.sum():.4e}, reversed pairs {rev.mean():.3f}, "
+              f"reversed probes {py[rev].sum():.3e} (searches), saved forward {px[rev].sum():.3e}")
