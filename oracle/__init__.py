@@ -50,6 +50,10 @@ def _load():
         lib.oracle_rsi.argtypes = [i64, _P, _P, _P, i32, _P, _P, ctypes.c_double, i64, _P, _P, _P, _P]
         lib.oracle_topk.restype = i64
         lib.oracle_topk.argtypes = [i64, _P, i64, _P, _P]
+        lib.oracle_mix64.restype = ctypes.c_uint64
+        lib.oracle_mix64.argtypes = [ctypes.c_uint64]
+        lib.oracle_awcc_removal.restype = i64
+        lib.oracle_awcc_removal.argtypes = [i64, _P, _P, _P, _P, i64, i32, i32, i32, i32, ctypes.c_uint64, _P, _P]
         _lib = lib
     return _lib
 
@@ -130,6 +134,25 @@ def topk(R, K):
     sc = np.zeros(max(K, 1), dtype=np.float64)
     cnt = _load().oracle_topk(R.size, _ptr(R), K, _ptr(ids), _ptr(sc))
     return ids[:cnt], sc[:cnt]
+
+
+def awcc_removal(g, S, mode="edge", step_pct=5, max_pct=75, trials=1, seed=0):
+    """NEXT-1 (P:667-676): per-trial |zeta_j(v)| int32[trials, J+1, |S|] and the
+    mean absolute AWCC per step float64[J+1] (step 0 = no removal = AWCC)."""
+    S = _c(S, np.int32)
+    J1 = max_pct // step_pct + 1
+    zeta = np.zeros((trials, J1, S.size), dtype=np.int32)
+    mean = np.zeros(J1, dtype=np.float64)
+    r = _load().oracle_awcc_removal(g.n, _ptr(_c(g.rowptr, np.int64)), _ptr(_c(g.col, np.int32)),
+                                    _ptr(_c(g.comm, np.int32)), _ptr(S), S.size, 0 if mode == "edge" else 1,
+                                    step_pct, max_pct, trials, int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(zeta), _ptr(mean))
+    if r < 0:
+        raise ValueError("oracle_awcc_removal: bad arguments")
+    return zeta, mean
+
+
+def mix64(z):
+    return int(_load().oracle_mix64(int(z) & 0xFFFFFFFFFFFFFFFF))
 
 
 @dataclass

@@ -266,3 +266,104 @@ int64_t oracle_topk(int64_t n, const double *R, int64_t K, int32_t *ids_out, dou
     free(s);
     return cnt;
 }
+
+/* ---- NEXT-1: absolute AWCC under cumulative random removal (PAPER §VII.B,
+ * P:667-676; SPEC awcc / absolute_awcc / simulate_removal).
+ *
+ * AWCC(S) = (1/|S|) sum_{v in S} |zeta(v)| / d(v), zeta(v) = the community ids
+ * of v's neighbours. The absolute variant recomputes zeta over the
+ * surviving edges/vertices while d(v) stays the original degree; a
+ * removed v in S contributes 0, as does d(v) = 0.
+ *
+ * Removal (DESIGN readings C-28/C-29): "random removal of 5% of the
+ * edges/nodes at each iteration ... until up to 75%" is cumulative
+ * within a trial: every item (undirected edge {u, v} with id
+ * min(u,v) << 32 | max(u,v), or vertex v) of trial t gets the key
+ * mix64(s_t ^ id), mix64 = the splitmix64 finaliser (a bijection on 64-bit
+ * words, so keys are distinct), s_t = mix64(seed + (2t + mode) * 0x9E3779B97F4A7C15)
+ * for mode 0 = edges, 1 = nodes; step j removes the r_j = floor(j * step% * M / 100)
+ * items of smallest key (M = |E| or |V|), i.e. those with key < T_j, T_j the key
+ * of rank r_j (all items when r_j = M). Ids are the caller's (original) ids.
+ * Here: all keys, one qsort, then zeta by scanning each v's row; the j-th
+ * per-trial value sums |zeta|/d(v) in S order and divides by |S|, the mean sums
+ * the trial values in trial order and divides by the trial count. ---- */
+uint64_t oracle_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static int cmp_u64(const void *a, const void *b) {
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* returns J + 1 (steps 0..J), or -1 on bad arguments */
+int64_t oracle_awcc_removal(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C,
+                            const int32_t *S, int64_t nS, int32_t mode, int32_t step_pct, int32_t max_pct,
+                            int32_t trials, uint64_t seed, int32_t *zeta_out, double *mean_out) {
+    if (nS < 1 || step_pct < 1 || max_pct < 0 || max_pct > 100 || trials < 1 || (mode != 0 && mode != 1)) return -1;
+    const int64_t J = max_pct / step_pct;
+    const int64_t m = rowptr[n] / 2;
+    const int64_t M = mode == 0 ? m : n;
+    uint64_t *keys = malloc(sizeof(uint64_t) * (M ? M : 1));
+    uint64_t *T = malloc(sizeof(uint64_t) * (J + 1));
+    int *all = malloc(sizeof(int) * (J + 1));
+    int64_t dmax = 1;
+    for (int64_t s = 0; s < nS; s++) {
+        const int64_t d = rowptr[S[s] + 1] - rowptr[S[s]];
+        if (d > dmax) dmax = d;
+    }
+    int32_t *cbuf = malloc(sizeof(int32_t) * dmax);
+    for (int64_t j = 0; j <= J; j++) mean_out[j] = 0.0;
+    for (int32_t t = 0; t < trials; t++) {
+        const uint64_t st = oracle_mix64(seed + (uint64_t)(2 * (int64_t)t + mode) * 0x9E3779B97F4A7C15ull);
+        /* keys of every item */
+        int64_t q = 0;
+        if (mode == 0) {
+            for (int64_t u = 0; u < n; u++)
+                for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++)
+                    if ((int64_t)col[e] > u) keys[q++] = oracle_mix64(st ^ (((uint64_t)u << 32) | (uint64_t)col[e]));
+        } else {
+            for (int64_t v = 0; v < n; v++) keys[q++] = oracle_mix64(st ^ (uint64_t)v);
+        }
+        qsort(keys, (size_t)M, sizeof(uint64_t), cmp_u64);
+        for (int64_t j = 0; j <= J; j++) {
+            const int64_t r = (j * step_pct * M) / 100;
+            all[j] = r >= M;
+            T[j] = r >= M ? 0 : keys[r];
+        }
+        for (int64_t j = 0; j <= J; j++) {
+            double acc = 0.0;
+            for (int64_t s = 0; s < nS; s++) {
+                const int64_t v = S[s];
+                const int64_t d = rowptr[v + 1] - rowptr[v];
+                int64_t z = 0;
+                int v_removed = 0;
+                if (mode == 1) v_removed = all[j] || oracle_mix64(st ^ (uint64_t)v) < T[j];
+                if (!v_removed) {
+                    int64_t nb = 0;   /* communities of the surviving neighbours, then distinct count */
+                    for (int64_t e = rowptr[v]; e < rowptr[v + 1]; e++) {
+                        const int64_t x = col[e];
+                        int removed;
+                        if (mode == 0) {
+                            const uint64_t id = ((uint64_t)(v < x ? v : x) << 32) | (uint64_t)(v < x ? x : v);
+                            removed = all[j] || oracle_mix64(st ^ id) < T[j];
+                        } else {
+                            removed = all[j] || oracle_mix64(st ^ (uint64_t)x) < T[j];
+                        }
+                        if (removed) continue;
+                        cbuf[nb++] = C[x];
+                    }
+                    qsort(cbuf, (size_t)nb, sizeof(int32_t), cmp_i32);
+                    for (int64_t i = 0; i < nb; i++) z += (i == 0 || cbuf[i] != cbuf[i - 1]);
+                }
+                zeta_out[((int64_t)t * (J + 1) + j) * nS + s] = (int32_t)z;
+                if (d > 0) acc += (double)z / (double)d;
+            }
+            mean_out[j] += acc / (double)nS;
+        }
+    }
+    for (int64_t j = 0; j <= J; j++) mean_out[j] /= (double)trials;
+    free(keys); free(T); free(all); free(cbuf);
+    return J + 1;
+}
