@@ -190,6 +190,29 @@ rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out);
 /* Number of librs kernels launched on ctx since creation (bench accounting). */
 int64_t rs_kernel_launches(const rs_ctx *ctx);
 
+/* ---- NEXT-1: robustness evaluation (PAPER §VII.B). ----
+ * Absolute AWCC of the vertex set S (original ids, e.g. the top-K of rs_topk)
+ * under cumulative random removal: AWCC = (1/|S|) sum_{v in S} |zeta(v)|/d(v),
+ * zeta(v) the community ids (as given to rs_set_communities) of v's surviving
+ * neighbours, d(v) the ORIGINAL degree; a removed v contributes 0.
+ * Trial t keys every item -- undirected edge {u, v} with id min << 32 | max, or
+ * vertex v -- with mix64(s_t ^ id), mix64 the SplitMix64 finaliser and
+ * s_t = mix64(seed + (2t + mode) * 0x9E3779B97F4A7C15); step j = 0..J
+ * (J = max_pct / step_pct) removes the floor(j * step_pct * M / 100) items of
+ * smallest key (M = |E| or |V|), so the removal sets are nested (DESIGN C-28,
+ * C-29). zeta_out int32[trials][J+1][|S|] (host, or NULL) receives |zeta_j(v)|;
+ * mean_out double[J+1] (host, or NULL) the mean over trials of each step's
+ * AWCC (per trial: sum over S in order of |zeta|/d, / |S|; then the trial sum
+ * in order, / trials); *steps_out = J + 1. S may be host or device memory.
+ * Requires rs_load_csr and rs_set_communities. RS_EINVAL on an empty S, an
+ * out-of-range id, a bad mode, step_pct < 1, max_pct outside [0, 100],
+ * trials < 1 or more than 126 steps; RS_ENOMEM / RS_ECUDA on device errors. */
+#define RS_REMOVE_EDGES 0
+#define RS_REMOVE_NODES 1
+rs_status rs_awcc_removal(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t mode, int32_t step_pct,
+                          int32_t max_pct, int32_t trials, uint64_t seed, int32_t *zeta_out, double *mean_out,
+                          int64_t *steps_out);
+
 /* ---- Multi-GPU host protocol. Pure host functions on host
  * arrays, no context, no device work; rs_create_dist / rs_topk call them, and
  * they are exported so that the protocol can be exercised without GPUs. ---- */

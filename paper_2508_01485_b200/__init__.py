@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_HERE, "librs.so")
 RS_OK, RS_EINVAL, RS_ESTATE, RS_ENOMEM, RS_ECUDA, RS_ENCCL = 0, -1, -2, -3, -4, -5
 RS_VALIDATE = 1
 RS_GATHER_SCORES = 1
+RS_REMOVE_EDGES, RS_REMOVE_NODES = 0, 1
 
 
 def RS_E_SHARES(s: int) -> int:
@@ -68,6 +69,8 @@ SIGNATURES = [
     ("rs_get_triad_counts", ctypes.c_int, [_P, _P, _P]),
     ("rs_get_targets", ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int32)]),
     ("rs_kernel_launches", ctypes.c_int64, [_P]),
+    ("rs_awcc_removal", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
     ("rs_split_ranges", ctypes.c_int, [ctypes.c_int64, _P, ctypes.c_int32, _P]),
     ("rs_merge_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P,
                                            ctypes.POINTER(ctypes.c_int64)]),
@@ -230,6 +233,23 @@ def rs_kernel_launches(ctx) -> int:
     return int(load_library().rs_kernel_launches(ctx))
 
 
+def rs_awcc_removal(ctx, S, mode: str = "edge", step_pct: int = 5, max_pct: int = 75, trials: int = 1,
+                    seed: int = 0):
+    """NEXT-1: (zeta int32[trials, J+1, |S|], mean float64[J+1]) of the
+    absolute AWCC of S under cumulative random edge or node removal."""
+    Sa = _as(S, np.int32)
+    nS = int(Sa.shape[0])
+    J1 = max_pct // step_pct + 1 if step_pct > 0 else 1
+    zeta = np.zeros((trials, J1, nS), dtype=np.int32)
+    mean = np.zeros(J1, dtype=np.float64)
+    steps = ctypes.c_int64(0)
+    m = RS_REMOVE_EDGES if mode == "edge" else RS_REMOVE_NODES
+    _check(ctx, load_library().rs_awcc_removal(ctx, _ptr(Sa), nS, m, int(step_pct), int(max_pct), int(trials),
+                                               int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(zeta), _ptr(mean),
+                                               ctypes.byref(steps)))
+    return zeta[:, :steps.value], mean[:steps.value]
+
+
 # ------------------------------------------------------------------ multi-GPU host protocol
 def rs_split_ranges(work_incl, world: int) -> np.ndarray:
     """bounds int64[world+1] of the balanced contiguous split (include/rs.h)."""
@@ -324,6 +344,9 @@ class Scorer:
 
     def targets(self):
         return rs_get_targets(self.ctx)
+
+    def awcc_removal(self, S, mode="edge", step_pct=5, max_pct=75, trials=1, seed=0):
+        return rs_awcc_removal(self.ctx, S, mode, step_pct, max_pct, trials, seed)
 
     def launches(self) -> int:
         return rs_kernel_launches(self.ctx)

@@ -564,6 +564,73 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
     return RS_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-1: robustness evaluation
+static uint64_t host_mix64(uint64_t z) {   // SplitMix64 finaliser (same generator as k_awcc.cu)
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+extern "C" rs_status rs_awcc_removal(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t mode, int32_t step_pct,
+                                     int32_t max_pct, int32_t trials, uint64_t seed, int32_t *zeta_out,
+                                     double *mean_out, int64_t *steps_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.has_comm) return fail(ctx, RS_ESTATE, "rs_awcc_removal: call rs_load_csr and rs_set_communities first");
+    if (!S || nS < 1) return fail(ctx, RS_EINVAL, "rs_awcc_removal: S must be a non-empty vertex set");
+    if (mode != RS_REMOVE_EDGES && mode != RS_REMOVE_NODES) return fail(ctx, RS_EINVAL, "rs_awcc_removal: bad mode");
+    if (step_pct < 1 || max_pct < 0 || max_pct > 100 || trials < 1)
+        return fail(ctx, RS_EINVAL, "rs_awcc_removal: need 1 <= step_pct, 0 <= max_pct <= 100, trials >= 1");
+    const int J1 = max_pct / step_pct + 1;
+    if (J1 > 127) return fail(ctx, RS_EINVAL, "rs_awcc_removal: at most 126 steps");
+    std::vector<int32_t> hS(nS);
+    CK(cudaMemcpy(hS.data(), S, sizeof(int32_t) * nS, is_device_ptr(S) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    for (int64_t i = 0; i < nS; i++)
+        if (hS[i] < 0 || hS[i] >= c.n) return fail(ctx, RS_EINVAL, "rs_awcc_removal: vertex id out of range");
+    const int64_t M = mode == RS_REMOVE_EDGES ? c.nnz / 2 : c.n;
+    int64_t cap = 2;
+    while (cap < 2 * std::max<int64_t>(c.d_max, 1)) cap <<= 1;          // per-vertex community table
+    const size_t sbytes = rs::awcc_scratch_bytes(M, J1, cap, nS);
+    char *buf = nullptr;
+    CK(cudaMalloc(&buf, sbytes + sizeof(int32_t) * (size_t)nS * (J1 + 1) + sizeof(int64_t) * nS + 1024));
+    int32_t *S_dev = (int32_t *)buf;
+    int32_t *zeta_dev = S_dev + nS;
+    int64_t *deg_dev = (int64_t *)(((uintptr_t)(zeta_dev + (size_t)nS * J1) + 15) & ~(uintptr_t)15);
+    void *scratch = (void *)(((uintptr_t)(deg_dev + nS) + 255) & ~(uintptr_t)255);
+    rs_status st_ret = RS_OK;
+    std::vector<int32_t> hz((size_t)nS * J1);
+    std::vector<int64_t> hdeg(nS);
+    std::vector<double> mean(J1, 0.0);
+    cudaError_t e = cudaMemcpyAsync(S_dev, hS.data(), sizeof(int32_t) * nS, cudaMemcpyHostToDevice, c.stream);
+    if (e == cudaSuccess) e = rs::launch_awcc_degrees(c, S_dev, nS, deg_dev);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hdeg.data(), deg_dev, sizeof(int64_t) * nS, cudaMemcpyDeviceToHost, c.stream);
+    for (int32_t t = 0; t < trials && e == cudaSuccess; t++) {
+        const uint64_t salt = host_mix64(seed + (uint64_t)(2 * (int64_t)t + mode) * 0x9E3779B97F4A7C15ull);
+        e = rs::launch_awcc_trial(c, S_dev, nS, mode, step_pct, J1, salt, zeta_dev, scratch, sbytes, cap);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hz.data(), zeta_dev, sizeof(int32_t) * nS * J1, cudaMemcpyDeviceToHost, c.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+        if (e != cudaSuccess) break;
+        // the trial's AWCC per step: |zeta|/d in S order, / |S| (the oracle's order)
+        for (int j = 0; j < J1; j++) {
+            double acc = 0.0;
+            for (int64_t s = 0; s < nS; s++) {
+                const int32_t z = hz[(size_t)j * nS + s];
+                if (zeta_out) zeta_out[((int64_t)t * J1 + j) * nS + s] = z;
+                if (hdeg[s] > 0) acc += (double)z / (double)hdeg[s];
+            }
+            mean[j] += acc / (double)nS;
+        }
+    }
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(ctx, RS_ECUDA, std::string("rs_awcc_removal: ") + cudaGetErrorString(e));
+    for (int j = 0; j < J1; j++) mean[j] /= (double)trials;
+    if (mean_out) memcpy(mean_out, mean.data(), sizeof(double) * J1);
+    if (steps_out) *steps_out = J1;
+    return st_ret;
+}
+
 // ------------------------------------------------------------------ multi-GPU host protocol
 extern "C" rs_status rs_split_ranges(int64_t n, const int64_t *work_incl, int32_t world, int64_t *bounds_out) {
     if (n < 0 || world < 1 || !bounds_out || (n > 0 && !work_incl)) return RS_EINVAL;

@@ -202,6 +202,10 @@ cudaError_t launch_phase_a(Ctx &c);
 cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
 cudaError_t launch_finalize(Ctx &c);
+size_t awcc_scratch_bytes(int64_t M, int J1, int64_t cap, int64_t nS);
+cudaError_t launch_awcc_degrees(Ctx &c, const int32_t *S_dev, int64_t nS, int64_t *deg_dev);
+cudaError_t launch_awcc_trial(Ctx &c, const int32_t *S_dev, int64_t nS, int mode, int step_pct, int J1, uint64_t st,
+                              int32_t *zeta_dev, void *scratch, size_t scratch_bytes, int64_t cap);
 cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light);
 cudaError_t launch_triangle_counts(Ctx &c);
 cudaError_t launch_e_items(Ctx &c);

@@ -230,3 +230,55 @@ def test_user_targets_and_errors():
     with pytest.raises(rsb.RsError):
         s.set_communities(-g.comm - 1, 2)
     s.close()
+
+
+# ---------------------------------------------------------------- NEXT-1: robustness evaluation
+@pytest.mark.parametrize("name,scale", [("karate", None), ("dblp", 0.02), ("orkut", 0.003), ("lj", 0.002)])
+@pytest.mark.parametrize("mode", ["edge", "node"])
+def test_awcc_removal_parity(name, scale, mode):
+    """|zeta_j(v)| bit-exact and the mean AWCC per step bit-identical to the
+    oracle (DESIGN C-28, C-29), S = the GPU's top-25 plus a random set."""
+    g = gen.load_fixture(name)[0] if scale is None else gen.config_graph(name, scale)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    k = 2 if name == "karate" else 5
+    s.set_communities(g.comm, k)
+    s.score()
+    top, _ = s.topk(min(25, g.n))
+    rng = np.random.default_rng(17)
+    S = np.concatenate([top, rng.choice(g.n, size=min(10, g.n), replace=False)]).astype(np.int32)
+    zg, mg = s.awcc_removal(S, mode, 5, 75, 3, 0xA11CE)
+    s.close()
+    zo, mo = oracle.awcc_removal(g, S, mode, 5, 75, 3, 0xA11CE)
+    assert np.array_equal(zg, zo)
+    assert np.array_equal(mg.view(np.uint64), mo.view(np.uint64))
+
+
+def test_awcc_removal_full_orkut_edges():
+    """full-size Orkut shape (117 M edges), one trial, 10 % steps to 100 %"""
+    g = gen.config_graph("orkut")
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, 5)
+    s.score()
+    top, _ = s.topk(25)
+    zg, mg = s.awcc_removal(top, "edge", 10, 100, 1, 7)
+    s.close()
+    zo, mo = oracle.awcc_removal(g, top, "edge", 10, 100, 1, 7)
+    assert np.array_equal(zg, zo)
+    assert np.array_equal(mg, mo)
+    assert (zg[0, -1] == 0).all()
+
+
+def test_awcc_removal_errors():
+    g, _ = gen.load_fixture("karate")
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    with pytest.raises(rsb.RsError):
+        s.awcc_removal([0, 1])                      # communities not set
+    s.set_communities(g.comm, 2)
+    for bad in [dict(S=[]), dict(S=[99]), dict(S=[0], step_pct=0), dict(S=[0], max_pct=101),
+                dict(S=[0], trials=0)]:
+        with pytest.raises((rsb.RsError, ValueError)):
+            s.awcc_removal(**bad)
+    s.close()
