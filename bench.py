@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--no-awcc", action="store_true", help="skip the NEXT-1 robustness-evaluation timing")
     p.add_argument("--config", default="orkut", choices=["orkut", "lj", "dblp", "karate", "friendster"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--K", type=int, default=25)
@@ -257,6 +258,25 @@ def main():
             if traffic else None,
             "phases": phases, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"}
 
+    # NEXT-1: absolute AWCC of the top-K under cumulative random
+    # edge / node removal, 5 %..75 % (16 steps), per trial; rs_awcc_removal is
+    # host-synchronous, so its wall time is its latency
+    awcc = None
+    if not a.no_awcc:
+        top = ids_d.cpu().numpy()
+        awcc = {"S": int(top.size), "steps": 16}
+        for mode in ("edge", "node"):
+            sc.awcc_removal(top, mode, 5, 75, 1, 1)            # warm-up
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            _, mean = sc.awcc_removal(top, mode, 5, 75, 3, 2)
+            torch.cuda.synchronize(dev)
+            dt = (time.perf_counter() - t0) / 3
+            items = m if mode == "edge" else n
+            awcc[f"{mode}_ms_per_trial"] = round(dt * 1e3, 3)
+            awcc[f"{mode}_Gitems_per_s"] = round(items / dt / 1e9, 2)
+            awcc[f"{mode}_awcc_0_75"] = [round(float(mean[0]), 6), round(float(mean[-1]), 6)]
+
     e2e = None
     if not a.no_e2e:
         e2e = measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st)
@@ -278,6 +298,7 @@ def main():
                        "parallelism": f"head-range x{world}" if world > 1 else "single GPU"},
             "roofline": roof,
             "topk_latency_ms": round(float(np.median(tk_ms)), 4),
+            "next_awcc_removal": awcc,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk_s, "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
         }
