@@ -50,6 +50,9 @@ def _load():
         lib.oracle_rsi.argtypes = [i64, _P, _P, _P, i32, _P, _P, ctypes.c_double, i64, _P, _P, _P, _P]
         lib.oracle_topk.restype = i64
         lib.oracle_topk.argtypes = [i64, _P, i64, _P, _P]
+        lib.oracle_weights_variant.argtypes = [i64, i32, _P, i32, _P]
+        lib.oracle_omega_max_eb.restype = ctypes.c_double
+        lib.oracle_omega_max_eb.argtypes = [i64, _P, _P, _P, i32, _P, _P, i32, _P]
         lib.oracle_mix64.restype = ctypes.c_uint64
         lib.oracle_mix64.argtypes = [ctypes.c_uint64]
         lib.oracle_awcc_removal.restype = i64
@@ -134,6 +137,42 @@ def topk(R, K):
     sc = np.zeros(max(K, 1), dtype=np.float64)
     cnt = _load().oracle_topk(R.size, _ptr(R), K, _ptr(ids), _ptr(sc))
     return ids[:cnt], sc[:cnt]
+
+
+LITERAL_L, GATE_L, WMAX_EB = 1, 2, 4   # NEXT-3 variant flags (oracle numbering)
+
+
+def weights_variant(f, flags):
+    """Eq. 3/5 weights under the literal |L| (flags & 1) and/or Algorithm 1's gate (flags & 2)"""
+    f = _c(f, np.int32)
+    n, k = f.shape
+    w = np.zeros((n, k), dtype=np.float64)
+    _load().oracle_weights_variant(n, k, _ptr(f), int(flags) & 3, _ptr(w))
+    return w
+
+
+def omega_max_eb(g, targets, f, w, flags):
+    """omega_max over Algorithm 1's E_b"""
+    targets = _c(targets, np.int32)
+    return _load().oracle_omega_max_eb(g.n, _ptr(_c(g.rowptr, np.int64)), _ptr(_c(g.col, np.int32)),
+                                       _ptr(_c(g.comm, np.int32)), targets.size, _ptr(targets),
+                                       _ptr(_c(f, np.int32)), int(flags) & 3, _ptr(_c(w, np.float64)))
+
+
+def run_variant(g, k, flags, K=25, targets=None):
+    """O0-O8 with the NEXT-3 variants: weights per flags & 3, omega_max over E_b if
+    flags & 4 (else over all cells)"""
+    if targets is None:
+        targets = select_targets(g.comm, k)
+    targets = _c(targets, np.int32)
+    b = border(g)
+    f, T = counts(g, targets)
+    w = weights_variant(f, flags)
+    wmax = omega_max_eb(g, targets, f, w, flags) if flags & WMAX_EB else omega_max(w)
+    off, pl = pred(g)
+    R, nI, nII = rsi(g, targets, w, wmax)
+    ids, sc = topk(R, K)
+    return OracleResult(targets, b, f, T, w, wmax, off, pl, R, nI, nII, ids, sc)
 
 
 def awcc_removal(g, S, mode="edge", step_pct=5, max_pct=75, trials=1, seed=0):

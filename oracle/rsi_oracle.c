@@ -156,6 +156,60 @@ double oracle_omega_max(int64_t n, int32_t k, const double *omega) {
     return m;
 }
 
+/* ---- NEXT-3: the paper's literal variants. ----
+ * flags & 1: |L(u,v)| as Eq. 2 defines L: the communities of N(v)
+ *            other than C(u) = C_i, i.e. L_all - [f_i > 0] (not Algorithm 2's
+ *            L_all - 1 for every column);
+ * flags & 2: Algorithm 1's gate: omega_v(C_i) = 0 unless |L| > 1.
+ * Entropy exactly as oracle_weights (Eq. 3, direct sum). */
+void oracle_weights_variant(int64_t n, int32_t k, const int32_t *f_all, int32_t flags, double *omega_out) {
+    for (int64_t v = 0; v < n; v++) {
+        const int32_t *f = f_all + v * k;
+        double *w = omega_out + v * k;
+        int64_t T = 0; int32_t L_all = 0;
+        for (int32_t j = 0; j < k; j++) { T += f[j]; if (f[j] > 0) L_all++; }
+        for (int32_t i = 0; i < k; i++) {
+            const int32_t L = (flags & 1) ? L_all - (f[i] > 0) : L_all - 1;
+            double H = 0.0;
+            const double Y = (double)(T - f[i]);
+            if (Y > 0.0)
+                for (int32_t j = 0; j < k; j++) {
+                    if (j == i || f[j] == 0) continue;
+                    double p = (double)f[j] / Y;
+                    H -= p * log2(p);
+                }
+            w[i] = ((flags & 2) && L <= 1) || L <= 0 ? 0.0 : H * (double)L;
+            if (w[i] == 0.0) w[i] = 0.0;   /* canonical +0 */
+        }
+    }
+}
+
+/* omega_max over Algorithm 1's E_b only ("max edge weight in E_b"):
+ * the pairs (u, v) of border vertices with C(u) = C(v) or v in N(u)
+ * whose |L(u,v)| > 1 (|L| per flags & 1 as above) give the edge
+ * (v -> u) of weight omega_v(C(u)). For v in V_b and target column i
+ * such a u exists iff C_i = C(v) (u = v; the loop includes it) or v has a
+ * neighbour in C_i (that neighbour is a border vertex). */
+double oracle_omega_max_eb(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C, int32_t k,
+                           const int32_t *targets, const int32_t *f_all, int32_t flags, const double *omega) {
+    double m = 0.0;
+    for (int64_t v = 0; v < n; v++) {
+        int border = 0;
+        for (int64_t e = rowptr[v]; e < rowptr[v + 1]; e++) if (C[col[e]] != C[v]) { border = 1; break; }
+        if (!border) continue;
+        const int32_t *f = f_all + v * k;
+        int32_t L_all = 0;
+        for (int32_t j = 0; j < k; j++) if (f[j] > 0) L_all++;
+        for (int32_t i = 0; i < k; i++) {
+            const int32_t L = (flags & 1) ? L_all - (f[i] > 0) : L_all - 1;
+            if (L <= 1) continue;
+            if (targets[i] != C[v] && f[i] == 0) continue;
+            if (omega[v * k + i] > m) m = omega[v * k + i];
+        }
+    }
+    return m;
+}
+
 /* ---- O5a. G' predecessor lists ((v->u) in E_b iff (u,v) in E, both
  * border and C(u) != C(v); adjacency + different communities already makes
  * both endpoints border vertices). pred_off is n+1; pred_out receives the
