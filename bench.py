@@ -277,6 +277,26 @@ def main():
             awcc[f"{mode}_Gitems_per_s"] = round(items / dt / 1e9, 2)
             awcc[f"{mode}_awcc_0_75"] = [round(float(mean[0]), 6), round(float(mean[-1]), 6)]
 
+    # NEXT-3: the step with every literal variant on (RS_LITERAL_L | RS_GATE_L | RS_WMAX_EB)
+    variants = None
+    if not a.no_awcc:
+        vf = rsb.RS_LITERAL_L | rsb.RS_GATE_L | rsb.RS_WMAX_EB
+        vms = []
+        for i in range(3 + a.warmup):
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sc.set_communities(comm_d, a.k)
+            sc.score(flags=vf)
+            sc.topk(a.K, ids_d, sco_d)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if i >= a.warmup:
+                vms.append(e0.elapsed_time(e1))
+        variants = {"flags": "literal_L|gate_L|wmax_eb", "ms_per_step": round(float(np.median(vms)), 4)}
+        sc.score()   # back to the adopted readings
+
     e2e = None
     if not a.no_e2e:
         e2e = measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st)
@@ -299,6 +319,7 @@ def main():
             "roofline": roof,
             "topk_latency_ms": round(float(np.median(tk_ms)), 4),
             "next_awcc_removal": awcc,
+            "next_literal_variants": variants,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk_s, "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
         }

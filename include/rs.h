@@ -74,6 +74,14 @@ typedef struct {
  * split by middle vertex (s = 2..255) on one GPU; results must not change. */
 #define RS_E_SHARES(s)    (((uint32_t)(s) & 0xFFu) << 8)
 #define RS_E_SHARES_OF(f) (((f) >> 8) & 0xFFu)
+/* NEXT-3 literal variants of the paper (DESIGN reading C-30; default = the
+ * adopted readings C-3, C-4, C-7): */
+#define RS_LITERAL_L (1u << 16) /* |L(u,v)| as Eq. 2 defines L: communities of
+                                   N(v) other than C(u), instead of Algorithm 2's
+                                   L_all - 1 for every column */
+#define RS_GATE_L    (1u << 17) /* Algorithm 1's gate: omega = 0 unless |L| > 1 */
+#define RS_WMAX_EB   (1u << 18) /* omega_max over Algorithm 1's E_b edges only:
+                                   border v, |L| > 1, c = C(v) or v has a neighbour in c */
 
 /* Create a context on CUDA device `device`. `cuda_stream` is a cudaStream_t
  * (NULL = the legacy default stream) on which all work is issued; the caller

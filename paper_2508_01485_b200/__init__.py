@@ -23,6 +23,7 @@ RS_OK, RS_EINVAL, RS_ESTATE, RS_ENOMEM, RS_ECUDA, RS_ENCCL = 0, -1, -2, -3, -4, 
 RS_VALIDATE = 1
 RS_GATHER_SCORES = 1
 RS_REMOVE_EDGES, RS_REMOVE_NODES = 0, 1
+RS_LITERAL_L, RS_GATE_L, RS_WMAX_EB = 1 << 16, 1 << 17, 1 << 18   # NEXT-3 variants (rs_score flags)
 
 
 def RS_E_SHARES(s: int) -> int:
@@ -316,8 +317,8 @@ class Scorer:
         rs_set_communities(self.ctx, comm, k, targets)
         self.k = int(k)
 
-    def score(self, scores_out=None, stats: bool = False, gather: bool = False):
-        return rs_score(self.ctx, scores_out, stats, RS_GATHER_SCORES if gather else 0)
+    def score(self, scores_out=None, stats: bool = False, gather: bool = False, flags: int = 0):
+        return rs_score(self.ctx, scores_out, stats, (RS_GATHER_SCORES if gather else 0) | flags)
 
     def scores(self) -> np.ndarray:
         out = np.empty(self.n, dtype=np.float64)

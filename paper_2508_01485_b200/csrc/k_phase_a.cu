@@ -31,6 +31,7 @@ struct PhaseAArgs {
     int64_t nverts;
     int32_t k;
     double wide_bound;                  // d^2 above which a head's Type-I sum needs 3 limbs
+    int variant;                        // NEXT-3 (rs_score flags >> 16): 1 literal |L|, 2 |L| > 1 gate, 4 E_b max
     int64_t n;
     int32_t *__restrict__ pplus;
     double *__restrict__ wps;
@@ -50,15 +51,31 @@ __device__ __forceinline__ double lg2(const PhaseAArgs &a, int64_t x) {
     return x < a.l2n ? __ldg(a.l2t + x) : log2((double)x);
 }
 
+// |L| of column c: Algorithm 2's L_all - 1 (reading C-3), or with the
+// NEXT-3 literal variant Eq. 2's communities other than c
+__device__ __forceinline__ int L_of(const PhaseAArgs &a, int fc, int L_all) {
+    return (a.variant & 1) ? L_all - (fc > 0) : L_all - 1;
+}
+
 // omega for column c of a row with T, L_all, X = sum f log2 f (Algorithm 2)
 __device__ __forceinline__ double weight_of(const PhaseAArgs &a, int fc, int T, int L_all, double X) {
     const int others = L_all - (fc > 0);   // nonzero columns of L(u, .) besides c
     if (L_all < 2 || others < 2) return 0.0; // one remaining community: H = 0 exactly
+    const int L = L_of(a, fc, L_all);
+    if ((a.variant & 2) && L <= 1) return 0.0;   // NEXT-3: Algorithm 1's gate
     const int Y = T - fc;                    // > 0
     const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
     const double H = lg2(a, Y) - (X - xc) / (double)Y;
-    const double w = H * (double)(L_all - 1);
+    const double w = H * (double)L;
     return w > 0.0 ? w : 0.0;                // canonical +0.0
+}
+
+// does cell (u, c) count towards omega_max? All cells (C-7), or with the NEXT-3
+// variant only Algorithm 1's E_b edges: u border, |L| > 1, and c = C(u)
+// or u has a neighbour in c
+__device__ __forceinline__ bool in_max(const PhaseAArgs &a, int fc, int L_all, int c, int lu, int pc) {
+    if (!(a.variant & 4)) return true;
+    return pc > 0 && L_of(a, fc, L_all) > 1 && (c == lu || fc > 0);
 }
 
 __device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, double a_self, int pc, uint8_t lu,
@@ -208,7 +225,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
         a.amat[u * k + c] = ac;
         a.f[u * k + c] = fc;
         a.bql[(int64_t)c * a.n + u].Q = ac * ac;
-        wmax = w > wmax ? w : wmax;
+        if (in_max(a, fc, L_all, c, lu, pc)) wmax = w > wmax ? w : wmax;
         if (c == (int)lu) a_self = ac;
     }
     const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
@@ -273,7 +290,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
         a.amat[u * k + c] = ac;
         a.f[u * k + c] = fc;
         a.bql[(int64_t)c * a.n + u].Q = ac * ac;
-        wmax = w > wmax ? w : wmax;
+        if (in_max(a, fc, L_all, c, lu, pc)) wmax = w > wmax ? w : wmax;
     }
     g.sync();
     if (g.lane == 0) {
@@ -379,6 +396,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
     // unnormalised grouped Type-I terms are < 2 * omega_max_bound; a head needs the
     // 3-limb accumulator when d^2 >= |P|^2 times that bound could reach 2^31 (fx_red2)
     a.wide_bound = wide_bound(c.k);
+    a.variant = c.variant;
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8 && c.d_max < (1ll << 22)) launch_bins_a<false>(c, a);

@@ -401,6 +401,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (!c.has_comm) return fail(ctx, RS_ESTATE, "rs_score: call rs_load_csr and rs_set_communities first");
     const int64_t n = c.n;
     c.e_shares = (int)RS_E_SHARES_OF(flags);
+    c.variant = (int)((flags >> 16) & 7u);
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
     CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));

@@ -154,6 +154,7 @@ struct Ctx {
     int64_t kn_alloc = 0;        // ... and n
     bool scored = false;
     int e_shares = 1;            // test hook: Phase E run as this many rank shares (rs_score flags)
+    int variant = 0;             // NEXT-3 literal variants (rs_score flags >> 16)
 
     // top-k scratch
     unsigned long long *tk_hist = nullptr;   // 256 * 8
@@ -188,8 +189,9 @@ enum {
 // (grouped terms are < 2 * omega_max <= 2 (k-1) log2(k-1)): such heads use the
 // 3-limb accumulator (fx_red3) instead of fx_red2.
 inline double wide_bound(int k) {
+    // omega <= H |L| <= log2(k - 1) * k covers the literal |L| (<= k) of NEXT-3 too
     const double km1 = (double)(k - 1);
-    const double wb = km1 > 1.0 ? km1 * __builtin_log2(km1) : 1.0;
+    const double wb = km1 > 1.0 ? (double)k * __builtin_log2(km1) : 2.0;
     return 2147483648.0 / (2.0 * wb);
 }
 

@@ -12,7 +12,7 @@ SCORE_RTOL = 1e-9      # BASELINE.json north_star: fp64 RSI within 1e-9 relative
 WEIGHT_RTOL = 1e-10    # closed-form entropy (GPU) vs direct Eq.3 (oracle), DESIGN.md §5
 
 
-def run_gpu(g, k=None, targets=None, K=25, validate=True, scorer=None):
+def run_gpu(g, k=None, targets=None, K=25, validate=True, scorer=None, flags=0):
     s = scorer or rsb.Scorer(0)
     s.load_csr(g.rowptr, g.col, validate=validate)
     if targets is not None:
@@ -20,7 +20,7 @@ def run_gpu(g, k=None, targets=None, K=25, validate=True, scorer=None):
         k = len(targets)
     s.set_communities(g.comm, k, targets)
     R = np.empty(g.n, dtype=np.float64)
-    stats = s.score(scores_out=R, stats=True)
+    stats = s.score(scores_out=R, stats=True, flags=flags)
     f, T = s.counts()
     w, wmax = s.weights()
     bv = s.border()

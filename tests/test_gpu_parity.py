@@ -282,3 +282,17 @@ def test_awcc_removal_errors():
         with pytest.raises((rsb.RsError, ValueError)):
             s.awcc_removal(**bad)
     s.close()
+
+
+# ---------------------------------------------------------------- NEXT-3: literal variants
+@pytest.mark.parametrize("vflags", [1, 2, 3, 4, 7])
+@pytest.mark.parametrize("name,scale,k", [("karate", None, 2), ("dblp", 0.02, 5), ("orkut", 0.003, 5),
+                                          ("lj", 0.002, 7)])
+def test_literal_variants_parity(vflags, name, scale, k):
+    """the literal Eq. 2 |L| (1), Algorithm 1's gate (2) and omega_max over E_b (4):
+    weights, omega_max, scores, triad counts and top-k against oracle.run_variant
+    (rs_score flags = oracle flags << 16: RS_LITERAL_L, RS_GATE_L, RS_WMAX_EB)"""
+    g = gen.load_fixture(name)[0] if scale is None else gen.config_graph(name, scale)
+    r_or = oracle.run_variant(g, k, vflags, K=g.n)
+    r_gpu = run_gpu(g, k=k, targets=r_or.targets, K=g.n, flags=vflags << 16)
+    compare_full(g, r_or, r_gpu)
