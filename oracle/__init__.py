@@ -53,6 +53,8 @@ def _load():
         lib.oracle_weights_variant.argtypes = [i64, i32, _P, i32, _P]
         lib.oracle_omega_max_eb.restype = ctypes.c_double
         lib.oracle_omega_max_eb.argtypes = [i64, _P, _P, _P, i32, _P, _P, i32, _P]
+        lib.oracle_shii.restype = ctypes.c_double
+        lib.oracle_shii.argtypes = [i64, _P, _P, _P, _P, i64, i32, ctypes.c_double, i32, ctypes.c_uint64, _P, _P]
         lib.oracle_mix64.restype = ctypes.c_uint64
         lib.oracle_mix64.argtypes = [ctypes.c_uint64]
         lib.oracle_awcc_removal.restype = i64
@@ -188,6 +190,18 @@ def awcc_removal(g, S, mode="edge", step_pct=5, max_pct=75, trials=1, seed=0):
     if r < 0:
         raise ValueError("oracle_awcc_removal: bad arguments")
     return zeta, mean
+
+
+def shii(g, S, model="ic", p=0.1, runs=10, seed=0):
+    """NEXT-4: (influenced int64[|S|, runs, 2] = {all, outside C(seed)},
+    per-seed SHII float64[|S|], mean over S)"""
+    S = _c(S, np.int32)
+    out = np.zeros((S.size, runs, 2), dtype=np.int64)
+    per = np.zeros(S.size, dtype=np.float64)
+    m = _load().oracle_shii(g.n, _ptr(_c(g.rowptr, np.int64)), _ptr(_c(g.col, np.int32)), _ptr(_c(g.comm, np.int32)),
+                            _ptr(S), S.size, 0 if model == "ic" else 1, float(p), int(runs),
+                            int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(out), _ptr(per))
+    return out, per, m
 
 
 def mix64(z):

@@ -421,3 +421,83 @@ int64_t oracle_awcc_removal(int64_t n, const int64_t *rowptr, const int32_t *col
     free(keys); free(T); free(all); free(cbuf);
     return J + 1;
 }
+
+/* ---- NEXT-4: structural hole influence index (PAPER §VII.A, P:602-605;
+ * SPEC diffuse / shii; DESIGN reading C-31).
+ * SHII(u_s) = (influenced outside C(u_s)) / (influenced), averaged over runs.
+ * Run r of model m (0 = IC, 1 = LT) draws from s_r = mix64(seed + (2r + m + 1)
+ * * 0xD1B54A32D192ED03):
+ *  IC (independent cascade with probability p): each newly active a gets one
+ *     chance per inactive neighbour b, succeeding iff mix64(s_r ^ (a << 32 | b))
+ *     < thr, thr = floor(p * 2^64) (every edge when p >= 1). The outcome is the
+ *     set reachable from the seed over those "live" directed edges (the coin of
+ *     a -> b is drawn once, whenever a is active), computed here by a queue.
+ *  LT (linear threshold): theta_v = mix64(s_r ^ v) / 2^64; an inactive v
+ *     activates once (active neighbours) / d(v) >= theta_v with at least one
+ *     active neighbour; iterated over all vertices to the fixpoint.
+ * The seed is always influenced. Per seed: out[(s * runs + r) * 2 + {0, 1}] =
+ * {influenced, influenced outside C(seed)}; shii_out[s] = the mean over runs of
+ * their ratio (summed in run order); returns the mean of shii_out over S. ---- */
+static int lt_ready(uint64_t key, int64_t d, int64_t act) {
+    /* act / d >= key / 2^64  <=>  act * 2^64 >= key * d, exactly (act >= 1) */
+    if (act < 1) return 0;
+    const unsigned __int128 lhs = (unsigned __int128)(uint64_t)act << 64;
+    const unsigned __int128 rhs = (unsigned __int128)key * (uint64_t)d;
+    return lhs >= rhs;
+}
+
+double oracle_shii(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C, const int32_t *S,
+                   int64_t nS, int32_t model, double p, int32_t runs, uint64_t seed, int64_t *out,
+                   double *shii_out) {
+    unsigned char *act = malloc(n ? n : 1);
+    int32_t *queue = malloc(sizeof(int32_t) * (n ? n : 1));
+    const int all_live = p >= 1.0;
+    const uint64_t thr = all_live ? 0 : (uint64_t)ldexp(p, 64);
+    double setmean = 0.0;
+    for (int64_t s = 0; s < nS; s++) {
+        const int32_t u0 = S[s];
+        double acc = 0.0;
+        for (int32_t r = 0; r < runs; r++) {
+            const uint64_t sr = oracle_mix64(seed + (uint64_t)(2 * (int64_t)r + model + 1) * 0xD1B54A32D192ED03ull);
+            memset(act, 0, n);
+            act[u0] = 1;
+            if (model == 0) {
+                int64_t qh = 0, qt = 0;
+                queue[qt++] = u0;
+                while (qh < qt) {
+                    const int64_t a = queue[qh++];
+                    for (int64_t e = rowptr[a]; e < rowptr[a + 1]; e++) {
+                        const int64_t b = col[e];
+                        if (act[b]) continue;
+                        const uint64_t key = oracle_mix64(sr ^ (((uint64_t)a << 32) | (uint64_t)b));
+                        if (all_live || key < thr) { act[b] = 1; queue[qt++] = (int32_t)b; }
+                    }
+                }
+            } else {
+                int changed = 1;
+                while (changed) {
+                    changed = 0;
+                    for (int64_t v = 0; v < n; v++) {
+                        if (act[v]) continue;
+                        int64_t a = 0;
+                        for (int64_t e = rowptr[v]; e < rowptr[v + 1]; e++) a += act[col[e]];
+                        if (lt_ready(oracle_mix64(sr ^ (uint64_t)v), rowptr[v + 1] - rowptr[v], a)) {
+                            act[v] = 1;
+                            changed = 1;
+                        }
+                    }
+                }
+            }
+            int64_t inf = 0, outc = 0;
+            for (int64_t v = 0; v < n; v++)
+                if (act[v]) { inf++; if (C[v] != C[u0]) outc++; }
+            out[(s * runs + r) * 2] = inf;
+            out[(s * runs + r) * 2 + 1] = outc;
+            acc += (double)outc / (double)inf;
+        }
+        shii_out[s] = acc / (double)runs;
+        setmean += shii_out[s];
+    }
+    free(act); free(queue);
+    return setmean / (double)nS;
+}
