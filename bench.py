@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--no-awcc", action="store_true", help="skip the NEXT-1 robustness-evaluation timing")
+    p.add_argument("--no-awcc", action="store_true", help="skip the NEXT-1/3/4 evaluation timings")
     p.add_argument("--config", default="orkut", choices=["orkut", "lj", "dblp", "karate", "friendster"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--K", type=int, default=25)
@@ -277,6 +277,20 @@ def main():
             awcc[f"{mode}_Gitems_per_s"] = round(items / dt / 1e9, 2)
             awcc[f"{mode}_awcc_0_75"] = [round(float(mean[0]), 6), round(float(mean[-1]), 6)]
 
+    # NEXT-4: SHII of the top-K under IC (p = 0.1, SPEC default) and LT, 2 runs each;
+    # host-synchronous (a BFS level per launch), so wall time is its latency
+    shii = None
+    if not a.no_awcc:
+        top = ids_d.cpu().numpy()
+        shii = {"S": int(top.size), "runs": 2}
+        for model in ("ic", "lt"):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            _, _, mean = sc.shii(top, model, 0.1, 2, 3)
+            dt = time.perf_counter() - t0
+            shii[f"{model}_ms_per_diffusion"] = round(dt * 1e3 / (top.size * 2), 3)
+            shii[f"{model}_mean_shii"] = round(float(mean), 6)
+
     # NEXT-3: the step with every literal variant on (RS_LITERAL_L | RS_GATE_L | RS_WMAX_EB)
     variants = None
     if not a.no_awcc:
@@ -320,6 +334,7 @@ def main():
             "topk_latency_ms": round(float(np.median(tk_ms)), 4),
             "next_awcc_removal": awcc,
             "next_literal_variants": variants,
+            "next_shii": shii,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk_s, "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
         }

@@ -221,6 +221,26 @@ rs_status rs_awcc_removal(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t mod
                           int32_t max_pct, int32_t trials, uint64_t seed, int32_t *zeta_out, double *mean_out,
                           int64_t *steps_out);
 
+/* ---- NEXT-4: structural hole influence index (PAPER §VII.A). ----
+ * SHII(u) = (influenced vertices outside C(u)) / (influenced vertices) of a
+ * diffusion seeded at u, averaged over `runs` Monte-Carlo runs (the seed is
+ * always influenced). Run r of model m draws from s_r = mix64(seed + (2r + m + 1)
+ * * 0xD1B54A32D192ED03) on the caller's (original) ids (DESIGN reading C-31):
+ * RS_DIFFUSE_IC, independent cascade with probability p: a newly active a
+ * activates an inactive neighbour b iff mix64(s_r ^ (a << 32 | b)) < floor(p 2^64)
+ * (always when p >= 1); RS_DIFFUSE_LT, linear threshold: theta_v = mix64(s_r ^ v)
+ * / 2^64, an inactive v activates once (active neighbours) / d(v) >= theta_v with
+ * at least one active neighbour (exact integer test). influenced_out
+ * int64[|S|][runs][2] (host or NULL) receives {influenced, outside C(seed)};
+ * shii_out double[|S|] (host or NULL) the per-seed means (summed in run order);
+ * *mean_out the mean over S (in order). S may be host or device memory.
+ * Requires rs_load_csr and rs_set_communities (C is community_of). RS_EINVAL on
+ * an empty S, an out-of-range id, a bad model, p outside [0, 1] or runs < 1. */
+#define RS_DIFFUSE_IC 0
+#define RS_DIFFUSE_LT 1
+rs_status rs_shii(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t model, double p, int32_t runs, uint64_t seed,
+                  int64_t *influenced_out, double *shii_out, double *mean_out);
+
 /* ---- Multi-GPU host protocol. Pure host functions on host
  * arrays, no context, no device work; rs_create_dist / rs_topk call them, and
  * they are exported so that the protocol can be exercised without GPUs. ---- */

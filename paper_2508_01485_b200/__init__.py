@@ -72,6 +72,8 @@ SIGNATURES = [
     ("rs_kernel_launches", ctypes.c_int64, [_P]),
     ("rs_awcc_removal", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int32, ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
+    ("rs_shii", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
+                               ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_double)]),
     ("rs_split_ranges", ctypes.c_int, [ctypes.c_int64, _P, ctypes.c_int32, _P]),
     ("rs_merge_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P,
                                            ctypes.POINTER(ctypes.c_int64)]),
@@ -251,6 +253,18 @@ def rs_awcc_removal(ctx, S, mode: str = "edge", step_pct: int = 5, max_pct: int 
     return zeta[:, :steps.value], mean[:steps.value]
 
 
+def rs_shii(ctx, S, model: str = "ic", p: float = 0.1, runs: int = 10, seed: int = 0):
+    """NEXT-4: (influenced int64[|S|, runs, 2], per-seed SHII float64[|S|], mean)"""
+    Sa = _as(S, np.int32)
+    nS = int(Sa.shape[0])
+    out = np.zeros((nS, max(runs, 1), 2), dtype=np.int64)
+    per = np.zeros(max(nS, 1), dtype=np.float64)
+    mean = ctypes.c_double(0.0)
+    _check(ctx, load_library().rs_shii(ctx, _ptr(Sa), nS, 0 if model == "ic" else 1, float(p), int(runs),
+                                       int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(out), _ptr(per), ctypes.byref(mean)))
+    return out, per[:nS], mean.value
+
+
 # ------------------------------------------------------------------ multi-GPU host protocol
 def rs_split_ranges(work_incl, world: int) -> np.ndarray:
     """bounds int64[world+1] of the balanced contiguous split (include/rs.h)."""
@@ -345,6 +359,9 @@ class Scorer:
 
     def targets(self):
         return rs_get_targets(self.ctx)
+
+    def shii(self, S, model="ic", p=0.1, runs=10, seed=0):
+        return rs_shii(self.ctx, S, model, p, runs, seed)
 
     def awcc_removal(self, S, mode="edge", step_pct=5, max_pct=75, trials=1, seed=0):
         return rs_awcc_removal(self.ctx, S, mode, step_pct, max_pct, trials, seed)

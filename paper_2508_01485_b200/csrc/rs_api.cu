@@ -632,6 +632,52 @@ extern "C" rs_status rs_awcc_removal(rs_ctx *ctx, const int32_t *S, int64_t nS, 
     return st_ret;
 }
 
+// ------------------------------------------------------------------ NEXT-4: SHII
+extern "C" rs_status rs_shii(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t model, double p, int32_t runs,
+                             uint64_t seed, int64_t *influenced_out, double *shii_out, double *mean_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.has_comm) return fail(ctx, RS_ESTATE, "rs_shii: call rs_load_csr and rs_set_communities first");
+    if (!S || nS < 1) return fail(ctx, RS_EINVAL, "rs_shii: S must be a non-empty vertex set");
+    if (model != RS_DIFFUSE_IC && model != RS_DIFFUSE_LT) return fail(ctx, RS_EINVAL, "rs_shii: bad model");
+    if (runs < 1 || !(p >= 0.0) || p > 1.0) return fail(ctx, RS_EINVAL, "rs_shii: need runs >= 1 and 0 <= p <= 1");
+    std::vector<int32_t> hS(nS);
+    CK(cudaMemcpy(hS.data(), S, sizeof(int32_t) * nS, is_device_ptr(S) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    for (int64_t i = 0; i < nS; i++)
+        if (hS[i] < 0 || hS[i] >= c.n) return fail(ctx, RS_EINVAL, "rs_shii: vertex id out of range");
+    char *buf = nullptr;
+    const size_t nb = sizeof(unsigned int) * c.n + 2 * sizeof(int32_t) * c.n + 64;
+    CK(cudaMalloc(&buf, nb));
+    unsigned long long *ctr = (unsigned long long *)buf;
+    unsigned int *act = (unsigned int *)(buf + 64);
+    int32_t *cnt = (int32_t *)(act + c.n);
+    int32_t *list = cnt + c.n;
+    cudaError_t e = cudaMemsetAsync(act, 0, sizeof(unsigned int) * c.n, c.stream);
+    double setmean = 0.0;
+    for (int64_t s = 0; s < nS && e == cudaSuccess; s++) {
+        double acc = 0.0;
+        for (int32_t r = 0; r < runs && e == cudaSuccess; r++) {
+            // run salt (shared by every seed of run r, as in the oracle)
+            const uint64_t st = host_mix64(seed + (uint64_t)(2 * (int64_t)r + model + 1) * 0xD1B54A32D192ED03ull);
+            int64_t o2[2] = {0, 0};
+            e = rs::launch_shii_run(c, hS[s], model, p, st, act, cnt, list, ctr, o2);
+            if (influenced_out) {
+                influenced_out[(s * runs + r) * 2] = o2[0];
+                influenced_out[(s * runs + r) * 2 + 1] = o2[1];
+            }
+            acc += (double)o2[1] / (double)o2[0];
+        }
+        const double sh = acc / (double)runs;
+        if (shii_out) shii_out[s] = sh;
+        setmean += sh;
+    }
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(ctx, RS_ECUDA, std::string("rs_shii: ") + cudaGetErrorString(e));
+    if (mean_out) *mean_out = setmean / (double)nS;
+    return RS_OK;
+}
+
 // ------------------------------------------------------------------ multi-GPU host protocol
 extern "C" rs_status rs_split_ranges(int64_t n, const int64_t *work_incl, int32_t world, int64_t *bounds_out) {
     if (n < 0 || world < 1 || !bounds_out || (n > 0 && !work_incl)) return RS_EINVAL;

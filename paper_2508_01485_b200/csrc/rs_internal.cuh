@@ -205,6 +205,8 @@ cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
 cudaError_t launch_finalize(Ctx &c);
 size_t awcc_scratch_bytes(int64_t M, int J1, int64_t cap, int64_t nS);
+cudaError_t launch_shii_run(Ctx &c, int32_t seed_o, int model, double p, uint64_t st, unsigned int *act,
+                            int32_t *cnt, int32_t *list, unsigned long long *ctr, int64_t out2[2]);
 cudaError_t launch_awcc_degrees(Ctx &c, const int32_t *S_dev, int64_t nS, int64_t *deg_dev);
 cudaError_t launch_awcc_trial(Ctx &c, const int32_t *S_dev, int64_t nS, int mode, int step_pct, int J1, uint64_t st,
                               int32_t *zeta_dev, void *scratch, size_t scratch_bytes, int64_t cap);

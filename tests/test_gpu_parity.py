@@ -296,3 +296,36 @@ def test_literal_variants_parity(vflags, name, scale, k):
     r_or = oracle.run_variant(g, k, vflags, K=g.n)
     r_gpu = run_gpu(g, k=k, targets=r_or.targets, K=g.n, flags=vflags << 16)
     compare_full(g, r_or, r_gpu)
+
+
+# ---------------------------------------------------------------- NEXT-4: SHII
+@pytest.mark.parametrize("model,p", [("ic", 0.05), ("ic", 0.2), ("ic", 1.0), ("lt", 0.0)])
+@pytest.mark.parametrize("name,scale", [("karate", None), ("dblp", 0.02), ("orkut", 0.003)])
+def test_shii_parity(model, p, name, scale):
+    """influenced counts per (seed, run) exact and the SHII means bit-identical to
+    the oracle (DESIGN C-31), S = the GPU's top-10 plus random seeds"""
+    g = gen.load_fixture(name)[0] if scale is None else gen.config_graph(name, scale)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, 2 if name == "karate" else 5)
+    s.score()
+    top, _ = s.topk(min(10, g.n))
+    rng = np.random.default_rng(23)
+    S = np.concatenate([top, rng.choice(g.n, size=min(5, g.n), replace=False)]).astype(np.int32)
+    og, pg, mg = s.shii(S, model, p, 3, 0x5111)
+    s.close()
+    oo, po, mo = oracle.shii(g, S, model, p, 3, 0x5111)
+    assert np.array_equal(og, oo)
+    assert np.array_equal(pg.view(np.uint64), po.view(np.uint64))
+    assert mg == mo
+
+
+def test_shii_errors():
+    g, _ = gen.load_fixture("karate")
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, 2)
+    for bad in [dict(S=[]), dict(S=[40]), dict(S=[0], p=1.5), dict(S=[0], runs=0)]:
+        with pytest.raises((rsb.RsError, ValueError)):
+            s.shii(**bad)
+    s.close()
