@@ -142,7 +142,6 @@ struct ESmem {             // one warp's shared memory
     int32_t pe[kChunkE];    // end of each list's pieces
     int2 q[kQCapE];         // candidates {((offset of z in P+(x)) + 4) << 6 | x slot, z}
     uint32_t ps[kPsWords];  // bit p: piece p is the first piece of a list
-    uint8_t zl[kPyCap];     // label of z in the target run of P+(y)
 };
 
 __host__ __device__ constexpr size_t e_stride_bytes(int k) {
@@ -207,7 +206,6 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             lxv[h] = xv[h] >= 0 ? (int)__ldg(a.lab + xv[h]) : kOther;
             axy[h] = (xv[h] >= 0 && ty) ? __ldg(a.amat + (int64_t)xv[h] * k + ly) : 0.0;
         }
-        const int lz0 = (z0 >= 0 && local && lane < pyt) ? (int)__ldg(a.lab + z0) : kOther;
         for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
         if (lane < k) Ay[lane] = ay0;
         for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
@@ -218,7 +216,6 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             atomicOr(&S.bm[b >> 5], 1u << (b & 31));
             if (local) {
                 S.py[i] = z;
-                if (i < pyt) S.zl[i] = (uint8_t)(i == lane ? lz0 : __ldg(a.lab + z));
             }
         }
         // the next item's record, in flight during this item
@@ -340,9 +337,8 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                         ntri++;
                         const int32_t x = (int32_t)((xe.y >> 32) & 0x7FFFFFFF);
                         const int lx = (int)((xe.y >> 24) & 0xFF);
-                        const int lz = zt ? (local ? (int)S.zl[iz] : (int)__ldg(a.lab + z)) : (int)kOther;
                         if constexpr (COUNT) {
-                            const bool tx = lx < k, tz = lz < k;
+                            const bool tx = lx < k, tz = zt;          // z's run of P+(x) is its target status
                             if (tx && (ty + tz) && owned(a, x)) atomicAdd(a.n1 + x, (unsigned long long)(ty + tz));
                             if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
                             cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
@@ -350,7 +346,9 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                             const double Axlz = __ldg(a.wps + xe.x + off);  // a_x(c_z), stored by Phase A
                             const double Axly = S.axy[slot];
                             const double Aylx = lx < k ? Ay[lx] : 0.0;
-                            const double Aylz = lz < k ? Ay[lz] : 0.0;
+                            // a_y(c_z), beside z in y's slot (the other run holds 0)
+                            const int64_t ypos = by + (zt ? iz : (local ? py - 1 - iz : pyt + iz));
+                            const double Aylz = __ldg(a.wps + ypos);
                             const double Azlx = amat_at(a, z, lx);
                             const double Azly = amat_at(a, z, ly);
                             const double tx = Aylx * Azlx * (Azly + Aylz);
@@ -558,9 +556,8 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 if (iz < 0) continue;
                 ntri++;
                 const bool txp = lxp < k, typ = lyp < k;
-                const int lz = zt ? (int)__ldg(a.lab + z) : (int)kOther;
                 if constexpr (COUNT) {
-                    const bool tz = lz < k;
+                    const bool tz = zt;                                     // the run is z's target status
                     if (txp && (typ + tz) && owned(a, xp)) atomicAdd(a.n1 + xp, (unsigned long long)(typ + tz));
                     if (tz && (txp + typ) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(txp + typ));
                     if (typ && (txp + tz) && owned(a, y)) atomicAdd(a.n1 + y, (unsigned long long)(txp + tz));

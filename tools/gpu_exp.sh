@@ -1,6 +1,6 @@
 # bench each experiment library: per-phase ms
 for L in librs.so "$@"; do
-  RS_LIBRARY=paper_2508_01485_b200/$L timeout 200 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/x.log 2>&1
+  RS_LIBRARY=paper_2508_01485_b200/$L timeout 200 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --no-awcc > gpurun_out/x.log 2>&1
   python - "$L" <<'P'
 import json, sys; l=[x for x in open("gpurun_out/x.log") if x.startswith("{")]
 d=json.loads(l[-1]) if l else None
