@@ -68,6 +68,9 @@ typedef struct {
 /* Flags for rs_load_csr. */
 #define RS_VALIDATE   1u   /* check the CSR contract on the device (see rs_load_csr) */
 
+/* rs_set_communities: every community is a target (sparse per-vertex tables). */
+#define RS_ALL_COMMUNITIES (-1)
+
 /* Flags for rs_score. */
 #define RS_GATHER_SCORES 1u /* multi-GPU: make scores_out complete on every rank */
 /* Test hook: run Phase E (Type-I) as s sequential shares of the multi-GPU
@@ -130,7 +133,16 @@ rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offsets, const 
  *   targets       int32[k] distinct community ids present in community_of,
  *                 in column order, or NULL = the k largest communities,
  *                 ties by ascending community id (C-15).
- *   k             2 <= k <= min(254, number of distinct communities).
+ *   k             2 <= k <= min(254, number of distinct communities), or
+ *                 RS_ALL_COMMUNITIES (targets must be NULL): every community
+ *                 is a target, k = the number of distinct communities (>= 2,
+ *                 any count; NEXT-2 all-communities mode). Columns are then
+ *                 ordered like the top-k selection (size descending, ties by
+ *                 ascending id) and rs_score keeps per-vertex sparse community
+ *                 tables instead of dense n*k ones (P:428 names the dense
+ *                 table's limit); scores are the same quantity as with
+ *                 explicit targets = all communities. The NEXT-3 variant flags
+ *                 of rs_score are not available in this mode (RS_EINVAL).
  * Target selection, the per-vertex column labels and the community-size
  * histogram run on the device. Errors: RS_EINVAL, RS_ESTATE, RS_ENOMEM, RS_ECUDA. */
 rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of, const int32_t *targets,
@@ -167,12 +179,15 @@ rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *scores_out, 
 
 /* Step 2a histogram: f_out int32[n*k] row-major, f[u*k+i] =
  * |{x in N(u): C(x) = targets[i]}|; total_out int32[n] = sum_i f[u*k+i]
- * (P:431 T). Either pointer may be NULL. Requires rs_score. */
+ * (P:431 T). Either pointer may be NULL. Requires rs_score. In the
+ * all-communities mode this is a dense view (n*k entries, k = number of
+ * communities) of the sparse tables. */
 rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_out);
 
 /* Step 2b weights before normalisation (Eq. 3, Eq. 5, Algorithm 2 |L| rule):
  * omega_out double[n*k] row-major (column i = omega_u(C_i), Lemma 1) or NULL;
- * omega_max_out double* or NULL. Requires rs_score. */
+ * omega_max_out double* or NULL. Requires rs_score. All-communities mode: a
+ * dense view (absent columns carry the row's f = 0 weight). */
 rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omega_max_out);
 
 /* Step 1 border vertices (over all communities): bv_out int32[|V_b|]
@@ -192,7 +207,8 @@ rs_status rs_get_pred(rs_ctx *ctx, int64_t *pred_off_out, int32_t *pred_out, int
  * Requires rs_score. */
 rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_t *type2_out);
 
-/* Target communities in column order (int32[k]) and k. Requires communities. */
+/* Target communities in column order (int32[k]) and k. Requires communities.
+ * In the all-communities mode k can be large: query k with targets_out = NULL. */
 rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out);
 
 /* Number of librs kernels launched on ctx since creation (bench accounting). */

@@ -24,6 +24,7 @@ RS_VALIDATE = 1
 RS_GATHER_SCORES = 1
 RS_REMOVE_EDGES, RS_REMOVE_NODES = 0, 1
 RS_LITERAL_L, RS_GATE_L, RS_WMAX_EB = 1 << 16, 1 << 17, 1 << 18   # NEXT-3 variants (rs_score flags)
+RS_ALL_COMMUNITIES = -1   # rs_set_communities k: every community a target (NEXT-2 sparse mode)
 
 
 def RS_E_SHARES(s: int) -> int:
@@ -226,8 +227,9 @@ def rs_get_triad_counts(ctx, n):
 
 
 def rs_get_targets(ctx):
-    buf = np.empty(254, dtype=np.int32)
     k = ctypes.c_int32(0)
+    _check(ctx, load_library().rs_get_targets(ctx, None, ctypes.byref(k)))
+    buf = np.empty(max(k.value, 1), dtype=np.int32)
     _check(ctx, load_library().rs_get_targets(ctx, _ptr(buf), ctypes.byref(k)))
     return buf[:k.value].copy()
 
@@ -328,8 +330,9 @@ class Scorer:
         self.nnz = int(col.shape[0])
 
     def set_communities(self, comm, k: int, targets=None):
+        """k = RS_ALL_COMMUNITIES: every community a target (self.k becomes their number)."""
         rs_set_communities(self.ctx, comm, k, targets)
-        self.k = int(k)
+        self.k = int(k) if k != RS_ALL_COMMUNITIES else len(rs_get_targets(self.ctx))
 
     def score(self, scores_out=None, stats: bool = False, gather: bool = False, flags: int = 0):
         return rs_score(self.ctx, scores_out, stats, (RS_GATHER_SCORES if gather else 0) | flags)

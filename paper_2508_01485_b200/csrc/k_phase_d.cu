@@ -21,7 +21,9 @@ namespace rs {
 // Phase A's B table), then the finalize pass adds the Type-I limbs and
 // normalises.
 // ============================================================================
-template <int U, class GR>
+// SPARSE (all-communities mode, k_sparse.cu): a_w(c_u) and the position of
+// B_w[c_u] in w's community table are stored beside w in P(u)
+template <int U, bool SPARSE, class GR>
 __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &g) {
     const VRec ru = a.vrec[u];
     if (!ru.head || u < a.head_lo || u >= a.head_hi) return;   // finalize writes R = 0
@@ -29,19 +31,36 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const double au = ru.a_self;
     const int pc = ru.pcnt;
     const int64_t beg = a.rowptr[u];
-    const BQL *bcol = a.bql + (int64_t)cu * a.n;
+    const BQL *bcol = SPARSE ? nullptr : a.bql + (int64_t)cu * a.n;
     U128 S = u128_zero();
     for (int base = 0; base < pc; base += GR::size * U) {
         int32_t w[U];
         BQL r[U];
+        int64_t pv[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
-            w[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
+            if constexpr (SPARSE) {
+                w[j] = i < pc ? 0 : -1;
+                pv[j] = i < pc ? __ldg(a.prv + beg + i) : 0;
+                r[j].Q = i < pc ? __ldg(a.pwr + beg + i) : 0.0;
+            } else {
+                w[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
+            }
         }
 #pragma unroll
-        for (int j = 0; j < U; j++)
-            if (w[j] >= 0) r[j] = bcol[w[j]];
+        for (int j = 0; j < U; j++) {
+            if constexpr (SPARSE) {
+                if (w[j] >= 0) {
+                    const ulonglong2 b = a.ctb[pv[j]];
+                    r[j].b0 = b.x;
+                    r[j].b1 = b.y;
+                    r[j].Q *= r[j].Q;
+                }
+            } else {
+                if (w[j] >= 0) r[j] = bcol[w[j]];
+            }
+        }
 #pragma unroll
         for (int j = 0; j < U; j++) {
             if (w[j] >= 0) {
@@ -83,19 +102,20 @@ __global__ void __launch_bounds__(256) k_finalize(CdeArgs a) {
     }
 }
 
-template <int G, int U>
+template <int G, int U, bool SPARSE>
 __global__ void __launch_bounds__(256) k_phase_d_warp(CdeArgs a) {
     WarpGroup<G> g;
     const int64_t gpb = blockDim.x / G;
     for (int64_t i = blockIdx.x * gpb + threadIdx.x / G; i < a.nverts; i += (int64_t)gridDim.x * gpb)
-        phase_d_vertex<U>(a, a.vlo + i, g);
+        phase_d_vertex<U, SPARSE>(a, a.vlo + i, g);
 }
 
+template <bool SPARSE>
 __global__ void __launch_bounds__(kCtaThreads) k_phase_d_cta(CdeArgs a) {
     __shared__ int s_i[kCtaWarps + 1];
     __shared__ unsigned long long s_u[2 * kCtaWarps];
     CtaGroup g(s_i, s_u);
-    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) phase_d_vertex<4>(a, a.vlo + i, g);
+    for (int64_t i = blockIdx.x; i < a.nverts; i += gridDim.x) phase_d_vertex<4, SPARSE>(a, a.vlo + i, g);
 }
 
 // ============================================================================
@@ -112,7 +132,8 @@ static void launch_grid(Ctx &c, K kern, int64_t groups, int gpb, cudaStream_t s,
 
 // Type-II pull bins (lanes x loads per lane; |P| is about a quarter of d):
 // [0,32):4x2 [32,64):4x4 [64,128):8x4 [128,2048):32x4 [2048,inf):CTAx4
-cudaError_t launch_phase_d(Ctx &c) {
+template <bool SPARSE>
+static cudaError_t launch_phase_d_t(Ctx &c) {
     CdeArgs base = cde_args(c);
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         CdeArgs a = base;
@@ -121,15 +142,16 @@ cudaError_t launch_phase_d(Ctx &c) {
         if (!a.nverts) continue;
         cudaStream_t s = c.side[cls];
         if (cls >= 6) {
-            k_phase_d_cta<<<(unsigned)std::min<int64_t>(a.nverts, 148 * 8), kCtaThreads, 0, s>>>(a);
+            k_phase_d_cta<SPARSE><<<(unsigned)std::min<int64_t>(a.nverts, 148 * 8), kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (cls == 5) launch_grid(c, k_phase_d_warp<32, 4>, a.nverts, 8, s, a);
-        else if (cls == 4) launch_grid(c, k_phase_d_warp<8, 4>, a.nverts, 32, s, a);
-        else if (cls == 3) launch_grid(c, k_phase_d_warp<4, 4>, a.nverts, 64, s, a);
-        else launch_grid(c, k_phase_d_warp<4, 2>, a.nverts, 64, s, a);
+        } else if (cls == 5) launch_grid(c, k_phase_d_warp<32, 4, SPARSE>, a.nverts, 8, s, a);
+        else if (cls == 4) launch_grid(c, k_phase_d_warp<8, 4, SPARSE>, a.nverts, 32, s, a);
+        else if (cls == 3) launch_grid(c, k_phase_d_warp<4, 4, SPARSE>, a.nverts, 64, s, a);
+        else launch_grid(c, k_phase_d_warp<4, 2, SPARSE>, a.nverts, 64, s, a);
     }
     return cudaGetLastError();
 }
+cudaError_t launch_phase_d(Ctx &c) { return c.sparse ? launch_phase_d_t<true>(c) : launch_phase_d_t<false>(c); }
 
 cudaError_t launch_finalize(Ctx &c) {
     CdeArgs a = cde_args(c);

@@ -148,12 +148,16 @@ __host__ __device__ constexpr size_t e_stride_bytes(int k) {
     return ((sizeof(ESmem) + 15) / 16) * 16 + ((8 * (size_t)k + 15) / 16) * 16;
 }
 
-template <bool COUNT>
+// SPARSE (all-communities mode, k_sparse.cu): every vertex is a target, P+(u)
+// is one ascending run in pidx, and the weights come from beside the list
+// entries (wps: a_u(c_w), pwr: a_w(c_u)) instead of the dense rows; Ay then
+// holds a_y(c_x) per x slot of the item.
+template <bool COUNT, bool SPARSE>
 __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems it, unsigned long long *queue_ctr) {
     extern __shared__ __align__(16) unsigned char e_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k;
-    unsigned char *base = e_smem + (size_t)wid * e_stride_bytes(k);
+    unsigned char *base = e_smem + (size_t)wid * e_stride_bytes(SPARSE ? kChunkE : k);
     ESmem &S = *reinterpret_cast<ESmem *>(base);
     double *Ay = (double *)(base + ((sizeof(ESmem) + 15) / 16) * 16);
     unsigned long long ntri = 0, nprobe = 0;
@@ -196,19 +200,28 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         // stored descending after the target run)
         auto py_at = [&](int i) -> int64_t { return i < pyt ? by + i : by + py - 1 - (i - pyt); };
         const int32_t z0 = lane < py ? __ldg(a.pplus + py_at(lane)) : -1;
-        const double ay0 = lane < k ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
+        const double ay0 = (!SPARSE && lane < k) ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
         PRec pcx[2];
         int lxv[2];
-        double axy[2];
+        double axy[2], ayx[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             pcx[h] = xv[h] >= 0 ? a.pc2[xv[h]] : PRec{0, 0, 0};
             lxv[h] = xv[h] >= 0 ? (int)__ldg(a.lab + xv[h]) : kOther;
-            axy[h] = (xv[h] >= 0 && ty) ? __ldg(a.amat + (int64_t)xv[h] * k + ly) : 0.0;
+            if constexpr (SPARSE) {
+                const int64_t q = by + py + start + 32 * h + lane;   // x's position in P(y)
+                axy[h] = xv[h] >= 0 ? __ldg(a.pwr + q) : 0.0;       // a_x(c_y)
+                ayx[h] = xv[h] >= 0 ? __ldg(a.wps + q) : 0.0;       // a_y(c_x)
+            } else {
+                axy[h] = (xv[h] >= 0 && ty) ? __ldg(a.amat + (int64_t)xv[h] * k + ly) : 0.0;
+                ayx[h] = 0.0;
+            }
         }
         for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
-        if (lane < k) Ay[lane] = ay0;
-        for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
+        if constexpr (!SPARSE) {
+            if (lane < k) Ay[lane] = ay0;
+            for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
+        }
         __syncwarp();
         for (int i = lane; i < py; i += 32) {
             const int32_t z = i == lane ? z0 : __ldg(a.pplus + py_at(i));
@@ -249,6 +262,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                 S.xl[slot] = make_longlong2(bx, ((long long)xv[h] << 32) | ((long long)(lx & 0xFF) << 24) | t);
                 S.xn[slot] = make_int2(lenx, 0);
                 S.axy[slot] = axy[h];
+                if constexpr (SPARSE) Ay[slot] = ayx[h];
                 S.xa[4 * slot] = 0u;
                 S.xa[4 * slot + 1] = 0u;
                 S.xa[4 * slot + 2] = 0u;
@@ -345,12 +359,12 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                         } else {
                             const double Axlz = __ldg(a.wps + xe.x + off);  // a_x(c_z), stored by Phase A
                             const double Axly = S.axy[slot];
-                            const double Aylx = lx < k ? Ay[lx] : 0.0;
+                            const double Aylx = SPARSE ? Ay[slot] : (lx < k ? Ay[lx] : 0.0);
                             // a_y(c_z), beside z in y's slot (the other run holds 0)
                             const int64_t ypos = by + (zt ? iz : (local ? py - 1 - iz : pyt + iz));
                             const double Aylz = __ldg(a.wps + ypos);
-                            const double Azlx = amat_at(a, z, lx);
-                            const double Azly = amat_at(a, z, ly);
+                            const double Azlx = SPARSE ? __ldg(a.pwr + xe.x + off) : amat_at(a, z, lx);
+                            const double Azly = SPARSE ? __ldg(a.pwr + ypos) : amat_at(a, z, ly);
                             const double tx = Aylx * Azlx * (Azly + Aylz);
                             const double tz = Axlz * Aylz * (Aylx + Axly);
                             accy = u128_add(accy, fx_quantize(Axly * Azly * (Azlx + Axlz)));
@@ -454,7 +468,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 // per round and looks it up by binary search in the matching run of P+(y)
 // (short, L1-resident), so the work per lane is uniform whatever the list
 // lengths. Terms go to the heads with one RED each.
-template <bool COUNT>
+template <bool COUNT, bool SPARSE>
 __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
     const int k = a.k;
     const int lane = threadIdx.x & 31;
@@ -500,19 +514,21 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
             const int ppj = __shfl_sync(0xffffffffu, pcl.x, j);            // |P+(y)|
             const int ly = __shfl_sync(0xffffffffu, lyl, j);
             int32_t x = -1;
-            if (q < total) x = __ldg(a.pidx + by + ppj + (q - (inc_j - cnt_j)));   // P-(y): the suffix, x > y
+            const int64_t qpos = by + ppj + (q - (inc_j - cnt_j));       // P-(y): the suffix, x > y
+            if (q < total) x = __ldg(a.pidx + qpos);
             PRec pcx{0, 0, 0};
             int lx = kOther;
             double Axly = 0.0;
             if (x >= 0) {
                 pcx = a.pc2[x];
                 lx = __ldg(a.lab + x);
-                Axly = amat_at(a, x, ly);
+                Axly = SPARSE ? __ldg(a.pwr + qpos) : amat_at(a, x, ly);
             }
             const bool tx = lx < k, ty = ly < k;
             const int t = (tx || ty) ? pr_plus_t(pcx) : 0;               // probed: the target run,
             const int np = t + ((tx && ty) ? pcx.x - pr_plus_t(pcx) : 0); // and the other if both
-            const double Aylx = (x >= 0 && tx) ? __ldg(a.amat + (y0 + j) * k + lx) : 0.0;
+            double Aylx = 0.0;
+            if (x >= 0 && tx) Aylx = SPARSE ? __ldg(a.wps + qpos) : __ldg(a.amat + (y0 + j) * k + lx);
             int incl2 = np;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -563,7 +579,8 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                     if (typ && (txp + tz) && owned(a, y)) atomicAdd(a.n1 + y, (unsigned long long)(txp + tz));
                 } else {
                     const double Axlz = __ldg(a.wps + pos), Aylz = __ldg(a.wps + ypos);
-                    const double Azlx = amat_at(a, z, lxp), Azly = amat_at(a, z, lyp);
+                    const double Azlx = SPARSE ? __ldg(a.pwr + pos) : amat_at(a, z, lxp);
+                    const double Azly = SPARSE ? __ldg(a.pwr + ypos) : amat_at(a, z, lyp);
                     const double ttx = Aylxp * Azlx * (Azly + Aylz);
                     const double tty = Axlyp * Azly * (Azlx + Axlz);
                     const double ttz = Axlz * Aylz * (Aylxp + Axlyp);
@@ -653,7 +670,7 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     return cudaGetLastError();
 }
 
-template <bool COUNT>
+template <bool COUNT, bool SPARSE>
 static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     CdeArgs a = cde_args(c);
     if (c.world > 1) {
@@ -673,14 +690,14 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
         cudaError_t e = build_e_items(c, it);
         if (e != cudaSuccess) return e;
     }
-    const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.k);
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[COUNT]) {
-        cudaFuncSetAttribute(k_phase_e<COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set[COUNT] = true;
+    const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.sparse ? kChunkE : c.k);
+    static bool attr_set[2][2] = {{false, false}, {false, false}};
+    if (!attr_set[COUNT][SPARSE]) {
+        cudaFuncSetAttribute(k_phase_e<COUNT, SPARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set[COUNT][SPARSE] = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase_e<COUNT>, kWarpsE * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase_e<COUNT, SPARSE>, kWarpsE * 32, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     for (int s = 0; s < shares; s++) {
@@ -692,20 +709,26 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
         if (n_heavy < c.n) {                              // light first (see rs_score)
             const int64_t threads = c.n - n_heavy;        // a warp per 32 vertices
             const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
-            k_phase_e_light<COUNT><<<(unsigned)blocks, 256, 0, light>>>(a, n_heavy);
+            k_phase_e_light<COUNT, SPARSE><<<(unsigned)blocks, 256, 0, light>>>(a, n_heavy);
             c.launches++;
         }
         if (n_heavy > 0) {
-            k_phase_e<COUNT><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
+            k_phase_e<COUNT, SPARSE><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
             c.launches++;
         }
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_phase_e(Ctx &c) { return launch_e<false>(c, c.stream); }
+cudaError_t launch_phase_e(Ctx &c) {
+    return c.sparse ? launch_e<false, true>(c, c.stream) : launch_e<false, false>(c, c.stream);
+}
 // light kernel on `light` (forked from c.stream by the caller)
-cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light) { return launch_e<false>(c, light); }
-cudaError_t launch_triangle_counts(Ctx &c) { return launch_e<true>(c, c.stream); }
+cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light) {
+    return c.sparse ? launch_e<false, true>(c, light) : launch_e<false, false>(c, light);
+}
+cudaError_t launch_triangle_counts(Ctx &c) {
+    return c.sparse ? launch_e<true, true>(c, c.stream) : launch_e<true, false>(c, c.stream);
+}
 
 }  // namespace rs

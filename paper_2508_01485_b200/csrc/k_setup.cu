@@ -100,7 +100,8 @@ __global__ void k_class_bounds(const uint32_t *__restrict__ deg_s, int64_t n, un
 // shared memory, keys < 2^bits; padding keys 2^bits - 1 sort last)
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) k_row_sort(const int64_t *__restrict__ rowptr, int64_t r0, int64_t r1,
-                                                      const int32_t *__restrict__ in, int32_t *out, int bits) {
+                                                      const int32_t *__restrict__ in, int32_t *out, int bits,
+                                                      const int32_t *__restrict__ map) {
     using BRS = cub::BlockRadixSort<uint32_t, THREADS, ITEMS>;
     __shared__ typename BRS::TempStorage ts;
     const uint32_t pad = bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u;
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(THREADS) k_row_sort(const int64_t *__restrict_
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
             const int idx = threadIdx.x * ITEMS + i;
-            keys[i] = idx < d ? (uint32_t)in[b + idx] : pad;
+            keys[i] = idx < d ? (uint32_t)(map ? __ldg(map + in[b + idx]) : in[b + idx]) : pad;
         }
         BRS(ts).Sort(keys, 0, bits);
 #pragma unroll
@@ -128,7 +129,8 @@ __global__ void __launch_bounds__(THREADS) k_row_sort(const int64_t *__restrict_
 // register swap), padding keys 0xFFFFFFFF sort last
 template <int J>
 __global__ void __launch_bounds__(256) k_row_sort_warp(const int64_t *__restrict__ rowptr, int64_t r0, int64_t r1,
-                                                       const int32_t *__restrict__ in, int32_t *out) {
+                                                       const int32_t *__restrict__ in, int32_t *out,
+                                                       const int32_t *__restrict__ map) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < r1; r += nw) {
@@ -136,7 +138,10 @@ __global__ void __launch_bounds__(256) k_row_sort_warp(const int64_t *__restrict
         const int d = (int)(rowptr[r + 1] - b);
         uint32_t v[J];
 #pragma unroll
-        for (int j = 0; j < J; j++) v[j] = 32 * j + lane < d ? (uint32_t)in[b + 32 * j + lane] : 0xFFFFFFFFu;
+        for (int j = 0; j < J; j++) {
+            const int i = 32 * j + lane;
+            v[j] = i < d ? (uint32_t)(map ? __ldg(map + in[b + i]) : in[b + i]) : 0xFFFFFFFFu;
+        }
 #pragma unroll
         for (int k = 2; k <= 32 * J; k <<= 1) {
 #pragma unroll
@@ -166,6 +171,58 @@ __global__ void __launch_bounds__(256) k_row_sort_warp(const int64_t *__restrict
         for (int j = 0; j < J; j++)
             if (32 * j + lane < d) out[b + 32 * j + lane] = (int32_t)v[j];
     }
+}
+
+// Sort every row of a CSR-shaped array (row r at [rowptr[r], rowptr[r+1])) by
+// key = map ? map[in[e]] : in[e] (keys < 2^bits). Rows are in degree-descending
+// order, so each length class is a contiguous range (c.rsplit, load time): rows
+// >= 8192 with CUB's segmented radix sort (mapped keys gathered first), [512,
+// 8192) one CTA per row (block radix sort sized to the class), < 512 a warp per
+// row (register bitonic). Used at load time (adjacency by internal id) and by
+// the all-communities mode (neighbour community codes, k_sparse.cu).
+__global__ void k_gather_keys(const int32_t *__restrict__ in, const int32_t *__restrict__ map, int64_t cnt,
+                              int32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __ldg(map + in[i]);
+}
+
+cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *out, int bits, void *tmp, size_t need) {
+    const int64_t n = c.n;
+    const int64_t r8192 = c.rsplit[0], r2048 = c.rsplit[1], r512 = c.rsplit[2];
+    const int64_t r128 = c.rsplit[3], r32 = c.rsplit[4];
+    cudaError_t e = cudaSuccess;
+    if (r8192 > 0) {
+        int64_t e8 = 0;
+        if ((e = cudaMemcpy(&e8, c.rowptr + r8192, sizeof(int64_t), cudaMemcpyDeviceToHost))) return e;
+        const int32_t *src = in;
+        if (map) {
+            // mapped keys of the long rows, staged at the front of tmp
+            int32_t *g = (int32_t *)tmp;
+            const size_t gb = ((size_t)4 * e8 + 255) & ~(size_t)255;
+            if (gb > need) return cudaErrorMemoryAllocation;
+            k_gather_keys<<<148 * 8, 256, 0, c.stream>>>(in, map, e8, g);
+            c.launches++;
+            src = g;
+            tmp = (char *)tmp + gb;
+            need -= gb;
+        }
+        size_t t1 = 0;
+        cub::DeviceSegmentedRadixSort::SortKeys(nullptr, t1, src, out, e8, (int)r8192, c.rowptr, c.rowptr + 1, 0,
+                                                bits, c.stream);
+        if (t1 > need) return cudaErrorMemoryAllocation;
+        t1 = need;
+        cub::DeviceSegmentedRadixSort::SortKeys(tmp, t1, src, out, e8, (int)r8192, c.rowptr, c.rowptr + 1, 0,
+                                                bits, c.stream);
+        c.launches++;
+    }
+    auto wgrid = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 7) / 8, 148 * 16)); };
+    auto rows = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(hi - lo, 148 * 32)); };
+    if (r2048 > r8192) { k_row_sort<256, 32><<<rows(r8192, r2048), 256, 0, c.stream>>>(c.rowptr, r8192, r2048, in, out, bits, map); c.launches++; }
+    if (r512 > r2048) { k_row_sort<256, 8><<<rows(r2048, r512), 256, 0, c.stream>>>(c.rowptr, r2048, r512, in, out, bits, map); c.launches++; }
+    if (r128 > r512) { k_row_sort_warp<16><<<wgrid(r512, r128), 256, 0, c.stream>>>(c.rowptr, r512, r128, in, out, map); c.launches++; }
+    if (r32 > r128) { k_row_sort_warp<4><<<wgrid(r128, r32), 256, 0, c.stream>>>(c.rowptr, r128, r32, in, out, map); c.launches++; }
+    if (n > r32) { k_row_sort_warp<1><<<wgrid(r32, n), 256, 0, c.stream>>>(c.rowptr, r32, n, in, out, map); c.launches++; }
+    return cudaGetLastError();
 }
 
 // temporaries of launch_relabel, carved from the caller's arena
@@ -213,30 +270,16 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, vo
     cudaMemcpyAsync(&dmax, deg_s, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream);
     if ((e = cudaStreamSynchronize(c.stream))) return e;
     if ((e = cudaGetLastError())) return e;
-    // every row sorted by internal id. Rows are in degree-descending order, so
-    // each length class is a contiguous range: rows >= 8192 with CUB's segmented
-    // radix sort, [512, 8192) one CTA per row (block radix sort sized to the
-    // class), < 512 a warp per row (register bitonic). Keys need log2(n) bits.
+    // every row sorted by internal id (sort_rows below). Keys need log2(n) bits.
+    c.rsplit[0] = (int64_t)ge[7];
+    c.rsplit[1] = (int64_t)ge[6];
+    c.rsplit[2] = (int64_t)ge[kNumBins];
+    c.rsplit[3] = (int64_t)ge[5];
+    c.rsplit[4] = (int64_t)ge[3];
     if (nnz) {
         int bits = 1;
         while (bits < 31 && (1ll << bits) < n) bits++;
-        const int64_t r8192 = (int64_t)ge[7], r2048 = (int64_t)ge[6], r512 = (int64_t)ge[kNumBins];
-        const int64_t r128 = (int64_t)ge[5], r32 = (int64_t)ge[3];
-        if (r8192 > 0) {
-            int64_t e8 = 0;
-            if ((e = cudaMemcpy(&e8, c.rowptr + r8192, sizeof(int64_t), cudaMemcpyDeviceToHost))) return e;
-            t1 = need;
-            cub::DeviceSegmentedRadixSort::SortKeys(tmp, t1, tmpcol, c.col, e8, (int)r8192, c.rowptr, c.rowptr + 1, 0,
-                                                    bits, c.stream);
-            c.launches++;
-        }
-        auto wgrid = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 7) / 8, 148 * 16)); };
-        auto rows = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(hi - lo, 148 * 32)); };
-        if (r2048 > r8192) { k_row_sort<256, 32><<<rows(r8192, r2048), 256, 0, c.stream>>>(c.rowptr, r8192, r2048, tmpcol, c.col, bits); c.launches++; }
-        if (r512 > r2048) { k_row_sort<256, 8><<<rows(r2048, r512), 256, 0, c.stream>>>(c.rowptr, r2048, r512, tmpcol, c.col, bits); c.launches++; }
-        if (r128 > r512) { k_row_sort_warp<16><<<wgrid(r512, r128), 256, 0, c.stream>>>(c.rowptr, r512, r128, tmpcol, c.col); c.launches++; }
-        if (r32 > r128) { k_row_sort_warp<4><<<wgrid(r128, r32), 256, 0, c.stream>>>(c.rowptr, r128, r32, tmpcol, c.col); c.launches++; }
-        if (n > r32) { k_row_sort_warp<1><<<wgrid(r32, n), 256, 0, c.stream>>>(c.rowptr, r32, n, tmpcol, c.col); c.launches++; }
+        if ((e = sort_rows(c, tmpcol, nullptr, c.col, bits, tmp, need))) return e;
     }
     // ge[cls] = #vertices with degree >= bin_lo(cls); class cls = [ge[cls+1], ge[cls])
     ge[0] = (unsigned long long)n;
@@ -422,6 +465,16 @@ __global__ void k_nwide(const int64_t *__restrict__ rowptr, int64_t n, double bo
         if (d * d >= bound) lo = mid + 1; else hi = mid;
     }
     *out = (unsigned long long)lo;
+}
+
+void launch_comm_hist(Ctx &c, int64_t nbins) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 255) / 256, 148 * 4));
+    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.n, c.chist, nbins);
+    c.launches++;
+}
+void launch_nwide(Ctx &c, double bound) {
+    k_nwide<<<1, 1, 0, c.stream>>>(c.rowptr, c.n, bound, c.scal + kScalNWide);
+    c.launches++;
 }
 
 cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user_targets) {

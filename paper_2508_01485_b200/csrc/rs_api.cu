@@ -199,6 +199,9 @@ static void free_graph(rs_ctx *ctx) {
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
     dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.wps); dfree(c.pc2); dfree(c.amat);
     dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bql);
+    dfree(c.cid); dfree(c.srec); dfree(c.ctk); dfree(c.cta); dfree(c.ctb); dfree(c.pwr); dfree(c.prv); dfree(c.aself);
+    dfree(c.xsum); dfree(c.n2s);
+    c.sp_cap = 0;
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
     ctx->l2n = 0;
@@ -210,7 +213,7 @@ extern "C" void rs_destroy(rs_ctx *ctx) {
     cudaSetDevice(c.device);
     if (c.stream) cudaStreamSynchronize(c.stream);
     free_graph(ctx);
-    dfree(c.chist); dfree(c.ccode); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist); dfree(c.arena);
+    dfree(c.chist); dfree(c.ccode); dfree(c.code32); dfree(c.csort); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist); dfree(c.arena);
     dfree(ctx->utargets); dfree(ctx->stage_i32); dfree(ctx->stage_f64); dfree(ctx->cand_key); dfree(ctx->cand_id);
     for (int i = 0; i < rs::kNumBins + 1; i++) {
         if (c.side[i]) cudaStreamDestroy(c.side[i]);
@@ -339,13 +342,48 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
 }
 
 // ------------------------------------------------------------------ communities
+// all-communities mode (NEXT-2): every community is a target, sparse tables
+static rs_status set_communities_all(rs_ctx *ctx, int64_t mx) {
+    Ctx &c = ctx->c;
+    const size_t need = rs::sparse_rank_bytes(mx + 1);
+    if (need > c.csort_bytes) {
+        dfree(c.csort);
+        c.csort_bytes = 0;
+        CK(cudaMalloc(&c.csort, need));
+        c.csort_bytes = need;
+    }
+    if (c.sp_cap < c.cap_nnz || !c.cid) {
+        const int64_t n = c.cap_n, nnz = std::max<int64_t>(c.cap_nnz, 1);
+        CK(dalloc(&c.cid, n)); CK(dalloc(&c.srec, n)); CK(dalloc(&c.aself, n)); CK(dalloc(&c.xsum, n));
+        CK(dalloc(&c.n2s, n));
+        CK(dalloc(&c.ctk, nnz)); CK(dalloc(&c.cta, nnz)); CK(dalloc(&c.ctb, nnz));
+        CK(dalloc(&c.pwr, nnz)); CK(dalloc(&c.prv, nnz));
+        c.sp_cap = c.cap_nnz;
+    }
+    int64_t nc = 0;
+    CK(rs::launch_set_communities_all(c, mx, &nc));
+    if (nc < 2) return fail(ctx, RS_EINVAL, "rs_set_communities: RS_ALL_COMMUNITIES needs at least 2 distinct communities");
+    if (nc >= (1ll << 31)) return fail(ctx, RS_EINVAL, "rs_set_communities: too many communities");
+    CK(cudaStreamSynchronize(c.stream));
+    unsigned long long nw = 0;
+    CK(cudaMemcpy(&nw, c.scal + rs::kScalNWide, sizeof(nw), cudaMemcpyDeviceToHost));
+    c.n_wide = (int64_t)nw;
+    c.k = (int32_t)nc;
+    c.sparse = true;
+    c.has_comm = true;
+    return RS_OK;
+}
+
 extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of, const int32_t *targets, int32_t k) {
     if (!ctx) return RS_EINVAL;
     Ctx &c = ctx->c;
     cudaSetDevice(c.device);
     if (!c.loaded) return fail(ctx, RS_ESTATE, "rs_set_communities: no graph loaded");
     if (!community_of) return fail(ctx, RS_EINVAL, "rs_set_communities: community_of is NULL");
-    if (k < 2 || k > rs::kMaxK) return fail(ctx, RS_EINVAL, "rs_set_communities: k must be in [2, 254]");
+    const bool all = k == RS_ALL_COMMUNITIES;
+    if (!all && (k < 2 || k > rs::kMaxK))
+        return fail(ctx, RS_EINVAL, "rs_set_communities: k must be in [2, 254] or RS_ALL_COMMUNITIES");
+    if (all && targets) return fail(ctx, RS_EINVAL, "rs_set_communities: RS_ALL_COMMUNITIES takes targets = NULL");
     c.scored = false;
     c.has_comm = false;
     CK(cudaMemcpyAsync(c.comm_in, community_of, sizeof(int32_t) * c.n,
@@ -358,8 +396,11 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
         int64_t cap = std::max<int64_t>(mx + 1, 1024);
         CK(dalloc(&c.chist, cap));
         CK(dalloc(&c.ccode, cap));
+        CK(dalloc(&c.code32, cap));
         c.ccap = cap;
     }
+    if (all) return set_communities_all(ctx, mx);
+    c.sparse = false;
     if (c.k_alloc != k || c.kn_alloc != c.n) {
         CK(dalloc(&c.f, (size_t)c.n * k));
         CK(dalloc(&c.omega, (size_t)c.n * k));
@@ -402,17 +443,30 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     const int64_t n = c.n;
     c.e_shares = (int)RS_E_SHARES_OF(flags);
     c.variant = (int)((flags >> 16) & 7u);
+    if (c.sparse && c.variant)
+        return fail(ctx, RS_EINVAL, "rs_score: the NEXT-3 variant flags need explicit targets (k <= 254)");
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
     CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, 2 * sizeof(unsigned long long), c.stream));   // NTri, NProbe
-    CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs (Q rewritten)
-    // Phase A: border + histogram + weights + P lists + omega_max partials, the
-    // orientation of G' and the B-table pushes
-    fork(c);
-    CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n));
-    join(c);
+    if (c.sparse) {
+        // all-communities mode: Steps 2a-2c into per-vertex community tables, then
+        // Step 2d (P lists, per-edge weights, B pushes); each a degree-binned pass
+        fork(c);
+        CK(rs::launch_sparse_tables(c, ctx->l2t, ctx->l2n));
+        join(c);
+        fork(c);
+        CK(rs::launch_sparse_lists(c));
+        join(c);
+    } else {
+        CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs (Q rewritten)
+        // Phase A: border + histogram + weights + P lists + omega_max partials, the
+        // orientation of G' and the B-table pushes
+        fork(c);
+        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n));
+        join(c);
+    }
     CK(cudaEventRecord(c.ev_phase[1], c.stream));
     CK(cudaEventRecord(c.ev_phase[2], c.stream));   // (Phase C folded into A: ms_phase[1] = 0)
     // Phase E (Type-I triangles) and Phase D (Type-II pull, which needs only
@@ -724,6 +778,17 @@ extern "C" rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_o
     int32_t *forig = nullptr;
     CK(cudaMalloc(&forig, sizeof(int32_t) * (size_t)c.n * c.k));
     rs_status s = RS_OK;
+    if (c.sparse) {
+        // dense view of the sparse community tables
+        int32_t *tot = (int32_t *)c.scratch;
+        cudaError_t e = cudaMemsetAsync(forig, 0, sizeof(int32_t) * (size_t)c.n * c.k, c.stream);
+        if (e == cudaSuccess) e = rs::launch_sparse_counts_dense(c, forig, tot);
+        if (e == cudaSuccess && f_out) s = out_copy(ctx, f_out, forig, (size_t)c.n * c.k);
+        if (e == cudaSuccess && s == RS_OK && total_out) s = out_copy(ctx, total_out, tot, (size_t)c.n);
+        cudaFree(forig);
+        CK(e);
+        return s;
+    }
     cudaError_t e = rs::launch_permute_i32(c, c.f, c.k, forig);
     if (e == cudaSuccess && f_out) s = out_copy(ctx, f_out, forig, (size_t)c.n * c.k);
     if (e == cudaSuccess && s == RS_OK && total_out) {
@@ -744,7 +809,8 @@ extern "C" rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omeg
     if (omega_out) {
         double *worig = nullptr;
         CK(cudaMalloc(&worig, sizeof(double) * (size_t)c.n * c.k));
-        cudaError_t e = rs::launch_permute_f64(c, c.omega, c.k, worig);
+        cudaError_t e = c.sparse ? rs::launch_sparse_weights_dense(c, ctx->l2t, ctx->l2n, worig)
+                                 : rs::launch_permute_f64(c, c.omega, c.k, worig);
         rs_status s = e == cudaSuccess ? out_copy(ctx, omega_out, worig, (size_t)c.n * c.k) : RS_OK;
         cudaFree(worig);
         CK(e);
@@ -817,7 +883,7 @@ extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_
         if (s) return s;
     }
     if (type2_out) {
-        CK(rs::launch_type2_counts(c, tmp));
+        CK(c.sparse ? rs::launch_sparse_type2(c, tmp) : rs::launch_type2_counts(c, tmp));
         rs_status s = out_copy(ctx, type2_out, tmp, (size_t)c.n);
         if (s) return s;
     }
@@ -828,7 +894,7 @@ extern "C" rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *
     if (!ctx) return RS_EINVAL;
     Ctx &c = ctx->c;
     if (!c.has_comm) return fail(ctx, RS_ESTATE, "rs_get_targets: call rs_set_communities first");
-    if (targets_out) memcpy(targets_out, c.h_targets, sizeof(int32_t) * c.k);
+    if (targets_out) memcpy(targets_out, c.sparse ? c.h_targets_all.data() : c.h_targets, sizeof(int32_t) * c.k);
     if (k_out) *k_out = c.k;
     return RS_OK;
 }

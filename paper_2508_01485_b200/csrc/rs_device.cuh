@@ -172,6 +172,18 @@ struct CtaGroup {
         return a;
     }
     __device__ __forceinline__ int sum(int v) { return (int)sum((long long)v); }
+    __device__ __forceinline__ double sum(double v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) s_u[w] = (unsigned long long)__double_as_longlong(v);
+        __syncthreads();
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < kCtaWarps; i++) a += __longlong_as_double((long long)s_u[i]);
+        __syncthreads();
+        return a;
+    }
     __device__ __forceinline__ unsigned long long sum(unsigned long long v) {
         return (unsigned long long)sum((long long)v);
     }

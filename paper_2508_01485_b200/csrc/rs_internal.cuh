@@ -85,6 +85,13 @@ struct __align__(32) BQL {
     double pad;
 };
 
+// Per-vertex record of the all-communities mode, gathered once per neighbour.
+struct __align__(16) SRec {
+    long long beg;     // rowptr[v]: v's community table and lists start here
+    int32_t L;         // number of distinct communities among N(v) (table length)
+    int32_t cid;       // column of C(v)
+};
+
 struct Bins {
     int64_t count[kNumBins] = {0};
     int64_t offset[kNumBins + 1] = {0};
@@ -114,6 +121,7 @@ struct Ctx {
     int32_t *perm = nullptr;     // n: original id of internal vertex r (degree-descending order)
     int32_t *inv = nullptr;      // n: internal id of original vertex v
     Bins bins;
+    int64_t rsplit[5] = {0};     // first row of degree < 8192, 2048, 512, 128, 32 (row-sort classes)
     int64_t d_max = 0;
     int64_t *e_pre = nullptr;    // Phase E work items: prefix of extra chunks of the e_nbig largest rows
     int64_t e_nbig = 0, e_extra = 0;
@@ -131,6 +139,26 @@ struct Ctx {
     int32_t k = 0;
     int32_t h_targets[kMaxK];
     bool has_comm = false;
+
+    // all-communities mode (NEXT-2, rs_set_communities with k = RS_ALL_COMMUNITIES):
+    // every community is a target (k = number of distinct communities, any size);
+    // per-vertex sparse community tables replace the dense n*k tables
+    bool sparse = false;
+    std::vector<int32_t> h_targets_all;  // the k target ids in column order
+    int32_t *cid = nullptr;      // n: column of C(u) (internal order)
+    int32_t *code32 = nullptr;   // community id -> column (ccap entries)
+    SRec *srec = nullptr;        // n: {rowptr, L(u), cid} gathered per neighbour
+    int2 *ctk = nullptr;         // nnz: u's distinct neighbour columns ascending at rowptr[u]: {column, count}
+    double *cta = nullptr;       // nnz: a_u(c) = omega_u(c)^(1/3) beside each column
+    ulonglong2 *ctb = nullptr;   // nnz: B_u[c] limbs (fx_red2) beside each column
+    double *pwr = nullptr;       // nnz: a_w(c_u) beside each w of P(u) (pidx order); wps holds a_u(c_w)
+    int64_t *prv = nullptr;      // nnz: position of c_u in w's table, beside each w of P(u)
+    double *aself = nullptr;     // n: a_u(c_u)
+    double *xsum = nullptr;      // n: X(u) = sum_c f_u(c) log2 f_u(c) (Algorithm 2)
+    unsigned long long *n2s = nullptr;  // n: Type-II triad counts (all-communities mode)
+    void *csort = nullptr;       // community ranking temporaries (grow-only)
+    size_t csort_bytes = 0;
+    int64_t sp_cap = 0;          // nnz the sparse buffers were sized for
 
     // score (per rs_score)
     int32_t *f = nullptr;        // n*k counts
@@ -222,6 +250,17 @@ cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int6
 cudaError_t launch_type2_counts(Ctx &c, int64_t *t2_dev);
 cudaError_t launch_type1_export(Ctx &c, int64_t *t1_dev);
 cudaError_t launch_stats(Ctx &c, int64_t out[4]);
+cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *out, int bits, void *tmp, size_t need);
+void launch_comm_hist(Ctx &c, int64_t nbins);
+void launch_nwide(Ctx &c, double bound);
+// all-communities mode (k_sparse.cu)
+size_t sparse_rank_bytes(int64_t nbins);
+cudaError_t launch_set_communities_all(Ctx &c, int64_t max_comm, int64_t *nc_out);
+cudaError_t launch_sparse_tables(Ctx &c, const double *l2t, int64_t l2n);
+cudaError_t launch_sparse_lists(Ctx &c);
+cudaError_t launch_sparse_counts_dense(Ctx &c, int32_t *f_dev, int32_t *total_dev);
+cudaError_t launch_sparse_weights_dense(Ctx &c, const double *l2t, int64_t l2n, double *w_dev);
+cudaError_t launch_sparse_type2(Ctx &c, int64_t *t2_dev);
 cudaError_t launch_minmax_i32(Ctx &c, const int32_t *a, int64_t n, int64_t *mn, int64_t *mx);
 
 }  // namespace rs

@@ -30,6 +30,10 @@ struct CdeArgs {
     int64_t head_lo, head_hi;           // owned head range (multi-GPU); [0, n) on one GPU
     int32_t e_rank, e_world;            // Phase E: this rank's share of the middle vertices
     int64_t n_wide;                     // heads [0, n_wide) use the 3-limb Type-I accumulator
+    // all-communities mode (k_sparse.cu): weights per G' edge instead of dense rows
+    const double *__restrict__ pwr;     // a_w(c_u) beside each w of P(u) (wps: a_u(c_w))
+    const int64_t *__restrict__ prv;    // position of c_u in w's community table
+    const ulonglong2 *__restrict__ ctb; // B_w[c] limbs beside each column of w's table
 };
 
 // VRec::wide by internal id: d(h)^2 >= wide_bound, d non-increasing in h
@@ -45,6 +49,8 @@ inline CdeArgs cde_args(Ctx &c) {
     a.n_wide = c.n_wide;
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
     a.e_rank = 0; a.e_world = 1;
+    a.pwr = c.pwr; a.prv = c.prv; a.ctb = c.ctb;
+    if (c.sparse) a.pplus = c.pidx;   // P+(u) is one ascending run: the prefix of P(u)
     return a;
 }
 
