@@ -311,6 +311,12 @@ def main():
         variants = {"flags": "literal_L|gate_L|wmax_eb", "ms_per_step": round(float(np.median(vms)), 4)}
         sc.score()   # back to the adopted readings
 
+    # NEXT-2: the all-communities mode (every community a target, sparse tables) on
+    # an LFR-style LiveJournal-shape graph with 10 000 communities (Zipf 0.8 sizes)
+    sparse = None
+    if not a.no_awcc and world == 1:
+        sparse = sparse_leg(a, rsb, dev, stream, sh, flush)
+
     e2e = None
     if not a.no_e2e:
         e2e = measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st)
@@ -335,6 +341,7 @@ def main():
             "next_awcc_removal": awcc,
             "next_literal_variants": variants,
             "next_shii": shii,
+            "next_all_communities": sparse,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk_s, "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
         }
@@ -342,6 +349,55 @@ def main():
     sc.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+SPARSE_CFG = dict(base="lj", n_comm=10_000, zipf_s=0.8)
+
+
+def sparse_leg(a, rsb, dev, stream, sh, flush):
+    """One step = rs_set_communities(RS_ALL_COMMUNITIES) + rs_score + rs_topk on a
+    device-resident LFR-style graph, L2 flushed between steps."""
+    import torch
+    t0 = time.time()
+    g2 = gen.config_graph(SPARSE_CFG["base"], n_comm=SPARSE_CFG["n_comm"], zipf_s=SPARSE_CFG["zipf_s"])
+    gen_s = time.time() - t0
+    sc2 = rsb.Scorer(dev.index, sh)
+    rp = torch.from_numpy(g2.rowptr).to(dev)
+    cl = torch.from_numpy(g2.col).to(dev)
+    cm = torch.from_numpy(g2.comm).to(dev)
+    ids = torch.empty(a.K, dtype=torch.int32, device=dev)
+    sco = torch.empty(a.K, dtype=torch.float64, device=dev)
+    sc2.load_csr(rp, cl)
+    ms, ph = [], []
+    for i in range(a.warmup + 5):
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sc2.set_communities(cm, rsb.RS_ALL_COMMUNITIES)
+        sc2.score()
+        sc2.topk(a.K, ids, sco)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= a.warmup:
+            ms.append(e0.elapsed_time(e1))
+    for i in range(3):
+        with torch.cuda.stream(stream):
+            flush.fill_(i)
+        s = sc2.score(stats=True)
+        ph.append([s["ms_phase"][0], s["ms_phase"][2], s["ms_phase"][3]])
+    ph = np.median(np.array(ph), axis=0)
+    step = float(np.median(ms))
+    out = {"workload": f"{SPARSE_CFG['base']}-shape DC-SBM, {SPARSE_CFG['n_comm']} communities "
+                       f"(Zipf {SPARSE_CFG['zipf_s']} sizes), targets = all", "n": g2.n, "m": g2.m, "k": sc2.k,
+           "ms_per_step": round(step, 4), "GTEPS": round(g2.m / (step * 1e-3) / 1e9, 4),
+           "phase_ms": {"tables_lists": round(float(ph[0]), 4), "ED_type1_type2": round(float(ph[1]), 4),
+                        "F_finalize": round(float(ph[2]), 4)},
+           "pred_entries": s["n_pred_entries"], "triangles": s["n_triangles"], "omega_max": s["omega_max"],
+           "gen_s": round(gen_s, 1)}
+    sc2.close()
+    del rp, cl, cm
+    return out
 
 
 def measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st):

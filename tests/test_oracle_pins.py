@@ -270,3 +270,41 @@ def test_select_targets_ties():
     assert list(oracle.select_targets(comm, 3)) == [7, 3, 5]        # size desc, id asc
     with pytest.raises(ValueError):
         oracle.select_targets(comm, 6)
+
+
+# ---------------------------------------------------------------- all communities (NEXT-2)
+def test_all_communities_singletons_closed_form():
+    """K_c with c singleton communities, targets = all (k = c > 254 possible):
+    every vertex sees c-1 communities once; its own column is absent (f = 0), so
+    omega_u(own) = H(uniform over c-1) (L_all - 1) = (c-2) log2(c-1) -- the
+    maximum cell, which only an omega_max over ALL cells (C-7) finds -- and
+    every present column has omega = (c-2) log2(c-2).  Each vertex closes
+    (c-1)(c-2) Type-I triads with term (h^3)^(1/3) = h, h = log2(c-2)/log2(c-1),
+    so R = h (m = 1)."""
+    c = 300
+    g = gen.from_adjacency(np.ones((c, c), dtype=bool), list(range(c)))
+    r = oracle.run(g, k=c, K=5)
+    assert r.omega_max == pytest.approx((c - 2) * math.log2(c - 1), rel=1e-14)
+    own = r.omega[np.arange(c), [list(r.targets).index(v) for v in range(c)]]
+    np.testing.assert_allclose(own, (c - 2) * math.log2(c - 1), rtol=1e-14)
+    np.testing.assert_allclose(r.R, math.log2(c - 2) / math.log2(c - 1), rtol=1e-13)
+    assert np.all(r.nI == (c - 1) * (c - 2)) and np.all(r.nII == 0)
+    assert list(r.targets) == list(range(c))          # equal sizes: ascending id (C-15)
+
+
+@pytest.mark.parametrize("n,c,seed", [(60, 20, 1), (120, 50, 2), (200, 100, 3), (150, 150, 4)])
+def test_all_communities_vs_bruteforce(n, c, seed):
+    """Many small communities, targets = all: most columns of a row have f = 0."""
+    rng = np.random.default_rng(seed + 3000)
+    g = gen.planted_partition(n, c, p_in=float(rng.uniform(0.3, 0.8)), p_out=float(rng.uniform(0.03, 0.1)),
+                              seed=seed + 3100)
+    k = len(np.unique(g.comm))
+    t_or = oracle.select_targets(g.comm, k)
+    assert list(t_or) == list(bf_select(g.comm, k))
+    r = oracle.run(g, targets=t_or, K=g.n)
+    b = brute(g, t_or)
+    assert np.array_equal(r.f, b["f"])
+    np.testing.assert_allclose(r.omega, b["omega"], rtol=1e-13, atol=1e-15)
+    assert r.omega_max == pytest.approx(b["omega_max"], rel=1e-13)
+    assert np.array_equal(r.nI, b["nI"]) and np.array_equal(r.nII, b["nII"])
+    np.testing.assert_allclose(r.R, b["R"], rtol=1e-12, atol=0)
