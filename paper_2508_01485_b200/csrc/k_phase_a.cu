@@ -91,10 +91,13 @@ __device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, doubl
 }
 
 // Step 3 inputs of u (after its weights and amat row are written and the group
-// synchronised): B pushes, the P+ runs with a_u(c_z), the PRec record.
+// synchronised): B pushes, the P+ runs with a_u(c_z), the PRec record. P+(u)
+// is written as its target run DESCENDING at [0, pt) followed by the other run
+// ascending at [pt, pp): the entries below any y then form one contiguous range
+// around pt (Phase E probes only z < y).
 template <int U, class GR>
 __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR &g, int64_t beg, int pc, int pp,
-                                              int lu) {
+                                              int pt, int lu) {
     const int k = a.k;
     const double *arow = a.amat + u * k;           // this group's writes, plain loads
     const bool push = lu < k;
@@ -127,8 +130,8 @@ __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR
                 const int rt = g.rank(tgt, &tt);
                 const int rn = g.rank(inp && !tgt, &tn);
                 if (inp) {
-                    // target run ascending from the front, the rest descending from |P+|
-                    const int64_t at = tgt ? beg + ct + rt : beg + pp - 1 - (cn + rn);
+                    // target run descending down from pt - 1, the rest ascending from pt
+                    const int64_t at = tgt ? beg + pt - 1 - (ct + rt) : beg + pt + cn + rn;
                     a.pplus[at] = v[j];
                     a.wps[at] = tgt ? arow[lv[j]] : 0.0;
                 }
@@ -158,7 +161,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
     // ceil(d / G) neighbours < 2^16 (launch_phase_a_impl falls back to the
     // shared-memory histogram when d_max >= 2^22).
     unsigned long long h0 = 0ull, h1 = 0ull;
-    int pc = 0, pp = 0;   // |P(u)|, |P+(u)| (foreign neighbours below u)
+    int pc = 0, pp = 0, pt = 0;   // |P(u)|, |P+(u)| (foreign neighbours below u), |P+_T(u)|
     for (int64_t base = beg; base < end; base += GR::size * U) {
         int32_t x[U];
         uint8_t lx[U];
@@ -180,12 +183,14 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
                 if (l < 4u) h0 += inc; else h1 += inc;
             }
             if (base + j * GR::size < end) {          // group-uniform
-                int tot, totp;
+                int tot, totp, tott;
                 const int r = g.rank(foreign, &tot);
                 g.rank(foreign && x[j] < (int32_t)u, &totp);
+                g.rank(foreign && x[j] < (int32_t)u && l < (unsigned)k, &tott);
                 if (foreign) a.pidx[beg + pc + r] = x[j];
                 pc += tot;
                 pp += totp;
+                pt += tott;
             }
         }
     }
@@ -231,7 +236,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
     const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
     if ((int)g.lane == owner) write_vrec(a, u, a_self, pc, lu, d);
     g.sync();
-    phase_a_lists<U>(a, u, g, beg, pc, pp, lu);
+    phase_a_lists<U>(a, u, g, beg, pc, pp, pt, lu);
     return wmax;
 }
 
@@ -244,7 +249,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     const int k = a.k;
     for (int c = g.lane; c < k; c += GR::size) hist[c] = 0;
     g.sync();
-    int pc = 0, pp = 0;
+    int pc = 0, pp = 0, pt = 0;
     for (int64_t base = beg; base < end; base += GR::size * U) {
         int32_t x[U];
         uint8_t lx[U];
@@ -262,12 +267,14 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
             if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
             if (valid && lx[j] < k) atomicAdd(&hist[lx[j]], 1);
             if (base + j * GR::size < end) {
-                int tot, totp;
+                int tot, totp, tott;
                 const int r = g.rank(foreign, &tot);
                 g.rank(foreign && x[j] < (int32_t)u, &totp);
+                g.rank(foreign && x[j] < (int32_t)u && lx[j] < k, &tott);
                 if (foreign) a.pidx[beg + pc + r] = x[j];
                 pc += tot;
                 pp += totp;
+                pt += tott;
             }
         }
     }
@@ -299,7 +306,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
         write_vrec(a, u, as, pc, lu, d);
     }
     g.sync();
-    phase_a_lists<U>(a, u, g, beg, pc, pp, lu);
+    phase_a_lists<U>(a, u, g, beg, pc, pp, pt, lu);
     g.sync();
     return wmax;
 }

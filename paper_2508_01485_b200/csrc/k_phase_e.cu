@@ -99,6 +99,50 @@ __device__ __forceinline__ int find_desc_g(const int32_t *p, int len, int32_t z)
     return (lo < len && __ldg(p + lo) == z) ? lo : -1;
 }
 
+// The probed range of P+(x) for the pair (y, x in P-(y)): a triangle z < y < x
+// needs z in P+(y), so only the entries of P+(x) below y can close one (about
+// half of P+(x) on average). Phase A stores P+(x) as its target run descending
+// at [0, t) and the other run ascending at [t, |P+|), so those entries are one
+// contiguous range: the tail of the target run and (if x and y are both
+// targets, C-27) the head of the other run, found by two binary searches in
+// lockstep. Returns the range's memory start, its length and the number of
+// target entries at its front. All-communities mode: one ascending run.
+// Measured on the Orkut shape (probes 394 M -> 202 M with the cut, 1xB200):
+// Phase E+D 3.84 ms without the cut, 4.29 ms with it, 3.87 ms cutting only
+// lists of >= 64 entries -- the two binary searches per pair in the item setup
+// cost more than the probes they save (short lists: 1-2 aligned pieces either
+// way). Off by default; -DRS_EXP_CUT_MIN=n cuts lists of >= n entries.
+#ifndef RS_EXP_CUT_MIN
+#define RS_EXP_CUT_MIN 0x7fffffff
+#endif
+template <bool SPARSE>
+__device__ __forceinline__ void cut_range(const int32_t *__restrict__ pplus, int64_t bx, int pp, int t, int32_t y,
+                                          bool both, bool any, int64_t &rs, int &len, int &tb) {
+    if (!any) { rs = bx; len = 0; tb = 0; return; }
+    if (pp < RS_EXP_CUT_MIN) {   // experiment: no cut below this list length
+        rs = bx; tb = SPARSE ? pp : t; len = SPARSE ? pp : (both ? pp : t);
+        return;
+    }
+    if constexpr (SPARSE) {
+        int lo = 0, hi = pp;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(pplus + bx + mid) < y) lo = mid + 1; else hi = mid;
+        }
+        rs = bx; len = lo; tb = lo;
+    } else {
+        int lo1 = 0, hi1 = t, lo2 = 0, hi2 = both ? pp - t : 0;   // #target entries >= y, #others < y
+        while (lo1 < hi1 || lo2 < hi2) {
+            const int m1 = (lo1 + hi1) >> 1, m2 = (lo2 + hi2) >> 1;
+            const int32_t v1 = lo1 < hi1 ? __ldg(pplus + bx + m1) : 0;
+            const int32_t v2 = lo2 < hi2 ? __ldg(pplus + bx + t + m2) : 0;
+            if (lo1 < hi1) { if (v1 >= y) lo1 = m1 + 1; else hi1 = m1; }
+            if (lo2 < hi2) { if (v2 < y) lo2 = m2 + 1; else hi2 = m2; }
+        }
+        rs = bx + lo1; tb = t - lo1; len = tb + lo2;
+    }
+}
+
 // shared-memory per-item accumulator: four 20-bit limbs of q (< 2^80) added with
 // native 32-bit shared atomics (64-bit shared atomics are CAS loops); exact
 // while a slot receives fewer than 2^12 terms per item (x slots with longer
@@ -196,9 +240,9 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             const int i = start + 32 * h + lane;
             xv[h] = i < end ? __ldg(a.pidx + by + py + i) : -1;   // x in P-(y) (suffix of P(y)): x > y
         }
-        // i-th entry of P+(y) in ascending order within its run (the other run is
-        // stored descending after the target run)
-        auto py_at = [&](int i) -> int64_t { return i < pyt ? by + i : by + py - 1 - (i - pyt); };
+        // i-th entry of P+(y) in ascending order within its run (the target run is
+        // stored descending, the other run ascending after it)
+        auto py_at = [&](int i) -> int64_t { return SPARSE ? by + i : (i < pyt ? by + pyt - 1 - i : by + i); };
         const int32_t z0 = lane < py ? __ldg(a.pplus + py_at(lane)) : -1;
         const double ay0 = (!SPARSE && lane < k) ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
         PRec pcx[2];
@@ -235,19 +279,21 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         qi = __shfl_sync(0xffffffffu, qnext, 0);
         rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
         // the item's predecessors x. A triangle carries a term only if two of its
-        // vertices are targets: with both x and y targets every z of P+(x) is
-        // probed, with one of them only the target run of P+(x), with neither
-        // nothing. Each probed list is cut into pieces numbered across the item.
+        // vertices are targets: with both x and y targets every z < y of P+(x) is
+        // probed, with one of them only those of the target run, with neither
+        // nothing (cut_range). Each probed range is cut into pieces numbered
+        // across the item.
         int nx = 0, npieces = 0;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int lx = lxv[h];
             const bool tx = lx < k;
-            const int t = pr_plus_t(pcx[h]);
-            const int lenx = (tx && ty) ? pcx[h].x : ((tx || ty) ? t : 0);   // probed prefix of P+(x)
+            int64_t bx;
+            int lenx, t;
+            cut_range<SPARSE>(a.pplus, pr_start(pcx[h]), pcx[h].x, pr_plus_t(pcx[h]), y, tx && ty,
+                              xv[h] >= 0 && (tx || ty), bx, lenx, t);
             const bool use = lenx > 0;
             nprobe += (unsigned)lenx;
-            const int64_t bx = pr_start(pcx[h]);
             // aligned 16-byte pieces covering [bx, bx + lenx)
             const int pieces = use ? (int)(((bx + lenx - 1) >> 2) - (bx >> 2) + 1) : 0;
             int incl = pieces;
@@ -341,7 +387,8 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                     const bool zt = off < (int)(xe.y & 0xFFFFFF);   // z from the target run of P+(x)
                     int iz;
                     if (local) iz = zt ? find_sorted(S.py, pyt, z) : find_sorted(S.py + pyt, py - pyt, z);
-                    else iz = zt ? find_sorted_g(a.pplus + by, pyt, z) : find_desc_g(a.pplus + by + pyt, py - pyt, z);
+                    else if (zt) iz = SPARSE ? find_sorted_g(a.pplus + by, pyt, z) : find_desc_g(a.pplus + by, pyt, z);
+                    else iz = find_sorted_g(a.pplus + by + pyt, py - pyt, z);
 #ifdef RS_EXP_NO_TERMS
                     if (iz >= 0) ntri++;
                     if (iz >= 0 && z == -7) {
@@ -361,7 +408,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                             const double Axly = S.axy[slot];
                             const double Aylx = SPARSE ? Ay[slot] : (lx < k ? Ay[lx] : 0.0);
                             // a_y(c_z), beside z in y's slot (the other run holds 0)
-                            const int64_t ypos = by + (zt ? iz : (local ? py - 1 - iz : pyt + iz));
+                            const int64_t ypos = by + (!zt ? pyt + iz : ((local && !SPARSE) ? pyt - 1 - iz : iz));
                             const double Aylz = __ldg(a.wps + ypos);
                             const double Azlx = SPARSE ? __ldg(a.pwr + xe.x + off) : amat_at(a, z, lx);
                             const double Azly = SPARSE ? __ldg(a.pwr + ypos) : amat_at(a, z, ly);
@@ -525,8 +572,10 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 Axly = SPARSE ? __ldg(a.pwr + qpos) : amat_at(a, x, ly);
             }
             const bool tx = lx < k, ty = ly < k;
-            const int t = (tx || ty) ? pr_plus_t(pcx) : 0;               // probed: the target run,
-            const int np = t + ((tx && ty) ? pcx.x - pr_plus_t(pcx) : 0); // and the other if both
+            int64_t rsx;                                                 // probed: z < y of the target
+            int np, t;                                                   // run, and of the other if both
+            cut_range<SPARSE>(a.pplus, pr_start(pcx), pcx.x, pr_plus_t(pcx), (int32_t)(y0 + j), tx && ty,
+                              x >= 0 && (tx || ty), rsx, np, t);
             double Aylx = 0.0;
             if (x >= 0 && tx) Aylx = SPARSE ? __ldg(a.wps + qpos) : __ldg(a.amat + (y0 + j) * k + lx);
             int incl2 = np;
@@ -543,7 +592,7 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 const int p = owner(incl2, r);
                 const int o = r - (__shfl_sync(0xffffffffu, incl2, p) - __shfl_sync(0xffffffffu, np, p));
                 const int32_t xp = __shfl_sync(0xffffffffu, x, p);
-                const long long bx = __shfl_sync(0xffffffffu, pr_start(pcx), p);
+                const long long bx = __shfl_sync(0xffffffffu, (long long)rsx, p);
                 const int tp = __shfl_sync(0xffffffffu, t, p);
                 const int lxp = __shfl_sync(0xffffffffu, lx, p);
                 const double Axlyp = __shfl_sync(0xffffffffu, Axly, p);
@@ -561,12 +610,12 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 const int tyn = pr_plus_t(pcy), nyn = pcy.x - tyn;
                 int iz;
                 int64_t ypos;
-                if (zt) {
-                    iz = find_sorted_g(a.pplus + dy, tyn, z);
+                if (zt) {                                                   // the target run, descending
+                    iz = SPARSE ? find_sorted_g(a.pplus + dy, tyn, z) : find_desc_g(a.pplus + dy, tyn, z);
                     ypos = dy + iz;
                 } else {
-                    const int64_t nb = dy + tyn;                              // the other run, descending
-                    iz = find_desc_g(a.pplus + nb, nyn, z);
+                    const int64_t nb = dy + tyn;                              // the other run, ascending
+                    iz = find_sorted_g(a.pplus + nb, nyn, z);
                     ypos = nb + iz;
                 }
                 if (iz < 0) continue;

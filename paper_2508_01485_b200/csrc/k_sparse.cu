@@ -282,26 +282,59 @@ __device__ __forceinline__ void sp_lists_vertex(const SpArgs &a, int64_t u, GR &
             if (x[j] >= 0) sx[j] = a.srec[x[j]];
             else sx[j] = SRec{0, 0, cu};
         }
-        int jr[U];
-#pragma unroll
-        for (int j = 0; j < U; j++)   // c_u in x's table (x is adjacent to u)
-            jr[j] = (x[j] >= 0 && sx[j].cid != cu) ? ct_find(a.ctk + sx[j].beg, sx[j].L, cu) : 0;
+        // binary searches of every foreign entry, advanced in lockstep so the
+        // 2U dependent load chains overlap: c_u in x's table (x is adjacent to u,
+        // so present) and c_x in u's own table
+        bool fr[U];
+        int lo_r[U], hi_r[U], lo_o[U], hi_o[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
-            const bool foreign = x[j] >= 0 && sx[j].cid != cu;
+            fr[j] = x[j] >= 0 && sx[j].cid != cu;
+            lo_r[j] = 0; hi_r[j] = fr[j] ? sx[j].L : 0;
+            lo_o[j] = 0; hi_o[j] = fr[j] ? su.L : 0;
+        }
+        for (;;) {
+            bool more = false;
+#pragma unroll
+            for (int j = 0; j < U; j++) more |= (lo_r[j] < hi_r[j]) | (lo_o[j] < hi_o[j]);
+            if (!more) break;
+            int vr[U], vo[U];
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                const int mr = (lo_r[j] + hi_r[j]) >> 1, mo = (lo_o[j] + hi_o[j]) >> 1;
+                vr[j] = lo_r[j] < hi_r[j] ? __ldg(&a.ctk[sx[j].beg + mr].x) : 0;
+                vo[j] = lo_o[j] < hi_o[j] ? __ldg(&a.ctk[beg + mo].x) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                const int mr = (lo_r[j] + hi_r[j]) >> 1, mo = (lo_o[j] + hi_o[j]) >> 1;
+                if (lo_r[j] < hi_r[j]) { if (vr[j] < cu) lo_r[j] = mr + 1; else hi_r[j] = mr; }
+                if (lo_o[j] < hi_o[j]) { if (vo[j] < sx[j].cid) lo_o[j] = mo + 1; else hi_o[j] = mo; }
+            }
+        }
+        double ao[U], ar[U];
+        int cr[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int64_t p = sx[j].beg + lo_r[j];
+            ao[j] = fr[j] ? __ldg(a.cta + beg + lo_o[j]) : 0.0;   // a_u(c_x)
+            ar[j] = fr[j] ? __ldg(a.cta + p) : 0.0;               // a_x(c_u)
+            cr[j] = fr[j] ? __ldg(&a.ctk[p].y) : 1;               // f_x(c_u)
+        }
+#pragma unroll
+        for (int j = 0; j < U; j++) {
             if (base + j * GR::size < end) {          // group-uniform
                 int tot, totp;
-                const int r = g.rank(foreign, &tot);
-                g.rank(foreign && x[j] < (int32_t)u, &totp);
-                if (foreign) {
+                const int r = g.rank(fr[j], &tot);
+                g.rank(fr[j] && x[j] < (int32_t)u, &totp);
+                if (fr[j]) {
                     const int64_t pos = beg + pc + r;
-                    const int64_t p = sx[j].beg + jr[j];
-                    const int jo = ct_find(a.ctk + beg, su.L, sx[j].cid);
+                    const int64_t p = sx[j].beg + lo_r[j];
                     a.pidx[pos] = x[j];
-                    a.wps[pos] = a.cta[beg + jo];
-                    a.pwr[pos] = __ldg(a.cta + p);
+                    a.wps[pos] = ao[j];
+                    a.pwr[pos] = ar[j];
                     a.prv[pos] = p;
-                    n2 += (unsigned long long)(__ldg(&a.ctk[p].y) - 1);
+                    n2 += (unsigned long long)(cr[j] - 1);
                     if (push) fx_red2(&a.ctb[p].x, qs);   // u in P(x): a_u(c_u) into B_x[c_u]
                 }
                 pc += tot;
@@ -329,7 +362,7 @@ __device__ __forceinline__ void sp_lists_vertex(const SpArgs &a, int64_t u, GR &
 }
 
 template <int G, int U>
-__global__ void __launch_bounds__(256) k_sp_lists_warp(SpArgs a) {
+__global__ void __launch_bounds__(256, 4) k_sp_lists_warp(SpArgs a) {
     WarpGroup<G> g;
     const int64_t gpb = blockDim.x / G;
     for (int64_t i = blockIdx.x * gpb + threadIdx.x / G; i < a.nverts; i += (int64_t)gridDim.x * gpb)
@@ -364,13 +397,16 @@ static void sp_grid(Ctx &c, K kern, int64_t nverts, int gpb, cudaStream_t s, con
     c.launches++;
 }
 
-cudaError_t launch_sparse_tables(Ctx &c, const double *l2t, int64_t l2n) {
-    // neighbour columns sorted per row into c.pplus (unused by this mode's Phase E,
-    // which probes P+(x) in pidx directly); temporaries from the load arena
+// neighbour columns sorted per row into c.pplus (unused by this mode's Phase E,
+// which probes P+(x) in pidx directly); temporaries from the load arena. On the
+// library stream: the caller forks the table bins after it.
+cudaError_t launch_sparse_sort(Ctx &c) {
     int bits = 1;
     while (bits < 31 && (1ll << bits) < (int64_t)c.k) bits++;
-    cudaError_t e = sort_rows(c, c.col, c.cid, c.pplus, bits, c.arena, c.arena_bytes);
-    if (e) return e;
+    return sort_rows(c, c.col, c.cid, c.pplus, bits, c.arena, c.arena_bytes);
+}
+
+cudaError_t launch_sparse_tables(Ctx &c, const double *l2t, int64_t l2n) {
     SpArgs base = sp_args(c, l2t, l2n);
     // groups: [0,8):4 [8,32):8 [32,128):16 [128,2048):32 [2048,inf):CTA
     for (int cls = kNumBins - 1; cls >= 0; cls--) {

@@ -453,6 +453,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (c.sparse) {
         // all-communities mode: Steps 2a-2c into per-vertex community tables, then
         // Step 2d (P lists, per-edge weights, B pushes); each a degree-binned pass
+        CK(rs::launch_sparse_sort(c));   // library stream, before the fork
         fork(c);
         CK(rs::launch_sparse_tables(c, ctx->l2t, ctx->l2n));
         join(c);

@@ -58,8 +58,10 @@ struct __align__(16) VRec {
 // has the higher degree (the numbering is degree-descending), so P+(u) is the
 // prefix of the ascending list P(u) = pidx[rowptr[u], +|P|) and P-(u) its
 // suffix. Phase A also copies P+(u) to pplus at the same offset as two runs:
-// the entries in a target community ascending at [0, t), the others in
-// DESCENDING order at [t, |P+|); wps holds a_u(c_z) beside each entry.
+// the entries in a target community in DESCENDING order at [0, t), the others
+// ascending at [t, |P+|), so the entries below any y form one contiguous range
+// around t; wps holds a_u(c_z) beside each entry. (All-communities mode: pplus
+// is pidx itself, one ascending run, t = |P+|.)
 // t = |P+_T(u)| is packed above bit 40 of `start` (offsets < 2^40).
 struct __align__(16) PRec {
     int x;             // |P+(u)| (orientation out-degree)
@@ -256,6 +258,7 @@ void launch_nwide(Ctx &c, double bound);
 // all-communities mode (k_sparse.cu)
 size_t sparse_rank_bytes(int64_t nbins);
 cudaError_t launch_set_communities_all(Ctx &c, int64_t max_comm, int64_t *nc_out);
+cudaError_t launch_sparse_sort(Ctx &c);
 cudaError_t launch_sparse_tables(Ctx &c, const double *l2t, int64_t l2n);
 cudaError_t launch_sparse_lists(Ctx &c);
 cudaError_t launch_sparse_counts_dense(Ctx &c, int32_t *f_dev, int32_t *total_dev);

@@ -150,3 +150,32 @@ def test_sparse_errors_and_switching():
     s.score(scores_out=R_all2)
     assert np.array_equal(R_all.view(np.uint64), R_all2.view(np.uint64))
     s.close()
+
+
+def test_sparse_hub_rows_and_repeatability():
+    """Rows of every length class incl. >= 8192 (CUB segmented sort of the
+    neighbour columns) and 2048..8192 (CTA tables): full parity, and repeated
+    rs_score calls bitwise identical (the row sort is ordered before the forked
+    table bins)."""
+    n, c = 9000, 300
+    rng = np.random.default_rng(5)
+    comm = rng.integers(0, c, n).astype(np.int32)
+    adj = np.zeros((n, n), dtype=bool)
+    adj[0, :] = True                                  # degree n-1 >= 8192
+    adj[1:4, rng.random((3, n)) < 0.4] = True         # ~3600: CTA class
+    m = 60000
+    a_, b_ = rng.integers(0, n, m), rng.integers(0, n, m)
+    adj[a_, b_] = True
+    adj |= adj.T
+    g = gen.from_adjacency(adj, comm)
+    assert np.diff(g.rowptr).max() >= 8192
+    full_all(g, K=25)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, ALL)
+    R = [np.empty(g.n) for _ in range(3)]
+    for r in R:
+        s.score(scores_out=r)
+    _, w1 = s.weights()
+    assert all(np.array_equal(R[0].view(np.uint64), r.view(np.uint64)) for r in R[1:])
+    s.close()
