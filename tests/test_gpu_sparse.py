@@ -162,7 +162,7 @@ def test_sparse_hub_rows_and_repeatability():
     comm = rng.integers(0, c, n).astype(np.int32)
     adj = np.zeros((n, n), dtype=bool)
     adj[0, :] = True                                  # degree n-1 >= 8192
-    adj[1:4, rng.random((3, n)) < 0.4] = True         # ~3600: CTA class
+    adj[1:4] |= rng.random((3, n)) < 0.4              # ~3600: CTA class
     m = 60000
     a_, b_ = rng.integers(0, n, m), rng.integers(0, n, m)
     adj[a_, b_] = True
