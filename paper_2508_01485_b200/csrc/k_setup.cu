@@ -194,6 +194,7 @@ cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *ou
     if (r8192 > 0) {
         int64_t e8 = 0;
         if ((e = cudaMemcpy(&e8, c.rowptr + r8192, sizeof(int64_t), cudaMemcpyDeviceToHost))) return e;
+        if (e8 > 0x7fffffff) return cudaErrorInvalidValue;   // CUB item counts are int
         const int32_t *src = in;
         if (map) {
             // mapped keys of the long rows, staged at the front of tmp
@@ -231,11 +232,12 @@ size_t relabel_arena_bytes(int64_t n, int64_t nnz) {
     cub::DeviceRadixSort::SortPairsDescending(nullptr, need_sort, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                               (int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, 32);
     cub::DeviceScan::ExclusiveSum(nullptr, need_scan, (int64_t *)nullptr, (int64_t *)nullptr, (int)(n + 1));
-    cub::DeviceSegmentedSort::SortKeys(nullptr, need_seg, (int32_t *)nullptr, (int32_t *)nullptr, nnz, (int)n,
-                                       (int64_t *)nullptr, (int64_t *)nullptr);
+    // CUB's segmented radix sort takes int item counts: it only ever sorts the
+    // rows of >= 8192 entries (sort_rows), whose total must stay below 2^31
+    const int seg_items = (int)std::min<int64_t>(nnz, 0x7fffffff);
     size_t need_rad = 0;
-    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, need_rad, (int32_t *)nullptr, (int32_t *)nullptr, nnz, (int)n,
-                                            (int64_t *)nullptr, (int64_t *)nullptr, 0, 32);
+    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, need_rad, (int32_t *)nullptr, (int32_t *)nullptr, seg_items,
+                                            (int)n, (int64_t *)nullptr, (int64_t *)nullptr, 0, 32);
     const size_t cub_b = std::max(std::max(need_sort, need_scan), std::max(need_seg, need_rad));
     return 3 * (4 * (size_t)n + 256) + (8 * (size_t)(n + 1) + 256) + (4 * (size_t)std::max<int64_t>(nnz, 1) + 256) +
            cub_b + 256;
