@@ -46,6 +46,10 @@ constexpr int kQCapE = 160;      // candidate queue (31 + 32 * kPiece < 160)
 constexpr int kPsWords = 128;    // piece-start bitmap: items of at most 4096 pieces (else binary search)
 constexpr int kSlotMaxHits = 4096;   // smem limbs of an x slot take at most this many terms
 constexpr int kWarpsE = 8;
+#ifndef RS_EXP_QBATCH
+#define RS_EXP_QBATCH 2
+#endif
+constexpr int kQBatch = RS_EXP_QBATCH;   // heavy work items per queue pop
 
 // membership filter bit of z (top 12 bits of a multiplicative hash)
 __device__ __forceinline__ uint32_t bm_bit(int32_t z) {
@@ -213,13 +217,17 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
     // the next item's index and its 32-byte record (word `lane` of it in lanes
     // 0-7) are fetched while the current item is processed
     const int32_t *items_w = reinterpret_cast<const int32_t *>(it.items);
+    // items are popped kQBatch at a time: one same-address atomic per batch (the
+    // queue counter is the one address every warp of the grid updates)
     unsigned long long qnext = 0;
-    if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);
-    unsigned long long qi = __shfl_sync(0xffffffffu, qnext, 0);
+    if (lane == 0) qnext = atomicAdd(queue_ctr, (unsigned long long)kQBatch);
+    unsigned long long qbase = __shfl_sync(0xffffffffu, qnext, 0);
+    unsigned long long qi = qbase;
     int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
     for (;;) {
         if (qi >= n_items) break;
-        if (lane == 0) qnext = atomicAdd(queue_ctr, 1ull);   // next item
+        const bool last_of_batch = qi - qbase == (unsigned long long)(kQBatch - 1);
+        if (last_of_batch && lane == 0) qnext = atomicAdd(queue_ctr, (unsigned long long)kQBatch);   // next batch
         // EItem words: by (0, 1), y (2), chunk (3), pyl (4), pm (5), pyt (6)
         const int64_t by = (int64_t)(uint32_t)__shfl_sync(0xffffffffu, rec, 0) |
                            ((int64_t)__shfl_sync(0xffffffffu, rec, 1) << 32);
@@ -276,7 +284,12 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             }
         }
         // the next item's record, in flight during this item
-        qi = __shfl_sync(0xffffffffu, qnext, 0);
+        if (last_of_batch) {
+            qbase = __shfl_sync(0xffffffffu, qnext, 0);
+            qi = qbase;
+        } else {
+            qi++;
+        }
         rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
         // the item's predecessors x. A triangle carries a term only if two of its
         // vertices are targets: with both x and y targets every z < y of P+(x) is
