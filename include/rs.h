@@ -207,6 +207,17 @@ rs_status rs_get_pred(rs_ctx *ctx, int64_t *pred_off_out, int32_t *pred_out, int
  * Requires rs_score. */
 rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_t *type2_out);
 
+/* All-communities mode only (RS_ALL_COMMUNITIES; RS_ESTATE otherwise): the
+ * per-vertex sparse rows of the Step 2a/2b tables (Eq. 3, Eq. 5),
+ * vertices in original order, each row's nonzero columns ascending (column i =
+ * rs_get_targets()[i]). off_out int64[n+1] (row v = [off[v], off[v+1])),
+ * cols_out / cnt_out int32[E], omega_out double[E] (omega_v(column)),
+ * omega_abs_out double[n] (omega_v(c) of every column absent from the row);
+ * any pointer may be NULL; n_entries_out receives E (query it first with the
+ * arrays NULL to size them). Requires rs_score. */
+rs_status rs_get_comm_tables(rs_ctx *ctx, int64_t *off_out, int32_t *cols_out, int32_t *cnt_out, double *omega_out,
+                             double *omega_abs_out, int64_t *n_entries_out);
+
 /* Target communities in column order (int32[k]) and k. Requires communities.
  * In the all-communities mode k can be large: query k with targets_out = NULL. */
 rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out);

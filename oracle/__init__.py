@@ -59,6 +59,10 @@ def _load():
         lib.oracle_mix64.argtypes = [ctypes.c_uint64]
         lib.oracle_awcc_removal.restype = i64
         lib.oracle_awcc_removal.argtypes = [i64, _P, _P, _P, _P, i64, i32, i32, i32, i32, ctypes.c_uint64, _P, _P]
+        lib.oracle_tables_all.restype = i64
+        lib.oracle_tables_all.argtypes = [i64, _P, _P, _P, i32, _P, _P, _P, _P, _P, _P, _P]
+        lib.oracle_rsi_all.argtypes = [i64, _P, _P, _P, i32, _P, _P, _P, _P, _P, ctypes.c_double, i64, _P, _P, _P,
+                                       _P]
         _lib = lib
     return _lib
 
@@ -239,3 +243,46 @@ def run(g, k=None, targets=None, K=25, heads=None) -> OracleResult:
     R, nI, nII = rsi(g, targets, w, wmax, heads)
     ids, sc = topk(R, K)
     return OracleResult(targets, b, f, T, w, wmax, off, pl, R, nI, nII, ids, sc)
+
+
+# ---- NEXT-2: every community a target, rows kept as their nonzero columns ----
+@dataclass
+class TablesAll:
+    targets: np.ndarray     # int32[k]: all communities, size desc / id asc (column order)
+    off: np.ndarray         # int64[n+1]
+    cols: np.ndarray        # int32[E]: nonzero columns of each row, ascending
+    cnt: np.ndarray         # int32[E]: f_u(column)
+    omega: np.ndarray       # f64[E]: omega_u(column)
+    omega_abs: np.ndarray   # f64[n]: omega_u(c) of every absent column c
+    omega_max: float
+
+
+def tables_all(g):
+    """O2-O4 with targets = all communities (oracle_tables_all)."""
+    k = len(np.unique(g.comm))
+    t = select_targets(g.comm, k)
+    rp, cl, cm = _c(g.rowptr, np.int64), _c(g.col, np.int32), _c(g.comm, np.int32)
+    E = max(g.nnz, 1)
+    off = np.zeros(g.n + 1, dtype=np.int64)
+    cols = np.zeros(E, dtype=np.int32)
+    cnt = np.zeros(E, dtype=np.int32)
+    om = np.zeros(E, dtype=np.float64)
+    oa = np.zeros(g.n, dtype=np.float64)
+    wm = ctypes.c_double(0.0)
+    tot = _load().oracle_tables_all(g.n, _ptr(rp), _ptr(cl), _ptr(cm), k, _ptr(t), _ptr(off), _ptr(cols), _ptr(cnt),
+                                    _ptr(om), _ptr(oa), ctypes.byref(wm))
+    return TablesAll(t, off, cols[:tot].copy(), cnt[:tot].copy(), om[:tot].copy(), oa, float(wm.value))
+
+
+def rsi_all(g, tab, heads):
+    """O5-O7 with targets = all on the given heads (oracle_rsi_all)."""
+    heads = _c(heads, np.int64)
+    nh = heads.size
+    R = np.zeros(nh, dtype=np.float64)
+    nI = np.zeros(nh, dtype=np.int64)
+    nII = np.zeros(nh, dtype=np.int64)
+    rp, cl, cm = _c(g.rowptr, np.int64), _c(g.col, np.int32), _c(g.comm, np.int32)
+    _load().oracle_rsi_all(g.n, _ptr(rp), _ptr(cl), _ptr(cm), tab.targets.size, _ptr(tab.targets), _ptr(tab.off),
+                           _ptr(tab.cols), _ptr(tab.omega), _ptr(tab.omega_abs), tab.omega_max, nh, _ptr(heads),
+                           _ptr(R), _ptr(nI), _ptr(nII))
+    return R, nI, nII

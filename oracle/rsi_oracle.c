@@ -303,6 +303,131 @@ void oracle_rsi(int64_t n, const int64_t *rowptr, const int32_t *col, const int3
     free(cols); free(mark);
 }
 
+/* ---- NEXT-2: every community a target (DESIGN reading C-32).
+ * Exactly O2-O4 and O5-O7 above with targets = all k distinct communities
+ * (column i = targets[i], oracle_select_targets order), except that each row of
+ * the n*k histogram is kept as its nonzero columns only -- a dense table is
+ * O(n * #communities). A column with f = 0 is still a cell: Eq.3 with Y = T
+ * (the whole row's entropy) times (L_all - 1), the same for every absent
+ * column of the row (omega_abs_out[u]); omega_max runs over all n*k cells
+ * (C-7), i.e. the present cells and, when L_all < k, the absent one. The
+ * present weights sum j ascending over the nonzero columns, the same order as
+ * oracle_weights, so both give identical bits.
+ * Outputs (caller-allocated, nnz = rowptr[n] entries suffice): off_out[n+1],
+ * cols_out / cnt_out / omega_out per (vertex, nonzero column), ascending
+ * columns. Returns the number of entries. ---- */
+int64_t oracle_tables_all(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C, int32_t k,
+                          const int32_t *targets, int64_t *off_out, int32_t *cols_out, int32_t *cnt_out,
+                          double *omega_out, double *omega_abs_out, double *wmax_out) {
+    int32_t cmax = 0;
+    for (int32_t i = 0; i < k; i++) if (targets[i] > cmax) cmax = targets[i];
+    int32_t *colmap = malloc(sizeof(int32_t) * ((size_t)cmax + 1));
+    for (int32_t i = 0; i < k; i++) colmap[targets[i]] = i;
+    int64_t dmax = 0;
+    for (int64_t u = 0; u < n; u++) if (rowptr[u + 1] - rowptr[u] > dmax) dmax = rowptr[u + 1] - rowptr[u];
+    int32_t *tmp = malloc(sizeof(int32_t) * (dmax ? dmax : 1));
+    double wmax = 0.0;
+    int64_t at = 0;
+    for (int64_t u = 0; u < n; u++) {
+        const int64_t d = rowptr[u + 1] - rowptr[u];
+        off_out[u] = at;
+        for (int64_t e = 0; e < d; e++) tmp[e] = colmap[C[col[rowptr[u] + e]]];
+        qsort(tmp, (size_t)d, sizeof(int32_t), cmp_i32);
+        const int64_t b = at;
+        for (int64_t e = 0; e < d; e++) {                 /* nonzero columns, ascending */
+            if (e == 0 || tmp[e] != tmp[e - 1]) { cols_out[at] = tmp[e]; cnt_out[at] = 0; at++; }
+            cnt_out[at - 1]++;
+        }
+        const int32_t L_all = (int32_t)(at - b);
+        const double T = (double)d;                        /* every neighbour is in a target */
+        for (int64_t i = b; i < at; i++) {                 /* Eq.3 / Eq.5 for a present column */
+            if (L_all <= 1) { omega_out[i] = 0.0; continue; }
+            const double Y = T - (double)cnt_out[i];
+            double H = 0.0;
+            for (int64_t j = b; j < at; j++) {
+                if (j == i) continue;
+                const double p = (double)cnt_out[j] / Y;
+                H -= p * log2(p);
+            }
+            omega_out[i] = H * (double)(L_all - 1);
+            if (omega_out[i] > wmax) wmax = omega_out[i];
+        }
+        double wabs = 0.0;                                 /* every absent column: Y = T */
+        if (L_all > 1) {
+            double H = 0.0;
+            for (int64_t j = b; j < at; j++) {
+                const double p = (double)cnt_out[j] / T;
+                H -= p * log2(p);
+            }
+            wabs = H * (double)(L_all - 1);
+        }
+        omega_abs_out[u] = wabs;
+        if (L_all < k && wabs > wmax) wmax = wabs;
+    }
+    off_out[n] = at;
+    *wmax_out = wmax;
+    free(tmp);
+    free(colmap);
+    return at;
+}
+
+/* omega_v(c) from the row tables of oracle_tables_all */
+static double omega_all(const int64_t *off, const int32_t *cols, const double *omega, const double *omega_abs,
+                        int64_t v, int32_t c) {
+    int64_t lo = off[v], hi = off[v + 1];
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (cols[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    return (lo < off[v + 1] && cols[lo] == c) ? omega[lo] : omega_abs[v];
+}
+
+/* O5-O7 with targets = all (every col(x) defined), weights from the row tables:
+ * the same enumeration, factors and exact sum as oracle_rsi. */
+void oracle_rsi_all(int64_t n, const int64_t *rowptr, const int32_t *col, const int32_t *C, int32_t k,
+                    const int32_t *targets, const int64_t *off, const int32_t *cols, const double *omega,
+                    const double *omega_abs, double wmax, int64_t nh, const int64_t *heads, double *R_out,
+                    int64_t *nI_out, int64_t *nII_out) {
+    int32_t cmax = 0;
+    for (int32_t i = 0; i < k; i++) if (targets[i] > cmax) cmax = targets[i];
+    int32_t *colmap = malloc(sizeof(int32_t) * ((size_t)cmax + 1));
+    for (int32_t i = 0; i < k; i++) colmap[targets[i]] = i;
+    int64_t *mark = malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int64_t x = 0; x < n; x++) mark[x] = -1;
+    for (int64_t h = 0; h < nh; h++) {
+        const int64_t u = heads[h];
+        const int64_t d = rowptr[u + 1] - rowptr[u];
+        const int32_t cu = colmap[C[u]];
+        R_out[h] = 0.0; nI_out[h] = 0; nII_out[h] = 0;
+        if (d < 2) continue;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) mark[col[e]] = u;
+        i128 S = 0;
+        int64_t nI = 0, nII = 0;
+        for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) {
+            const int32_t w = col[e];
+            if (C[w] == C[u]) continue;
+            for (int64_t e2 = rowptr[w]; e2 < rowptr[w + 1]; e2++) {
+                const int32_t v = col[e2];
+                if (v == u || C[v] == C[w]) continue;
+                int32_t cv;
+                if (C[v] == C[u]) { cv = cu; nII++; }
+                else if (mark[v] == u) { cv = colmap[C[v]]; nI++; }
+                else continue;
+                const double f1 = omega_all(off, cols, omega, omega_abs, v, cu);
+                const double f2 = omega_all(off, cols, omega, omega_abs, w, cv);
+                const double f3 = omega_all(off, cols, omega, omega_abs, w, cu);
+                if (wmax <= 0.0 || f1 == 0.0 || f2 == 0.0 || f3 == 0.0) continue;
+                const double t = cbrt((f1 / wmax) * (f2 / wmax) * (f3 / wmax));
+                S += quantize80(t);
+            }
+        }
+        nI_out[h] = nI; nII_out[h] = nII;
+        R_out[h] = wmax > 0.0 ? from_fixed80(S) / ((double)d * (double)(d - 1)) : 0.0;
+    }
+    free(colmap);
+    free(mark);
+}
+
 /* ---- O8. Top-K (Algorithm 1 optional Step 4): the K highest R,
  * ties by ascending vertex id (C-14: zeros eligible, K clamped to n). ---- */
 typedef struct { double r; int32_t id; } scored;

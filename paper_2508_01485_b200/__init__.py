@@ -64,6 +64,7 @@ SIGNATURES = [
     ("rs_set_communities", ctypes.c_int, [_P, _P, _P, ctypes.c_int32]),
     ("rs_score", ctypes.c_int, [_P, _P, ctypes.POINTER(rs_stats), ctypes.c_uint32]),
     ("rs_topk", ctypes.c_int, [_P, ctypes.c_int64, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
+    ("rs_get_comm_tables", ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
     ("rs_get_counts", ctypes.c_int, [_P, _P, _P]),
     ("rs_get_weights", ctypes.c_int, [_P, _P, _P]),
     ("rs_get_border", ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int64)]),
@@ -226,6 +227,21 @@ def rs_get_triad_counts(ctx, n):
     return t1, t2
 
 
+def rs_get_comm_tables(ctx, n):
+    """All-communities mode: (off int64[n+1], cols int32[E], cnt int32[E], omega f64[E], omega_abs f64[n])."""
+    lib = load_library()
+    E = ctypes.c_int64(0)
+    _check(ctx, lib.rs_get_comm_tables(ctx, None, None, None, None, None, ctypes.byref(E)))
+    off = np.empty(n + 1, dtype=np.int64)
+    cols = np.empty(max(E.value, 1), dtype=np.int32)
+    cnt = np.empty(max(E.value, 1), dtype=np.int32)
+    om = np.empty(max(E.value, 1), dtype=np.float64)
+    oa = np.empty(n, dtype=np.float64)
+    _check(ctx, lib.rs_get_comm_tables(ctx, _ptr(off), _ptr(cols), _ptr(cnt), _ptr(om), _ptr(oa), ctypes.byref(E)))
+    e = E.value
+    return off, cols[:e], cnt[:e], om[:e], oa
+
+
 def rs_get_targets(ctx):
     k = ctypes.c_int32(0)
     _check(ctx, load_library().rs_get_targets(ctx, None, ctypes.byref(k)))
@@ -359,6 +375,9 @@ class Scorer:
 
     def triad_counts(self):
         return rs_get_triad_counts(self.ctx, self.n)
+
+    def comm_tables(self):
+        return rs_get_comm_tables(self.ctx, self.n)
 
     def targets(self):
         return rs_get_targets(self.ctx)

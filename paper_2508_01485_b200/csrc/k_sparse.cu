@@ -496,6 +496,53 @@ cudaError_t launch_sparse_weights_dense(Ctx &c, const double *l2t, int64_t l2n, 
     return cudaGetLastError();
 }
 
+// the sparse tables themselves in original vertex order (rs_get_comm_tables):
+// row lengths, offsets by scan, then columns / counts / weights per row
+__global__ void k_sp_len(const SRec *__restrict__ srec, const int32_t *__restrict__ perm, int64_t n, int64_t *len) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        len[perm[u]] = srec[u].L;
+}
+__global__ void k_sp_export(const SRec *__restrict__ srec, const int2 *__restrict__ ctk,
+                            const double *__restrict__ xsum, const int64_t *__restrict__ rowptr,
+                            const int32_t *__restrict__ perm, const int64_t *__restrict__ off,
+                            const double *__restrict__ l2t, int64_t l2n, int64_t n, int32_t *cols, int32_t *cnt,
+                            double *omega, double *omega_abs) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        const SRec r = srec[u];
+        const int64_t o = perm[u], dst = off[o];
+        const int64_t d = rowptr[u + 1] - rowptr[u];
+        const double X = xsum[u];
+        for (int j = 0; j < r.L; j++) {
+            const int2 t = ctk[r.beg + j];
+            if (cols) cols[dst + j] = t.x;
+            if (cnt) cnt[dst + j] = t.y;
+            if (omega) omega[dst + j] = sp_weight(l2t, l2n, t.y, d, r.L, X);
+        }
+        if (omega_abs) omega_abs[o] = sp_weight(l2t, l2n, 0, d, r.L, X);
+    }
+}
+cudaError_t launch_sparse_offsets(Ctx &c, int64_t *off_dev, int64_t *total) {
+    int64_t *len = (int64_t *)c.scratch;
+    void *tmp = (void *)(((uintptr_t)(len + c.n + 1) + 255) & ~(uintptr_t)255);
+    const size_t used = (size_t)((char *)tmp - (char *)c.scratch);
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, len, off_dev, (int)(c.n + 1), c.stream);
+    if (used + need > c.scratch_bytes) return cudaErrorMemoryAllocation;
+    cudaMemsetAsync(len + c.n, 0, sizeof(int64_t), c.stream);
+    k_sp_len<<<148 * 4, 256, 0, c.stream>>>(c.srec, c.perm, c.n, len);
+    cub::DeviceScan::ExclusiveSum(tmp, need, len, off_dev, (int)(c.n + 1), c.stream);
+    c.launches += 2;
+    cudaMemcpyAsync(total, off_dev + c.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+    return cudaStreamSynchronize(c.stream);
+}
+cudaError_t launch_sparse_export(Ctx &c, const int64_t *off_dev, const double *l2t, int64_t l2n, int32_t *cols,
+                                 int32_t *cnt, double *omega, double *omega_abs) {
+    k_sp_export<<<148 * 4, 256, 0, c.stream>>>(c.srec, c.ctk, c.xsum, c.rowptr, c.perm, off_dev, l2t, l2n, c.n, cols,
+                                              cnt, omega, omega_abs);
+    c.launches++;
+    return cudaGetLastError();
+}
+
 // n_II in original order (owned heads; 0 elsewhere)
 __global__ void k_sp_type2(const unsigned long long *__restrict__ n2s, const int32_t *__restrict__ perm, int64_t n,
                            int64_t lo, int64_t hi, int64_t *out) {

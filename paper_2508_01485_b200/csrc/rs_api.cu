@@ -891,6 +891,37 @@ extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_
     return RS_OK;
 }
 
+extern "C" rs_status rs_get_comm_tables(rs_ctx *ctx, int64_t *off_out, int32_t *cols_out, int32_t *cnt_out,
+                                        double *omega_out, double *omega_abs_out, int64_t *n_entries_out) {
+    if (!ctx) return RS_EINVAL;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_comm_tables: call rs_score first");
+    if (!c.sparse) return fail(ctx, RS_ESTATE, "rs_get_comm_tables: needs the RS_ALL_COMMUNITIES mode");
+    int64_t *off = nullptr;
+    CK(cudaMalloc(&off, sizeof(int64_t) * (size_t)(c.n + 1)));
+    int64_t tot = 0;
+    cudaError_t e = rs::launch_sparse_offsets(c, off, &tot);
+    int32_t *cols = nullptr, *cnt = nullptr;
+    double *om = nullptr, *oa = nullptr;
+    const size_t E = (size_t)std::max<int64_t>(tot, 1);
+    if (e == cudaSuccess && cols_out) e = cudaMalloc(&cols, sizeof(int32_t) * E);
+    if (e == cudaSuccess && cnt_out) e = cudaMalloc(&cnt, sizeof(int32_t) * E);
+    if (e == cudaSuccess && omega_out) e = cudaMalloc(&om, sizeof(double) * E);
+    if (e == cudaSuccess && omega_abs_out) e = cudaMalloc(&oa, sizeof(double) * (size_t)c.n);
+    if (e == cudaSuccess) e = rs::launch_sparse_export(c, off, ctx->l2t, ctx->l2n, cols, cnt, om, oa);
+    rs_status s = RS_OK;
+    if (e == cudaSuccess && off_out) s = out_copy(ctx, off_out, off, (size_t)(c.n + 1));
+    if (e == cudaSuccess && s == RS_OK && cols_out && tot) s = out_copy(ctx, cols_out, cols, (size_t)tot);
+    if (e == cudaSuccess && s == RS_OK && cnt_out && tot) s = out_copy(ctx, cnt_out, cnt, (size_t)tot);
+    if (e == cudaSuccess && s == RS_OK && omega_out && tot) s = out_copy(ctx, omega_out, om, (size_t)tot);
+    if (e == cudaSuccess && s == RS_OK && omega_abs_out) s = out_copy(ctx, omega_abs_out, oa, (size_t)c.n);
+    cudaFree(off); cudaFree(cols); cudaFree(cnt); cudaFree(om); cudaFree(oa);
+    CK(e);
+    if (n_entries_out) *n_entries_out = tot;
+    return s;
+}
+
 extern "C" rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out) {
     if (!ctx) return RS_EINVAL;
     Ctx &c = ctx->c;

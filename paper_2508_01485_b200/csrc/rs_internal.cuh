@@ -264,6 +264,9 @@ cudaError_t launch_sparse_lists(Ctx &c);
 cudaError_t launch_sparse_counts_dense(Ctx &c, int32_t *f_dev, int32_t *total_dev);
 cudaError_t launch_sparse_weights_dense(Ctx &c, const double *l2t, int64_t l2n, double *w_dev);
 cudaError_t launch_sparse_type2(Ctx &c, int64_t *t2_dev);
+cudaError_t launch_sparse_offsets(Ctx &c, int64_t *off_dev, int64_t *total);
+cudaError_t launch_sparse_export(Ctx &c, const int64_t *off_dev, const double *l2t, int64_t l2n, int32_t *cols,
+                                 int32_t *cnt, double *omega, double *omega_abs);
 cudaError_t launch_minmax_i32(Ctx &c, const int32_t *a, int64_t n, int64_t *mn, int64_t *mx);
 
 }  // namespace rs

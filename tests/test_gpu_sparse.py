@@ -10,7 +10,7 @@ import pytest
 
 import gen
 import oracle
-from rsgpu import compare_full, run_gpu
+from rsgpu import assert_scores_close, compare_full, run_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -178,4 +178,67 @@ def test_sparse_hub_rows_and_repeatability():
         s.score(scores_out=r)
     _, w1 = s.weights()
     assert all(np.array_equal(R[0].view(np.uint64), r.view(np.uint64)) for r in R[1:])
+    s.close()
+
+
+def _check_tables(s, tab):
+    """The GPU's sparse rows against oracle.tables_all: columns and counts
+    bit-exact for every vertex, weights (present and absent) within 1e-10."""
+    off, cols, cnt, om, oa = s.comm_tables()
+    assert np.array_equal(off, tab.off)
+    assert np.array_equal(cols, tab.cols) and np.array_equal(cnt, tab.cnt)
+    for got, want in ((om, tab.omega), (oa, tab.omega_abs)):
+        nz = want != 0
+        assert np.array_equal(got != 0, nz)
+        if nz.any():
+            assert np.max(np.abs(got[nz] - want[nz]) / want[nz]) <= 1e-10
+
+
+@pytest.mark.parametrize("name,scale,n_comm", [("lj", 0.003, 600), ("orkut", 0.004, 2000)])
+def test_comm_tables_getter(name, scale, n_comm):
+    g = gen.config_graph(name, scale=scale, n_comm=n_comm, zipf_s=0.8)
+    tab = oracle.tables_all(g)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, ALL)
+    assert np.array_equal(s.targets(), tab.targets)
+    R = np.empty(g.n)
+    st = s.score(scores_out=R, stats=True)
+    assert abs(st["omega_max"] - tab.omega_max) <= 1e-10 * tab.omega_max
+    _check_tables(s, tab)
+    heads = np.arange(g.n)
+    Ro, nI, nII = oracle.rsi_all(g, tab, heads)
+    assert_scores_close(Ro, R)
+    t1, t2 = s.triad_counts()
+    assert np.array_equal(nI, t1) and np.array_equal(nII, t2)
+    s.close()
+
+
+def test_full_size_all_communities_sampled():
+    """The bench's NEXT-2 workload (bench.SPARSE_CFG: LiveJournal shape, 10 000
+    communities) in its launch configuration: every vertex's sparse row (columns,
+    counts, weights), omega_max and borders against the oracle, scores and triad
+    counts on sampled heads (random + the GPU's top-25 + the highest degrees),
+    and the top-K property on the sample."""
+    from bench import SPARSE_CFG
+    g = gen.config_graph(SPARSE_CFG["base"], n_comm=SPARSE_CFG["n_comm"], zipf_s=SPARSE_CFG["zipf_s"])
+    tab = oracle.tables_all(g)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, ALL)
+    assert np.array_equal(s.targets(), tab.targets)
+    R = np.empty(g.n)
+    st = s.score(scores_out=R, stats=True)
+    assert abs(st["omega_max"] - tab.omega_max) <= 1e-10 * tab.omega_max
+    _check_tables(s, tab)
+    assert np.array_equal(np.nonzero(oracle.border(g))[0].astype(np.int32), s.border())
+    top_ids, top_sc = s.topk(25)
+    t1, t2 = s.triad_counts()
+    rng = np.random.default_rng(7)
+    deg = np.diff(g.rowptr)
+    heads = np.unique(np.concatenate([rng.integers(0, g.n, 400), top_ids.astype(np.int64), np.argsort(deg)[-20:]]))
+    Ro, nI, nII = oracle.rsi_all(g, tab, heads)
+    assert_scores_close(Ro, R[heads])
+    assert np.array_equal(nI, t1[heads]) and np.array_equal(nII, t2[heads])
+    assert np.all(Ro[~np.isin(heads, top_ids)] <= top_sc[-1] * (1 + 1e-9))
     s.close()

@@ -308,3 +308,46 @@ def test_all_communities_vs_bruteforce(n, c, seed):
     assert r.omega_max == pytest.approx(b["omega_max"], rel=1e-13)
     assert np.array_equal(r.nI, b["nI"]) and np.array_equal(r.nII, b["nII"])
     np.testing.assert_allclose(r.R, b["R"], rtol=1e-12, atol=0)
+
+
+def _dense_from_tables(tab, n):
+    k = tab.targets.size
+    f = np.zeros((n, k), dtype=np.int32)
+    w = np.repeat(tab.omega_abs[:, None], k, axis=1)
+    rows = np.repeat(np.arange(n), np.diff(tab.off))
+    f[rows, tab.cols] = tab.cnt
+    w[rows, tab.cols] = tab.omega
+    return f, w
+
+
+@pytest.mark.parametrize("n,c,seed", [(60, 20, 1), (120, 50, 2), (200, 100, 3), (150, 150, 4), (300, 6, 5)])
+def test_tables_all_vs_dense_and_bruteforce(n, c, seed):
+    """oracle_tables_all / oracle_rsi_all (row tables, targets = all) against the
+    dense oracle (identical bits: same sums in the same order) and the brute force."""
+    rng = np.random.default_rng(seed + 4000)
+    g = gen.planted_partition(n, c, p_in=float(rng.uniform(0.3, 0.8)), p_out=float(rng.uniform(0.03, 0.1)),
+                              seed=seed + 4100)
+    tab = oracle.tables_all(g)
+    k = tab.targets.size
+    r = oracle.run(g, k=k, K=5)
+    assert np.array_equal(tab.targets, r.targets)
+    f, w = _dense_from_tables(tab, g.n)
+    assert np.array_equal(f, r.f)
+    assert np.array_equal(w, r.omega)
+    assert tab.omega_max == r.omega_max
+    R, nI, nII = oracle.rsi_all(g, tab, np.arange(g.n))
+    assert np.array_equal(R, r.R) and np.array_equal(nI, r.nI) and np.array_equal(nII, r.nII)
+    b = brute(g, r.targets)
+    np.testing.assert_allclose(R, b["R"], rtol=1e-12, atol=0)
+    assert np.array_equal(nI, b["nI"]) and np.array_equal(nII, b["nII"])
+
+
+def test_tables_all_singletons():
+    c = 300
+    g = gen.from_adjacency(np.ones((c, c), dtype=bool), list(range(c)))
+    tab = oracle.tables_all(g)
+    assert tab.omega_max == pytest.approx((c - 2) * math.log2(c - 1), rel=1e-14)
+    np.testing.assert_allclose(tab.omega_abs, (c - 2) * math.log2(c - 1), rtol=1e-14)
+    np.testing.assert_allclose(tab.omega, (c - 2) * math.log2(c - 2), rtol=1e-14)
+    R, nI, nII = oracle.rsi_all(g, tab, np.arange(0, c, 37))
+    np.testing.assert_allclose(R, math.log2(c - 2) / math.log2(c - 1), rtol=1e-13)
