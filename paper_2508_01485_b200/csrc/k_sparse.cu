@@ -112,8 +112,7 @@ struct SpArgs {
     int64_t vlo, nverts, n, nc;
     double wide_bound;
     SRec *__restrict__ srec;
-    int2 *__restrict__ ctk;
-    double *__restrict__ cta;
+    CtEnt *__restrict__ ctk;
     ulonglong2 *__restrict__ ctb;
     double *__restrict__ aself;
     double *__restrict__ xsum;          // X(u) = sum_c f log2 f (getters recompute weights from it)
@@ -144,16 +143,6 @@ __device__ __forceinline__ double sp_weight(const double *l2t, int64_t l2n, int 
     return w > 0.0 ? w : 0.0;
 }
 
-// position of column c in the ascending table t[0, len) (present by construction)
-__device__ __forceinline__ int ct_find(const int2 *t, int len, int c) {
-    int lo = 0, hi = len;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(&t[mid].x) < c) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
 template <class GR>
 __device__ __forceinline__ double sp_table_vertex(const SpArgs &a, int64_t u, GR &g) {
     const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
@@ -171,7 +160,10 @@ __device__ __forceinline__ double sp_table_vertex(const SpArgs &a, int64_t u, GR
         }
         int tot;
         const int r = g.rank(st, &tot);
-        if (st) a.ctk[beg + L + r] = make_int2(s, (int)(e - beg));
+        if (st) {
+            a.ctk[beg + L + r].x = s;
+            a.ctk[beg + L + r].y = (int)(e - beg);
+        }
         L += tot;
     }
     g.sync();
@@ -198,13 +190,13 @@ __device__ __forceinline__ double sp_table_vertex(const SpArgs &a, int64_t u, GR
     double as = 0.0;
     int found = 0;
     for (int j = (int)g.lane; j < L; j += GR::size) {
-        const int2 t = a.ctk[beg + j];
-        const double w = sp_weight(a.l2t, a.l2n, t.y, d, L, X);
+        const int tx = a.ctk[beg + j].x, ty = a.ctk[beg + j].y;
+        const double w = sp_weight(a.l2t, a.l2n, ty, d, L, X);
         const double ac = w > 0.0 ? cbrt(w) : 0.0;
-        a.cta[beg + j] = ac;
+        a.ctk[beg + j].a = ac;
         a.ctb[beg + j] = make_ulonglong2(0ull, 0ull);
         wmax = w > wmax ? w : wmax;
-        if (t.x == cu) { as = ac; found = 1; }
+        if (tx == cu) { as = ac; found = 1; }
     }
     as = g.sum(as);           // at most one lane holds a non-zero value: exact
     found = g.sum(found);
@@ -317,8 +309,8 @@ __device__ __forceinline__ void sp_lists_vertex(const SpArgs &a, int64_t u, GR &
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int64_t p = sx[j].beg + lo_r[j];
-            ao[j] = fr[j] ? __ldg(a.cta + beg + lo_o[j]) : 0.0;   // a_u(c_x)
-            ar[j] = fr[j] ? __ldg(a.cta + p) : 0.0;               // a_x(c_u)
+            ao[j] = fr[j] ? __ldg(&a.ctk[beg + lo_o[j]].a) : 0.0;   // a_u(c_x)
+            ar[j] = fr[j] ? __ldg(&a.ctk[p].a) : 0.0;               // a_x(c_u)
             cr[j] = fr[j] ? __ldg(&a.ctk[p].y) : 1;               // f_x(c_u)
         }
 #pragma unroll
@@ -382,7 +374,7 @@ static SpArgs sp_args(Ctx &c, const double *l2t, int64_t l2n) {
     a.vlo = 0; a.nverts = 0; a.n = c.n; a.nc = c.k;
     const int keff = (int)std::max<int64_t>(2, std::min<int64_t>((int64_t)c.k, c.d_max + 1));
     a.wide_bound = wide_bound(keff);
-    a.srec = c.srec; a.ctk = c.ctk; a.cta = c.cta; a.ctb = c.ctb; a.aself = c.aself; a.xsum = c.xsum;
+    a.srec = c.srec; a.ctk = c.ctk; a.ctb = c.ctb; a.aself = c.aself; a.xsum = c.xsum;
     a.pidx = c.pidx; a.wps = c.wps; a.pwr = c.pwr; a.prv = c.prv; a.vrec = c.vrec; a.pc2 = c.pc2; a.n2s = c.n2s;
     a.scal = c.scal;
     return a;
@@ -450,7 +442,7 @@ cudaError_t launch_sparse_lists(Ctx &c) {
 // ------------------------------------------------------------ getters (dense views)
 // counts f[v][c] (original vertex order, column order = rs_get_targets) and
 // T(v) = d(v); the output is zeroed by the caller
-__global__ void k_sp_counts_dense(const SRec *__restrict__ srec, const int2 *__restrict__ ctk,
+__global__ void k_sp_counts_dense(const SRec *__restrict__ srec, const CtEnt *__restrict__ ctk,
                                   const int64_t *__restrict__ rowptr, const int32_t *__restrict__ perm, int64_t n,
                                   int64_t k, int32_t *f, int32_t *total) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
@@ -458,7 +450,7 @@ __global__ void k_sp_counts_dense(const SRec *__restrict__ srec, const int2 *__r
         const int64_t o = perm[u];
         if (f)
             for (int j = 0; j < r.L; j++) {
-                const int2 t = ctk[r.beg + j];
+                const CtEnt t = ctk[r.beg + j];
                 f[o * k + t.x] = t.y;
             }
         if (total) total[o] = (int32_t)(rowptr[u + 1] - rowptr[u]);
@@ -472,7 +464,7 @@ cudaError_t launch_sparse_counts_dense(Ctx &c, int32_t *f_dev, int32_t *total_de
 
 // weights omega[v][c] for every cell (absent columns: the row's f = 0 weight),
 // from the same X and expression Step 2b used
-__global__ void k_sp_weights_dense(const SRec *__restrict__ srec, const int2 *__restrict__ ctk,
+__global__ void k_sp_weights_dense(const SRec *__restrict__ srec, const CtEnt *__restrict__ ctk,
                                    const double *__restrict__ xsum, const int64_t *__restrict__ rowptr,
                                    const int32_t *__restrict__ perm, const double *__restrict__ l2t, int64_t l2n,
                                    int64_t n, int64_t k, double *w) {
@@ -484,7 +476,7 @@ __global__ void k_sp_weights_dense(const SRec *__restrict__ srec, const int2 *__
         const double wabs = sp_weight(l2t, l2n, 0, d, r.L, X);
         for (int64_t c = 0; c < k; c++) w[o * k + c] = wabs;
         for (int j = 0; j < r.L; j++) {
-            const int2 t = ctk[r.beg + j];
+            const CtEnt t = ctk[r.beg + j];
             w[o * k + t.x] = sp_weight(l2t, l2n, t.y, d, r.L, X);
         }
     }
@@ -502,7 +494,7 @@ __global__ void k_sp_len(const SRec *__restrict__ srec, const int32_t *__restric
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
         len[perm[u]] = srec[u].L;
 }
-__global__ void k_sp_export(const SRec *__restrict__ srec, const int2 *__restrict__ ctk,
+__global__ void k_sp_export(const SRec *__restrict__ srec, const CtEnt *__restrict__ ctk,
                             const double *__restrict__ xsum, const int64_t *__restrict__ rowptr,
                             const int32_t *__restrict__ perm, const int64_t *__restrict__ off,
                             const double *__restrict__ l2t, int64_t l2n, int64_t n, int32_t *cols, int32_t *cnt,
@@ -513,7 +505,7 @@ __global__ void k_sp_export(const SRec *__restrict__ srec, const int2 *__restric
         const int64_t d = rowptr[u + 1] - rowptr[u];
         const double X = xsum[u];
         for (int j = 0; j < r.L; j++) {
-            const int2 t = ctk[r.beg + j];
+            const CtEnt t = ctk[r.beg + j];
             if (cols) cols[dst + j] = t.x;
             if (cnt) cnt[dst + j] = t.y;
             if (omega) omega[dst + j] = sp_weight(l2t, l2n, t.y, d, r.L, X);

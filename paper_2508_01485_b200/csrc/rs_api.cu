@@ -199,7 +199,7 @@ static void free_graph(rs_ctx *ctx) {
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
     dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.wps); dfree(c.pc2); dfree(c.amat);
     dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bql);
-    dfree(c.cid); dfree(c.srec); dfree(c.ctk); dfree(c.cta); dfree(c.ctb); dfree(c.pwr); dfree(c.prv); dfree(c.aself);
+    dfree(c.cid); dfree(c.srec); dfree(c.ctk); dfree(c.ctb); dfree(c.pwr); dfree(c.prv); dfree(c.aself);
     dfree(c.xsum); dfree(c.n2s);
     c.sp_cap = 0;
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
@@ -356,7 +356,7 @@ static rs_status set_communities_all(rs_ctx *ctx, int64_t mx) {
         const int64_t n = c.cap_n, nnz = std::max<int64_t>(c.cap_nnz, 1);
         CK(dalloc(&c.cid, n)); CK(dalloc(&c.srec, n)); CK(dalloc(&c.aself, n)); CK(dalloc(&c.xsum, n));
         CK(dalloc(&c.n2s, n));
-        CK(dalloc(&c.ctk, nnz)); CK(dalloc(&c.cta, nnz)); CK(dalloc(&c.ctb, nnz));
+        CK(dalloc(&c.ctk, nnz)); CK(dalloc(&c.ctb, nnz));
         CK(dalloc(&c.pwr, nnz)); CK(dalloc(&c.prv, nnz));
         c.sp_cap = c.cap_nnz;
     }

@@ -94,6 +94,15 @@ struct __align__(16) SRec {
     int32_t cid;       // column of C(v)
 };
 
+// One entry of a vertex's sparse community table (all-communities mode): the
+// column, its count and a_u(c) = omega_u(c)^(1/3) in one 16-byte record, so the
+// binary search that finds a column also brings its weight.
+struct __align__(16) CtEnt {
+    int32_t x;         // column (community rank)
+    int32_t y;         // f_u(column)
+    double a;          // a_u(column)
+};
+
 struct Bins {
     int64_t count[kNumBins] = {0};
     int64_t offset[kNumBins + 1] = {0};
@@ -150,8 +159,7 @@ struct Ctx {
     int32_t *cid = nullptr;      // n: column of C(u) (internal order)
     int32_t *code32 = nullptr;   // community id -> column (ccap entries)
     SRec *srec = nullptr;        // n: {rowptr, L(u), cid} gathered per neighbour
-    int2 *ctk = nullptr;         // nnz: u's distinct neighbour columns ascending at rowptr[u]: {column, count}
-    double *cta = nullptr;       // nnz: a_u(c) = omega_u(c)^(1/3) beside each column
+    CtEnt *ctk = nullptr;        // nnz: u's distinct neighbour columns ascending at rowptr[u]: {column, f_u(c), a_u(c)}
     ulonglong2 *ctb = nullptr;   // nnz: B_u[c] limbs (fx_red2) beside each column
     double *pwr = nullptr;       // nnz: a_w(c_u) beside each w of P(u) (pidx order); wps holds a_u(c_w)
     int64_t *prv = nullptr;      // nnz: position of c_u in w's table, beside each w of P(u)
