@@ -216,15 +216,24 @@ def main():
     ms_per_step = float(tot.item()) / a.steps
     value = m / (ms_per_step * 1e-3) / 1e9
 
-    # top-k latency (rs_topk alone, device-resident scores -> device ids)
-    tk_ms = []
-    for i in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        sc.topk(a.K, ids_d, sco_d)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        tk_ms.append(e0.elapsed_time(e1))
+    # top-k latency (rs_topk alone, device-resident scores -> device ids), for the
+    # bench's K and SURVEY §8(d)'s K = 5 and K = 1000
+    def topk_ms(K):
+        ib = torch.empty(K, dtype=torch.int32, device=dev)
+        sb = torch.empty(K, dtype=torch.float64, device=dev)
+        sc.topk(K, ib, sb)
+        out = []
+        for i in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sc.topk(K, ib, sb)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            out.append(e0.elapsed_time(e1))
+        return float(np.median(out))
+    tk_ms = [topk_ms(a.K)]
+    tk_more = {f"K={K}": round(topk_ms(K), 4) for K in (5, 1000)}
+    sc.topk(a.K, ids_d, sco_d)
 
     # per-phase split of one step (stats on), for the roofline of the dominant phase
     ph = []
@@ -338,6 +347,12 @@ def main():
                        "parallelism": f"head-range x{world}" if world > 1 else "single GPU"},
             "roofline": roof,
             "topk_latency_ms": round(float(np.median(tk_ms)), 4),
+            "topk_latency_ms_more": tk_more,
+            # the method's lower bound is one fused pass (col_idx +
+            # a 1-byte label per adjacency entry, offsets / own label / score per
+            # vertex); the step time against that traffic at the HBM roof
+            "lower_bound": {"bytes": int(5 * D + 20 * n), "ms_at_peak": round((5 * D + 20 * n) / (hbm_peak * 1e6), 4),
+                            "frac_of_step": round((5 * D + 20 * n) / (hbm_peak * 1e6) / ms_per_step, 4)},
             "next_awcc_removal": awcc,
             "next_literal_variants": variants,
             "next_shii": shii,
