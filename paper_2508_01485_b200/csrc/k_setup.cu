@@ -72,16 +72,6 @@ __global__ void k_inv_perm(const int32_t *__restrict__ perm, int64_t n, int32_t 
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) d64[n] = 0;
 }
-__global__ void k_relabel_rows(const int64_t *__restrict__ rp_o, const int32_t *__restrict__ col_o,
-                               const int32_t *__restrict__ perm, const int32_t *__restrict__ inv,
-                               const int64_t *__restrict__ rp, int64_t n, int32_t *out) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; r < n;
-         r += ((int64_t)gridDim.x * blockDim.x) / 32) {
-        const int64_t src = perm[r], b = rp_o[src], d = rp_o[src + 1] - b, o = rp[r];
-        for (int64_t i = lane; i < d; i += 32) out[o + i] = inv[col_o[b + i]];
-    }
-}
 // number of vertices with degree >= bin_lo(cls), cls = 1..7 (degrees sorted descending)
 // (out[kNumBins]: degree >= 512, a split point of the row sorts)
 __global__ void k_class_bounds(const uint32_t *__restrict__ deg_s, int64_t n, unsigned long long *out) {
@@ -124,9 +114,39 @@ __global__ void __launch_bounds__(THREADS) k_row_sort(const int64_t *__restrict_
     }
 }
 
-// rows of at most 32 J entries: a warp per row, bitonic sort in registers
-// (element i = 32 j + lane; partners across lanes by shuffle, within a lane by
-// register swap), padding keys 0xFFFFFFFF sort last
+// bitonic sort of 32 J keys held by a warp (element i = 32 j + lane; partners
+// across lanes by shuffle, within a lane by register swap), ascending
+template <int J>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[J], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * J; k <<= 1) {
+#pragma unroll
+        for (int s = k >> 1; s > 0; s >>= 1) {
+            if (s >= 32) {
+#pragma unroll
+                for (int j = 0; j < J; j++) {
+                    const int pj = j ^ (s >> 5);
+                    if (pj > j) {
+                        const bool up = ((32 * j + lane) & k) == 0;
+                        const uint32_t a = v[j], c = v[pj];
+                        if ((a > c) == up) { v[j] = c; v[pj] = a; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < J; j++) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[j], s);
+                    const bool up = ((32 * j + lane) & k) == 0;
+                    const bool low = (lane & s) == 0;
+                    v[j] = (low == up) ? min(v[j], o) : max(v[j], o);
+                }
+            }
+        }
+    }
+}
+
+// rows of at most 32 J entries: a warp per row, bitonic sort in registers,
+// padding keys 0xFFFFFFFF sort last
 template <int J>
 __global__ void __launch_bounds__(256) k_row_sort_warp(const int64_t *__restrict__ rowptr, int64_t r0, int64_t r1,
                                                        const int32_t *__restrict__ in, int32_t *out,
@@ -142,34 +162,86 @@ __global__ void __launch_bounds__(256) k_row_sort_warp(const int64_t *__restrict
             const int i = 32 * j + lane;
             v[j] = i < d ? (uint32_t)(map ? __ldg(map + in[b + i]) : in[b + i]) : 0xFFFFFFFFu;
         }
-#pragma unroll
-        for (int k = 2; k <= 32 * J; k <<= 1) {
-#pragma unroll
-            for (int s = k >> 1; s > 0; s >>= 1) {
-                if (s >= 32) {
-#pragma unroll
-                    for (int j = 0; j < J; j++) {
-                        const int pj = j ^ (s >> 5);
-                        if (pj > j) {
-                            const bool up = ((32 * j + lane) & k) == 0;
-                            const uint32_t a = v[j], c = v[pj];
-                            if ((a > c) == up) { v[j] = c; v[pj] = a; }
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < J; j++) {
-                        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[j], s);
-                        const bool up = ((32 * j + lane) & k) == 0;
-                        const bool low = (lane & s) == 0;
-                        v[j] = (low == up) ? min(v[j], o) : max(v[j], o);
-                    }
-                }
-            }
-        }
+        warp_bitonic<J>(v, lane);
 #pragma unroll
         for (int j = 0; j < J; j++)
             if (32 * j + lane < d) out[b + 32 * j + lane] = (int32_t)v[j];
+    }
+}
+
+// Load time, rows of the ORIGINAL numbering [v0, v1) (a chunk whose col_idx has
+// arrived): each row is relabelled to internal ids and written at its internal
+// position; rows shorter than 512 are sorted right here in registers (a warp per
+// row), longer ones go unsorted to tmp for the class sorts of relabel_finish.
+// Chunks let the host->device copy of col_idx overlap this pass.
+template <int J>
+__device__ __forceinline__ void relabel_sort_row(const int32_t *__restrict__ col_o, const int32_t *__restrict__ inv,
+                                                 int64_t b, int d, int lane, int32_t *out) {
+    uint32_t v[J];
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+        const int i = 32 * j + lane;
+        v[j] = i < d ? (uint32_t)__ldg(inv + __ldg(col_o + b + i)) : 0xFFFFFFFFu;
+    }
+    warp_bitonic<J>(v, lane);
+#pragma unroll
+    for (int j = 0; j < J; j++)
+        if (32 * j + lane < d) out[32 * j + lane] = (int32_t)v[j];
+}
+// rows of 512..8191 entries: a CTA per internal row r in [r0, r1) whose original
+// row perm[r] lies in the chunk [v0, v1): relabel + block radix sort
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) k_relabel_sort_cta(const int64_t *__restrict__ rp_o,
+                                                              const int32_t *__restrict__ col_o,
+                                                              const int32_t *__restrict__ perm,
+                                                              const int32_t *__restrict__ inv,
+                                                              const int64_t *__restrict__ rp, int64_t r0, int64_t r1,
+                                                              int64_t v0, int64_t v1, int32_t *out, int bits) {
+    using BRS = cub::BlockRadixSort<uint32_t, THREADS, ITEMS>;
+    __shared__ typename BRS::TempStorage ts;
+    const uint32_t pad = bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u;
+    for (int64_t r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const int64_t v = perm[r];
+        if (v < v0 || v >= v1) continue;   // CTA-uniform
+        const int64_t b = rp_o[v];
+        const int d = (int)(rp_o[v + 1] - b);
+        const int64_t o = rp[r];
+        uint32_t keys[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const int idx = threadIdx.x * ITEMS + i;
+            keys[i] = idx < d ? (uint32_t)__ldg(inv + __ldg(col_o + b + idx)) : pad;
+        }
+        BRS(ts).Sort(keys, 0, bits);
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const int idx = threadIdx.x * ITEMS + i;
+            if (idx < d) out[o + idx] = (int32_t)keys[i];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_relabel_fused(const int64_t *__restrict__ rp_o, const int32_t *__restrict__ col_o,
+                                                       const int32_t *__restrict__ inv, const int64_t *__restrict__ rp,
+                                                       int64_t v0, int64_t v1, int32_t *tmp, int32_t *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = v0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < v1; v += nw) {
+        const int64_t b = rp_o[v];
+        const int64_t d = rp_o[v + 1] - b;
+        const int64_t o = rp[inv[v]];
+        if (d >= 8192) {
+            for (int64_t i = lane; i < d; i += 32) tmp[o + i] = __ldg(inv + __ldg(col_o + b + i));
+        } else if (d >= 512) {
+            continue;   // k_relabel_sort_cta
+        } else if (d > 128) {
+            relabel_sort_row<16>(col_o, inv, b, (int)d, lane, out + o);
+        } else if (d > 32) {
+            relabel_sort_row<4>(col_o, inv, b, (int)d, lane, out + o);
+        } else if (d > 0) {
+            relabel_sort_row<1>(col_o, inv, b, (int)d, lane, out + o);
+        }
     }
 }
 
@@ -186,10 +258,12 @@ __global__ void k_gather_keys(const int32_t *__restrict__ in, const int32_t *__r
         out[i] = __ldg(map + in[i]);
 }
 
-cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *out, int bits, void *tmp, size_t need) {
-    const int64_t n = c.n;
-    const int64_t r8192 = c.rsplit[0], r2048 = c.rsplit[1], r512 = c.rsplit[2];
-    const int64_t r128 = c.rsplit[3], r32 = c.rsplit[4];
+cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *out, int bits, void *tmp, size_t need,
+                      int64_t upto) {
+    // rows [0, upto) only: the class boundaries are clipped to it
+    const int64_t n = std::min<int64_t>(c.n, upto);
+    const int64_t r8192 = std::min(c.rsplit[0], n), r2048 = std::min(c.rsplit[1], n), r512 = std::min(c.rsplit[2], n);
+    const int64_t r128 = std::min(c.rsplit[3], n), r32 = std::min(c.rsplit[4], n);
     cudaError_t e = cudaSuccess;
     if (r8192 > 0) {
         int64_t e8 = 0;
@@ -243,7 +317,11 @@ size_t relabel_arena_bytes(int64_t n, int64_t nnz) {
            cub_b + 256;
 }
 
-cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, void *arena, size_t arena_bytes) {
+// Internal numbering, in three calls so that a host col_idx can stream in
+// while rows are relabelled (rs_load_csr): prepare (degrees, permutation,
+// internal offsets, degree classes; needs row_offsets only), rows (a chunk of
+// original rows: relabel + sort the short ones), finish (sort the long rows).
+cudaError_t launch_relabel_prepare(Ctx &c, const int64_t *rp_o, void *arena, size_t arena_bytes) {
     const int64_t n = c.n, nnz = c.nnz;
     char *ap = (char *)arena;
     auto carve = [&](size_t b) { void *p = ap; ap += (b + 255) & ~(size_t)255; return p; };
@@ -251,10 +329,12 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, vo
     uint32_t *deg_s = (uint32_t *)carve(4 * (size_t)n);
     int32_t *iota = (int32_t *)carve(4 * (size_t)n);
     int64_t *d64 = (int64_t *)carve(8 * (size_t)(n + 1));
-    int32_t *tmpcol = (int32_t *)carve(4 * (size_t)std::max<int64_t>(nnz, 1));
-    void *tmp = ap;
+    c.rl_tmpcol = (int32_t *)carve(4 * (size_t)std::max<int64_t>(nnz, 1));
+    c.rl_tmp = ap;
     if ((size_t)(ap - (char *)arena) > arena_bytes) return cudaErrorMemoryAllocation;
-    const size_t need = arena_bytes - (size_t)(ap - (char *)arena);
+    c.rl_need = arena_bytes - (size_t)(ap - (char *)arena);
+    void *tmp = c.rl_tmp;
+    const size_t need = c.rl_need;
     cudaError_t e = cudaSuccess;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
     k_deg_iota<<<blocks, 256, 0, c.stream>>>(rp_o, n, deg, iota);
@@ -263,26 +343,19 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, vo
     k_inv_perm<<<blocks, 256, 0, c.stream>>>(c.perm, n, c.inv, deg_s, d64);
     t1 = need;
     cub::DeviceScan::ExclusiveSum(tmp, t1, d64, c.rowptr, (int)(n + 1), c.stream);
-    k_relabel_rows<<<148 * 16, 256, 0, c.stream>>>(rp_o, col_o, c.perm, c.inv, c.rowptr, n, tmpcol);
     k_class_bounds<<<1, 32, 0, c.stream>>>(deg_s, n, c.scal + kScalTk);
-    c.launches += 6;
+    c.launches += 5;
     unsigned long long ge[kNumBins + 1] = {0};
     uint32_t dmax = 0;
     cudaMemcpyAsync(ge, c.scal + kScalTk, sizeof(ge), cudaMemcpyDeviceToHost, c.stream);
     cudaMemcpyAsync(&dmax, deg_s, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream);
     if ((e = cudaStreamSynchronize(c.stream))) return e;
     if ((e = cudaGetLastError())) return e;
-    // every row sorted by internal id (sort_rows below). Keys need log2(n) bits.
     c.rsplit[0] = (int64_t)ge[7];
     c.rsplit[1] = (int64_t)ge[6];
     c.rsplit[2] = (int64_t)ge[kNumBins];
     c.rsplit[3] = (int64_t)ge[5];
     c.rsplit[4] = (int64_t)ge[3];
-    if (nnz) {
-        int bits = 1;
-        while (bits < 31 && (1ll << bits) < n) bits++;
-        if ((e = sort_rows(c, tmpcol, nullptr, c.col, bits, tmp, need))) return e;
-    }
     // ge[cls] = #vertices with degree >= bin_lo(cls); class cls = [ge[cls+1], ge[cls])
     ge[0] = (unsigned long long)n;
     for (int cls = 0; cls < kNumBins; cls++) {
@@ -293,6 +366,44 @@ cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, vo
     }
     c.d_max = dmax;
     return cudaSuccess;
+}
+
+cudaError_t launch_relabel_rows(Ctx &c, const int64_t *rp_o, const int32_t *col_o, int64_t v0, int64_t v1) {
+    if (v1 <= v0) return cudaSuccess;
+    const int64_t warps = v1 - v0;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 16));
+    k_relabel_fused<<<blocks, 256, 0, c.stream>>>(rp_o, col_o, c.inv, c.rowptr, v0, v1, c.rl_tmpcol, c.col);
+    c.launches++;
+    // rows of 512..8191 entries (internal [r8192, r512)) whose original row is in the chunk
+    int bits = 1;
+    while (bits < 31 && (1ll << bits) < c.n) bits++;
+    const int64_t r8192 = c.rsplit[0], r2048 = c.rsplit[1], r512 = c.rsplit[2];
+    auto rows = [&](int64_t lo, int64_t hi) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(hi - lo, 148 * 8)); };
+    if (r2048 > r8192) {
+        k_relabel_sort_cta<256, 32><<<rows(r8192, r2048), 256, 0, c.stream>>>(rp_o, col_o, c.perm, c.inv, c.rowptr,
+                                                                               r8192, r2048, v0, v1, c.col, bits);
+        c.launches++;
+    }
+    if (r512 > r2048) {
+        k_relabel_sort_cta<256, 8><<<rows(r2048, r512), 256, 0, c.stream>>>(rp_o, col_o, c.perm, c.inv, c.rowptr,
+                                                                             r2048, r512, v0, v1, c.col, bits);
+        c.launches++;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_relabel_finish(Ctx &c) {
+    if (!c.nnz || c.rsplit[0] == 0) return cudaSuccess;   // no row of >= 8192 entries
+    int bits = 1;
+    while (bits < 31 && (1ll << bits) < c.n) bits++;
+    return sort_rows(c, c.rl_tmpcol, nullptr, c.col, bits, c.rl_tmp, c.rl_need, c.rsplit[0]);
+}
+
+cudaError_t launch_relabel(Ctx &c, const int64_t *rp_o, const int32_t *col_o, void *arena, size_t arena_bytes) {
+    cudaError_t e = launch_relabel_prepare(c, rp_o, arena, arena_bytes);
+    if (e == cudaSuccess) e = launch_relabel_rows(c, rp_o, col_o, 0, c.n);
+    if (e == cudaSuccess) e = launch_relabel_finish(c);
+    return e;
 }
 
 // ---------------------------------------------------------------- log2 table

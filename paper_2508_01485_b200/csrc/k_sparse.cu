@@ -395,7 +395,7 @@ static void sp_grid(Ctx &c, K kern, int64_t nverts, int gpb, cudaStream_t s, con
 cudaError_t launch_sparse_sort(Ctx &c) {
     int bits = 1;
     while (bits < 31 && (1ll << bits) < (int64_t)c.k) bits++;
-    return sort_rows(c, c.col, c.cid, c.pplus, bits, c.arena, c.arena_bytes);
+    return sort_rows(c, c.col, c.cid, c.pplus, bits, c.arena, c.arena_bytes, c.n);
 }
 
 cudaError_t launch_sparse_tables(Ctx &c, const double *l2t, int64_t l2n) {

@@ -71,6 +71,8 @@ struct rs_ctx {
 };
 
 static std::string g_create_err;
+static constexpr int64_t kPipeMin = 1 << 24;     // pipelined host col_idx copy from this many entries
+static constexpr int64_t kPipeChunk = 1 << 24;   // entries per copied chunk (64 MB)
 
 static rs_status fail(rs_ctx *ctx, rs_status s, const std::string &m) {
     if (ctx) ctx->c.err = m; else g_create_err = m;
@@ -220,6 +222,7 @@ extern "C" void rs_destroy(rs_ctx *ctx) {
         if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
     }
     if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+    for (cudaEvent_t ev : c.ev_chunk) cudaEventDestroy(ev);
     for (int i = 0; i < 8; i++) if (c.ev_phase[i]) cudaEventDestroy(c.ev_phase[i]);
 #ifdef RS_WITH_NCCL
     if (c.comm) NCCL.CommDestroy(c.comm);
@@ -277,10 +280,14 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         CK(cudaMemcpyAsync(rp_tmp, row_offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c.stream));
         rp_o = rp_tmp;
     }
+    // host col_idx without validation: copied in chunks on a side stream while
+    // the rows already there are relabelled (launch_relabel_rows below)
+    const bool pipe = !dev_ci && !dev_ro && !(flags & RS_VALIDATE) && nnz >= (int64_t)kPipeMin;
+    int32_t *col_tmp = nullptr;
     if (!dev_ci) {
-        int32_t *col_tmp = (int32_t *)ap;
+        col_tmp = (int32_t *)ap;
         ap += (4 * (size_t)std::max<int64_t>(nnz, 1) + 255) & ~(size_t)255;
-        if (nnz) CK(cudaMemcpyAsync(col_tmp, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+        if (nnz && !pipe) CK(cudaMemcpyAsync(col_tmp, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
         col_o = col_tmp;
     }
     if (flags & RS_VALIDATE) {
@@ -324,8 +331,42 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         c.cap_n = n;
         c.cap_nnz = nnz;
     }
-    // internal degree-descending numbering (k_setup.cu launch_relabel)
-    CK(rs::launch_relabel(c, rp_o, col_o, ap, c.arena_bytes - (size_t)(ap - (char *)c.arena)));
+    // internal degree-descending numbering (k_setup.cu launch_relabel*)
+    if (pipe) {
+        // chunks of about kPipeChunk entries at original row boundaries
+        std::vector<int64_t> cut{0};
+        for (int64_t v = 0; v < n;) {
+            const int64_t target = row_offsets[v] + (int64_t)kPipeChunk;
+            int64_t w = std::upper_bound(row_offsets + v + 1, row_offsets + n + 1, target) - row_offsets - 1;
+            if (w <= v) w = v + 1;
+            if (w > n) w = n;
+            cut.push_back(w);
+            v = w;
+        }
+        const size_t nch = cut.size() - 1;
+        while (c.ev_chunk.size() < nch) {
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            c.ev_chunk.push_back(ev);
+        }
+        cudaStream_t cs = c.side[rs::kNumBins];
+        CK(cudaEventRecord(c.ev_fork, c.stream));   // the arena is free once earlier work is done
+        CK(cudaStreamWaitEvent(cs, c.ev_fork, 0));
+        for (size_t i = 0; i < nch; i++) {
+            const int64_t e0 = row_offsets[cut[i]], e1 = row_offsets[cut[i + 1]];
+            if (e1 > e0)
+                CK(cudaMemcpyAsync(col_tmp + e0, col_idx + e0, sizeof(int32_t) * (e1 - e0), cudaMemcpyHostToDevice, cs));
+            CK(cudaEventRecord(c.ev_chunk[i], cs));
+        }
+        CK(rs::launch_relabel_prepare(c, rp_o, ap, c.arena_bytes - (size_t)(ap - (char *)c.arena)));
+        for (size_t i = 0; i < nch; i++) {
+            CK(cudaStreamWaitEvent(c.stream, c.ev_chunk[i], 0));
+            CK(rs::launch_relabel_rows(c, rp_o, col_o, cut[i], cut[i + 1]));
+        }
+        CK(rs::launch_relabel_finish(c));
+    } else {
+        CK(rs::launch_relabel(c, rp_o, col_o, ap, c.arena_bytes - (size_t)(ap - (char *)c.arena)));
+    }
     CK(rs::launch_e_items(c));
     const int64_t l2n = std::min<int64_t>(c.d_max + 1, 1ll << 20);
     if (l2n > ctx->l2n) {

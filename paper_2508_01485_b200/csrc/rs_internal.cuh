@@ -133,6 +133,10 @@ struct Ctx {
     int32_t *inv = nullptr;      // n: internal id of original vertex v
     Bins bins;
     int64_t rsplit[5] = {0};     // first row of degree < 8192, 2048, 512, 128, 32 (row-sort classes)
+    int32_t *rl_tmpcol = nullptr;   // load-time temporaries (arena): unsorted long rows,
+    void *rl_tmp = nullptr;         //   CUB scratch
+    size_t rl_need = 0;
+    std::vector<cudaEvent_t> ev_chunk;   // col_idx chunks copied (host input, rs_load_csr)
     int64_t d_max = 0;
     int64_t *e_pre = nullptr;    // Phase E work items: prefix of extra chunks of the e_nbig largest rows
     int64_t e_nbig = 0, e_extra = 0;
@@ -260,7 +264,11 @@ cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int6
 cudaError_t launch_type2_counts(Ctx &c, int64_t *t2_dev);
 cudaError_t launch_type1_export(Ctx &c, int64_t *t1_dev);
 cudaError_t launch_stats(Ctx &c, int64_t out[4]);
-cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *out, int bits, void *tmp, size_t need);
+cudaError_t sort_rows(Ctx &c, const int32_t *in, const int32_t *map, int32_t *out, int bits, void *tmp, size_t need,
+                      int64_t upto);
+cudaError_t launch_relabel_prepare(Ctx &c, const int64_t *rp_o, void *arena, size_t arena_bytes);
+cudaError_t launch_relabel_rows(Ctx &c, const int64_t *rp_o, const int32_t *col_o, int64_t v0, int64_t v1);
+cudaError_t launch_relabel_finish(Ctx &c);
 void launch_comm_hist(Ctx &c, int64_t nbins);
 void launch_nwide(Ctx &c, double bound);
 // all-communities mode (k_sparse.cu)
