@@ -67,6 +67,10 @@ typedef struct {
 
 /* Flags for rs_load_csr. */
 #define RS_VALIDATE   1u   /* check the CSR contract on the device (see rs_load_csr) */
+/* Test hook: copy a host col_idx in chunks of 2^e entries (e = 4..30) with the
+ * rows of each chunk relabelled as it arrives, whatever nnz (by default only
+ * from 2^24 entries, in 2^24-entry chunks). Results must not change. */
+#define RS_LOAD_CHUNK_LOG2(e) ((((uint32_t)(e)) & 0x1Fu) << 8)
 
 /* rs_set_communities: every community is a target (sparse per-vertex tables). */
 #define RS_ALL_COMMUNITIES (-1)

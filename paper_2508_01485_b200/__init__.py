@@ -27,6 +27,11 @@ RS_LITERAL_L, RS_GATE_L, RS_WMAX_EB = 1 << 16, 1 << 17, 1 << 18   # NEXT-3 varia
 RS_ALL_COMMUNITIES = -1   # rs_set_communities k: every community a target (NEXT-2 sparse mode)
 
 
+def RS_LOAD_CHUNK_LOG2(e: int) -> int:
+    """rs_load_csr test hook: pipelined host col_idx copy in chunks of 2^e entries."""
+    return (int(e) & 0x1F) << 8
+
+
 def RS_E_SHARES(s: int) -> int:
     """rs_score test hook: Phase E as s sequential shares of the multi-GPU split."""
     return (int(s) & 0xFF) << 8
@@ -340,8 +345,8 @@ class Scorer:
         except Exception:
             pass
 
-    def load_csr(self, rowptr, col, validate: bool = False):
-        rs_load_csr(self.ctx, rowptr, col, RS_VALIDATE if validate else 0)
+    def load_csr(self, rowptr, col, validate: bool = False, flags: int = 0):
+        rs_load_csr(self.ctx, rowptr, col, (RS_VALIDATE if validate else 0) | flags)
         self.n = int(rowptr.shape[0]) - 1
         self.nnz = int(col.shape[0])
 

@@ -282,7 +282,9 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     }
     // host col_idx without validation: copied in chunks on a side stream while
     // the rows already there are relabelled (launch_relabel_rows below)
-    const bool pipe = !dev_ci && !dev_ro && !(flags & RS_VALIDATE) && nnz >= (int64_t)kPipeMin;
+    const int chunk_log2 = (int)((flags >> 8) & 0x1Fu);   // RS_LOAD_CHUNK_LOG2 test hook
+    const int64_t pipe_chunk = chunk_log2 >= 4 ? (1ll << chunk_log2) : kPipeChunk;
+    const bool pipe = !dev_ci && !dev_ro && !(flags & RS_VALIDATE) && (nnz >= kPipeMin || chunk_log2 >= 4) && nnz > 0;
     int32_t *col_tmp = nullptr;
     if (!dev_ci) {
         col_tmp = (int32_t *)ap;
@@ -336,7 +338,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         // chunks of about kPipeChunk entries at original row boundaries
         std::vector<int64_t> cut{0};
         for (int64_t v = 0; v < n;) {
-            const int64_t target = row_offsets[v] + (int64_t)kPipeChunk;
+            const int64_t target = row_offsets[v] + pipe_chunk;
             int64_t w = std::upper_bound(row_offsets + v + 1, row_offsets + n + 1, target) - row_offsets - 1;
             if (w <= v) w = v + 1;
             if (w > n) w = n;

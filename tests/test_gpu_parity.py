@@ -329,3 +329,34 @@ def test_shii_errors():
         with pytest.raises((rsb.RsError, ValueError)):
             s.shii(**bad)
     s.close()
+
+
+@pytest.mark.parametrize("log2", [4, 7, 12])
+def test_pipelined_load_chunks(log2):
+    """rs_load_csr from host arrays with the col_idx copy cut into chunks of
+    2^log2 entries (rows relabelled and sorted as each chunk arrives, rows of
+    every length class incl. >= 512 and >= 8192): scores and every artefact
+    bitwise identical to the one-piece load."""
+    g = gen.config_graph("orkut", scale=0.004)
+    n = g.n
+    # a hub row of >= 8192 entries so that every sort path runs
+    extra = np.arange(1, min(n, 9000), dtype=np.int64)
+    adj_rows = [set(g.col[g.rowptr[u]:g.rowptr[u + 1]].tolist()) for u in range(n)]
+    for v in extra:
+        adj_rows[0].add(int(v)); adj_rows[int(v)].add(0)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    rowptr[1:] = np.cumsum([len(r) for r in adj_rows])
+    col = np.concatenate([np.array(sorted(r), dtype=np.int32) for r in adj_rows])
+    out = []
+    for flags in (0, rsb.RS_LOAD_CHUNK_LOG2(log2)):
+        s = rsb.Scorer(0)
+        s.load_csr(rowptr, col, flags=flags)
+        s.set_communities(g.comm, 5)
+        R = np.empty(n)
+        s.score(scores_out=R)
+        off, pl = s.pred()
+        t1, t2 = s.triad_counts()
+        out.append((R, off, pl, t1, t2, s.topk(25)[0]))
+        s.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
