@@ -143,6 +143,7 @@ static rs_status create_common(rs_ctx **out, int device, void *cuda_stream) {
         CK(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
     CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_zero, cudaEventDisableTiming));
     for (int i = 0; i < 8; i++) CK(cudaEventCreate(&c.ev_phase[i]));
     CK(dalloc(&c.scal, rs::kScalCount));
     CK(cudaMemset(c.scal, 0, sizeof(unsigned long long) * rs::kScalCount));
@@ -222,6 +223,7 @@ extern "C" void rs_destroy(rs_ctx *ctx) {
         if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
     }
     if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+    if (c.ev_zero) cudaEventDestroy(c.ev_zero);
     for (cudaEvent_t ev : c.ev_chunk) cudaEventDestroy(ev);
     for (int i = 0; i < 8; i++) if (c.ev_phase[i]) cudaEventDestroy(c.ev_phase[i]);
 #ifdef RS_WITH_NCCL
@@ -259,6 +261,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     const bool fits = c.cap_n >= n && c.cap_nnz >= nnz;
     if (!fits) free_graph(ctx);
     c.loaded = c.has_comm = c.scored = false;
+    c.acc_zero = c.bql_zero = false;
     c.n = n;
     c.nnz = nnz;
     // arena: host-input staging + relabel temporaries (grow-only)
@@ -448,6 +451,7 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
         CK(dalloc(&c.f, (size_t)c.n * k));
         CK(dalloc(&c.omega, (size_t)c.n * k));
         CK(dalloc(&c.bql, (size_t)c.n * k));
+        c.bql_zero = false;
         CK(dalloc(&c.amat, (size_t)c.n * k));
         c.k_alloc = k;
         c.kn_alloc = c.n;
@@ -489,8 +493,14 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (c.sparse && c.variant)
         return fail(ctx, RS_EINVAL, "rs_score: the NEXT-3 variant flags need explicit targets (k <= 254)");
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
-    CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
-    CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
+    // the accumulators (and the dense B table) were zeroed on a side stream at the
+    // end of the previous rs_score, overlapping rs_topk; otherwise zero them here
+    if (c.acc_zero || (!c.sparse && c.bql_zero)) CK(cudaStreamWaitEvent(c.stream, c.ev_zero, 0));
+    if (!c.acc_zero) {
+        CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
+        CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
+    }
+    c.acc_zero = false;
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, 2 * sizeof(unsigned long long), c.stream));   // NTri, NProbe
     if (c.sparse) {
@@ -504,7 +514,8 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(rs::launch_sparse_lists(c));
         join(c);
     } else {
-        CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs (Q rewritten)
+        if (!c.bql_zero) CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs
+        c.bql_zero = false;
         // Phase A: border + histogram + weights + P lists + omega_max partials, the
         // orientation of G' and the B-table pushes
         fork(c);
@@ -547,6 +558,19 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         NK(NCCL.GroupEnd());
     }
 #endif
+    // zero the accumulators (and the dense B table) for the next rs_score on a side
+    // stream: it overlaps whatever the caller does next (rs_topk, getters)
+    {
+        cudaStream_t zs = c.side[rs::kNumBins];
+        CK(cudaEventRecord(c.ev_fork, c.stream));
+        CK(cudaStreamWaitEvent(zs, c.ev_fork, 0));
+        CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, zs));
+        CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, zs));
+        if (!c.sparse) CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, zs));
+        CK(cudaEventRecord(c.ev_zero, zs));
+        c.acc_zero = true;
+        if (!c.sparse) c.bql_zero = true;
+    }
     c.scored = true;
     if (scores_out) {
         const bool dev = is_device_ptr(scores_out);

@@ -114,6 +114,9 @@ struct Ctx {
     cudaStream_t side[kNumBins + 1] = {nullptr};   // forked streams: concurrent bins (+ light Phase E)
     cudaEvent_t ev_fork = nullptr, ev_join[kNumBins + 1] = {nullptr};
     cudaEvent_t ev_phase[8] = {nullptr};
+    cudaEvent_t ev_zero = nullptr;   // accumulators zeroed for the next rs_score (side stream)
+    bool acc_zero = false;           // acc1 / acc_hub are zero once ev_zero completes
+    bool bql_zero = false;           // the dense B table's limbs are zero once ev_zero completes
     std::string err;
     int64_t launches = 0;
 
