@@ -32,6 +32,7 @@ struct PhaseAArgs {
     int32_t k;
     double wide_bound;                  // d^2 above which a head's Type-I sum needs 3 limbs
     int variant;                        // NEXT-3 (rs_score flags >> 16): 1 literal |L|, 2 |L| > 1 gate, 4 E_b max
+    int parity;                         // 1: getter pass, writes only the parity tables f and omega
     int64_t n;
     int32_t *__restrict__ pplus;
     double *__restrict__ wps;
@@ -187,7 +188,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
                 const int r = g.rank(foreign, &tot);
                 g.rank(foreign && x[j] < (int32_t)u, &totp);
                 g.rank(foreign && x[j] < (int32_t)u && l < (unsigned)k, &tott);
-                if (foreign) a.pidx[beg + pc + r] = x[j];
+                if (foreign && !a.parity) a.pidx[beg + pc + r] = x[j];
                 pc += tot;
                 pp += totp;
                 pt += tott;
@@ -226,13 +227,17 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
         for (int j = 0; j < 8; j++) fc = (j == c) ? cnt[j] : fc;
         const double w = weight_of(a, fc, T, L_all, X);
         const double ac = w > 0.0 ? cbrt(w) : 0.0;
-        a.omega[u * k + c] = w;
-        a.amat[u * k + c] = ac;
-        a.f[u * k + c] = fc;
-        a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+        if (a.parity) {            // the parity tables, written only for the getters
+            a.omega[u * k + c] = w;
+            a.f[u * k + c] = fc;
+        } else {
+            a.amat[u * k + c] = ac;
+            a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+        }
         if (in_max(a, fc, L_all, c, lu, pc)) wmax = w > wmax ? w : wmax;
         if (c == (int)lu) a_self = ac;
     }
+    if (a.parity) return wmax;
     const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
     if ((int)g.lane == owner) write_vrec(a, u, a_self, pc, lu, d);
     g.sync();
@@ -271,7 +276,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
                 const int r = g.rank(foreign, &tot);
                 g.rank(foreign && x[j] < (int32_t)u, &totp);
                 g.rank(foreign && x[j] < (int32_t)u && lx[j] < k, &tott);
-                if (foreign) a.pidx[beg + pc + r] = x[j];
+                if (foreign && !a.parity) a.pidx[beg + pc + r] = x[j];
                 pc += tot;
                 pp += totp;
                 pt += tott;
@@ -293,13 +298,17 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
         const int fc = hist[c];
         const double w = weight_of(a, fc, T, L_all, X);
         const double ac = w > 0.0 ? cbrt(w) : 0.0;
-        a.omega[u * k + c] = w;
-        a.amat[u * k + c] = ac;
-        a.f[u * k + c] = fc;
-        a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+        if (a.parity) {
+            a.omega[u * k + c] = w;
+            a.f[u * k + c] = fc;
+        } else {
+            a.amat[u * k + c] = ac;
+            a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+        }
         if (in_max(a, fc, L_all, c, lu, pc)) wmax = w > wmax ? w : wmax;
     }
     g.sync();
+    if (a.parity) return wmax;
     if (g.lane == 0) {
         double as = 0.0;
         if (lu < k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cbrt(w) : 0.0; }
@@ -396,7 +405,7 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
     }
 }
 
-cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
+cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity) {
     PhaseAArgs a;
     a.rowptr = c.rowptr; a.col = c.col; a.comm = c.comm_id; a.lab = c.lab;
     a.vlo = 0; a.nverts = 0; a.k = c.k; a.l2t = l2t; a.l2n = l2n;
@@ -404,6 +413,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n) {
     // 3-limb accumulator when d^2 >= |P|^2 times that bound could reach 2^31 (fx_red2)
     a.wide_bound = wide_bound(c.k);
     a.variant = c.variant;
+    a.parity = parity ? 1 : 0;
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8 && c.d_max < (1ll << 22)) launch_bins_a<false>(c, a);

@@ -12,7 +12,7 @@
 
 namespace rs {
 cudaError_t launch_log2_table(Ctx &c, double *t, int64_t len);
-cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n);
+cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity);
 cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
                                int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi);
 cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
@@ -501,6 +501,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
     }
     c.acc_zero = false;
+    c.parity_ok = false;
     CK(cudaMemsetAsync(c.scal + rs::kScalOmegaMaxBits, 0, sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(c.scal + rs::kScalNTri, 0, 2 * sizeof(unsigned long long), c.stream));   // NTri, NProbe
     if (c.sparse) {
@@ -519,7 +520,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         // Phase A: border + histogram + weights + P lists + omega_max partials, the
         // orientation of G' and the B-table pushes
         fork(c);
-        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n));
+        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, false));
         join(c);
     }
     CK(cudaEventRecord(c.ev_phase[1], c.stream));
@@ -838,6 +839,19 @@ static rs_status out_copy(rs_ctx *ctx, T *dst, const T *src_dev, size_t count) {
     return RS_OK;
 }
 
+// the dense parity tables f and omega are not written by rs_score: the first
+// getter after it re-runs the Phase A histogram in its parity mode (same
+// kernels, same arithmetic, only those two tables written)
+static cudaError_t ensure_parity_tables(rs_ctx *ctx) {
+    Ctx &c = ctx->c;
+    if (c.parity_ok) return cudaSuccess;
+    fork(c);
+    cudaError_t e = rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, true);
+    join(c);
+    if (e == cudaSuccess) c.parity_ok = true;
+    return e;
+}
+
 extern "C" rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_out) {
     if (!ctx) return RS_EINVAL;
     Ctx &c = ctx->c;
@@ -857,7 +871,8 @@ extern "C" rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_o
         CK(e);
         return s;
     }
-    cudaError_t e = rs::launch_permute_i32(c, c.f, c.k, forig);
+    cudaError_t e = ensure_parity_tables(ctx);
+    if (e == cudaSuccess) e = rs::launch_permute_i32(c, c.f, c.k, forig);
     if (e == cudaSuccess && f_out) s = out_copy(ctx, f_out, forig, (size_t)c.n * c.k);
     if (e == cudaSuccess && s == RS_OK && total_out) {
         int32_t *tmp = (int32_t *)c.scratch;
@@ -878,7 +893,8 @@ extern "C" rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omeg
         double *worig = nullptr;
         CK(cudaMalloc(&worig, sizeof(double) * (size_t)c.n * c.k));
         cudaError_t e = c.sparse ? rs::launch_sparse_weights_dense(c, ctx->l2t, ctx->l2n, worig)
-                                 : rs::launch_permute_f64(c, c.omega, c.k, worig);
+                                 : ensure_parity_tables(ctx);
+        if (e == cudaSuccess && !c.sparse) e = rs::launch_permute_f64(c, c.omega, c.k, worig);
         rs_status s = e == cudaSuccess ? out_copy(ctx, omega_out, worig, (size_t)c.n * c.k) : RS_OK;
         cudaFree(worig);
         CK(e);

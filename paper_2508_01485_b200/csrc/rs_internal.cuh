@@ -117,6 +117,7 @@ struct Ctx {
     cudaEvent_t ev_zero = nullptr;   // accumulators zeroed for the next rs_score (side stream)
     bool acc_zero = false;           // acc1 / acc_hub are zero once ev_zero completes
     bool bql_zero = false;           // the dense B table's limbs are zero once ev_zero completes
+    bool parity_ok = false;          // f / omega written for the last rs_score (getters)
     std::string err;
     int64_t launches = 0;
 
