@@ -244,77 +244,6 @@ __global__ void __launch_bounds__(256) k_relabel_fused(const int64_t *__restrict
         }
     }
 }
-// rows of 512..8191 entries: a CTA per internal row r in [r0, r1) whose original
-// row perm[r] lies in the chunk [v0, v1): relabel + block radix sort
-template <int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS) k_relabel_sort_cta(const int64_t *__restrict__ rp_o,
-                                                              const int32_t *__restrict__ col_o,
-                                                              const int32_t *__restrict__ perm,
-                                                              const int32_t *__restrict__ inv,
-                                                              const int64_t *__restrict__ rp, int64_t r0, int64_t r1,
-                                                              int64_t v0, int64_t v1, int32_t *out, int bits) {
-    using BRS = cub::BlockRadixSort<uint32_t, THREADS, ITEMS>;
-    __shared__ typename BRS::TempStorage ts;
-    const uint32_t pad = bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u;
-    for (int64_t r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
-        const int64_t v = perm[r];
-        if (v < v0 || v >= v1) continue;   // CTA-uniform
-        const int64_t b = rp_o[v];
-        const int d = (int)(rp_o[v + 1] - b);
-        const int64_t o = rp[r];
-        uint32_t keys[ITEMS];
-#pragma unroll
-        for (int i = 0; i < ITEMS; i++) {
-            const int idx = threadIdx.x * ITEMS + i;
-            keys[i] = idx < d ? (uint32_t)__ldg(inv + __ldg(col_o + b + idx)) : pad;
-        }
-        BRS(ts).Sort(keys, 0, bits);
-#pragma unroll
-        for (int i = 0; i < ITEMS; i++) {
-            const int idx = threadIdx.x * ITEMS + i;
-            if (idx < d) out[o + idx] = (int32_t)keys[i];
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(256) k_relabel_fused(const int64_t *__restrict__ rp_o, const int32_t *__restrict__ col_o,
-                                                       const int32_t *__restrict__ inv, const int64_t *__restrict__ rp,
-                                                       int64_t v0, int64_t v1, int32_t *tmp, int32_t *out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t v = v0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < v1; v += nw) {
-        const int64_t b = rp_o[v];
-        const int64_t d = rp_o[v + 1] - b;
-        const int64_t o = rp[inv[v]];
-        if (d >= 8192) {
-            for (int64_t i = lane; i < d; i += 32) tmp[o + i] = __ldg(inv + __ldg(col_o + b + i));
-        } else if (d >= 512) {
-            continue;   // k_relabel_sort_cta
-        } else if (d > 128) {
-            relabel_sort_row<16>(col_o, inv, b, (int)d, lane, out + o);
-        } else if (d > 32) {
-            relabel_sort_row<4>(col_o, inv, b, (int)d, lane, out + o);
-        } else if (d > 0) {
-            relabel_sort_row<1>(col_o, inv, b, (int)d, lane, out + o);
-        }
-    }
-}
-// rows of at most 32 entries (most rows of a sparse graph) in a kernel of their
-// own: a third of the registers of k_relabel_fused, so twice the warps in flight
-// for what is a chain of dependent gathers per row
-__global__ void __launch_bounds__(256) k_relabel_small(const int64_t *__restrict__ rp_o, const int32_t *__restrict__ col_o,
-                                                       const int32_t *__restrict__ inv, const int64_t *__restrict__ rp,
-                                                       int64_t v0, int64_t v1, int32_t *out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t v = v0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < v1; v += nw) {
-        const int64_t b = rp_o[v];
-        const int64_t d = rp_o[v + 1] - b;
-        if (d == 0 || d > 32) continue;
-        relabel_sort_row<1>(col_o, inv, b, (int)d, lane, out + rp[inv[v]]);
-    }
-}
 
 // Sort every row of a CSR-shaped array (row r at [rowptr[r], rowptr[r+1])) by
 // key = map ? map[in[e]] : in[e] (keys < 2^bits). Rows are in degree-descending
