@@ -33,6 +33,7 @@ struct PhaseAArgs {
     double wide_bound;                  // d^2 above which a head's Type-I sum needs 3 limbs
     int variant;                        // NEXT-3 (rs_score flags >> 16): 1 literal |L|, 2 |L| > 1 gate, 4 E_b max
     int parity;                         // 1: getter pass, writes only the parity tables f and omega
+    int bq;                             // B table grid: 2^-bq
     int64_t n;
     int32_t *__restrict__ pplus;
     double *__restrict__ wps;
@@ -101,8 +102,8 @@ __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR
                                               int pt, int lu) {
     const int k = a.k;
     const double *arow = a.amat + u * k;           // this group's writes, plain loads
-    const bool push = lu < k;
-    const U128 qs = push ? fx_quantize(arow[lu]) : u128_zero();
+    const unsigned long long qs = lu < k ? bq_quantize(arow[lu], a.bq) : 0ull;
+    const bool push = qs != 0ull;
     BQL *bcol = a.bql + (int64_t)(push ? lu : 0) * a.n;
     int ct = 0, cn = 0;
     for (int base = 0; base < pc; base += GR::size * U) {
@@ -122,7 +123,7 @@ __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
 #ifndef RS_EXP_NO_BPUSH
-            if (push && v[j] >= 0) fx_red2(&bcol[v[j]].b0, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
+            if (push && v[j] >= 0) atomicAdd(&bcol[v[j]].b, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
 #endif
             if (base + j * GR::size < pp) {                      // group-uniform
                 const bool inp = v[j] >= 0 && i < pp;
@@ -414,6 +415,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.wide_bound = wide_bound(c.k);
     a.variant = c.variant;
     a.parity = parity ? 1 : 0;
+    a.bq = c.bq;
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8 && c.d_max < (1ll << 22)) launch_bins_a<false>(c, a);

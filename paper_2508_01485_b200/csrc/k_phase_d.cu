@@ -32,18 +32,20 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const int pc = ru.pcnt;
     const int64_t beg = a.rowptr[u];
     const BQL *bcol = SPARSE ? nullptr : a.bql + (int64_t)cu * a.n;
+    const unsigned long long qa = SPARSE ? 0ull : bq_quantize(au, a.bq);   // a_u(c_u) on the B grid
     U128 S = u128_zero();
     for (int base = 0; base < pc; base += GR::size * U) {
         int32_t w[U];
-        BQL r[U];
+        double Q[U], diff[U];
         int64_t pv[U];
+        unsigned long long bq[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
             if constexpr (SPARSE) {
                 w[j] = i < pc ? 0 : -1;
                 pv[j] = i < pc ? __ldg(a.prv + beg + i) : 0;
-                r[j].Q = i < pc ? __ldg(a.pwr + beg + i) : 0.0;
+                Q[j] = i < pc ? __ldg(a.pwr + beg + i) : 0.0;
             } else {
                 w[j] = i < pc ? __ldg(a.pidx + beg + i) : -1;
             }
@@ -52,22 +54,28 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
         for (int j = 0; j < U; j++) {
             if constexpr (SPARSE) {
                 if (w[j] >= 0) {
+                    // B_w[c_u] (exact 2-limb sum, rounded once) includes a_u: the
+                    // difference is >= 0 and exactly 0 when u is w's only such neighbour
                     const ulonglong2 b = a.ctb[pv[j]];
-                    r[j].b0 = b.x;
-                    r[j].b1 = b.y;
-                    r[j].Q *= r[j].Q;
+                    const unsigned long long l2[2] = {b.x, b.y};
+                    diff[j] = fx_to_double(fx_from2(l2)) - au;
+                    Q[j] *= Q[j];
                 }
             } else {
-                if (w[j] >= 0) r[j] = bcol[w[j]];
+                if (w[j] >= 0) {
+                    const BQL r = bcol[w[j]];
+                    bq[j] = r.b;
+                    Q[j] = r.Q;
+                }
             }
         }
 #pragma unroll
         for (int j = 0; j < U; j++) {
             if (w[j] >= 0) {
-                // B_w[c_u] (exact sum, rounded once) includes a_u, so the difference is
-                // >= 0 and exactly 0 when u is w's only neighbour in C(u) (v != u)
-                const double B = fx_to_double(fx_from2(&r[j].b0));
-                const double t = r[j].Q * (B - au);
+                // dense: B_w[c_u] - a_u(c_u) in integers on the B grid (exact; 0 when
+                // u is w's only neighbour in C(u), v != u), converted once
+                if constexpr (!SPARSE) diff[j] = bq_to_double(bq[j] - qa, a.bq);
+                const double t = Q[j] * diff[j];
                 S = u128_add(S, fx_quantize(t));
             }
         }

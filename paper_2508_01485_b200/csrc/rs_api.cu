@@ -473,6 +473,15 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     CK(cudaMemcpyAsync(&nw, c.scal + rs::kScalNWide, sizeof(nw), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     c.n_wide = (int64_t)nw;
+    {
+        // B table grid: a <= (k log2(k - 1))^(1/3) (the wide_bound weight bound) and
+        // B_w[c] sums at most d_max of them; keep 2 spare bits below 2^64
+        const double wb = 2147483648.0 / (2.0 * rs::wide_bound(k));
+        const double bmax = std::cbrt(wb) * (double)std::max<int64_t>(c.d_max, 1);
+        int q = 40;
+        while (q > 16 && bmax * std::ldexp(1.0, q) >= std::ldexp(1.0, 62)) q--;
+        c.bq = q;
+    }
     if (er == 10)
         return fail(ctx, RS_EINVAL, "rs_set_communities: k = " + std::to_string(k) + " exceeds the " +
                                         std::to_string((long long)ndist) + " distinct communities");

@@ -90,6 +90,15 @@ __device__ __forceinline__ U128 fx_from2(const unsigned long long *acc2) {
     return u128_add(U128{l0, 0ull}, U128{l1 << 32, l1 >> 32});
 }
 
+// B-table grid (BQL): round-to-nearest of a * 2^q as an integer (a >= 0, the
+// scaling by a power of two is exact), and back
+__device__ __forceinline__ unsigned long long bq_quantize(double a, int q) {
+    return __double2ull_rn(a * __longlong_as_double((long long)(1023 + q) << 52));
+}
+__device__ __forceinline__ double bq_to_double(unsigned long long v, int q) {
+    return __ull2double_rn(v) * __longlong_as_double((long long)(1023 - q) << 52);
+}
+
 // ---------------------------------------------------------------------------
 // Vertex groups. A group of G lanes (G in {4, 8, 16, 32}) owns one vertex and
 // walks its adjacency G entries per step; 32/G groups share a warp. Lanes of

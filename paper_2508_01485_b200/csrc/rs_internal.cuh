@@ -78,13 +78,16 @@ __host__ __device__ __forceinline__ int ceil4(int v) { return (v + 3) & ~3; }
 __host__ __device__ __forceinline__ long long pr_start(const PRec &r) { return r.start & ((1ll << kPrShift) - 1); }
 __host__ __device__ __forceinline__ int pr_plus_t(const PRec &r) { return (int)(r.start >> kPrShift); }
 
-// Per (vertex, column) record read by the Type-II pull (Phase D), one sector.
+// Per (vertex, column) record read by the Type-II pull (Phase D), half a sector.
 // B_w[c] = sum_{v in P(w), col(v)=c} a_v(c) is pushed by every such v during
-// Phase A (v is in P(w) iff w is in P(v)) as exact 2-limb REDs (fx_red2).
-struct __align__(32) BQL {
-    unsigned long long b0, b1;   // fx_red2 limbs of B_w[c]
+// Phase A (v is in P(w) iff w is in P(v)) as one 64-bit integer RED of a_v(c)
+// rounded once to the 2^-bq grid (bq_quantize): the sum is exact and order-free,
+// and B_w[c] - a_u(c) is taken in integers, so it is exactly 0 when u is w's
+// only such neighbour. bq = 40 unless a_max * d_max needs more integer bits
+// (Ctx::bq); the rounding of each a (>= 0.01 when non-zero) is < 5e-11 relative.
+struct __align__(16) BQL {
+    unsigned long long b;        // sum of bq_quantize(a_v(c)) over the pushes
     double Q;                    // a_w(c)^2 = omega_w(c)^(2/3), written by w
-    double pad;
 };
 
 // Per-vertex record of the all-communities mode, gathered once per neighbour.
@@ -189,6 +192,7 @@ struct Ctx {
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQL *bql = nullptr;          // k*n, column-major: bql[c*n + w]
     int64_t n_wide = 0;          // vertices [0, n_wide) (degree^2 >= wide_bound) use 3 Type-I limbs
+    int bq = 40;                 // fraction bits of the B table's integer sums (BQL)
     unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)
     unsigned long long *acc_hub = nullptr;  // kHubStripes copies of the limbs of the first n_hub vertices
     int64_t n_hub = 0;                   //   (the highest degrees: contended heads), summed by Phase D

@@ -34,6 +34,7 @@ struct CdeArgs {
     const double *__restrict__ pwr;     // a_w(c_u) beside each w of P(u) (wps: a_u(c_w))
     const int64_t *__restrict__ prv;    // position of c_u in w's community table
     const ulonglong2 *__restrict__ ctb; // B_w[c] limbs beside each column of w's table
+    int bq;                             // B table grid 2^-bq (dense mode)
 };
 
 // VRec::wide by internal id: d(h)^2 >= wide_bound, d non-increasing in h
@@ -49,7 +50,7 @@ inline CdeArgs cde_args(Ctx &c) {
     a.n_wide = c.n_wide;
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
     a.e_rank = 0; a.e_world = 1;
-    a.pwr = c.pwr; a.prv = c.prv; a.ctb = c.ctb;
+    a.pwr = c.pwr; a.prv = c.prv; a.ctb = c.ctb; a.bq = c.bq;
     if (c.sparse) a.pplus = c.pidx;   // P+(u) is one ascending run: the prefix of P(u)
     return a;
 }
