@@ -127,11 +127,12 @@ def phase_bytes(n, D, Db, k, ntri, nb, nprobe):
     volume (4 B per probed P+ entry), 20 B per G' edge (the P-
     entry and the predecessor's record), 32 B per Type-I triangle (weights and
     head updates) and y's weight rows."""
-    # A: row, labels, P(u) writes, weights, vrec; then P(u) re-read, the P+ runs
-    # with their weights (half of P), the B pushes (16 B per P entry), PRec
-    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 28 * k * n + 16 * n + 4 * Db + 6 * Db + 16 * Db + 16 * n
+    # A: row, labels, P(u) writes, weights (a and a^2 per column), vrec; then P(u)
+    # re-read, the P+ runs with their weights (half of P), the B pushes (8 B per
+    # P entry), PRec
+    A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 16 * k * n + 16 * n + 4 * Db + 6 * Db + 8 * Db + 16 * n
     E = 4 * nprobe + 20 * (Db // 2) + 32 * ntri + 8 * k * n
-    D_ = 4 * Db + 32 * Db + 16 * n + 16 * n                   # Type-II pull (concurrent with E)
+    D_ = 4 * Db + 16 * Db + 16 * n + 16 * n                   # Type-II pull (16 B B records; concurrent with E)
     F = 16 * n + 24 * n + 16 * n + 8 * n + 4 * n + 8 * n      # finalize: sums, vrec, rowptr, perm, score
     return {"A": A, "ED": E + D_, "F": F}
 
