@@ -32,7 +32,7 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
     const int pc = ru.pcnt;
     const int64_t beg = a.rowptr[u];
     const BQL *bcol = SPARSE ? nullptr : a.bql + (int64_t)cu * a.n;
-    const unsigned long long qa = SPARSE ? 0ull : bq_quantize(au, a.bq);   // a_u(c_u) on the B grid
+    const unsigned long long qa = bq_quantize(au, a.bq);   // a_u(c_u) on the B grid
     U128 S = u128_zero();
     for (int base = 0; base < pc; base += GR::size * U) {
         int32_t w[U];
@@ -54,11 +54,7 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
         for (int j = 0; j < U; j++) {
             if constexpr (SPARSE) {
                 if (w[j] >= 0) {
-                    // B_w[c_u] (exact 2-limb sum, rounded once) includes a_u: the
-                    // difference is >= 0 and exactly 0 when u is w's only such neighbour
-                    const ulonglong2 b = a.ctb[pv[j]];
-                    const unsigned long long l2[2] = {b.x, b.y};
-                    diff[j] = fx_to_double(fx_from2(l2)) - au;
+                    bq[j] = a.ctb[pv[j]];
                     Q[j] *= Q[j];
                 }
             } else {
@@ -74,7 +70,7 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
             if (w[j] >= 0) {
                 // dense: B_w[c_u] - a_u(c_u) in integers on the B grid (exact; 0 when
                 // u is w's only neighbour in C(u), v != u), converted once
-                if constexpr (!SPARSE) diff[j] = bq_to_double(bq[j] - qa, a.bq);
+                diff[j] = bq_to_double(bq[j] - qa, a.bq);
                 const double t = Q[j] * diff[j];
                 S = u128_add(S, fx_quantize(t));
             }

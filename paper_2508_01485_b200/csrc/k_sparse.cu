@@ -98,6 +98,11 @@ cudaError_t launch_set_communities_all(Ctx &c, int64_t max_comm, int64_t *nc_out
     // with L <= min(k, d_max), so the k <= 254 bound with k_eff = min(k, d_max + 1)
     const int keff = (int)std::max<int64_t>(2, std::min<int64_t>((int64_t)nc, c.d_max + 1));
     launch_nwide(c, wide_bound(keff));
+    // B grid (BQL): a <= (keff log2(keff - 1))^(1/3), B sums at most d_max of them
+    const double bmax = std::cbrt(2147483648.0 / (2.0 * wide_bound(keff))) * (double)std::max<int64_t>(c.d_max, 1);
+    int q = 40;
+    while (q > 16 && bmax * std::ldexp(1.0, q) >= std::ldexp(1.0, 62)) q--;
+    c.bq = q;
     return cudaStreamSynchronize(c.stream);
 }
 
@@ -113,7 +118,8 @@ struct SpArgs {
     double wide_bound;
     SRec *__restrict__ srec;
     CtEnt *__restrict__ ctk;
-    ulonglong2 *__restrict__ ctb;
+    unsigned long long *__restrict__ ctb;
+    int bq;
     double *__restrict__ aself;
     double *__restrict__ xsum;          // X(u) = sum_c f log2 f (getters recompute weights from it)
     int32_t *__restrict__ pidx;
@@ -194,7 +200,7 @@ __device__ __forceinline__ double sp_table_vertex(const SpArgs &a, int64_t u, GR
         const double w = sp_weight(a.l2t, a.l2n, ty, d, L, X);
         const double ac = w > 0.0 ? cbrt(w) : 0.0;
         a.ctk[beg + j].a = ac;
-        a.ctb[beg + j] = make_ulonglong2(0ull, 0ull);
+        a.ctb[beg + j] = 0ull;
         wmax = w > wmax ? w : wmax;
         if (tx == cu) { as = ac; found = 1; }
     }
@@ -257,8 +263,8 @@ __device__ __forceinline__ void sp_lists_vertex(const SpArgs &a, int64_t u, GR &
     const SRec su = a.srec[u];
     const int cu = su.cid;
     const double au = a.aself[u];
-    const U128 qs = fx_quantize(au);
-    const bool push = au > 0.0;
+    const unsigned long long qs = bq_quantize(au, a.bq);   // the B grid (BQL)
+    const bool push = qs != 0ull;
     int pc = 0, pp = 0;
     unsigned long long n2 = 0;
     for (int64_t base = beg; base < end; base += GR::size * U) {
@@ -327,7 +333,7 @@ __device__ __forceinline__ void sp_lists_vertex(const SpArgs &a, int64_t u, GR &
                     a.pwr[pos] = ar[j];
                     a.prv[pos] = p;
                     n2 += (unsigned long long)(cr[j] - 1);
-                    if (push) fx_red2(&a.ctb[p].x, qs);   // u in P(x): a_u(c_u) into B_x[c_u]
+                    if (push) atomicAdd(&a.ctb[p], qs);   // u in P(x): a_u(c_u) into B_x[c_u]
                 }
                 pc += tot;
                 pp += totp;
@@ -374,7 +380,7 @@ static SpArgs sp_args(Ctx &c, const double *l2t, int64_t l2n) {
     a.vlo = 0; a.nverts = 0; a.n = c.n; a.nc = c.k;
     const int keff = (int)std::max<int64_t>(2, std::min<int64_t>((int64_t)c.k, c.d_max + 1));
     a.wide_bound = wide_bound(keff);
-    a.srec = c.srec; a.ctk = c.ctk; a.ctb = c.ctb; a.aself = c.aself; a.xsum = c.xsum;
+    a.srec = c.srec; a.ctk = c.ctk; a.ctb = c.ctb; a.bq = c.bq; a.aself = c.aself; a.xsum = c.xsum;
     a.pidx = c.pidx; a.wps = c.wps; a.pwr = c.pwr; a.prv = c.prv; a.vrec = c.vrec; a.pc2 = c.pc2; a.n2s = c.n2s;
     a.scal = c.scal;
     return a;

@@ -171,7 +171,7 @@ struct Ctx {
     int32_t *code32 = nullptr;   // community id -> column (ccap entries)
     SRec *srec = nullptr;        // n: {rowptr, L(u), cid} gathered per neighbour
     CtEnt *ctk = nullptr;        // nnz: u's distinct neighbour columns ascending at rowptr[u]: {column, f_u(c), a_u(c)}
-    ulonglong2 *ctb = nullptr;   // nnz: B_u[c] limbs (fx_red2) beside each column
+    unsigned long long *ctb = nullptr;   // nnz: B_u[c] on the 2^-bq grid (see BQL) beside each column
     double *pwr = nullptr;       // nnz: a_w(c_u) beside each w of P(u) (pidx order); wps holds a_u(c_w)
     int64_t *prv = nullptr;      // nnz: position of c_u in w's table, beside each w of P(u)
     double *aself = nullptr;     // n: a_u(c_u)

@@ -33,8 +33,8 @@ struct CdeArgs {
     // all-communities mode (k_sparse.cu): weights per G' edge instead of dense rows
     const double *__restrict__ pwr;     // a_w(c_u) beside each w of P(u) (wps: a_u(c_w))
     const int64_t *__restrict__ prv;    // position of c_u in w's community table
-    const ulonglong2 *__restrict__ ctb; // B_w[c] limbs beside each column of w's table
-    int bq;                             // B table grid 2^-bq (dense mode)
+    const unsigned long long *__restrict__ ctb;   // B_w[c] beside each column of w's table
+    int bq;                             // B grid 2^-bq (BQL, ctb)
 };
 
 // VRec::wide by internal id: d(h)^2 >= wide_bound, d non-increasing in h
