@@ -59,17 +59,23 @@ __device__ __forceinline__ int L_of(const PhaseAArgs &a, int fc, int L_all) {
     return (a.variant & 1) ? L_all - (fc > 0) : L_all - 1;
 }
 
-// omega for column c of a row with T, L_all, X = sum f log2 f (Algorithm 2)
-__device__ __forceinline__ double weight_of(const PhaseAArgs &a, int fc, int T, int L_all, double X) {
+// omega for column c of a row with T, L_all, X = sum f log2 f (Algorithm 2),
+// given xc = f_c log2 f_c and lgY = log2(T - f_c)
+__device__ __forceinline__ double weight_from(const PhaseAArgs &a, int fc, int T, int L_all, double X, double xc,
+                                              double lgY) {
     const int others = L_all - (fc > 0);   // nonzero columns of L(u, .) besides c
     if (L_all < 2 || others < 2) return 0.0; // one remaining community: H = 0 exactly
     const int L = L_of(a, fc, L_all);
     if ((a.variant & 2) && L <= 1) return 0.0;   // NEXT-3: Algorithm 1's gate
     const int Y = T - fc;                    // > 0
-    const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
-    const double H = lg2(a, Y) - (X - xc) / (double)Y;
+    const double H = lgY - (X - xc) / (double)Y;
     const double w = H * (double)L;
     return w > 0.0 ? w : 0.0;                // canonical +0.0
+}
+__device__ __forceinline__ double weight_of(const PhaseAArgs &a, int fc, int T, int L_all, double X) {
+    if (L_all < 2 || L_all - (fc > 0) < 2) return 0.0;
+    const double xc = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
+    return weight_from(a, fc, T, L_all, X, xc, lg2(a, T - fc));
 }
 
 // does cell (u, c) count towards omega_max? All cells (C-7), or with the NEXT-3
@@ -213,21 +219,40 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
         }
     }
     int T = 0, L_all = 0;
-    double X = 0.0;
 #pragma unroll
     for (int c = 0; c < 8; c++) {
         T += cnt[c];
         L_all += cnt[c] > 0;
-        if (cnt[c] > 1) X += (double)cnt[c] * lg2(a, cnt[c]);
     }
-    const int64_t d = end - beg;
-    double wmax = 0.0, a_self = 0.0;
-    for (int c = g.lane; c < k; c += GR::size) {
+    // Algorithm 2's X = sum f log2 f and every column's log2(T - f) with ONE
+    // round of log2-table loads: lane l takes the columns l, l + G, ... (a
+    // vertex's weights are a dependent chain after its row walk; a second
+    // round of loads there cost ~0.4 ms of Phase A), X by a group sum
+    constexpr int NC = GR::size >= 8 ? 1 : 8 / GR::size;
+    int fcs[NC];
+    double xcs[NC], lys[NC];
+    double xpart = 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; i++) {
+        const int c = (int)g.lane + i * GR::size;
         int fc = 0;
 #pragma unroll
         for (int j = 0; j < 8; j++) fc = (j == c) ? cnt[j] : fc;
-        const double w = weight_of(a, fc, T, L_all, X);
-        const double ac = w > 0.0 ? cbrt(w) : 0.0;
+        fcs[i] = fc;
+        xcs[i] = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
+        lys[i] = (c < k && T - fc > 0) ? lg2(a, T - fc) : 0.0;
+        xpart += xcs[i];
+    }
+    const double X = g.sum(xpart);
+    const int64_t d = end - beg;
+    double wmax = 0.0, a_self = 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; i++) {
+        const int c = (int)g.lane + i * GR::size;
+        if (c >= k) continue;
+        const int fc = fcs[i];
+        const double w = weight_from(a, fc, T, L_all, X, xcs[i], lys[i]);
+        const double ac = w > 0.0 ? cube_root(w) : 0.0;
         if (a.parity) {            // the parity tables, written only for the getters
             a.omega[u * k + c] = w;
             a.f[u * k + c] = fc;
@@ -298,7 +323,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     for (int c = g.lane; c < k; c += GR::size) {
         const int fc = hist[c];
         const double w = weight_of(a, fc, T, L_all, X);
-        const double ac = w > 0.0 ? cbrt(w) : 0.0;
+        const double ac = w > 0.0 ? cube_root(w) : 0.0;
         if (a.parity) {
             a.omega[u * k + c] = w;
             a.f[u * k + c] = fc;
@@ -312,7 +337,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     if (a.parity) return wmax;
     if (g.lane == 0) {
         double as = 0.0;
-        if (lu < k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cbrt(w) : 0.0; }
+        if (lu < k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cube_root(w) : 0.0; }
         write_vrec(a, u, as, pc, lu, d);
     }
     g.sync();

@@ -198,7 +198,7 @@ __device__ __forceinline__ double sp_table_vertex(const SpArgs &a, int64_t u, GR
     for (int j = (int)g.lane; j < L; j += GR::size) {
         const int tx = a.ctk[beg + j].x, ty = a.ctk[beg + j].y;
         const double w = sp_weight(a.l2t, a.l2n, ty, d, L, X);
-        const double ac = w > 0.0 ? cbrt(w) : 0.0;
+        const double ac = w > 0.0 ? cube_root(w) : 0.0;
         a.ctk[beg + j].a = ac;
         a.ctb[beg + j] = 0ull;
         wmax = w > wmax ? w : wmax;
@@ -206,7 +206,7 @@ __device__ __forceinline__ double sp_table_vertex(const SpArgs &a, int64_t u, GR
     }
     as = g.sum(as);           // at most one lane holds a non-zero value: exact
     found = g.sum(found);
-    if (!found) as = wabs > 0.0 ? cbrt(wabs) : 0.0;
+    if (!found) as = wabs > 0.0 ? cube_root(wabs) : 0.0;
     if (g.lane == 0) {
         SRec r;
         r.beg = beg;
