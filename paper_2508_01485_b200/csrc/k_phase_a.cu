@@ -310,14 +310,18 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
         }
     }
     g.sync();
-    int T = 0, L_all = 0;
-    double X = 0.0;
-    for (int c = 0; c < k; c++) {
+    // T, L_all and X = sum f log2 f over the k columns, lane-strided + group sums
+    // (one round of log2-table loads instead of k in sequence per lane)
+    int Tp = 0, Lp = 0;
+    double Xp = 0.0;
+    for (int c = g.lane; c < k; c += GR::size) {
         const int v = hist[c];
-        T += v;
-        L_all += v > 0;
-        if (v > 1) X += (double)v * lg2(a, v);
+        Tp += v;
+        Lp += v > 0;
+        if (v > 1) Xp += (double)v * lg2(a, v);
     }
+    const int T = g.sum(Tp), L_all = g.sum(Lp);
+    const double X = g.sum(Xp);
     const int64_t d = end - beg;
     double wmax = 0.0;
     for (int c = g.lane; c < k; c += GR::size) {
