@@ -38,11 +38,11 @@ METRIC = "RSI-scored edges/sec (GTEPS)"
 # DRAM bytes per launch of the dominant phase from the committed ncu captures
 # (profiles/); filled per round, None when not captured for that config
 # ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per step of the
-# dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 5.490 +
-# 0.117 GB, light 1.591 + 0.017 GB) + the Phase D launches of
-# profiles/r01_full_phaseAD_summary.txt (1.689 + 0.053 GB); ncu flushes the L2
+# dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 5.488 +
+# 0.121 GB, light 1.592 + 0.018 GB) + the Phase D launches of
+# profiles/r01_full_phaseAD_summary.txt (1.687 + 0.050 GB); ncu flushes the L2
 # before each kernel, so this bounds the in-step traffic from above
-TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 8.957e9}}
+TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 8.956e9}}
 UNIT = "GTEPS"
 
 
@@ -83,33 +83,50 @@ class ClockSampler:
         self._t = None
         self.err = None
 
+    def _sample(self):
+        N = self._N
+        clk = N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM)
+        rs = N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        self.rows.append((clk, [k for k, v in self._bits.items() if rs & v]))
+
     def _run(self):
         try:
-            import pynvml as N
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self.maxclk = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
-                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
-                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
-                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap,
-                    "hw_power_brake": N.nvmlClocksEventReasonHwPowerBrakeSlowdown}
             while not self._stop.is_set():
-                clk = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((clk, [k for k, v in bits.items() if rs & v]))
+                self._sample()
                 self._stop.wait(self.period)
-        except Exception as e:  # NVML unavailable: report it
+        except Exception as e:  # NVML failure mid-run: report it
             self.err = repr(e)
 
     def __enter__(self):
+        # NVML is initialised and a first sample taken before the timed region
+        # starts (the sampling thread alone could miss a short region)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self._N = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.maxclk = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
+            self._bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                          "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                          "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                          "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap,
+                          "hw_power_brake": N.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+            self._sample()
+        except Exception as e:  # NVML unavailable: report it
+            self.err = repr(e)
+            return self
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
+            try:
+                self._sample()   # and one at the end of the region
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
@@ -294,6 +311,7 @@ def main():
         top = ids_d.cpu().numpy()
         shii = {"S": int(top.size), "runs": 2}
         for model in ("ic", "lt"):
+            sc.shii(top[:1], model, 0.1, 1, 1)             # warm-up (buffers)
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             _, _, mean = sc.shii(top, model, 0.1, 2, 3)
