@@ -578,19 +578,17 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
             if (q < total) x = __ldg(a.pidx + qpos);
             PRec pcx{0, 0, 0};
             int lx = kOther;
-            double Axly = 0.0;
             if (x >= 0) {
                 pcx = a.pc2[x];
                 lx = __ldg(a.lab + x);
-                Axly = SPARSE ? __ldg(a.pwr + qpos) : amat_at(a, x, ly);
             }
             const bool tx = lx < k, ty = ly < k;
             int64_t rsx;                                                 // probed: z < y of the target
             int np, t;                                                   // run, and of the other if both
             cut_range<SPARSE>(a.pplus, pr_start(pcx), pcx.x, pr_plus_t(pcx), (int32_t)(y0 + j), tx && ty,
                               x >= 0 && (tx || ty), rsx, np, t);
-            double Aylx = 0.0;
-            if (x >= 0 && tx) Aylx = SPARSE ? __ldg(a.wps + qpos) : __ldg(a.amat + (y0 + j) * k + lx);
+            // a_x(c_y) and a_y(c_x) are gathered by the probe lanes that find a
+            // triangle (few of the pairs close one), not per pair
             int incl2 = np;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -608,8 +606,7 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 const long long bx = __shfl_sync(0xffffffffu, (long long)rsx, p);
                 const int tp = __shfl_sync(0xffffffffu, t, p);
                 const int lxp = __shfl_sync(0xffffffffu, lx, p);
-                const double Axlyp = __shfl_sync(0xffffffffu, Axly, p);
-                const double Aylxp = __shfl_sync(0xffffffffu, Aylx, p);
+                const long long qp = __shfl_sync(0xffffffffu, (long long)qpos, p);   // x's position in P(y)
                 const int jp = __shfl_sync(0xffffffffu, j, p);               // y's lane
                 const PRec pcy{__shfl_sync(0xffffffffu, pcl.x, jp), __shfl_sync(0xffffffffu, pcl.y, jp),
                                __shfl_sync(0xffffffffu, pcl.start, jp)};
@@ -640,6 +637,8 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                     if (tz && (txp + typ) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(txp + typ));
                     if (typ && (txp + tz) && owned(a, y)) atomicAdd(a.n1 + y, (unsigned long long)(txp + tz));
                 } else {
+                    const double Axlyp = SPARSE ? __ldg(a.pwr + qp) : amat_at(a, xp, lyp);
+                    const double Aylxp = txp ? (SPARSE ? __ldg(a.wps + qp) : __ldg(a.amat + (int64_t)y * k + lxp)) : 0.0;
                     const double Axlz = __ldg(a.wps + pos), Aylz = __ldg(a.wps + ypos);
                     const double Azlx = SPARSE ? __ldg(a.pwr + pos) : amat_at(a, z, lxp);
                     const double Azly = SPARSE ? __ldg(a.pwr + ypos) : amat_at(a, z, lyp);
