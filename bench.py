@@ -39,10 +39,10 @@ METRIC = "RSI-scored edges/sec (GTEPS)"
 # (profiles/); filled per round, None when not captured for that config
 # ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per step of the
 # dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 5.488 +
-# 0.121 GB, light 1.592 + 0.018 GB) + the Phase D launches of
-# profiles/r01_full_phaseAD_summary.txt (1.687 + 0.050 GB); ncu flushes the L2
+# 0.116 GB, light 1.226 + 0.017 GB) + the Phase D launches of
+# profiles/r01_full_phaseAD_summary.txt (1.688 + 0.052 GB); ncu flushes the L2
 # before each kernel, so this bounds the in-step traffic from above
-TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 8.956e9}}
+TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 8.587e9}}
 UNIT = "GTEPS"
 
 
