@@ -185,7 +185,6 @@ struct ESmem {             // one warp's shared memory
     int32_t py[kPyCap];     // P+(y): target run, then the other run, each ascending
     longlong2 xl[kChunkE];  // {x's slot start, (x << 32) | (lab(x) << 24) | |P+_T(x)|}
     int2 xn[kChunkE];       // {probed length of P+(x) (its target run, or all of it), -}
-    double axy[kChunkE];    // a_x(c_y)
     uint32_t xa[4 * kChunkE];
     int32_t pe[kChunkE];    // end of each list's pieces
     int2 q[kQCapE];         // candidates {((offset of z in P+(x)) + 4) << 6 | x slot, z}
@@ -198,14 +197,13 @@ __host__ __device__ constexpr size_t e_stride_bytes(int k) {
 
 // SPARSE (all-communities mode, k_sparse.cu): every vertex is a target, P+(u)
 // is one ascending run in pidx, and the weights come from beside the list
-// entries (wps: a_u(c_w), pwr: a_w(c_u)) instead of the dense rows; Ay then
-// holds a_y(c_x) per x slot of the item.
+// entries (wps: a_u(c_w), pwr: a_w(c_u)) instead of the dense rows.
 template <bool COUNT, bool SPARSE>
 __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems it, unsigned long long *queue_ctr) {
     extern __shared__ __align__(16) unsigned char e_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k;
-    unsigned char *base = e_smem + (size_t)wid * e_stride_bytes(SPARSE ? kChunkE : k);
+    unsigned char *base = e_smem + (size_t)wid * e_stride_bytes(SPARSE ? 0 : k);
     ESmem &S = *reinterpret_cast<ESmem *>(base);
     double *Ay = (double *)(base + ((sizeof(ESmem) + 15) / 16) * 16);
     unsigned long long ntri = 0, nprobe = 0;
@@ -253,21 +251,15 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         auto py_at = [&](int i) -> int64_t { return SPARSE ? by + i : (i < pyt ? by + pyt - 1 - i : by + i); };
         const int32_t z0 = lane < py ? __ldg(a.pplus + py_at(lane)) : -1;
         const double ay0 = (!SPARSE && lane < k) ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
+        // x's record and label; its weight a_x(c_y) (and, all-communities mode,
+        // a_y(c_x)) is gathered only by the lanes that verify a triangle (most
+        // (y, x) pairs close none), from x's position kept in S.xn[slot].y
         PRec pcx[2];
         int lxv[2];
-        double axy[2], ayx[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             pcx[h] = xv[h] >= 0 ? a.pc2[xv[h]] : PRec{0, 0, 0};
             lxv[h] = xv[h] >= 0 ? (int)__ldg(a.lab + xv[h]) : kOther;
-            if constexpr (SPARSE) {
-                const int64_t q = by + py + start + 32 * h + lane;   // x's position in P(y)
-                axy[h] = xv[h] >= 0 ? __ldg(a.pwr + q) : 0.0;       // a_x(c_y)
-                ayx[h] = xv[h] >= 0 ? __ldg(a.wps + q) : 0.0;       // a_y(c_x)
-            } else {
-                axy[h] = (xv[h] >= 0 && ty) ? __ldg(a.amat + (int64_t)xv[h] * k + ly) : 0.0;
-                ayx[h] = 0.0;
-            }
         }
         for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
         if constexpr (!SPARSE) {
@@ -319,9 +311,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             if (use) {
                 const int slot = nx + __popc(has & ((1u << lane) - 1u));
                 S.xl[slot] = make_longlong2(bx, ((long long)xv[h] << 32) | ((long long)(lx & 0xFF) << 24) | t);
-                S.xn[slot] = make_int2(lenx, 0);
-                S.axy[slot] = axy[h];
-                if constexpr (SPARSE) Ay[slot] = ayx[h];
+                S.xn[slot] = make_int2(lenx, start + 32 * h + lane);   // x's position in P-(y)
                 S.xa[4 * slot] = 0u;
                 S.xa[4 * slot + 1] = 0u;
                 S.xa[4 * slot + 2] = 0u;
@@ -418,8 +408,11 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
                             cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
                         } else {
                             const double Axlz = __ldg(a.wps + xe.x + off);  // a_x(c_z), stored by Phase A
-                            const double Axly = S.axy[slot];
-                            const double Aylx = SPARSE ? Ay[slot] : (lx < k ? Ay[lx] : 0.0);
+                            // a_x(c_y) (and, all-communities mode, a_y(c_x)) gathered per
+                            // verified triangle rather than per (y, x) pair: most pairs close none
+                            const int64_t xq = by + py + S.xn[slot].y;
+                            const double Axly = SPARSE ? __ldg(a.pwr + xq) : (ty ? __ldg(a.amat + (int64_t)x * k + ly) : 0.0);
+                            const double Aylx = SPARSE ? __ldg(a.wps + xq) : (lx < k ? Ay[lx] : 0.0);
                             // a_y(c_z), beside z in y's slot (the other run holds 0)
                             const int64_t ypos = by + (!zt ? pyt + iz : ((local && !SPARSE) ? pyt - 1 - iz : iz));
                             const double Aylz = __ldg(a.wps + ypos);
@@ -751,7 +744,7 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
         cudaError_t e = build_e_items(c, it);
         if (e != cudaSuccess) return e;
     }
-    const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.sparse ? kChunkE : c.k);
+    const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.sparse ? 0 : c.k);
     static bool attr_set[2][2] = {{false, false}, {false, false}};
     if (!attr_set[COUNT][SPARSE]) {
         cudaFuncSetAttribute(k_phase_e<COUNT, SPARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
