@@ -762,7 +762,10 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
         cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
         if (n_heavy < c.n) {                              // light first (see rs_score)
             const int64_t threads = c.n - n_heavy;        // a warp per 32 vertices
-            const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * 32);
+#ifndef RS_EXP_LIGHT_BLK
+#define RS_EXP_LIGHT_BLK 4   // 148 x 4 blocks of 8 warps: 32 warps per SM beside the heavy kernel and Phase D
+#endif
+            const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * RS_EXP_LIGHT_BLK);
             k_phase_e_light<COUNT, SPARSE><<<(unsigned)blocks, 256, 0, light>>>(a, n_heavy);
             c.launches++;
         }
