@@ -397,11 +397,14 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_a_cta(PhaseAArgs a) {
     block_max_to_scal(wmax, a.scal);
 }
 
+#ifndef RS_EXP_A_BLK
+#define RS_EXP_A_BLK 16   // warp-class grids: 148 x RS_EXP_A_BLK blocks of 8 warps (grid-stride)
+#endif
 template <int G, int U, bool SMEM>
 static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
     const int64_t gpb = 256 / G;
     int64_t blocks = (a.nverts + gpb - 1) / gpb;
-    blocks = std::min<int64_t>(blocks, 148 * 16);
+    blocks = std::min<int64_t>(blocks, 148 * RS_EXP_A_BLK);
     if (blocks < 1) return;
     k_phase_a_warp<G, U, SMEM><<<(unsigned)blocks, 256, 0, s>>>(a);
     c.launches++;

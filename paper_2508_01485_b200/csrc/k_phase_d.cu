@@ -125,10 +125,13 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_d_cta(CdeArgs a) {
 // ============================================================================
 // launchers
 // ============================================================================
+#ifndef RS_EXP_D_BLK
+#define RS_EXP_D_BLK 16   // warp-class grids: 148 x RS_EXP_D_BLK blocks of 8 warps (grid-stride)
+#endif
 template <class K>
 static void launch_grid(Ctx &c, K kern, int64_t groups, int gpb, cudaStream_t s, const CdeArgs &a) {
     int64_t blocks = (groups + gpb - 1) / gpb;
-    blocks = std::min<int64_t>(blocks, 148 * 16);
+    blocks = std::min<int64_t>(blocks, 148 * RS_EXP_D_BLK);
     if (blocks < 1) return;
     kern<<<(unsigned)blocks, 256, 0, s>>>(a);
     c.launches++;
