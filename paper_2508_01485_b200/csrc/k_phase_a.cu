@@ -410,10 +410,23 @@ static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
     c.launches++;
 }
 
+// experiment knobs (lanes per vertex of classes 2-4, loads in flight of class 1)
+#ifndef RS_EXP_A_G4
+#define RS_EXP_A_G4 32
+#endif
+#ifndef RS_EXP_A_G3
+#define RS_EXP_A_G3 8
+#endif
+#ifndef RS_EXP_A_G2
+#define RS_EXP_A_G2 8
+#endif
+#ifndef RS_EXP_A_U1
+#define RS_EXP_A_U1 4
+#endif
 template <bool SMEM>
 static void launch_bins_a(Ctx &c, PhaseAArgs base) {
     // class -> (lanes per vertex, loads in flight per lane), G*U about the row length:
-    // [0,8):4x2 [8,16):4x4 [16,32):8x4 [32,64):16x4 [64,2048):32x4 [2048,inf):CTAx4
+    // [0,8):4x2 [8,16):4x4 [16,32):8x4 [32,64):8x4 [64,2048):32x4 [2048,inf):CTAx4
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         PhaseAArgs a = base;
         a.vlo = c.bins.offset[cls];
@@ -424,14 +437,16 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
             int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
             k_phase_a_cta<SMEM><<<(unsigned)blocks, kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (SMEM || cls >= 4) {
+        } else if (SMEM || cls >= 5) {
             launch_warp_bin<32, 4, SMEM>(c, a, s);
+        } else if (cls == 4) {
+            launch_warp_bin<RS_EXP_A_G4, 4, SMEM>(c, a, s);
         } else if (cls == 3) {
-            launch_warp_bin<16, 4, SMEM>(c, a, s);
+            launch_warp_bin<RS_EXP_A_G3, 4, SMEM>(c, a, s);
         } else if (cls == 2) {
-            launch_warp_bin<8, 4, SMEM>(c, a, s);
+            launch_warp_bin<RS_EXP_A_G2, 4, SMEM>(c, a, s);
         } else if (cls == 1) {
-            launch_warp_bin<4, 4, SMEM>(c, a, s);
+            launch_warp_bin<4, RS_EXP_A_U1, SMEM>(c, a, s);
         } else {
             launch_warp_bin<4, 2, SMEM>(c, a, s);
         }
