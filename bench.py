@@ -38,11 +38,11 @@ METRIC = "RSI-scored edges/sec (GTEPS)"
 # DRAM bytes per launch of the dominant phase from the committed ncu captures
 # (profiles/); filled per round, None when not captured for that config
 # ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per step of the
-# dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 4.315 +
-# 0.113 GB, light 1.222 + 0.020 GB) + the Phase D launches of
-# profiles/r01_full_phaseAD_summary.txt (1.687 + 0.056 GB); ncu flushes the L2
+# dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 4.325 +
+# 0.114 GB, light 1.222 + 0.018 GB) + the Phase D launches of
+# profiles/r01_full_phaseAD_summary.txt (1.689 + 0.053 GB); ncu flushes the L2
 # before each kernel, so this bounds the in-step traffic from above
-TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 7.413e9}}
+TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 7.421e9}}
 UNIT = "GTEPS"
 
 
