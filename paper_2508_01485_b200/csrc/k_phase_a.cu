@@ -420,6 +420,15 @@ static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
 #ifndef RS_EXP_A_G2
 #define RS_EXP_A_G2 8
 #endif
+#ifndef RS_EXP_A_U3
+#define RS_EXP_A_U3 4
+#endif
+#ifndef RS_EXP_A_U2
+#define RS_EXP_A_U2 4
+#endif
+#ifndef RS_EXP_A_CTA_CLS
+#define RS_EXP_A_CTA_CLS 6   // first degree class run by a CTA per vertex
+#endif
 #ifndef RS_EXP_A_U1
 #define RS_EXP_A_U1 4
 #endif
@@ -433,7 +442,7 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
         a.nverts = c.bins.count[cls];
         if (a.nverts == 0) continue;
         cudaStream_t s = c.side[cls];
-        if (cls >= 6) {
+        if (cls >= RS_EXP_A_CTA_CLS) {
             int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
             k_phase_a_cta<SMEM><<<(unsigned)blocks, kCtaThreads, 0, s>>>(a);
             c.launches++;
@@ -442,9 +451,9 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
         } else if (cls == 4) {
             launch_warp_bin<RS_EXP_A_G4, 4, SMEM>(c, a, s);
         } else if (cls == 3) {
-            launch_warp_bin<RS_EXP_A_G3, 4, SMEM>(c, a, s);
+            launch_warp_bin<RS_EXP_A_G3, RS_EXP_A_U3, SMEM>(c, a, s);
         } else if (cls == 2) {
-            launch_warp_bin<RS_EXP_A_G2, 4, SMEM>(c, a, s);
+            launch_warp_bin<RS_EXP_A_G2, RS_EXP_A_U2, SMEM>(c, a, s);
         } else if (cls == 1) {
             launch_warp_bin<4, RS_EXP_A_U1, SMEM>(c, a, s);
         } else {
