@@ -427,7 +427,7 @@ static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
 #define RS_EXP_A_U2 4
 #endif
 #ifndef RS_EXP_A_CTA_CLS
-#define RS_EXP_A_CTA_CLS 6   // first degree class run by a CTA per vertex
+#define RS_EXP_A_CTA_CLS 7   // first degree class run by a CTA per vertex (class 6 on 32-lane groups)
 #endif
 #ifndef RS_EXP_A_U1
 #define RS_EXP_A_U1 4
@@ -435,7 +435,7 @@ static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
 template <bool SMEM>
 static void launch_bins_a(Ctx &c, PhaseAArgs base) {
     // class -> (lanes per vertex, loads in flight per lane), G*U about the row length:
-    // [0,8):4x2 [8,16):4x4 [16,32):8x4 [32,64):8x4 [64,2048):32x4 [2048,inf):CTAx4
+    // [0,8):4x2 [8,16):4x4 [16,32):8x4 [32,64):8x4 [64,8192):32x4 [8192,inf):CTAx4 (bins: kNumBins)
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         PhaseAArgs a = base;
         a.vlo = c.bins.offset[cls];
