@@ -139,6 +139,9 @@ static void launch_grid(Ctx &c, K kern, int64_t groups, int gpb, cudaStream_t s,
 
 // Type-II pull bins (lanes x loads per lane; |P| is about a quarter of d):
 // [0,32):4x2 [32,64):4x4 [64,128):8x4 [128,2048):32x4 [2048,inf):CTAx4
+#ifndef RS_EXP_D_CTA_CLS
+#define RS_EXP_D_CTA_CLS 6   // first degree class run by a CTA per head
+#endif
 template <bool SPARSE>
 static cudaError_t launch_phase_d_t(Ctx &c) {
     CdeArgs base = cde_args(c);
@@ -148,10 +151,10 @@ static cudaError_t launch_phase_d_t(Ctx &c) {
         a.nverts = c.bins.count[cls];
         if (!a.nverts) continue;
         cudaStream_t s = c.side[cls];
-        if (cls >= 6) {
+        if (cls >= RS_EXP_D_CTA_CLS) {
             k_phase_d_cta<SPARSE><<<(unsigned)std::min<int64_t>(a.nverts, 148 * 8), kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (cls == 5) launch_grid(c, k_phase_d_warp<32, 4, SPARSE>, a.nverts, 8, s, a);
+        } else if (cls >= 5) launch_grid(c, k_phase_d_warp<32, 4, SPARSE>, a.nverts, 8, s, a);
         else if (cls == 4) launch_grid(c, k_phase_d_warp<8, 4, SPARSE>, a.nverts, 32, s, a);
         else if (cls == 3) launch_grid(c, k_phase_d_warp<4, 4, SPARSE>, a.nverts, 64, s, a);
         else launch_grid(c, k_phase_d_warp<4, 2, SPARSE>, a.nverts, 64, s, a);
