@@ -35,14 +35,6 @@ sys.path.insert(0, REPO)
 import gen  # noqa: E402
 
 METRIC = "RSI-scored edges/sec (GTEPS)"
-# DRAM bytes per launch of the dominant phase from the committed ncu captures
-# (profiles/); filled per round, None when not captured for that config
-# ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per step of the
-# dominant phase (E || D): profiles/r01_full_phaseE_summary.txt (heavy 4.325 +
-# 0.114 GB, light 1.222 + 0.018 GB) + the Phase D launches of
-# profiles/r01_full_phaseAD_summary.txt (1.689 + 0.053 GB); ncu flushes the L2
-# before each kernel, so this bounds the in-step traffic from above
-TRAFFIC_NCU = {"orkut": {"ED_type1_type2": 7.421e9}}
 UNIT = "GTEPS"
 
 
@@ -138,20 +130,53 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def phase_bytes(n, D, Db, k, ntri, nb, nprobe):
-    """Algorithmic DRAM bytes of each phase: what it must read or write at least
-    once (per-unit figures x units). Phase E: its intersection
-    volume (4 B per probed P+ entry), 20 B per G' edge (the P-
-    entry and the predecessor's record), 32 B per Type-I triangle (weights and
-    head updates) and y's weight rows."""
-    # A: row, labels, P(u) writes, weights (a and a^2 per column), vrec; then P(u)
-    # re-read, the P+ runs with their weights (half of P), the B pushes (8 B per
-    # P entry), PRec
+def survey_bytes(n, D, Db, k, ntri, nprobe):
+    """SURVEY §8(d)'s algorithmic-bytes table, term by term (4-byte ids, 1-byte
+    labels, 8-byte values): the HEADLINE roofline bytes. librs's Phase A fuses
+    §8(d)'s phases A (border + histogram + weights), B (P-list build) and C (B
+    table), so its bytes are their sum; E || D is §8(d)'s D (Type-II) + E
+    (Type-I: 4 B per probed entry + 16 B per matched triad); F is finalize."""
+    A = 4 * D + 8 * n + 1 * D + 4 * n + 8 * k * n + 8 * n
+    B = 4 * D + 8 * n + 1 * D + 4 * Db + 8 * n
+    C = 4 * Db + 8 * Db + 8 * k * n
+    Dt2 = 4 * Db + 8 * Db + 8 * Db + 8 * n
+    E = 4 * nprobe + 16 * ntri
+    F = 8 * n * 3
+    return {"A": A + B + C, "ED": Dt2 + E, "F": F}
+
+
+def fused_bytes(n, D, Db, k, ntri, nprobe):
+    """The bytes librs's fused pipeline moves at least once (DESIGN.md §6
+    kernel table): reported beside the survey figure, not as the headline."""
     A = 8 * (n + 1) + 4 * D + 1 * D + 1 * n + 4 * Db + 16 * k * n + 16 * n + 4 * Db + 6 * Db + 8 * Db + 16 * n
     E = 4 * nprobe + 20 * (Db // 2) + 32 * ntri + 8 * k * n
-    D_ = 4 * Db + 16 * Db + 16 * n + 16 * n                   # Type-II pull (16 B B records; concurrent with E)
-    F = 16 * n + 24 * n + 16 * n + 8 * n + 4 * n + 8 * n      # finalize: sums, vrec, rowptr, perm, score
+    D_ = 4 * Db + 16 * Db + 16 * n + 16 * n
+    F = 16 * n + 24 * n + 16 * n + 8 * n + 4 * n + 8 * n
     return {"A": A, "ED": E + D_, "F": F}
+
+
+def build_hash():
+    """sha256 (16 hex) of librs's sources: ties an ncu capture to the build it measured."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    for p in sorted(glob.glob(os.path.join(REPO, "paper_2508_01485_b200", "csrc", "*"))):
+        with open(p, "rb") as fh:
+            h.update(os.path.basename(p).encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_record(config):
+    """per-kernel ncu figures of the committed capture (profiles/ncu_kernels.json,
+    written by tools/ncu_kernels.py from one `ncu --set full` run of bench.py)"""
+    p = os.path.join(REPO, "profiles", "ncu_kernels.json")
+    if not os.path.exists(p):
+        return None
+    rec = json.load(open(p))
+    if rec.get("config") != config:
+        return None
+    rec["build_match"] = rec.get("build") == build_hash()
+    return rec
 
 
 def main():
@@ -264,26 +289,37 @@ def main():
     ph = np.median(np.array(ph), axis=0)
     names = ["A_hist_weights_lists", "ED_type1_type2", "F_finalize"]
     Db, nb, ntri, nprobe = st["n_pred_entries"], st["n_border"], st["n_triangles"], st["n_probes"]
-    pb = phase_bytes(n, D, Db, a.k, ntri, nb, nprobe)
+    sb = survey_bytes(n, D, Db, a.k, ntri, nprobe)
+    fb = fused_bytes(n, D, Db, a.k, ntri, nprobe)
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_peak = float(peaks.get("hbm_gbs", 6550.0))
     # every phase against the HBM roof (phase time = CUDA events on the library
-    # stream around the phase's launches); the dominant one is the headline
+    # stream around the phase's launches, median of 3 steps); the dominant one is
+    # the headline, with SURVEY §8(d)'s bytes (fused-pipeline bytes beside them)
     keys = {"A_hist_weights_lists": "A", "ED_type1_type2": "ED", "F_finalize": "F"}
     phases = {}
     for nm, ms in zip(names, ph):
-        by = pb[keys[nm]]
+        by, byf = sb[keys[nm]], fb[keys[nm]]
         gbs = by / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-        phases[nm] = {"ms": round(float(ms), 4), "alg_bytes": int(by), "GBps": round(gbs, 1),
-                      "frac": round(gbs / hbm_peak, 4)}
+        gbf = byf / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        phases[nm] = {"ms": round(float(ms), 4), "survey_bytes": int(by), "GBps": round(gbs, 1),
+                      "frac": round(gbs / hbm_peak, 4), "fused_bytes": int(byf), "fused_frac": round(gbf / hbm_peak, 4)}
     dom = max(phases, key=lambda x: phases[x]["ms"])
-    traffic = TRAFFIC_NCU.get(a.config, {}).get(dom)
+    ncu = ncu_record(a.config)
+    traffic, kernels = None, None
+    if ncu:
+        per = ncu.get("phase_dram_bytes", {}).get(keys[dom])
+        traffic = per
+        kernels = ncu.get("kernels")
     roof = {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["GBps"], "peak": hbm_peak, "unit": "GB/s",
             "frac": phases[dom]["frac"], "traffic": traffic,
-            "traffic_source": "profiles/ ncu --set full dram__bytes_read.sum+dram__bytes_write.sum per launch"
-            if traffic else None,
-            "phases": phases, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"}
+            "traffic_over_alg": round(traffic / phases[dom]["survey_bytes"], 3) if traffic else None,
+            "bytes_formula": "SURVEY §8(d) table (bench.py survey_bytes); fused-pipeline bytes as fused_*",
+            "traffic_source": (f"profiles/ncu_kernels.json ({ncu.get('source')}, build {ncu.get('build')}, "
+                               f"matches this build: {ncu['build_match']})") if ncu else None,
+            "phases": phases, "ncu_kernels": kernels,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"}
 
     # NEXT-1: absolute AWCC of the top-K under cumulative random
     # edge / node removal, 5 %..75 % (16 steps), per trial; rs_awcc_removal is
@@ -350,7 +386,7 @@ def main():
         e2e = measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = cpu_baseline(g, a.k, budget_s=15.0)
+        cpu = cpu_baseline(g, a.k, budget_s=15.0, config=a.config)
 
     if rank == 0:
         clk_s = clk.summary()
@@ -485,9 +521,9 @@ def measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st):
 
 
 # ------------------------------------------------------------------ oracle arms
-def oracle_sample_step(g, k, n_heads, rng):
-    """O0-O4 over the whole graph + O5-O7 for n_heads sampled heads; returns
-    (seconds of O0-O4, seconds of the head sample, heads)."""
+def oracle_globals(g, k):
+    """O0-O4 over the whole graph (targets, border, counts, weights, omega_max)
+    and the G' lists; returns (targets, w, wmax, seconds)."""
     import oracle
     t0 = time.perf_counter()
     t = oracle.select_targets(g.comm, k)
@@ -496,61 +532,102 @@ def oracle_sample_step(g, k, n_heads, rng):
     w = oracle.weights(f)
     wmax = oracle.omega_max(w)
     oracle.pred(g)
-    t1 = time.perf_counter()
-    heads = rng.choice(g.n, size=min(n_heads, g.n), replace=False).astype(np.int64)
+    return t, w, wmax, time.perf_counter() - t0
+
+
+def oracle_heads(g, t, w, wmax, heads):
+    """O5-O7 on the given heads, single thread; returns (seconds, edges scored =
+    sum of d(u)/2 over the heads: an undirected edge is scored through both ends)"""
+    import oracle
+    t0 = time.perf_counter()
     oracle.rsi(g, t, w, wmax, heads)
-    t2 = time.perf_counter()
-    return t1 - t0, t2 - t1, heads.size
+    dt = time.perf_counter() - t0
+    return dt, float(np.diff(g.rowptr)[heads].sum()) / 2.0
 
 
-def oracle_rate(g, k, budget_s, rng):
-    # size the head sample so the whole sample takes about budget_s
-    glob_s, s_small, nh = oracle_sample_step(g, k, 200, rng)
-    per_head = max(s_small / nh, 1e-7)
-    nh2 = int(max(200, min(g.n, (max(budget_s - glob_s, 1.0)) / per_head)))
-    glob_s, head_s, nh2 = oracle_sample_step(g, k, nh2, rng)
-    full_s = glob_s + head_s * (g.n / nh2)       # extrapolated single-thread full run
-    return g.m / full_s / 1e9, glob_s, head_s, nh2, full_s
+def full_oracle_record(config):
+    """the committed full single-thread oracle run of this config (tools/oracle_timed.py)"""
+    p = os.path.join(REPO, "profiles", f"oracle_{config}.json")
+    if not os.path.exists(p):
+        return None
+    r = json.load(open(p))
+    return {"total_s": r.get("total_s"), "GTEPS": r.get("GTEPS"), "cpu": r.get("cpu"),
+            "source": f"profiles/oracle_{config}.json (tools/oracle_timed.py, full, 1 thread)"}
 
 
-def cpu_baseline(g, k, budget_s=15.0):
+def cpu_baseline(g, k, budget_s=15.0, config=""):
+    """The oracle as it stands, one thread: O0-O4 over the whole graph, then
+    O5-O7 on random head batches for about budget_s; the rate is edges scored /
+    s over the batches (mean and standard error over the batches) and the
+    single-thread whole-graph time it implies; the full run is cited if one
+    was recorded for this config."""
     import oracle
     oracle.build()
     rng = np.random.default_rng(0)
-    val, glob_s, head_s, nh, full_s = oracle_rate(g, k, budget_s, rng)
-    return {"value": round(val, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"O0-O4 on the whole graph ({glob_s:.1f}s) + O5-O7 on {nh} random heads ({head_s:.1f}s), "
-                      f"extrapolated to all {g.n} heads: {full_s:.0f}s single-thread",
-            "host_cores": os.cpu_count()}
+    t, w, wmax, glob_s = oracle_globals(g, k)
+    probe_s, _ = oracle_heads(g, t, w, wmax, rng.choice(g.n, size=min(200, g.n), replace=False).astype(np.int64))
+    per_head = max(probe_s / min(200, g.n), 1e-7)
+    nb = 10
+    batch = int(max(50, min(g.n // nb, budget_s / nb / per_head)))
+    rates, heads_done, secs = [], 0, 0.0
+    for _ in range(nb):
+        h = rng.choice(g.n, size=batch, replace=False).astype(np.int64)
+        dt, e = oracle_heads(g, t, w, wmax, h)
+        rates.append(e / dt / 1e9)
+        heads_done += h.size
+        secs += dt
+    rates = np.array(rates)
+    mean, se = float(rates.mean()), float(rates.std(ddof=1) / np.sqrt(len(rates)))
+    full_s = glob_s + g.m / (mean * 1e9)
+    return {"value": round(g.m / full_s / 1e9, 7), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"O0-O4 on the whole graph ({glob_s:.1f}s) + O5-O7 on {nb} batches of {batch} random heads "
+                      f"({secs:.1f}s): {mean:.3e} +- {se:.1e} (SE) GTEPS over the batches, i.e. ~{full_s:.0f}s "
+                      f"single-thread for the whole graph",
+            "batch_GTEPS_mean": mean, "batch_GTEPS_se": se, "extrapolated_full_s": round(full_s, 1),
+            "full_run": full_oracle_record(config), "host_cores": os.cpu_count()}
 
 
 def reference_arm(a, rank, world):
+    """--impl reference: the oracle as it stands (oracle/, one thread) on the
+    repo arm's workload. O0-O4 run once, untimed, before the steps; each
+    (warm-up or timed) step is O5-O7 on a fresh random sample of heads sized so
+    the run stays within minutes. ms_per_step is the measured time of exactly
+    that work, value = edges scored by the sampled heads / time; the
+    whole-graph extrapolation is a separate field."""
     if rank != 0:
         return
     import oracle
     oracle.build()
     g = load_graph(a.config)
     rng = np.random.default_rng(0)
-    budget = 8.0 if a.config in ("orkut", "lj", "friendster") else 2.0
-    # size the per-step head sample once
-    glob_s, s_small, nh = oracle_sample_step(g, a.k, 100, rng)
-    per_head = max(s_small / nh, 1e-7)
-    nh_step = int(max(100, min(g.n, max(budget - glob_s, 0.5) / per_head)))
-    vals = []
+    t, w, wmax, glob_s = oracle_globals(g, a.k)
+    probe_s, _ = oracle_heads(g, t, w, wmax, rng.choice(g.n, size=min(100, g.n), replace=False).astype(np.int64))
+    per_head = max(probe_s / min(100, g.n), 1e-7)
+    budget = 6.0 if a.config in ("orkut", "lj", "friendster") else 1.0
+    nh = int(max(50, min(g.n, budget / per_head)))
+    secs, edges = [], []
     for i in range(a.warmup + a.steps):
-        gs, hs, nh2 = oracle_sample_step(g, a.k, nh_step, rng)
+        h = rng.choice(g.n, size=nh, replace=False).astype(np.int64)
+        dt, e = oracle_heads(g, t, w, wmax, h)
         if i >= a.warmup:
-            vals.append(gs + hs * (g.n / nh2))
-    full_s = float(np.mean(vals))
-    value = g.m / full_s / 1e9
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(full_s * 1e3, 1), "higher_is_better": True,
+            secs.append(dt)
+            edges.append(e)
+    ms = 1e3 * float(np.mean(secs))
+    value = float(np.sum(edges)) / float(np.sum(secs)) / 1e9
+    full_s = glob_s + g.m / (value * 1e9)
+    cpu = {"value": round(value, 7), "unit": UNIT, "kind": "oracle", "cores": 1,
+           "sample": f"per step: O5-O7 on {nh} random heads (one thread); O0-O4 over the whole graph ran once "
+                     f"before the steps ({glob_s:.1f}s, untimed)"}
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 7), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{a.config}-shape DC-SBM (SURVEY §8(d))", "n": g.n, "m": g.m, "k_targets": a.k},
-            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "kind": "oracle", "cores": 1,
-                             "sample": f"per step: O0-O4 on the whole graph + O5-O7 on {nh_step} random heads, "
-                                       f"extrapolated to all {g.n} heads (single thread)"},
-            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": f"{a.config}-shape DC-SBM (SURVEY §8(d))", "n": g.n, "m": g.m, "k_targets": a.k,
+                       "heads_per_step": nh},
+            "cpu_baseline": cpu,
+            "extrapolated_full_graph": {"seconds": round(full_s, 1), "GTEPS": round(g.m / full_s / 1e9, 7),
+                                        "how": "O0-O4 time + m / measured edge rate (not timed as one run)",
+                                        "full_run": full_oracle_record(a.config)},
+            "e2e": {"value": round(value, 7), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 

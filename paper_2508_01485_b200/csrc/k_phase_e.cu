@@ -745,11 +745,9 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
         if (e != cudaSuccess) return e;
     }
     const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.sparse ? 0 : c.k);
-    static bool attr_set[2][2] = {{false, false}, {false, false}};
-    if (!attr_set[COUNT][SPARSE]) {
-        cudaFuncSetAttribute(k_phase_e<COUNT, SPARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set[COUNT][SPARSE] = true;
-    }
+    // per launch: the attribute is per device (a process may hold contexts on
+    // several GPUs), and the call is cheap next to the kernel
+    cudaFuncSetAttribute(k_phase_e<COUNT, SPARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase_e<COUNT, SPARSE>, kWarpsE * 32, smem);
     int sms = 148;

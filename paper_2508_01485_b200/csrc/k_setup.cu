@@ -453,13 +453,20 @@ cudaError_t launch_minmax_i32(Ctx &c, const int32_t *a, int64_t n, int64_t *mn, 
 
 constexpr int kHistSmem = 8192;
 
-__global__ void k_comm_hist(const int32_t *__restrict__ comm, int64_t n, int32_t *hist, int64_t nbins) {
+// community sizes; an id outside [0, nbins) is not counted but flagged in
+// scal[kScalErr] (12: negative, 13: >= nbins, i.e. the histogram must grow)
+__global__ void k_comm_hist(const int32_t *__restrict__ comm, int64_t n, int32_t *hist, int64_t nbins,
+                            unsigned long long *scal) {
     __shared__ int s[kHistSmem];
     const bool priv = nbins <= kHistSmem;
     if (priv) for (int i = threadIdx.x; i < nbins; i += blockDim.x) s[i] = 0;
     __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t cid = comm[i];
+        if (cid < 0 || cid >= nbins) {
+            atomicMax(&scal[kScalErr], cid < 0 ? 12ull : 13ull);
+            continue;
+        }
         if (priv) atomicAdd(&s[cid], 1); else atomicAdd(&hist[cid], 1);
     }
     __syncthreads();
@@ -582,7 +589,7 @@ __global__ void k_nwide(const int64_t *__restrict__ rowptr, int64_t n, double bo
 
 void launch_comm_hist(Ctx &c, int64_t nbins) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((c.n + 255) / 256, 148 * 4));
-    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.n, c.chist, nbins);
+    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.n, c.chist, nbins, c.scal);
     c.launches++;
 }
 void launch_nwide(Ctx &c, double bound) {
@@ -595,7 +602,7 @@ cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user
     cudaMemsetAsync(c.chist, 0, sizeof(int32_t) * nbins, c.stream);
     int blocks = (int)std::min<int64_t>((c.n + 255) / 256, 148 * 4);
     if (blocks < 1) blocks = 1;
-    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.n, c.chist, nbins);
+    k_comm_hist<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.n, c.chist, nbins, c.scal);
     c.launches++;
     k_select<<<1, kSelThreads, 0, c.stream>>>(c.chist, nbins, c.k, user_targets, c.targets, c.ccode, c.scal);
     c.launches++;

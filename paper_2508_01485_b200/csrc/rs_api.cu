@@ -434,18 +434,32 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     c.has_comm = false;
     CK(cudaMemcpyAsync(c.comm_in, community_of, sizeof(int32_t) * c.n,
                        is_device_ptr(community_of) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
-    int64_t mn = 0, mx = 0;
-    CK(rs::launch_minmax_i32(c, c.comm_in, c.n, &mn, &mx));
-    if (mn < 0) return fail(ctx, RS_EINVAL, "rs_set_communities: negative community id");
-    if (mx >= (1ll << 28)) return fail(ctx, RS_EINVAL, "rs_set_communities: community id >= 2^28");
-    if (mx + 1 > c.ccap) {
-        int64_t cap = std::max<int64_t>(mx + 1, 1024);
-        CK(dalloc(&c.chist, cap));
-        CK(dalloc(&c.ccode, cap));
-        CK(dalloc(&c.code32, cap));
-        c.ccap = cap;
+    // the id range sizes the community histogram: measured (one host round trip)
+    // on the first call and whenever an id reaches the current capacity; in the
+    // steady state the histogram kernel itself flags out-of-range ids, so the
+    // call synchronises with the host once (to report errors and the targets)
+    auto grow = [&](bool &is_all_ok) -> rs_status {
+        int64_t mn = 0, mx = 0;
+        CK(rs::launch_minmax_i32(c, c.comm_in, c.n, &mn, &mx));
+        if (mn < 0) return fail(ctx, RS_EINVAL, "rs_set_communities: negative community id");
+        if (mx >= (1ll << 28)) return fail(ctx, RS_EINVAL, "rs_set_communities: community id >= 2^28");
+        if (mx + 1 > c.ccap) {
+            int64_t cap = std::max<int64_t>(mx + 1, 1024);
+            CK(dalloc(&c.chist, cap));
+            CK(dalloc(&c.ccode, cap));
+            CK(dalloc(&c.code32, cap));
+            c.ccap = cap;
+        }
+        c.cmax = mx;
+        is_all_ok = true;
+        return RS_OK;
+    };
+    bool ok = false;
+    if (all || c.ccap == 0) {
+        rs_status st = grow(ok);
+        if (st != RS_OK) return st;
     }
-    if (all) return set_communities_all(ctx, mx);
+    if (all) return set_communities_all(ctx, c.cmax);
     c.sparse = false;
     if (c.k_alloc != k || c.kn_alloc != c.n) {
         CK(dalloc(&c.f, (size_t)c.n * k));
@@ -463,15 +477,22 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
                            is_device_ptr(targets) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
         ut = ctx->utargets;
     }
-    CK(cudaMemsetAsync(c.scal + rs::kScalErr, 0, sizeof(unsigned long long), c.stream));
-    CK(rs::launch_set_communities(c, mx, ut));
-    unsigned long long er = 0, ndist = 0;
-    CK(cudaMemcpyAsync(&er, c.scal + rs::kScalErr, sizeof(er), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaMemcpyAsync(&ndist, c.scal + rs::kScalCnt0, sizeof(ndist), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaMemcpyAsync(c.h_targets, c.targets, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c.stream));
-    unsigned long long nw = 0;
-    CK(cudaMemcpyAsync(&nw, c.scal + rs::kScalNWide, sizeof(nw), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
+    unsigned long long er = 0, ndist = 0, nw = 0;
+    for (int attempt = 0; attempt < 2; attempt++) {
+        CK(cudaMemsetAsync(c.scal + rs::kScalErr, 0, sizeof(unsigned long long), c.stream));
+        // histogram over the whole capacity (ids beyond the largest seen count 0)
+        CK(rs::launch_set_communities(c, c.ccap - 1, ut));
+        CK(cudaMemcpyAsync(&er, c.scal + rs::kScalErr, sizeof(er), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(&ndist, c.scal + rs::kScalCnt0, sizeof(ndist), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(c.h_targets, c.targets, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(&nw, c.scal + rs::kScalNWide, sizeof(nw), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        if (er != 12 && er != 13) break;
+        // an id outside the histogram: measure the range (errors) and grow, once
+        rs_status st = grow(ok);
+        if (st != RS_OK) return st;
+    }
+    if (er == 12 || er == 13) return fail(ctx, RS_EINVAL, "rs_set_communities: community id out of range");
     c.n_wide = (int64_t)nw;
     {
         // B table grid: a <= (k log2(k - 1))^(1/3) (the wide_bound weight bound) and
@@ -976,6 +997,9 @@ extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_
         if (s) return s;
     }
     if (type2_out) {
+        // dense mode: n_II(u) = sum_{w in P(u)} (f_w[c_u] - 1) reads the count table f,
+        // which rs_score does not write (parity tables, filled on demand)
+        if (!c.sparse) CK(ensure_parity_tables(ctx));
         CK(c.sparse ? rs::launch_sparse_type2(c, tmp) : rs::launch_type2_counts(c, tmp));
         rs_status s = out_copy(ctx, type2_out, tmp, (size_t)c.n);
         if (s) return s;

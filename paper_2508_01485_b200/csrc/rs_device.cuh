@@ -12,7 +12,9 @@ namespace rs {
 // IEEE bits) and the grid integers are summed exactly in 128 bits, so the sum
 // does not depend on the order threads add them (C-12). Terms are
 // unnormalised (omega_max is applied once in the epilogue), bounded by
-// omega_max <= (k-1) log2(k-1) < 2^11, so every per-head sum is < 2^96.
+// omega_max <= k log2(k-1) (wide_bound): < 2^11 for the dense k <= 254, about
+// 2^17 in the all-communities mode at 10^4 communities, so a term is < 2^18 and
+// every per-head sum stays far below 2^128.
 // ---------------------------------------------------------------------------
 struct U128 {
     unsigned long long lo, hi;

@@ -157,6 +157,7 @@ struct Ctx {
     int32_t *chist = nullptr;    // community sizes, cap entries
     uint8_t *ccode = nullptr;    // community id -> 8-bit code
     int64_t ccap = 0;
+    int64_t cmax = 0;            // largest community id measured (sizes the histogram)
     int32_t *targets = nullptr;  // kMaxK
     int32_t k = 0;
     int32_t h_targets[kMaxK];

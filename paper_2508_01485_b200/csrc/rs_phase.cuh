@@ -2,6 +2,8 @@
 #pragma once
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
+#include <algorithm>
+#include <cmath>
 
 namespace rs {
 

@@ -3,6 +3,8 @@
 compare element by element."""
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 import oracle
@@ -47,20 +49,27 @@ def assert_scores_close(R_or, R_gpu, rtol=SCORE_RTOL, heads=None):
         assert rel[i] <= rtol, f"max rel err {rel[i]:.3e} at {np.nonzero(nz)[0][i]}"
 
 
-def assert_topk(ids_or, ids_gpu, R_or_of, rtol=SCORE_RTOL):
-    """IDs exact; a position may differ only between vertices whose oracle
-    scores are equal within rtol (near-tie, reading C-13)."""
+NEAR_TIE_RTOL = 1e-12  # SURVEY C-13: an id swap is a numerics near-tie only inside this window
+
+
+def assert_topk(ids_or, ids_gpu, R_or_of, rtol=NEAR_TIE_RTOL):
+    """IDs exact; a position may differ only between vertices whose ORACLE
+    scores are equal within 1e-12 relative (a near-tie, SURVEY reading C-13,
+    where last-ulp differences between libm implementations can flip the id
+    order). Returns the list of near-tie swaps (reported by the callers)."""
     ids_or = list(map(int, ids_or))
     ids_gpu = list(map(int, ids_gpu))
     assert len(ids_or) == len(ids_gpu)
     if ids_or == ids_gpu:
-        return 0
-    swaps = 0
+        return []
+    swaps = []
     for a, b in zip(ids_or, ids_gpu):
         if a != b:
             ra, rb = R_or_of(a), R_or_of(b)
             assert abs(ra - rb) <= rtol * max(abs(ra), abs(rb)), f"top-k differs: oracle {a}({ra!r}) gpu {b}({rb!r})"
-            swaps += 1
+            swaps.append((a, b, ra, rb))
+    if swaps:
+        warnings.warn(f"top-K near-tie swaps (oracle scores within {rtol:g}): {swaps[:5]}")
     return swaps
 
 
@@ -83,8 +92,10 @@ def compare_full(g, r_or, r_gpu, exact_topk=False):
     np.testing.assert_array_equal(r_or.nI, r_gpu["nI"])
     np.testing.assert_array_equal(r_or.nII, r_gpu["nII"])
     assert_scores_close(r_or.R, r_gpu["R"])
+    swaps = []
     if exact_topk:
         assert list(r_or.top_ids) == list(r_gpu["top_ids"])
     else:
-        assert_topk(r_or.top_ids, r_gpu["top_ids"], lambda v: r_or.R[v])
+        swaps = assert_topk(r_or.top_ids, r_gpu["top_ids"], lambda v: r_or.R[v])
     np.testing.assert_allclose(r_gpu["top_scores"], r_gpu["R"][r_gpu["top_ids"]], rtol=0, atol=0)
+    return swaps

@@ -110,36 +110,6 @@ def test_dblp_full_size():
     full(g, k=5, K=25)
 
 
-@pytest.mark.parametrize("name", ["lj", "orkut"])
-def test_full_size_sampled(name):
-    """BASELINE-size graphs in the bench's launch configuration: every vertex's
-    counts / weights / G' list bit-exact, scores on a sample of heads (random +
-    the GPU's top-25 + the highest-degree heads) against the oracle one by one,
-    and the top-k property on the sample."""
-    g = gen.config_graph(name)
-    r_gpu = run_gpu(g, k=5, K=25, validate=False)
-    t = oracle.select_targets(g.comm, 5)
-    assert np.array_equal(t, r_gpu["targets"])
-    f, T = oracle.counts(g, t)
-    assert np.array_equal(f, r_gpu["f"]) and np.array_equal(T, r_gpu["T"])
-    w = oracle.weights(f)
-    wmax = oracle.omega_max(w)
-    nz = w != 0
-    assert np.array_equal(nz, r_gpu["omega"] != 0)
-    assert np.max(np.abs(r_gpu["omega"][nz] - w[nz]) / w[nz]) <= 1e-10
-    assert np.array_equal(np.nonzero(oracle.border(g))[0].astype(np.int32), r_gpu["border"])
-    rng = np.random.default_rng(1)
-    deg = np.diff(g.rowptr)
-    heads = np.unique(np.concatenate([rng.integers(0, g.n, 400), r_gpu["top_ids"].astype(np.int64),
-                                      np.argsort(deg)[-20:]]))
-    R, nI, nII = oracle.rsi(g, t, w, wmax, heads)
-    assert_scores_close(R, r_gpu["R"][heads])
-    np.testing.assert_array_equal(nI, r_gpu["nI"][heads])
-    np.testing.assert_array_equal(nII, r_gpu["nII"][heads])
-    kth = r_gpu["top_scores"][-1]
-    assert np.all(R[~np.isin(heads, r_gpu["top_ids"])] <= kth * (1 + 1e-9))
-
-
 # ---------------------------------------------------------------- API behaviour
 def test_determinism_and_reuse():
     g = gen.config_graph("orkut", scale=0.003)
@@ -171,6 +141,28 @@ def test_phase_e_rank_split_emulated(shares):
     assert np.array_equal(R1.view(np.uint64), R2.view(np.uint64))
     assert np.array_equal(t1a, t1b)
     assert st1["n_triangles"] == st2["n_triangles"] and st1["n_probes"] == st2["n_probes"]
+
+
+def test_triad_counts_right_after_score():
+    """rs_get_triad_counts straight after rs_score, with no other getter before it,
+    on a fresh context and again after switching to other communities (and another
+    k): n_I and n_II (the removal sets, C-1) must be the oracle's both times
+    (regression: n_II once read a count table only the counts getter filled)."""
+    g = gen.config_graph("orkut", scale=0.003)
+    rng = np.random.default_rng(31)
+    comm2 = rng.permutation(np.max(g.comm) + 1).astype(np.int32)[g.comm]   # relabelled communities
+    comm2[rng.integers(0, g.n, g.n // 5)] = 7                               # and a different partition
+    g2 = gen.Graph(g.rowptr, g.col, comm2)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    for gg, k in ((g, 5), (g2, 4), (g, 6)):
+        s.set_communities(gg.comm, k)
+        s.score()
+        t1, t2 = s.triad_counts()
+        r_or = oracle.run(gg, k=k, K=10)
+        np.testing.assert_array_equal(r_or.nI, t1)
+        np.testing.assert_array_equal(r_or.nII, t2)
+    s.close()
 
 
 def test_topk_edges_and_device_outputs():
