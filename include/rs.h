@@ -229,6 +229,12 @@ rs_status rs_get_targets(rs_ctx *ctx, int32_t *targets_out, int32_t *k_out);
 /* Number of librs kernels launched on ctx since creation (bench accounting). */
 int64_t rs_kernel_launches(const rs_ctx *ctx);
 
+/* Test hook, process-wide: byte in [0, 255] = every device allocation librs
+ * makes from now on is filled with that byte before use; -1 = off (default).
+ * A result that changes with the byte reveals a read of memory no kernel wrote
+ * (tests/test_gpu_hygiene.py; the stand-in for compute-sanitizer initcheck). */
+void rs_debug_poison(int32_t byte);
+
 /* ---- NEXT-1: robustness evaluation (PAPER §VII.B). ----
  * Absolute AWCC of the vertex set S (original ids, e.g. the top-K of rs_topk)
  * under cumulative random removal: AWCC = (1/|S|) sum_{v in S} |zeta(v)|/d(v),

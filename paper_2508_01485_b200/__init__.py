@@ -77,6 +77,7 @@ SIGNATURES = [
     ("rs_get_triad_counts", ctypes.c_int, [_P, _P, _P]),
     ("rs_get_targets", ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_int32)]),
     ("rs_kernel_launches", ctypes.c_int64, [_P]),
+    ("rs_debug_poison", None, [ctypes.c_int32]),
     ("rs_awcc_removal", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int32, ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
     ("rs_shii", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
@@ -253,6 +254,11 @@ def rs_get_targets(ctx):
     buf = np.empty(max(k.value, 1), dtype=np.int32)
     _check(ctx, load_library().rs_get_targets(ctx, _ptr(buf), ctypes.byref(k)))
     return buf[:k.value].copy()
+
+
+def rs_debug_poison(byte: int) -> None:
+    """test hook: fill every new librs device allocation with ``byte`` (-1 = off)"""
+    load_library().rs_debug_poison(int(byte))
 
 
 def rs_kernel_launches(ctx) -> int:

@@ -120,11 +120,11 @@ cudaError_t launch_pred_export(Ctx &c, int64_t *off_dev, int32_t *pred_dev, int6
     if (pred_dev && tot) {
         int32_t *unsorted = nullptr;
         void *stmp = nullptr;
-        if ((e = cudaMalloc(&unsorted, sizeof(int32_t) * tot))) return e;
+        if ((e = rs::dmalloc(&unsorted, sizeof(int32_t) * tot))) return e;
         k_pred_copy<<<148 * 8, 256, 0, c.stream>>>(c.rowptr, c.pidx, c.pc2, c.inv, c.perm, off, n, unsorted);
         size_t sneed = 0;
         cub::DeviceSegmentedSort::SortKeys(nullptr, sneed, unsorted, pred_dev, tot, (int)n, off, off + 1, c.stream);
-        if ((e = cudaMalloc(&stmp, std::max<size_t>(sneed, 1)))) { cudaFree(unsorted); return e; }
+        if ((e = rs::dmalloc(&stmp, std::max<size_t>(sneed, 1)))) { cudaFree(unsorted); return e; }
         cub::DeviceSegmentedSort::SortKeys(stmp, sneed, unsorted, pred_dev, tot, (int)n, off, off + 1, c.stream);
         c.launches += 2;
         e = cudaStreamSynchronize(c.stream);

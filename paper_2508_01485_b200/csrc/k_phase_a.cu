@@ -1,21 +1,30 @@
 // Phase A — one streaming pass over the CSR:
 //   Step 1 border test (Algorithm 1 lines P:254-263),
+//   Step 2d G' predecessor list P(u) = {x in N(u): C(x) != C(u)} (P:493), written
+//           in place at offset rowptr[u] (no scan needed), ascending, with the
+//           8-bit label of each entry beside it (plab),
 //   Step 2a neighbour-community histogram f[u][i] over the k targets,
+//           read off P(u): a target column c != C(u) counts the entries of P(u)
+//           labelled c, and f_u(C(u)) = d(u) - |P(u)| (every other neighbour
+//           shares u's community),
 //   Step 2b weights omega_u(C_i) = H(L_i) * (L_all - 1) (Eq. 3, Eq. 5, Algorithm 2
 //           P:457-482, closed form of Eq. H_optimal P:417 with exact zeros) and
 //           their cube roots a_u(C_i) used by every triad term (Eq. 4),
 //   Step 2c omega_max partial maxima,
-//   Step 2d G' predecessor list P(u) = {x in N(u): C(x) != C(u)} (P:493), written
-//           in place at offset rowptr[u] (no scan needed), ascending,
 // and, once u's weights are known, the inputs of Step 3: the orientation of G'
 // by internal id (P+(u) = the prefix of P(u) below u, split into its target run
 // and the rest, with a_u(c_z) beside each z) and u's pushes of a_u(c_u) into
-// B_w[c_u] for every w in P(u) (v in P(w) iff w in P(v)), exact 2-limb REDs.
+// B_w[c_u] for every w in P(u) (v in P(w) iff w in P(v)), exact integer REDs.
+//
+// The row walk is the only per-neighbour work: one coalesced column load, one
+// 1-byte label gather, one compare and one ballot per neighbour (profiled
+// round 1: the histogram, the P+ counts and their three ballots per neighbour
+// made the walk instruction-bound at ~145 warp instructions per 32 neighbours).
+// Everything else runs over P(u) (a quarter of the row at mu = 0.2).
 // Labels are the 8-bit community codes of rs_set_communities; only vertices of
 // two uncoded ("other") communities fall back to comparing full int32 ids.
 // Degree-binned: a group of G lanes (or a whole CTA for hubs) owns a vertex;
-// each lane keeps U independent loads in flight (the row walk is
-// latency-bound otherwise).
+// each lane keeps U independent loads in flight.
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
 
@@ -46,6 +55,7 @@ struct PhaseAArgs {
     double *__restrict__ amat;
     VRec *__restrict__ vrec;
     int32_t *__restrict__ pidx;
+    uint8_t *__restrict__ plab;         // label of each P(u) entry, beside it
     unsigned long long *scal;
 };
 
@@ -86,124 +96,181 @@ __device__ __forceinline__ bool in_max(const PhaseAArgs &a, int fc, int L_all, i
     return pc > 0 && L_of(a, fc, L_all) > 1 && (c == lu || fc > 0);
 }
 
-__device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, double a_self, int pc, uint8_t lu,
+__device__ __forceinline__ void write_vrec(const PhaseAArgs &a, int64_t u, double a_self, int pc, uint32_t lu,
                                            int64_t d) {
     VRec r;
     r.a_self = a_self;
     r.pcnt = pc;
-    r.lab = lu;
-    r.head = (lu < a.k && d >= 2) ? 1 : 0;
+    r.lab = (uint8_t)lu;
+    r.head = (lu < (uint32_t)a.k && d >= 2) ? 1 : 0;
     r.wide = ((double)d * (double)d >= a.wide_bound) ? 1 : 0;   // = (u < n_wide), degree-descending ids
     r.pad = 0;
     a.vrec[u] = r;
 }
 
-// Step 3 inputs of u (after its weights and amat row are written and the group
-// synchronised): B pushes, the P+ runs with a_u(c_z), the PRec record. P+(u)
-// is written as its target run DESCENDING at [0, pt) followed by the other run
-// ascending at [pt, pp): the entries below any y then form one contiguous range
-// around pt (Phase E probes only z < y).
-template <int U, class GR>
-__device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, int64_t u, GR &g, int64_t beg, int pc, int pp,
-                                              int pt, int lu) {
-    const int k = a.k;
-    const double *arow = a.amat + u * k;           // this group's writes, plain loads
-    const unsigned long long qs = lu < k ? bq_quantize(arow[lu], a.bq) : 0ull;
-    const bool push = qs != 0ull;
-    BQL *bcol = a.bql + (int64_t)(push ? lu : 0) * a.n;
-    int ct = 0, cn = 0;
-    for (int base = 0; base < pc; base += GR::size * U) {
-        int32_t v[U];
-        int lv[U];
+// Steps 1 + 2d for u: walk the row once and write P(u) (the foreign neighbours,
+// ascending) and their labels in place at rowptr[u]. Returns |P(u)| and |P+(u)|
+// (foreign neighbours below u) in every lane of the group. OTHER: u's
+// community has no 8-bit code of its own, so neighbours coded kOther are
+// compared by full community id.
+template <int U, bool OTHER, class GR>
+__device__ __forceinline__ void walk_row(const PhaseAArgs &a, int64_t u, int64_t beg, int d, uint32_t lu,
+                                         int32_t cfull, GR &g, int &pc_out, int &pp_out) {
+    const int32_t *__restrict__ row = a.col + beg;
+    int32_t *__restrict__ pout = a.pidx + beg;
+    uint8_t *__restrict__ lout = a.plab + beg;
+    int pc = 0, ppl = 0;
+    for (int base = 0; base < d; base += GR::size * U) {
+        int32_t x[U];
+        uint32_t l[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const int i = base + j * GR::size + (int)g.lane;
-            v[j] = i < pc ? a.pidx[beg + i] : -1;  // plain load: written by this group
+            x[j] = i < d ? __ldcs(row + i) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < U; j++) {
-            const int i = base + j * GR::size + (int)g.lane;
-            lv[j] = (v[j] >= 0 && i < pp) ? (int)__ldg(a.lab + v[j]) : (int)kOther;
-        }
+        for (int j = 0; j < U; j++) l[j] = x[j] >= 0 ? (uint32_t)__ldg(a.lab + x[j]) : lu;
+        bool f[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
-            const int i = base + j * GR::size + (int)g.lane;
-#ifndef RS_EXP_NO_BPUSH
-            if (push && v[j] >= 0) atomicAdd(&bcol[v[j]].b, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
-#endif
-            if (base + j * GR::size < pp) {                      // group-uniform
-                const bool inp = v[j] >= 0 && i < pp;
-                const bool tgt = inp && lv[j] < k;
-                int tt, tn;
-                const int rt = g.rank(tgt, &tt);
-                const int rn = g.rank(inp && !tgt, &tn);
-                if (inp) {
-                    // target run descending down from pt - 1, the rest ascending from pt
-                    const int64_t at = tgt ? beg + pt - 1 - (ct + rt) : beg + pt + cn + rn;
-                    a.pplus[at] = v[j];
-                    a.wps[at] = tgt ? arow[lv[j]] : 0.0;
-                }
-                ct += tt;
-                cn += tn;
+            f[j] = l[j] != lu;
+            if (OTHER && x[j] >= 0 && l[j] == kOther) f[j] = __ldg(a.comm + x[j]) != cfull;
+            ppl += (f[j] && x[j] < (int32_t)u) ? 1 : 0;
+        }
+        int r[U], tot[U];
+        g.template rank_u<U>(f, r, tot);
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            if (f[j]) {
+                pout[pc + r[j]] = x[j];
+                lout[pc + r[j]] = (uint8_t)l[j];
             }
+            pc += tot[j];
         }
     }
-    if (g.lane == 0) {
-        PRec r;
-        r.x = pp;
-        r.y = pc;
-        r.start = beg | ((long long)ct << kPrShift);
-        a.pc2[u] = r;
+    pc_out = pc;
+    pp_out = g.sum(ppl);
+}
+
+// Step 3 inputs of u (after its weights are known; au(c) = a_u(c)): B pushes
+// and the P+ runs with a_u(c_z), reading P(u) and its labels back from this
+// group's writes (k > 8 path). P+(u) is written as its
+// target run DESCENDING at [0, pt) followed by the other run ascending at
+// [pt, pp): an entry i of the prefix P+ has i predecessors in it, so its rank in
+// the other run is i minus the targets before it (one ballot).
+template <int U, class GR, class AU>
+__device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, GR &g, int64_t beg, int pc, int pp, int pt,
+                                              uint32_t lu, AU au) {
+    const uint32_t k = (uint32_t)a.k;
+    const unsigned long long qs = lu < k ? bq_quantize(au(lu), a.bq) : 0ull;
+    const bool push = qs != 0ull;
+    BQL *bcol = a.bql + (int64_t)(push ? lu : 0) * a.n;
+    const int32_t *__restrict__ pin = a.pidx + beg;
+    const uint8_t *__restrict__ lin = a.plab + beg;
+    int ct = 0;
+    for (int base = 0; base < pc; base += GR::size * U) {
+        int32_t v[U];
+        uint32_t lv[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            v[j] = i < pc ? pin[i] : -1;
+            lv[j] = i < pc ? (uint32_t)lin[i] : kOther;
+        }
+#ifndef RS_EXP_NO_BPUSH
+        if (push) {
+#pragma unroll
+            for (int j = 0; j < U; j++)
+                if (v[j] >= 0) atomicAdd(&bcol[v[j]].b, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
+        }
+#endif
+        if (base < pp) {                                     // group-uniform: P+ is the prefix [0, pp)
+            bool t[U];
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                const int i = base + j * GR::size + (int)g.lane;
+                t[j] = i < pp && lv[j] < k;
+            }
+            int rt[U], tt[U];
+            g.template rank_u<U>(t, rt, tt);
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                const int i = base + j * GR::size + (int)g.lane;
+                if (i < pp) {
+                    const int tb = ct + rt[j];                // target entries before i
+                    const int64_t at = t[j] ? beg + pt - 1 - tb : beg + pt + (i - tb);
+                    a.pplus[at] = v[j];
+                    a.wps[at] = t[j] ? au(lv[j]) : 0.0;
+                }
+                ct += tt[j];
+            }
+        }
     }
 }
 
-// k <= 8: per-lane register histogram.
+// k <= 8: Steps 1, 2a-2d and the Step 3 inputs of u, in lockstep over the
+// groups of a warp (LockGroup: warp-uniform loop bounds; u < 0 = no vertex).
+// The row walk keeps per-lane packed 16-bit histograms and P+ counts; one
+// ballot per neighbour compacts P(u). The lists pass reads P(u) and its labels
+// back (L2) and takes a_u(c) from the lane that computed it (shuffle).
 template <int U, class GR>
 __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
-    const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
-    const uint8_t lu = a.lab[u];
-    const int32_t cfull = (lu == kOther) ? a.comm[u] : 0;
-    const int k = a.k;
-    // per-lane histogram as 16-bit counters packed in two words (columns 0-3,
-    // 4-7): one shift and one add per neighbour. A lane sees at most
-    // ceil(d / G) neighbours < 2^16 (launch_phase_a_impl falls back to the
-    // shared-memory histogram when d_max >= 2^22).
+    const uint32_t k = (uint32_t)a.k;
+    const bool valid = u >= 0;
+    int64_t beg = 0;
+    int d = 0;
+    uint32_t lu = kOther;
+    int32_t cfull = 0;
+    if (valid) {
+        beg = a.rowptr[u];
+        d = (int)(a.rowptr[u + 1] - beg);
+        lu = a.lab[u];
+        if (lu == kOther) cfull = a.comm[u];
+    }
+    const bool other = lu == kOther;                 // compare kOther neighbours by full id
+    const bool wr = valid && !a.parity;
+    int32_t *__restrict__ pout = a.pidx + beg;
+    uint8_t *__restrict__ lout = a.plab + beg;
     unsigned long long h0 = 0ull, h1 = 0ull;
-    int pc = 0, pp = 0, pt = 0;   // |P(u)|, |P+(u)| (foreign neighbours below u), |P+_T(u)|
-    for (int64_t base = beg; base < end; base += GR::size * U) {
+    int pc = 0, ppl = 0, ptl = 0;
+    const int dw = g.umax(d);
+    for (int base = 0; base < dw; base += GR::size * U) {
         int32_t x[U];
-        uint8_t lx[U];
+        uint32_t l[U];
+        bool f[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
-            const int64_t e = base + j * GR::size + g.lane;
-            x[j] = e < end ? __ldcs(a.col + e) : -1;
+            const int i = base + j * GR::size + (int)g.lane;
+            x[j] = i < d ? __ldcs(a.col + beg + i) : -1;
         }
 #pragma unroll
-        for (int j = 0; j < U; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
+        for (int j = 0; j < U; j++) l[j] = x[j] >= 0 ? (uint32_t)__ldg(a.lab + x[j]) : lu;
 #pragma unroll
         for (int j = 0; j < U; j++) {
-            const bool valid = x[j] >= 0;
-            bool foreign = valid && (lx[j] != lu);
-            if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
-            const unsigned l = lx[j];
-            if (l < (unsigned)k) {
-                const unsigned long long inc = 1ull << ((l & 3u) * 16u);
-                if (l < 4u) h0 += inc; else h1 += inc;
+            f[j] = l[j] != lu;
+            if (other && x[j] >= 0 && l[j] == kOther) f[j] = __ldg(a.comm + x[j]) != cfull;
+            if (x[j] >= 0 && l[j] < k) {
+                const unsigned long long inc = 1ull << ((l[j] & 3u) * 16u);
+                if (l[j] < 4u) h0 += inc; else h1 += inc;
             }
-            if (base + j * GR::size < end) {          // group-uniform
-                int tot, totp, tott;
-                const int r = g.rank(foreign, &tot);
-                g.rank(foreign && x[j] < (int32_t)u, &totp);
-                g.rank(foreign && x[j] < (int32_t)u && l < (unsigned)k, &tott);
-                if (foreign && !a.parity) a.pidx[beg + pc + r] = x[j];
-                pc += tot;
-                pp += totp;
-                pt += tott;
+            const bool below = f[j] && x[j] < (int32_t)u;    // P+(u): foreign and above u
+            ppl += below ? 1 : 0;
+            ptl += (below && l[j] < k) ? 1 : 0;
+        }
+        int r[U], tot[U];
+        g.template rank_u<U>(f, r, tot);
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            if (f[j] && wr) {
+                pout[pc + r[j]] = x[j];
+                lout[pc + r[j]] = (uint8_t)l[j];
             }
+            pc += tot[j];
         }
     }
+    const int pp = g.sum(ppl), pt = g.sum(ptl);
     int cnt[8];
-    if (end - beg < 65536) {          // group totals still fit the 16-bit fields
+    if (dw < 65536) {         // group totals still fit the 16-bit fields
         h0 = g.sum(h0);
         h1 = g.sum(h1);
 #pragma unroll
@@ -226,8 +293,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
     }
     // Algorithm 2's X = sum f log2 f and every column's log2(T - f) with ONE
     // round of log2-table loads: lane l takes the columns l, l + G, ... (a
-    // vertex's weights are a dependent chain after its row walk; a second
-    // round of loads there cost ~0.4 ms of Phase A), X by a group sum
+    // vertex's weights are a dependent chain after its row walk), X by a group sum
     constexpr int NC = GR::size >= 8 ? 1 : 8 / GR::size;
     int fcs[NC];
     double xcs[NC], lys[NC];
@@ -240,78 +306,136 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
         for (int j = 0; j < 8; j++) fc = (j == c) ? cnt[j] : fc;
         fcs[i] = fc;
         xcs[i] = fc > 1 ? (double)fc * lg2(a, fc) : 0.0;
-        lys[i] = (c < k && T - fc > 0) ? lg2(a, T - fc) : 0.0;
+        lys[i] = (c < (int)k && T - fc > 0) ? lg2(a, T - fc) : 0.0;
         xpart += xcs[i];
     }
     const double X = g.sum(xpart);
-    const int64_t d = end - beg;
-    double wmax = 0.0, a_self = 0.0;
+    double wmax = 0.0;
+    double acn[NC];
 #pragma unroll
     for (int i = 0; i < NC; i++) {
         const int c = (int)g.lane + i * GR::size;
-        if (c >= k) continue;
+        acn[i] = 0.0;
+        if (c >= (int)k) continue;
         const int fc = fcs[i];
         const double w = weight_from(a, fc, T, L_all, X, xcs[i], lys[i]);
         const double ac = w > 0.0 ? cube_root(w) : 0.0;
-        if (a.parity) {            // the parity tables, written only for the getters
-            a.omega[u * k + c] = w;
-            a.f[u * k + c] = fc;
-        } else {
-            a.amat[u * k + c] = ac;
-            a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+        acn[i] = ac;
+        if (valid) {
+            if (a.parity) {            // the parity tables, written only for the getters
+                a.omega[u * k + c] = w;
+                a.f[u * k + c] = fc;
+            } else {
+                a.amat[u * k + c] = ac;
+                a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+            }
+            if (in_max(a, fc, L_all, c, (int)lu, pc)) wmax = w > wmax ? w : wmax;
         }
-        if (in_max(a, fc, L_all, c, lu, pc)) wmax = w > wmax ? w : wmax;
-        if (c == (int)lu) a_self = ac;
     }
     if (a.parity) return wmax;
-    const int owner = (lu < k) ? (int)(lu % GR::size) : 0;
-    if ((int)g.lane == owner) write_vrec(a, u, a_self, pc, lu, d);
+    // a_u(c) of a column c < k: from the lane (c % G, slot c / G) that computed it
+    const double *arow = a.amat + u * k;
+    auto au = [&](uint32_t c) -> double {
+        if constexpr (GR::size <= 32) {
+            double v = 0.0;
+#pragma unroll
+            for (int i = 0; i < NC; i++) {
+                const double t = g.from(acn[i], (int)(c % GR::size));
+                v = ((int)(c / GR::size) == i) ? t : v;
+            }
+            return v;
+        } else {
+            return arow[c];                      // CTA: this block's writes (after the barrier)
+        }
+    };
     g.sync();
-    phase_a_lists<U>(a, u, g, beg, pc, pp, pt, lu);
+    const double aself = au(lu < k ? lu : 0u);
+    if (valid && g.lane == 0) write_vrec(a, u, lu < k ? aself : 0.0, pc, lu, d);
+    // Step 3 inputs: B pushes and the P+ runs, reading P(u) back
+    const unsigned long long qs = (valid && lu < k) ? bq_quantize(aself, a.bq) : 0ull;
+    BQL *bcol = a.bql + (int64_t)(qs ? lu : 0) * a.n;
+    const int32_t *__restrict__ pin = a.pidx + beg;
+    const uint8_t *__restrict__ lin = a.plab + beg;
+    int ct = 0;
+    const int pcw = g.umax(wr ? pc : 0);
+    for (int base = 0; base < pcw; base += GR::size * U) {
+        int32_t v[U];
+        uint32_t lv[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            v[j] = (wr && i < pc) ? pin[i] : -1;
+            lv[j] = (wr && i < pc) ? (uint32_t)lin[i] : kOther;
+        }
+#ifndef RS_EXP_NO_BPUSH
+#pragma unroll
+        for (int j = 0; j < U; j++)
+            if (qs && v[j] >= 0) atomicAdd(&bcol[v[j]].b, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
+#endif
+        bool t[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            t[j] = v[j] >= 0 && i < pp && lv[j] < k;
+        }
+        int rt[U], tt[U];
+        g.template rank_u<U>(t, rt, tt);
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const int i = base + j * GR::size + (int)g.lane;
+            const double aw = au(lv[j] < k ? lv[j] : 0u);
+            if (v[j] >= 0 && i < pp) {
+                const int tb = ct + rt[j];                // target entries of P+ before i
+                const int64_t at = t[j] ? beg + pt - 1 - tb : beg + pt + (i - tb);
+                a.pplus[at] = v[j];
+                a.wps[at] = t[j] ? aw : 0.0;
+            }
+            ct += tt[j];
+        }
+    }
+    if (wr && g.lane == 0) {
+        PRec r;
+        r.x = pp;
+        r.y = pc;
+        r.start = beg | ((long long)pt << kPrShift);
+        a.pc2[u] = r;
+    }
     return wmax;
 }
 
 // k > 8: histogram in shared memory (one warp or one CTA per vertex)
 template <int U, class GR>
 __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64_t u, GR &g, int *hist) {
-    const int64_t beg = a.rowptr[u], end = a.rowptr[u + 1];
-    const uint8_t lu = a.lab[u];
-    const int32_t cfull = (lu == kOther) ? a.comm[u] : 0;
+    const int64_t beg = a.rowptr[u];
+    const int d = (int)(a.rowptr[u + 1] - beg);
+    const uint32_t lu = a.lab[u];
     const int k = a.k;
     for (int c = g.lane; c < k; c += GR::size) hist[c] = 0;
-    g.sync();
-    int pc = 0, pp = 0, pt = 0;
-    for (int64_t base = beg; base < end; base += GR::size * U) {
-        int32_t x[U];
-        uint8_t lx[U];
-#pragma unroll
-        for (int j = 0; j < U; j++) {
-            const int64_t e = base + j * GR::size + g.lane;
-            x[j] = e < end ? __ldcs(a.col + e) : -1;
-        }
-#pragma unroll
-        for (int j = 0; j < U; j++) lx[j] = x[j] >= 0 ? __ldg(a.lab + x[j]) : kOther;
-#pragma unroll
-        for (int j = 0; j < U; j++) {
-            const bool valid = x[j] >= 0;
-            bool foreign = valid && (lx[j] != lu);
-            if (valid && lx[j] == kOther && lu == kOther) foreign = __ldg(a.comm + x[j]) != cfull;
-            if (valid && lx[j] < k) atomicAdd(&hist[lx[j]], 1);
-            if (base + j * GR::size < end) {
-                int tot, totp, tott;
-                const int r = g.rank(foreign, &tot);
-                g.rank(foreign && x[j] < (int32_t)u, &totp);
-                g.rank(foreign && x[j] < (int32_t)u && lx[j] < k, &tott);
-                if (foreign && !a.parity) a.pidx[beg + pc + r] = x[j];
-                pc += tot;
-                pp += totp;
-                pt += tott;
-            }
-        }
+    int pc, pp;
+    if (a.parity) {
+        pc = a.vrec[u].pcnt;
+        pp = a.pc2[u].x;
+    } else if (lu == kOther) {
+        walk_row<U, true>(a, u, beg, d, lu, a.comm[u], g, pc, pp);
+    } else {
+        walk_row<U, false>(a, u, beg, d, lu, 0, g, pc, pp);
     }
     g.sync();
+    // Step 2a from the P list: shared-memory counts of the target labels
+    const uint8_t *__restrict__ lp = a.plab + beg;
+    int ptl = 0;
+    for (int i = g.lane; i < pc; i += GR::size) {
+        const uint32_t l = lp[i];
+        if (l < (uint32_t)k) {
+            atomicAdd(&hist[l], 1);
+            ptl += i < pp;
+        }
+    }
+    const int pt = g.sum(ptl);
+    g.sync();
+    if (lu < (uint32_t)k && g.lane == 0) hist[lu] = d - pc;
+    g.sync();
     // T, L_all and X = sum f log2 f over the k columns, lane-strided + group sums
-    // (one round of log2-table loads instead of k in sequence per lane)
     int Tp = 0, Lp = 0;
     double Xp = 0.0;
     for (int c = g.lane; c < k; c += GR::size) {
@@ -322,7 +446,6 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     }
     const int T = g.sum(Tp), L_all = g.sum(Lp);
     const double X = g.sum(Xp);
-    const int64_t d = end - beg;
     double wmax = 0.0;
     for (int c = g.lane; c < k; c += GR::size) {
         const int fc = hist[c];
@@ -335,17 +458,25 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
             a.amat[u * k + c] = ac;
             a.bql[(int64_t)c * a.n + u].Q = ac * ac;
         }
-        if (in_max(a, fc, L_all, c, lu, pc)) wmax = w > wmax ? w : wmax;
+        if (in_max(a, fc, L_all, c, (int)lu, pc)) wmax = w > wmax ? w : wmax;
     }
     g.sync();
     if (a.parity) return wmax;
     if (g.lane == 0) {
         double as = 0.0;
-        if (lu < k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cube_root(w) : 0.0; }
+        if (lu < (uint32_t)k) { const double w = weight_of(a, hist[lu], T, L_all, X); as = w > 0.0 ? cube_root(w) : 0.0; }
         write_vrec(a, u, as, pc, lu, d);
     }
     g.sync();
-    phase_a_lists<U>(a, u, g, beg, pc, pp, pt, lu);
+    const double *arow = a.amat + u * k;            // this group's writes, plain loads
+    phase_a_lists<U>(a, g, beg, pc, pp, pt, lu, [&](uint32_t c) { return arow[c]; });
+    if (g.lane == 0) {
+        PRec r;
+        r.x = pp;
+        r.y = pc;
+        r.start = beg | ((long long)pt << kPrShift);
+        a.pc2[u] = r;
+    }
     g.sync();
     return wmax;
 }
@@ -363,19 +494,31 @@ __device__ __forceinline__ void block_max_to_scal(double v, unsigned long long *
 }
 
 template <int G, int U, bool SMEM>
-__global__ void __launch_bounds__(256) k_phase_a_warp(PhaseAArgs a) {
+__global__ void __launch_bounds__(256, 4) k_phase_a_warp(PhaseAArgs a) {
     __shared__ int hist[SMEM ? 8 * 256 : 1];
-    WarpGroup<G> g;
-    const int64_t groups_per_block = blockDim.x / G;
-    const int64_t gid = blockIdx.x * groups_per_block + threadIdx.x / G;
-    const int64_t ngroups = (int64_t)gridDim.x * groups_per_block;
     double wmax = 0.0;
-    for (int64_t i = gid; i < a.nverts; i += ngroups) {
-        const int64_t u = (a.vlo + i);
-        double w;
-        if constexpr (SMEM) w = phase_a_vertex_smem<U>(a, u, g, hist + (threadIdx.x / 32) * 256);
-        else w = phase_a_vertex<U>(a, u, g);
-        wmax = w > wmax ? w : wmax;
+    if constexpr (SMEM) {
+        WarpGroup<G> g;
+        const int64_t groups_per_block = blockDim.x / G;
+        const int64_t gid = blockIdx.x * groups_per_block + threadIdx.x / G;
+        const int64_t ngroups = (int64_t)gridDim.x * groups_per_block;
+        for (int64_t i = gid; i < a.nverts; i += ngroups) {
+            const double w = phase_a_vertex_smem<U>(a, a.vlo + i, g, hist + (threadIdx.x / 32) * 256);
+            wmax = w > wmax ? w : wmax;
+        }
+    } else {
+        // lockstep: a warp takes 32 / G consecutive vertices per step, all its
+        // lanes iterate together (a group past the end takes no vertex)
+        LockGroup<G> g;
+        constexpr int gpw = 32 / G;
+        const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        const int gi = (int)((threadIdx.x & 31u) / G);
+        for (int64_t i0 = warp * gpw; i0 < a.nverts; i0 += nwarps * gpw) {
+            const int64_t i = i0 + gi;
+            const double w = phase_a_vertex<U>(a, i < a.nverts ? a.vlo + i : -1, g);
+            wmax = w > wmax ? w : wmax;
+        }
     }
     block_max_to_scal(wmax, a.scal);
 }
@@ -410,32 +553,20 @@ static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
     c.launches++;
 }
 
-// experiment knobs (lanes per vertex of classes 2-4, loads in flight of class 1)
-#ifndef RS_EXP_A_G4
-#define RS_EXP_A_G4 32
-#endif
-#ifndef RS_EXP_A_G3
-#define RS_EXP_A_G3 8
-#endif
-#ifndef RS_EXP_A_G2
-#define RS_EXP_A_G2 8
-#endif
-#ifndef RS_EXP_A_U3
-#define RS_EXP_A_U3 4
-#endif
-#ifndef RS_EXP_A_U2
-#define RS_EXP_A_U2 4
-#endif
 #ifndef RS_EXP_A_CTA_CLS
 #define RS_EXP_A_CTA_CLS 7   // first degree class run by a CTA per vertex (class 6 on 32-lane groups)
 #endif
-#ifndef RS_EXP_A_U1
-#define RS_EXP_A_U1 4
+#ifndef RS_EXP_A_G3
+#define RS_EXP_A_G3 8        // class [32, 64): lanes per vertex
 #endif
+#ifndef RS_EXP_A_G2
+#define RS_EXP_A_G2 8        // class [16, 32)
+#endif
+// class -> (lanes per vertex G, loads in flight per lane U), G * U about the
+// row length: [0,8) 4x2, [8,16) 4x4, [16,32) 8x4, [32,64) 8x4, [64,8192) 32x4,
+// [8192, inf) a CTA x 4; the warp kernels run their groups in lockstep
 template <bool SMEM>
 static void launch_bins_a(Ctx &c, PhaseAArgs base) {
-    // class -> (lanes per vertex, loads in flight per lane), G*U about the row length:
-    // [0,8):4x2 [8,16):4x4 [16,32):8x4 [32,64):8x4 [64,8192):32x4 [8192,inf):CTAx4 (bins: kNumBins)
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         PhaseAArgs a = base;
         a.vlo = c.bins.offset[cls];
@@ -446,18 +577,16 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
             int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
             k_phase_a_cta<SMEM><<<(unsigned)blocks, kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (SMEM || cls >= 5) {
+        } else if (SMEM || cls >= 4) {
             launch_warp_bin<32, 4, SMEM>(c, a, s);
-        } else if (cls == 4) {
-            launch_warp_bin<RS_EXP_A_G4, 4, SMEM>(c, a, s);
         } else if (cls == 3) {
-            launch_warp_bin<RS_EXP_A_G3, RS_EXP_A_U3, SMEM>(c, a, s);
+            launch_warp_bin<RS_EXP_A_G3, 4, false>(c, a, s);
         } else if (cls == 2) {
-            launch_warp_bin<RS_EXP_A_G2, RS_EXP_A_U2, SMEM>(c, a, s);
+            launch_warp_bin<RS_EXP_A_G2, 4, false>(c, a, s);
         } else if (cls == 1) {
-            launch_warp_bin<4, RS_EXP_A_U1, SMEM>(c, a, s);
+            launch_warp_bin<4, 4, false>(c, a, s);
         } else {
-            launch_warp_bin<4, 2, SMEM>(c, a, s);
+            launch_warp_bin<4, 2, false>(c, a, s);
         }
     }
 }
@@ -473,8 +602,9 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.parity = parity ? 1 : 0;
     a.bq = c.bq;
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
+    a.plab = c.plab;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
-    if (c.k <= 8 && c.d_max < (1ll << 22)) launch_bins_a<false>(c, a);
+    if (c.k <= 8) launch_bins_a<false>(c, a);
     else launch_bins_a<true>(c, a);
     return cudaGetLastError();
 }

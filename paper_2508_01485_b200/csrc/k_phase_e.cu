@@ -701,7 +701,7 @@ cudaError_t launch_e_items(Ctx &c) {
     if (c.e_pre) cudaFree(c.e_pre);
     c.e_pre = nullptr;
     c.e_bytes = 0;
-    if ((e = cudaMalloc(&c.e_pre, bytes))) return e;
+    if ((e = rs::dmalloc(&c.e_pre, bytes))) return e;
     c.e_bytes = bytes;
     return cudaSuccess;
 }

@@ -22,6 +22,10 @@ cudaError_t launch_partition(Ctx &c);
 
 using rs::Ctx;
 
+int rs::g_poison = -1;
+
+extern "C" void rs_debug_poison(int32_t byte) { rs::g_poison = (byte >= 0 && byte <= 255) ? (int)byte : -1; }
+
 #ifdef RS_WITH_NCCL
 const rs::NcclApi *rs::nccl_api(std::string *err) {
     static rs::NcclApi api;
@@ -105,7 +109,7 @@ template <class T>
 static cudaError_t dalloc(T **p, size_t count) {
     if (*p) { cudaFree(*p); *p = nullptr; }
     if (count == 0) count = 1;
-    return cudaMalloc((void **)p, sizeof(T) * count);
+    return rs::dmalloc(p, sizeof(T) * count);
 }
 template <class T>
 static void dfree(T *&p) {
@@ -200,7 +204,7 @@ extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream,
 static void free_graph(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     dfree(c.rowptr); dfree(c.col); dfree(c.perm); dfree(c.inv); dfree(c.scratch); dfree(ctx->l2t); dfree(c.e_pre); c.e_bytes = 0;
-    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.pplus); dfree(c.wps); dfree(c.pc2); dfree(c.amat);
+    dfree(c.comm_in); dfree(c.comm_id); dfree(c.lab); dfree(c.vrec); dfree(c.pidx); dfree(c.plab); dfree(c.pplus); dfree(c.wps); dfree(c.pc2); dfree(c.amat);
     dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bql);
     dfree(c.cid); dfree(c.srec); dfree(c.ctk); dfree(c.ctb); dfree(c.pwr); dfree(c.prv); dfree(c.aself);
     dfree(c.xsum); dfree(c.n2s);
@@ -270,7 +274,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     if (arena_need > c.arena_bytes) {
         dfree(c.arena);
         c.arena_bytes = 0;
-        CK(cudaMalloc(&c.arena, arena_need));
+        CK(rs::dmalloc(&c.arena, arena_need));
         c.arena_bytes = arena_need;
     }
     char *ap = (char *)c.arena;
@@ -317,13 +321,14 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         CK(dalloc(&c.perm, n));
         CK(dalloc(&c.inv, n));
         const size_t scratch = 24 * (size_t)(n + 1) + (64u << 20);
-        CK(cudaMalloc(&c.scratch, scratch));
+        CK(rs::dmalloc(&c.scratch, scratch));
         c.scratch_bytes = scratch;
         CK(dalloc(&c.comm_in, n));
         CK(dalloc(&c.comm_id, n));
         CK(dalloc(&c.lab, n));
         CK(dalloc(&c.vrec, n));
         CK(dalloc(&c.pidx, nnz));
+        CK(dalloc(&c.plab, nnz));
         CK(dalloc(&c.pplus, nnz + 4));   // + 4: aligned 16-byte probes may read past the end
         CK(dalloc(&c.wps, nnz));
         CK(dalloc(&c.pc2, n));
@@ -395,7 +400,7 @@ static rs_status set_communities_all(rs_ctx *ctx, int64_t mx) {
     if (need > c.csort_bytes) {
         dfree(c.csort);
         c.csort_bytes = 0;
-        CK(cudaMalloc(&c.csort, need));
+        CK(rs::dmalloc(&c.csort, need));
         c.csort_bytes = need;
     }
     if (c.sp_cap < c.cap_nnz || !c.cid) {
@@ -747,7 +752,7 @@ extern "C" rs_status rs_awcc_removal(rs_ctx *ctx, const int32_t *S, int64_t nS, 
     while (cap < 2 * std::max<int64_t>(c.d_max, 1)) cap <<= 1;          // per-vertex community table
     const size_t sbytes = rs::awcc_scratch_bytes(M, J1, cap, nS);
     char *buf = nullptr;
-    CK(cudaMalloc(&buf, sbytes + sizeof(int32_t) * (size_t)nS * (J1 + 1) + sizeof(int64_t) * nS + 1024));
+    CK(rs::dmalloc(&buf, sbytes + sizeof(int32_t) * (size_t)nS * (J1 + 1) + sizeof(int64_t) * nS + 1024));
     int32_t *S_dev = (int32_t *)buf;
     int32_t *zeta_dev = S_dev + nS;
     int64_t *deg_dev = (int64_t *)(((uintptr_t)(zeta_dev + (size_t)nS * J1) + 15) & ~(uintptr_t)15);
@@ -801,7 +806,7 @@ extern "C" rs_status rs_shii(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t 
         if (hS[i] < 0 || hS[i] >= c.n) return fail(ctx, RS_EINVAL, "rs_shii: vertex id out of range");
     char *buf = nullptr;
     const size_t nb = sizeof(unsigned int) * c.n + 2 * sizeof(int32_t) * c.n + 64;
-    CK(cudaMalloc(&buf, nb));
+    CK(rs::dmalloc(&buf, nb));
     unsigned long long *ctr = (unsigned long long *)buf;
     unsigned int *act = (unsigned int *)(buf + 64);
     int32_t *cnt = (int32_t *)(act + c.n);
@@ -888,7 +893,7 @@ extern "C" rs_status rs_get_counts(rs_ctx *ctx, int32_t *f_out, int32_t *total_o
     cudaSetDevice(c.device);
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_counts: call rs_score first");
     int32_t *forig = nullptr;
-    CK(cudaMalloc(&forig, sizeof(int32_t) * (size_t)c.n * c.k));
+    CK(rs::dmalloc(&forig, sizeof(int32_t) * (size_t)c.n * c.k));
     rs_status s = RS_OK;
     if (c.sparse) {
         // dense view of the sparse community tables
@@ -921,7 +926,7 @@ extern "C" rs_status rs_get_weights(rs_ctx *ctx, double *omega_out, double *omeg
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_weights: call rs_score first");
     if (omega_out) {
         double *worig = nullptr;
-        CK(cudaMalloc(&worig, sizeof(double) * (size_t)c.n * c.k));
+        CK(rs::dmalloc(&worig, sizeof(double) * (size_t)c.n * c.k));
         cudaError_t e = c.sparse ? rs::launch_sparse_weights_dense(c, ctx->l2t, ctx->l2n, worig)
                                  : ensure_parity_tables(ctx);
         if (e == cudaSuccess && !c.sparse) e = rs::launch_permute_f64(c, c.omega, c.k, worig);
@@ -946,7 +951,7 @@ extern "C" rs_status rs_get_border(rs_ctx *ctx, int32_t *bv_out, int64_t *nb_out
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_border: call rs_score first");
     int64_t nb = 0;
     int32_t *tmp = nullptr;
-    CK(cudaMalloc(&tmp, sizeof(int32_t) * (size_t)c.n));
+    CK(rs::dmalloc(&tmp, sizeof(int32_t) * (size_t)c.n));
     cudaError_t e = rs::launch_border_list(c, tmp, &nb);
     if (e != cudaSuccess) { cudaFree(tmp); CK(e); }
     rs_status s = RS_OK;
@@ -964,8 +969,8 @@ extern "C" rs_status rs_get_pred(rs_ctx *ctx, int64_t *pred_off_out, int32_t *pr
     int64_t *off = nullptr;
     int32_t *pr = nullptr;
     int64_t ne = 0;
-    CK(cudaMalloc(&off, sizeof(int64_t) * (size_t)(c.n + 1)));
-    CK(cudaMalloc(&pr, sizeof(int32_t) * (size_t)std::max<int64_t>(c.nnz, 1)));
+    CK(rs::dmalloc(&off, sizeof(int64_t) * (size_t)(c.n + 1)));
+    CK(rs::dmalloc(&pr, sizeof(int32_t) * (size_t)std::max<int64_t>(c.nnz, 1)));
     cudaError_t e = rs::launch_pred_export(c, off, pr, &ne);
     if (e != cudaSuccess) { cudaFree(off); cudaFree(pr); CK(e); }
     rs_status s = RS_OK;
@@ -1015,16 +1020,16 @@ extern "C" rs_status rs_get_comm_tables(rs_ctx *ctx, int64_t *off_out, int32_t *
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_comm_tables: call rs_score first");
     if (!c.sparse) return fail(ctx, RS_ESTATE, "rs_get_comm_tables: needs the RS_ALL_COMMUNITIES mode");
     int64_t *off = nullptr;
-    CK(cudaMalloc(&off, sizeof(int64_t) * (size_t)(c.n + 1)));
+    CK(rs::dmalloc(&off, sizeof(int64_t) * (size_t)(c.n + 1)));
     int64_t tot = 0;
     cudaError_t e = rs::launch_sparse_offsets(c, off, &tot);
     int32_t *cols = nullptr, *cnt = nullptr;
     double *om = nullptr, *oa = nullptr;
     const size_t E = (size_t)std::max<int64_t>(tot, 1);
-    if (e == cudaSuccess && cols_out) e = cudaMalloc(&cols, sizeof(int32_t) * E);
-    if (e == cudaSuccess && cnt_out) e = cudaMalloc(&cnt, sizeof(int32_t) * E);
-    if (e == cudaSuccess && omega_out) e = cudaMalloc(&om, sizeof(double) * E);
-    if (e == cudaSuccess && omega_abs_out) e = cudaMalloc(&oa, sizeof(double) * (size_t)c.n);
+    if (e == cudaSuccess && cols_out) e = rs::dmalloc(&cols, sizeof(int32_t) * E);
+    if (e == cudaSuccess && cnt_out) e = rs::dmalloc(&cnt, sizeof(int32_t) * E);
+    if (e == cudaSuccess && omega_out) e = rs::dmalloc(&om, sizeof(double) * E);
+    if (e == cudaSuccess && omega_abs_out) e = rs::dmalloc(&oa, sizeof(double) * (size_t)c.n);
     if (e == cudaSuccess) e = rs::launch_sparse_export(c, off, ctx->l2t, ctx->l2n, cols, cnt, om, oa);
     rs_status s = RS_OK;
     if (e == cudaSuccess && off_out) s = out_copy(ctx, off_out, off, (size_t)(c.n + 1));

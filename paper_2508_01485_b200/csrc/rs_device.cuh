@@ -144,6 +144,16 @@ struct WarpGroup {
         *tot = __popc(b);
         return __popc(b & ((1u << lane) - 1u));
     }
+    // number of lanes of the group with p set
+    __device__ __forceinline__ int count(bool p) const {
+        return __popc(__ballot_sync(gmask, p) & gmask);
+    }
+    // U independent ranks (one per unrolled slot); warps need no batching
+    template <int U>
+    __device__ __forceinline__ void rank_u(const bool (&p)[U], int (&r)[U], int (&tot)[U]) {
+#pragma unroll
+        for (int j = 0; j < U; j++) r[j] = rank(p[j], &tot[j]);
+    }
     template <class T>
     __device__ __forceinline__ T sum(T v) const {
 #pragma unroll
@@ -162,6 +172,51 @@ struct WarpGroup {
     __device__ __forceinline__ T bcast(T v, int src) const {
         return __shfl_sync(gmask, v, src, G);
     }
+};
+
+// Lockstep vertex groups: like WarpGroup, but every lane of the warp executes
+// every step together (loop bounds are the warp maximum, a group with a shorter
+// row or no vertex just has its lanes masked by predicates), so collectives use
+// the full warp mask and groups never diverge. Round 1's profile of the 8-lane
+// classes: the groups of a warp, at different iterations of their own loops,
+// were serialised -- the ballots alone were 22% of the instructions.
+template <int G>
+struct LockGroup {
+    static constexpr int size = G;
+    unsigned lane;   // 0..G-1
+    unsigned shift;  // first lane of the group in the warp
+    __device__ __forceinline__ LockGroup() {
+        const unsigned l = threadIdx.x & 31u;
+        lane = l & (G - 1);
+        shift = l & ~(unsigned)(G - 1);
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    // warp-uniform loop bound: the largest v over the warp's groups
+    __device__ __forceinline__ int umax(int v) const { return (int)__reduce_max_sync(0xffffffffu, (unsigned)v); }
+    __device__ __forceinline__ unsigned bits(bool p) const {
+        const unsigned b = __ballot_sync(0xffffffffu, p);
+        return G == 32 ? b : (b >> shift) & ((1u << G) - 1u);
+    }
+    __device__ __forceinline__ int rank(bool p, int *tot) const {
+        const unsigned b = bits(p);
+        *tot = __popc(b);
+        return __popc(b & ((1u << lane) - 1u));
+    }
+    __device__ __forceinline__ int count(bool p) const { return __popc(bits(p)); }
+    template <int U>
+    __device__ __forceinline__ void rank_u(const bool (&p)[U], int (&r)[U], int (&tot)[U]) const {
+#pragma unroll
+        for (int j = 0; j < U; j++) r[j] = rank(p[j], &tot[j]);
+    }
+    template <class T>
+    __device__ __forceinline__ T sum(T v) const {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+        return v;
+    }
+    // v of the group's lane src (src may differ per lane)
+    template <class T>
+    __device__ __forceinline__ T from(T v, int src) const { return __shfl_sync(0xffffffffu, v, (int)shift + src); }
 };
 
 // A whole CTA (blockDim.x == kCtaThreads) owning one vertex (degree hubs).
@@ -186,6 +241,43 @@ struct CtaGroup {
         __syncthreads();
         *tot = all;
         return before + __popc(b & ((1u << l) - 1u));
+    }
+    __device__ __forceinline__ int count(bool p) {
+        int tot;
+        rank(p, &tot);
+        return tot;
+    }
+    __device__ __forceinline__ int umax(int v) const { return v; }   // one vertex per CTA: uniform already
+    __device__ __forceinline__ double bcast(double v, int src) {
+        if ((int)threadIdx.x == src) s_u[0] = (unsigned long long)__double_as_longlong(v);
+        __syncthreads();
+        const double r = __longlong_as_double((long long)s_u[0]);
+        __syncthreads();
+        return r;
+    }
+    // U ranks with ONE pair of barriers (the warp counts of all U slots go to
+    // shared memory together): slot j's order is warp-major, as rank()'s
+    template <int U>
+    __device__ __forceinline__ void rank_u(const bool (&p)[U], int (&r)[U], int (&tot)[U]) {
+        static_assert(U * kCtaWarps <= 4 * kCtaWarps, "shared scratch holds 4 slots");
+        int *cnt = reinterpret_cast<int *>(s_u);   // 2 * kCtaWarps u64 = U * kCtaWarps ints for U <= 4
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        unsigned b[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            b[j] = __ballot_sync(0xffffffffu, p[j]);
+            if (l == 0) cnt[j * kCtaWarps + w] = __popc(b[j]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            int before = 0, all = 0;
+#pragma unroll
+            for (int i = 0; i < kCtaWarps; i++) { const int c = cnt[j * kCtaWarps + i]; before += (i < w) ? c : 0; all += c; }
+            tot[j] = all;
+            r[j] = before + __popc(b[j] & ((1u << l) - 1u));
+        }
+        __syncthreads();
     }
     __device__ __forceinline__ long long sum(long long v) {
 #pragma unroll

@@ -14,6 +14,19 @@
 
 namespace rs {
 
+// Test hook (rs_debug_poison): when >= 0, every device allocation librs makes
+// is filled with this byte before use, so a kernel that reads memory nobody
+// wrote gives results that change with the byte (tests/test_gpu_hygiene.py
+// runs the pipeline under several bytes and requires identical bits; this
+// stands in for compute-sanitizer initcheck, which is closed on this pool).
+extern int g_poison;
+template <class T>
+inline cudaError_t dmalloc(T **p, size_t bytes) {
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e == cudaSuccess && g_poison >= 0) e = cudaMemset((void *)*p, g_poison, bytes);
+    return e;
+}
+
 #ifdef RS_WITH_NCCL
 // NCCL is resolved at run time (dlopen) so that librs uses the libnccl already
 // loaded in the process (e.g. the one torch.distributed brought) instead of
@@ -187,6 +200,7 @@ struct Ctx {
     double *omega = nullptr;     // n*k weights (unnormalised)
     VRec *vrec = nullptr;        // n
     int32_t *pidx = nullptr;     // nnz, P(u) ascending at rowptr[u] (P+(u) its prefix, see PRec)
+    uint8_t *plab = nullptr;     // nnz, the 8-bit label of each P(u) entry, beside it (Phase A)
     int32_t *pplus = nullptr;    // nnz, P+(u) at rowptr[u] as a target run and the other run
     double *wps = nullptr;       // nnz, a_u(c_z) beside each z of P+(u)
     PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, rowptr[u] | |P+_T(u)| << 40}
