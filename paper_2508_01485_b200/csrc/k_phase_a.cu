@@ -27,6 +27,8 @@
 // each lane keeps U independent loads in flight.
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
+#include <cstdio>
+#include <cstdlib>
 
 namespace rs {
 
@@ -556,15 +558,35 @@ static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
 #ifndef RS_EXP_A_CTA_CLS
 #define RS_EXP_A_CTA_CLS 7   // first degree class run by a CTA per vertex (class 6 on 32-lane groups)
 #endif
-#ifndef RS_EXP_A_G3
-#define RS_EXP_A_G3 8        // class [32, 64): lanes per vertex
-#endif
-#ifndef RS_EXP_A_G2
-#define RS_EXP_A_G2 8        // class [16, 32)
-#endif
-// class -> (lanes per vertex G, loads in flight per lane U), G * U about the
-// row length: [0,8) 4x2, [8,16) 4x4, [16,32) 8x4, [32,64) 8x4, [64,8192) 32x4,
-// [8192, inf) a CTA x 4; the warp kernels run their groups in lockstep
+// lanes per vertex G and loads in flight per lane U of the warp classes 0..6
+// (lockstep groups); the environment variables RS_A_LANES="g0,...,g6" and
+// RS_A_LOADS="u0,...,u6" override them (experiments)
+static void a_config(int cls, int *G, int *U) {
+    static int lanes[7] = {4, 4, 4, 8, 16, 16, 32};
+    static int loads[7] = {2, 4, 4, 4, 4, 4, 4};
+    static bool init = false;
+    if (!init) {
+        init = true;
+        int v[7];
+        if (const char *e = getenv("RS_A_LANES")) {
+            const int n = sscanf(e, "%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4, v + 5, v + 6);
+            for (int i = 0; i < n; i++)
+                if (v[i] == 4 || v[i] == 8 || v[i] == 16 || v[i] == 32) lanes[i] = v[i];
+        }
+        if (const char *e = getenv("RS_A_LOADS")) {
+            const int n = sscanf(e, "%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4, v + 5, v + 6);
+            for (int i = 0; i < n; i++)
+                if (v[i] == 2 || v[i] == 4 || v[i] == 8) loads[i] = v[i];
+        }
+    }
+    *G = lanes[cls];
+    *U = loads[cls];
+}
+
+// class -> lanes per vertex G (a_lanes) x loads in flight per lane U (4; 2 for
+// the class [0, 8)); [8192, inf) a CTA x 4. The warp kernels run their groups
+// in lockstep: consecutive vertices of the degree-descending numbering have
+// nearly equal degrees, so the warp-maximum trip count wastes little.
 template <bool SMEM>
 static void launch_bins_a(Ctx &c, PhaseAArgs base) {
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
@@ -577,16 +599,24 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
             int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
             k_phase_a_cta<SMEM><<<(unsigned)blocks, kCtaThreads, 0, s>>>(a);
             c.launches++;
-        } else if (SMEM || cls >= 4) {
-            launch_warp_bin<32, 4, SMEM>(c, a, s);
-        } else if (cls == 3) {
-            launch_warp_bin<RS_EXP_A_G3, 4, false>(c, a, s);
-        } else if (cls == 2) {
-            launch_warp_bin<RS_EXP_A_G2, 4, false>(c, a, s);
-        } else if (cls == 1) {
-            launch_warp_bin<4, 4, false>(c, a, s);
+        } else if (SMEM) {
+            launch_warp_bin<32, 4, true>(c, a, s);
         } else {
-            launch_warp_bin<4, 2, false>(c, a, s);
+            int G, U;
+            a_config(cls, &G, &U);
+            const int key = G * 10 + U;
+            switch (key) {
+                case 42: launch_warp_bin<4, 2, false>(c, a, s); break;
+                case 44: launch_warp_bin<4, 4, false>(c, a, s); break;
+                case 82: launch_warp_bin<8, 2, false>(c, a, s); break;
+                case 84: launch_warp_bin<8, 4, false>(c, a, s); break;
+                case 162: launch_warp_bin<16, 2, false>(c, a, s); break;
+                case 164: launch_warp_bin<16, 4, false>(c, a, s); break;
+                case 168: launch_warp_bin<16, 8, false>(c, a, s); break;
+                case 324: launch_warp_bin<32, 4, false>(c, a, s); break;
+                case 328: launch_warp_bin<32, 8, false>(c, a, s); break;
+                default: launch_warp_bin<32, 4, false>(c, a, s); break;
+            }
         }
     }
 }

@@ -4,9 +4,9 @@
 T=${1:-q}; K=${2:-""}
 mkdir -p gpurun_out
 if [ -n "$K" ]; then
-  timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hygiene.py tests/test_gpu_sparse.py -x -q -p no:cacheprovider -k "$K" > gpurun_out/${T}_tests.log 2>&1
+  timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hygiene.py tests/test_gpu_sparse.py -x -q -p no:cacheprovider --timeout=240 -k "$K" > gpurun_out/${T}_tests.log 2>&1
 else
-  timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hygiene.py tests/test_gpu_sparse.py -x -q -p no:cacheprovider > gpurun_out/${T}_tests.log 2>&1
+  timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hygiene.py tests/test_gpu_sparse.py -x -q -p no:cacheprovider --timeout=240 > gpurun_out/${T}_tests.log 2>&1
 fi
 echo "tests rc=$?"; tail -3 gpurun_out/${T}_tests.log
 for cfg in orkut lj; do
