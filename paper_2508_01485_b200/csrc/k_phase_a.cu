@@ -397,7 +397,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
     }
     if (wr && g.lane == 0) {
         PRec r;
-        r.x = pp;
+        r.x = pr_pack(pp, lu);
         r.y = pc;
         r.start = beg | ((long long)pt << kPrShift);
         a.pc2[u] = r;
@@ -416,7 +416,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     int pc, pp;
     if (a.parity) {
         pc = a.vrec[u].pcnt;
-        pp = a.pc2[u].x;
+        pp = pr_plus(a.pc2[u]);
     } else if (lu == kOther) {
         walk_row<U, true>(a, u, beg, d, lu, a.comm[u], g, pc, pp);
     } else {
@@ -474,7 +474,7 @@ __device__ __forceinline__ double phase_a_vertex_smem(const PhaseAArgs &a, int64
     phase_a_lists<U>(a, g, beg, pc, pp, pt, lu, [&](uint32_t c) { return arow[c]; });
     if (g.lane == 0) {
         PRec r;
-        r.x = pp;
+        r.x = pr_pack(pp, lu);
         r.y = pc;
         r.start = beg | ((long long)pt << kPrShift);
         a.pc2[u] = r;

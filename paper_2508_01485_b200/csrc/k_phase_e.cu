@@ -258,8 +258,8 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         int lxv[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            pcx[h] = xv[h] >= 0 ? a.pc2[xv[h]] : PRec{0, 0, 0};
-            lxv[h] = xv[h] >= 0 ? (int)__ldg(a.lab + xv[h]) : kOther;
+            pcx[h] = xv[h] >= 0 ? a.pc2[xv[h]] : PRec{(int)0xFF000000, 0, 0};
+            lxv[h] = pr_lab(pcx[h]);                      // the label rides in the record
         }
         for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
         if constexpr (!SPARSE) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             const bool tx = lx < k;
             int64_t bx;
             int lenx, t;
-            cut_range<SPARSE>(a.pplus, pr_start(pcx[h]), pcx[h].x, pr_plus_t(pcx[h]), y, tx && ty,
+            cut_range<SPARSE>(a.pplus, pr_start(pcx[h]), pr_plus(pcx[h]), pr_plus_t(pcx[h]), y, tx && ty,
                               xv[h] >= 0 && (tx || ty), bx, lenx, t);
             const bool use = lenx > 0;
             nprobe += (unsigned)lenx;
@@ -542,14 +542,11 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
         const int64_t y0 = ylo + 32 * t;
         // ---- y level: lane j holds y0 + j
         const int64_t yl = y0 + lane;
-        PRec pcl{0, 0, 0};
-        int lyl = kOther;
-        if (yl < a.n) {
-            pcl = a.pc2[yl];
-            lyl = a.lab[yl];
-        }
+        PRec pcl{(int)0xFF000000, 0, 0};
+        if (yl < a.n) pcl = a.pc2[yl];
+        const int lyl = pr_lab(pcl);
         const int64_t rpl = pr_start(pcl);                 // rowptr[y]
-        const int cnt = pcl.x > 0 ? pcl.y - pcl.x : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
+        const int cnt = pr_plus(pcl) > 0 ? pcl.y - pr_plus(pcl) : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
         int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -564,21 +561,18 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
             const int inc_j = __shfl_sync(0xffffffffu, incl, j);
             const int cnt_j = __shfl_sync(0xffffffffu, cnt, j);
             const long long by = __shfl_sync(0xffffffffu, rpl, j);
-            const int ppj = __shfl_sync(0xffffffffu, pcl.x, j);            // |P+(y)|
+            const int ppj = __shfl_sync(0xffffffffu, pr_plus(pcl), j);     // |P+(y)|
             const int ly = __shfl_sync(0xffffffffu, lyl, j);
             int32_t x = -1;
             const int64_t qpos = by + ppj + (q - (inc_j - cnt_j));       // P-(y): the suffix, x > y
             if (q < total) x = __ldg(a.pidx + qpos);
-            PRec pcx{0, 0, 0};
-            int lx = kOther;
-            if (x >= 0) {
-                pcx = a.pc2[x];
-                lx = __ldg(a.lab + x);
-            }
+            PRec pcx{(int)0xFF000000, 0, 0};
+            if (x >= 0) pcx = a.pc2[x];
+            const int lx = pr_lab(pcx);                   // the label rides in the record
             const bool tx = lx < k, ty = ly < k;
             int64_t rsx;                                                 // probed: z < y of the target
             int np, t;                                                   // run, and of the other if both
-            cut_range<SPARSE>(a.pplus, pr_start(pcx), pcx.x, pr_plus_t(pcx), (int32_t)(y0 + j), tx && ty,
+            cut_range<SPARSE>(a.pplus, pr_start(pcx), pr_plus(pcx), pr_plus_t(pcx), (int32_t)(y0 + j), tx && ty,
                               x >= 0 && (tx || ty), rsx, np, t);
             // a_x(c_y) and a_y(c_x) are gathered by the probe lanes that find a
             // triangle (few of the pairs close one), not per pair
@@ -610,7 +604,7 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
                 const int64_t pos = bx + o;                                 // the probed prefix of P+(x)
                 const int32_t z = __ldg(a.pplus + pos);
                 const int64_t dy = pr_start(pcy);
-                const int tyn = pr_plus_t(pcy), nyn = pcy.x - tyn;
+                const int tyn = pr_plus_t(pcy), nyn = pr_plus(pcy) - tyn;
                 int iz;
                 int64_t ypos;
                 if (zt) {                                                   // the target run, descending
@@ -659,7 +653,7 @@ __global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int32_t
         int c = 0;
         if (y < n_heavy) {
             const PRec p = pc2[y];
-            if (p.x > 0 && p.y > p.x) c = (p.y - p.x + kChunkE - 1) / kChunkE;   // chunks of P-(y)
+            if (pr_plus(p) > 0 && p.y > pr_plus(p)) c = (p.y - pr_plus(p) + kChunkE - 1) / kChunkE;   // chunks of P-(y)
         }
         cnt[y] = c;
     }
@@ -675,8 +669,8 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         EItem e;
         e.by = rowptr[y];
         e.y = (int32_t)y;
-        e.pyl = p.x | ((int32_t)lab[y] << 24);
-        e.pm = p.y - p.x;
+        e.pyl = p.x;                                  // |P+(y)| | lab(y) << 24
+        e.pm = p.y - pr_plus(p);
         e.pyt = pr_plus_t(p);
         e.pad = 0;
         for (int j = 0; j < c; j++) {

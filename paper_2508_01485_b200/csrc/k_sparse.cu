@@ -351,7 +351,7 @@ __device__ __forceinline__ void sp_lists_vertex(const SpArgs &a, int64_t u, GR &
         r.pad = 0;
         a.vrec[u] = r;
         PRec q;
-        q.x = pp;
+        q.x = pr_pack(pp, 0u);            // all-communities mode: every label is 0 (k_sparse lab)
         q.y = pc;
         q.start = beg | ((long long)pp << kPrShift);   // P+(u) is one (target) run
         a.pc2[u] = q;

@@ -76,12 +76,18 @@ struct __align__(16) VRec {
 // around t; wps holds a_u(c_z) beside each entry. (All-communities mode: pplus
 // is pidx itself, one ascending run, t = |P+|.)
 // t = |P+_T(u)| is packed above bit 40 of `start` (offsets < 2^40).
+// x also carries u's 8-bit label above bit 24, so Phase E gets a predecessor's
+// label with the record it gathers anyway (one random 1-byte gather less per
+// (y, x) pair); |P+(u)| < 2^24.
 struct __align__(16) PRec {
-    int x;             // |P+(u)| (orientation out-degree)
+    int x;             // |P+(u)| (orientation out-degree) | lab(u) << 24
     int y;             // |P(u)|
     long long start;   // rowptr[u] | (|P+_T(u)| << 40)
 };
 constexpr int kPrShift = 40;
+__host__ __device__ __forceinline__ int pr_plus(const PRec &r) { return r.x & 0xFFFFFF; }
+__host__ __device__ __forceinline__ int pr_lab(const PRec &r) { return (int)((unsigned)r.x >> 24); }
+__host__ __device__ __forceinline__ int pr_pack(int pp, unsigned lab) { return (int)((unsigned)pp | (lab << 24)); }
 // Type-I accumulation of the n_hub highest-degree heads is striped over
 // kHubStripes copies (a RED picks its copy by warp): a hub closes up to
 // millions of triangles, and same-address atomics serialise in the L2.
