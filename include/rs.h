@@ -99,13 +99,33 @@ rs_status rs_create(rs_ctx **out, int device, void *cuda_stream);
 /* Multi-GPU context: rank `rank` of `world` processes, one GPU each, that all
  * call the same sequence with the same inputs. `nccl_id` is the
  * 128-byte ncclUniqueId produced by rs_nccl_unique_id on rank 0 and broadcast
- * by the caller (e.g. with torch.distributed). Heads are split into
- * work-balanced contiguous ranges; the exchange steps are NCCL collectives on
- * the context stream. Errors: RS_EINVAL, RS_ECUDA, RS_ENCCL. */
+ * by the caller (e.g. with torch.distributed). Vertices are split into
+ * work-balanced contiguous ranges (internal degree-descending numbering): a
+ * rank runs Phase A (Steps 1-2) on its own vertices, exchanges what the other
+ * phases read of the 2-hop neighbourhood (omega_max, the B table, the
+ * cube-root rows, per-vertex records and the oriented P+ runs; DESIGN.md §7
+ * gives the bytes), takes a share of the Type-I middle vertices (the per-head
+ * limbs are then summed over the ranks) and finalizes its own heads; rs_topk
+ * all-gathers K candidates per rank and merges them identically everywhere.
+ * Supports explicit k <= 8 targets (RS_EINVAL otherwise, at
+ * rs_set_communities); rs_get_pred is not available (a rank holds only its own
+ * P lists; RS_ESTATE). Errors: RS_EINVAL, RS_ECUDA, RS_ENCCL. */
 rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream, int rank, int world,
                          const uint8_t nccl_id[128]);
 /* Fill `id_out` (128 bytes, host) with a fresh ncclUniqueId. */
 rs_status rs_nccl_unique_id(uint8_t id_out[128]);
+
+/* Emulated multi-GPU world (tests, one GPU): `world` ranks are host threads of
+ * one process, each with its own context from rs_create_emulated on the same
+ * device, each calling the same sequence as on a GPU of its own; the
+ * collectives are host barriers plus device-to-device copies between the
+ * contexts (no kernel waits on another). Everything else is the multi-GPU path
+ * of rs_create_dist. rs_emu_world_create: 1 <= world <= 16, RS_EINVAL
+ * otherwise; destroy the world after every context of it. */
+typedef struct rs_emu_world rs_emu_world;
+rs_status rs_emu_world_create(rs_emu_world **out, int32_t world);
+void rs_emu_world_destroy(rs_emu_world *w);
+rs_status rs_create_emulated(rs_ctx **out, int device, void *cuda_stream, int rank, int world, rs_emu_world *w);
 
 /* Free every device buffer owned by ctx. NULL is a no-op. */
 void rs_destroy(rs_ctx *ctx);
@@ -290,6 +310,15 @@ rs_status rs_shii(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t model, doub
  * RS_EINVAL if n < 0, world < 1 or a pointer is NULL (work_incl may be NULL
  * when n == 0). */
 rs_status rs_split_ranges(int64_t n, const int64_t *work_incl, int32_t world, int64_t *bounds_out);
+
+/* A rank's candidate list of Step 4, on the host: the first min(K,
+ * count) of the (score, id) pairs by (key descending, id ascending) -- key =
+ * the IEEE bits of the non-negative score, -0.0 folded to +0.0 -- then
+ * padding (0, INT32_MAX) up to K entries, into keys_out uint64[K] / ids_out
+ * int32[K]. The same order and padding as the GPU's filtered local select of
+ * rs_topk; used by the CPU tests of the protocol. RS_EINVAL on bad arguments. */
+rs_status rs_local_candidates(int64_t count, const double *scores, const int32_t *ids, int64_t K,
+                              uint64_t *keys_out, int32_t *ids_out);
 
 /* Step 4 merge of the per-rank top-K candidate lists gathered from all
  * ranks: keys uint64[count] are the IEEE-754 bits of the non-negative scores

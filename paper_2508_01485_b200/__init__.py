@@ -82,6 +82,10 @@ SIGNATURES = [
                                        ctypes.c_int32, ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_int64)]),
     ("rs_shii", ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
                                ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_double)]),
+    ("rs_emu_world_create", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32]),
+    ("rs_emu_world_destroy", None, [_P]),
+    ("rs_create_emulated", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, _P]),
+    ("rs_local_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P]),
     ("rs_split_ranges", ctypes.c_int, [ctypes.c_int64, _P, ctypes.c_int32, _P]),
     ("rs_merge_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P,
                                            ctypes.POINTER(ctypes.c_int64)]),
@@ -305,6 +309,36 @@ def rs_split_ranges(work_incl, world: int) -> np.ndarray:
     return b
 
 
+def rs_local_candidates(scores, ids, K: int):
+    """(keys uint64[K], ids int32[K]): a rank's Step-4 candidates, padded (0, INT32_MAX)."""
+    sc = np.ascontiguousarray(scores, dtype=np.float64)
+    i = np.ascontiguousarray(ids, dtype=np.int32)
+    ko = np.empty(max(K, 1), dtype=np.uint64)
+    io = np.empty(max(K, 1), dtype=np.int32)
+    st = load_library().rs_local_candidates(int(sc.shape[0]), _ptr(sc) if sc.size else None,
+                                            _ptr(i) if i.size else None, int(K), _ptr(ko), _ptr(io))
+    if st != RS_OK:
+        raise RsError(st, "rs_local_candidates: invalid arguments")
+    return ko[:K].copy(), io[:K].copy()
+
+
+class EmuWorld:
+    """An emulated multi-GPU world (rs_emu_world): ``world`` ranks as host threads
+    on one GPU, each with a Scorer(..., emu=this, rank=r, world=world)."""
+
+    def __init__(self, world: int):
+        h = _P()
+        st = load_library().rs_emu_world_create(ctypes.byref(h), int(world))
+        if st != RS_OK:
+            raise RsError(st, "rs_emu_world_create: invalid world size")
+        self.h, self.world = h, int(world)
+
+    def close(self):
+        if self.h is not None:
+            load_library().rs_emu_world_destroy(self.h)
+            self.h = None
+
+
 def rs_merge_candidates(keys, ids, K: int):
     """(ids, scores) of the merged top-K of gathered (key, id) candidates."""
     k = np.ascontiguousarray(keys, dtype=np.uint64)
@@ -333,8 +367,14 @@ class Scorer:
     ``torch.cuda.current_stream().cuda_stream``) or None for the default stream."""
 
     def __init__(self, device: int = 0, stream: int | None = None, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None):
-        if world > 1:
+                 nccl_id: bytes | None = None, emu: "EmuWorld | None" = None):
+        if emu is not None:
+            h = _P()
+            st = load_library().rs_create_emulated(ctypes.byref(h), int(device), stream, int(rank), int(world), emu.h)
+            if st != RS_OK:
+                raise RsError(st, load_library().rs_last_error(None).decode())
+            self.ctx = h
+        elif world > 1:
             self.ctx = rs_create_dist(device, stream, rank, world, nccl_id)
         else:
             self.ctx = rs_create(device, stream)

@@ -588,12 +588,12 @@ static void a_config(int cls, int *G, int *U) {
 // in lockstep: consecutive vertices of the degree-descending numbering have
 // nearly equal degrees, so the warp-maximum trip count wastes little.
 template <bool SMEM>
-static void launch_bins_a(Ctx &c, PhaseAArgs base) {
+static void launch_bins_a(Ctx &c, PhaseAArgs base, int64_t lo, int64_t hi) {
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         PhaseAArgs a = base;
-        a.vlo = c.bins.offset[cls];
-        a.nverts = c.bins.count[cls];
-        if (a.nverts == 0) continue;
+        a.vlo = std::max<int64_t>(c.bins.offset[cls], lo);   // the class, restricted to [lo, hi)
+        a.nverts = std::min<int64_t>(c.bins.offset[cls] + c.bins.count[cls], hi) - a.vlo;
+        if (a.nverts <= 0) continue;
         cudaStream_t s = c.side[cls];
         if (cls >= RS_EXP_A_CTA_CLS) {
             int64_t blocks = std::min<int64_t>(a.nverts, 148 * 8);
@@ -621,7 +621,8 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base) {
     }
 }
 
-cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity) {
+// vertices [lo, hi) only (a rank's own range in the multi-GPU path)
+cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity, int64_t lo, int64_t hi) {
     PhaseAArgs a;
     a.rowptr = c.rowptr; a.col = c.col; a.comm = c.comm_id; a.lab = c.lab;
     a.vlo = 0; a.nverts = 0; a.k = c.k; a.l2t = l2t; a.l2n = l2n;
@@ -634,8 +635,8 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.plab = c.plab;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
-    if (c.k <= 8) launch_bins_a<false>(c, a);
-    else launch_bins_a<true>(c, a);
+    if (c.k <= 8) launch_bins_a<false>(c, a, lo, hi);
+    else launch_bins_a<true>(c, a, lo, hi);
     return cudaGetLastError();
 }
 

@@ -147,9 +147,9 @@ static cudaError_t launch_phase_d_t(Ctx &c) {
     CdeArgs base = cde_args(c);
     for (int cls = kNumBins - 1; cls >= 0; cls--) {
         CdeArgs a = base;
-        a.vlo = c.bins.offset[cls];
-        a.nverts = c.bins.count[cls];
-        if (!a.nverts) continue;
+        a.vlo = std::max<int64_t>(c.bins.offset[cls], c.head_lo);   // owned heads of the class
+        a.nverts = std::min<int64_t>(c.bins.offset[cls] + c.bins.count[cls], c.head_hi) - a.vlo;
+        if (a.nverts <= 0) continue;
         cudaStream_t s = c.side[cls];
         if (cls >= RS_EXP_D_CTA_CLS) {
             k_phase_d_cta<SPARSE><<<(unsigned)std::min<int64_t>(a.nverts, 148 * 8), kCtaThreads, 0, s>>>(a);

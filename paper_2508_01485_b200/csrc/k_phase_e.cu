@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 // (short, L1-resident), so the work per lane is uniform whatever the list
 // lengths. Terms go to the heads with one RED each.
 template <bool COUNT, bool SPARSE>
-__global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
+__global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo, int64_t yhi) {
     const int k = a.k;
     const int lane = threadIdx.x & 31;
     unsigned long long ntri = 0, nprobe = 0;   // nprobe: warp-uniform
@@ -538,12 +538,12 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
     };
     // warp task t covers y in [ylo + 32 t, +32); multi-GPU: rank r takes t = r mod world
     for (int64_t t = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * a.e_world + a.e_rank;
-         ylo + 32 * t < a.n; t += nwarps * a.e_world) {
+         ylo + 32 * t < yhi; t += nwarps * a.e_world) {
         const int64_t y0 = ylo + 32 * t;
         // ---- y level: lane j holds y0 + j
         const int64_t yl = y0 + lane;
         PRec pcl{(int)0xFF000000, 0, 0};
-        if (yl < a.n) pcl = a.pc2[yl];
+        if (yl < yhi) pcl = a.pc2[yl];
         const int lyl = pr_lab(pcl);
         const int64_t rpl = pr_start(pcl);                 // rowptr[y]
         const int cnt = pr_plus(pcl) > 0 ? pcl.y - pr_plus(pcl) : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
@@ -648,10 +648,10 @@ __global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo) {
 // Heavy middle vertices (degree >= 128) are cut into chunks of kChunkE
 // positions of P(y); the chunk counts depend on the communities, so the item
 // list is rebuilt every step (count, scan, scatter), heaviest vertices first.
-__global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int32_t *cnt) {
+__global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t lo, int64_t hi, int32_t *cnt) {
     for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
         int c = 0;
-        if (y < n_heavy) {
+        if (y < n_heavy && y >= lo && y < hi) {   // multi-GPU: this rank's middle vertices only
             const PRec p = pc2[y];
             if (pr_plus(p) > 0 && p.y > pr_plus(p)) c = (p.y - pr_plus(p) + kChunkE - 1) / kChunkE;   // chunks of P-(y)
         }
@@ -706,7 +706,10 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     int32_t *off = cnt + (nh + 1);
     EItem *items = (EItem *)(((uintptr_t)(off + (nh + 1)) + 15) & ~(uintptr_t)15);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nh + 256) / 256, 148 * 4));
-    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, cnt);
+    // multi-GPU: a rank takes the middle vertices of its own range (their P-(y)
+    // lists live only there); one GPU: all
+    const int64_t lo = c.world > 1 ? c.head_lo : 0, hi = c.world > 1 ? c.head_hi : c.n;
+    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, lo, hi, cnt);
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
     if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
@@ -721,13 +724,15 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
 template <bool COUNT, bool SPARSE>
 static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     CdeArgs a = cde_args(c);
+    int64_t ylo = 0, yhi = c.n;
     if (c.world > 1) {
-        // the middle vertices are shared out; every head's terms are accumulated
-        // here and summed over the ranks afterwards (exact integer limbs)
+        // a rank takes the middle vertices of its own range (P-(y) is local); every
+        // head's terms are accumulated here and summed over the ranks afterwards
+        // (exact integer limbs)
         a.head_lo = 0;
         a.head_hi = c.n;
-        a.e_rank = c.rank;
-        a.e_world = c.world;
+        ylo = c.head_lo;
+        yhi = c.head_hi;
     }
     // test hook (RS_E_SHARES): the rank split run as sequential shares on one GPU
     const int shares = c.world > 1 ? 1 : std::max(1, c.e_shares);
@@ -752,13 +757,14 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
             a.e_world = shares;
         }
         cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
-        if (n_heavy < c.n) {                              // light first (see rs_score)
-            const int64_t threads = c.n - n_heavy;        // a warp per 32 vertices
+        const int64_t l0 = std::max<int64_t>(n_heavy, ylo);
+        if (l0 < yhi) {                                   // light first (see rs_score)
+            const int64_t threads = yhi - l0;             // a warp per 32 vertices
 #ifndef RS_EXP_LIGHT_BLK
 #define RS_EXP_LIGHT_BLK 4   // 148 x 4 blocks of 8 warps: 32 warps per SM beside the heavy kernel and Phase D
 #endif
             const int64_t blocks = std::min<int64_t>((threads + 255) / 256, 148 * RS_EXP_LIGHT_BLK);
-            k_phase_e_light<COUNT, SPARSE><<<(unsigned)blocks, 256, 0, light>>>(a, n_heavy);
+            k_phase_e_light<COUNT, SPARSE><<<(unsigned)blocks, 256, 0, light>>>(a, l0, yhi);
             c.launches++;
         }
         if (n_heavy > 0) {

@@ -5,6 +5,7 @@
 // id-ordered block scan; the K survivors are sorted (key desc, id asc).
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
+#include "rs_protocol.h"
 #include <cub/cub.cuh>
 
 namespace rs {
@@ -16,8 +17,7 @@ constexpr int kTkSortMax = 4096;   // in-smem bitonic sort capacity
 // state slots at scal + kScalTk: [0] prefix, [1] krem (keys still to take at
 // the threshold), [2] count of keys strictly above the current prefix
 __device__ __forceinline__ unsigned long long score_key(double s) {
-    unsigned long long b = (unsigned long long)__double_as_longlong(s);
-    return (b == 0x8000000000000000ull) ? 0ull : b;   // -0.0 -> +0.0
+    return score_key_bits((unsigned long long)__double_as_longlong(s));   // -0.0 -> +0.0 (rs_protocol.h)
 }
 
 struct TkFilter {             // multi-GPU: only original ids whose internal id is owned

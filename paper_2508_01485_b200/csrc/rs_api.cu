@@ -7,12 +7,13 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <climits>
 #include <string>
 #include <dlfcn.h>
 
 namespace rs {
 cudaError_t launch_log2_table(Ctx &c, double *t, int64_t len);
-cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity);
+cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity, int64_t lo, int64_t hi);
 cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
                                int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi);
 cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
@@ -97,6 +98,15 @@ static rs_status fail(rs_ctx *ctx, rs_status s, const std::string &m) {
     } while (0)
 #define NCCL (*rs::nccl_api(nullptr))
 #endif
+
+// a collective of the exchange layer (rs_xport.cu)
+#define XK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, RS_ENCCL, std::string(#expr) + ": " +                            \
+                                           (c.xp->msg.empty() ? cudaGetErrorString(e_) : c.xp->msg)); \
+    } while (0)
 
 static bool is_device_ptr(const void *p) {
     if (!p) return false;
@@ -193,12 +203,31 @@ extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream,
         ncclUniqueId id;
         memcpy(&id, nccl_id, 128);
         NK(NCCL.CommInitRank(&ctx->c.comm, world, id, rank));
+        ctx->c.xp = rs::make_nccl_xport(ctx->c.comm, world);
     }
     return RS_OK;
 #else
     if (world > 1) return fail(ctx, RS_ENCCL, "librs built without NCCL");
     return RS_OK;
 #endif
+}
+
+namespace rs {
+EmuWorld *emu_world_of(rs_emu_world *w);
+int emu_world_size(EmuWorld *w);
+}  // namespace rs
+
+extern "C" rs_status rs_create_emulated(rs_ctx **out, int device, void *cuda_stream, int rank, int world,
+                                        rs_emu_world *w) {
+    if (!w || world < 1 || rank < 0 || rank >= world) return fail(nullptr, RS_EINVAL, "rs_create_emulated: bad rank/world");
+    rs::EmuWorld *ew = rs::emu_world_of(w);
+    if (!ew || rs::emu_world_size(ew) != world) return fail(nullptr, RS_EINVAL, "rs_create_emulated: world size mismatch");
+    rs_status s = create_common(out, device, cuda_stream);
+    if (s != RS_OK) return s;
+    (*out)->c.rank = rank;
+    (*out)->c.world = world;
+    if (world > 1) (*out)->c.xp = rs::make_emu_xport(ew, rank);
+    return RS_OK;
 }
 
 static void free_graph(rs_ctx *ctx) {
@@ -208,6 +237,7 @@ static void free_graph(rs_ctx *ctx) {
     dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bql);
     dfree(c.cid); dfree(c.srec); dfree(c.ctk); dfree(c.ctb); dfree(c.pwr); dfree(c.prv); dfree(c.aself);
     dfree(c.xsum); dfree(c.n2s);
+    dfree(c.pk_id); dfree(c.pk_w); c.pk_cap = 0;
     c.sp_cap = 0;
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
@@ -222,6 +252,9 @@ extern "C" void rs_destroy(rs_ctx *ctx) {
     free_graph(ctx);
     dfree(c.chist); dfree(c.ccode); dfree(c.code32); dfree(c.csort); dfree(c.targets); dfree(c.scal); dfree(c.tk_hist); dfree(c.arena);
     dfree(ctx->utargets); dfree(ctx->stage_i32); dfree(ctx->stage_f64); dfree(ctx->cand_key); dfree(ctx->cand_id);
+    dfree(c.tk_gkey); dfree(c.tk_gid);
+    delete c.xp;
+    c.xp = nullptr;
     for (int i = 0; i < rs::kNumBins + 1; i++) {
         if (c.side[i]) cudaStreamDestroy(c.side[i]);
         if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
@@ -435,6 +468,8 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     if (!all && (k < 2 || k > rs::kMaxK))
         return fail(ctx, RS_EINVAL, "rs_set_communities: k must be in [2, 254] or RS_ALL_COMMUNITIES");
     if (all && targets) return fail(ctx, RS_EINVAL, "rs_set_communities: RS_ALL_COMMUNITIES takes targets = NULL");
+    if (c.world > 1 && (all || k > 8))
+        return fail(ctx, RS_EINVAL, "rs_set_communities: the multi-GPU path takes k <= 8 explicit-k targets");
     c.scored = false;
     c.has_comm = false;
     CK(cudaMemcpyAsync(c.comm_in, community_of, sizeof(int32_t) * c.n,
@@ -516,6 +551,61 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
     return RS_OK;
 }
 
+// ------------------------------------------------------------------ multi-GPU exchange
+// After each rank's Phase A shard (vertices [head_lo, head_hi)), every rank needs
+// for ALL vertices: omega_max (max), the B table (sums of every rank's pushes;
+// Q = a^2 is written by the owner only and the table is zeroed, so the same
+// integer sum copies it), the cube-root rows, vrec and pc2 (written by the
+// owner: all-gathered by segment), and the oriented runs P+(x) with their
+// weights (packed, all-gathered, unpacked into the slots). Exact: every value
+// is either copied bit for bit or an integer sum.
+static rs_status exchange_phase_a(rs_ctx *ctx) {
+    Ctx &c = ctx->c;
+    const int W = c.world;
+    const int64_t n = c.n, k = c.k;
+    std::vector<size_t> off(W), len(W);
+    auto seg = [&](size_t per) {
+        for (int r = 0; r < W; r++) {
+            off[r] = (size_t)c.bounds[r] * per;
+            len[r] = (size_t)(c.bounds[r + 1] - c.bounds[r]) * per;
+        }
+    };
+    XK(c.xp->allreduce_u64(c.scal + rs::kScalOmegaMaxBits, 1, true, c.stream));
+    XK(c.xp->allreduce_u64((unsigned long long *)c.bql, (size_t)(2 * n * k), false, c.stream));
+    seg(sizeof(double) * k);
+    XK(c.xp->allgatherv(c.amat, off.data(), len.data(), c.stream));
+    seg(sizeof(rs::VRec));
+    XK(c.xp->allgatherv(c.vrec, off.data(), len.data(), c.stream));
+    seg(sizeof(rs::PRec));
+    XK(c.xp->allgatherv(c.pc2, off.data(), len.data(), c.stream));
+    // the P+ runs: gpre = prefix of |P+| in vertex order (every rank computes the same)
+    int64_t *gpre = (int64_t *)c.scratch;
+    CK(rs::launch_plus_prefix(c, gpre));
+    std::vector<int64_t> gb(W + 1);
+    for (int r = 0; r <= W; r++)
+        CK(cudaMemcpyAsync(&gb[r], gpre + c.bounds[r], sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    const int64_t total = gb[W];
+    if (total > c.pk_cap) {
+        CK(dalloc(&c.pk_id, (size_t)total));
+        CK(dalloc(&c.pk_w, (size_t)total));
+        c.pk_cap = total;
+    }
+    CK(rs::launch_plus_pack(c, gpre, false));
+    for (int r = 0; r < W; r++) {
+        off[r] = (size_t)gb[r] * sizeof(int32_t);
+        len[r] = (size_t)(gb[r + 1] - gb[r]) * sizeof(int32_t);
+    }
+    XK(c.xp->allgatherv(c.pk_id, off.data(), len.data(), c.stream));
+    for (int r = 0; r < W; r++) {
+        off[r] = (size_t)gb[r] * sizeof(double);
+        len[r] = (size_t)(gb[r + 1] - gb[r]) * sizeof(double);
+    }
+    XK(c.xp->allgatherv(c.pk_w, off.data(), len.data(), c.stream));
+    CK(rs::launch_plus_pack(c, gpre, true));
+    return RS_OK;
+}
+
 // ------------------------------------------------------------------ score
 extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_out, uint32_t flags) {
     if (!ctx) return RS_EINVAL;
@@ -555,11 +645,17 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         // Phase A: border + histogram + weights + P lists + omega_max partials, the
         // orientation of G' and the B-table pushes
         fork(c);
-        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, false));
+        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, false, c.head_lo, c.head_hi));   // own range
         join(c);
     }
     CK(cudaEventRecord(c.ev_phase[1], c.stream));
-    CK(cudaEventRecord(c.ev_phase[2], c.stream));   // (Phase C folded into A: ms_phase[1] = 0)
+    if (c.world > 1) {
+        // multi-GPU: Phase A ran on this rank's vertices only; exchange what the
+        // other phases read of the 2-hop neighbourhood (ms_phase[1])
+        rs_status st = exchange_phase_a(ctx);
+        if (st != RS_OK) return st;
+    }
+    CK(cudaEventRecord(c.ev_phase[2], c.stream));
     // Phase E (Type-I triangles) and Phase D (Type-II pull, which needs only
     // Phase A's B table) run concurrently: E heavy on the library stream, E light
     // and the D bins on the forked streams
@@ -567,33 +663,32 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(rs::launch_phase_d(c));                           // first: their blocks are queued ahead of
     CK(rs::launch_phase_e_on(c, c.side[rs::kNumBins]));  // the persistent heavy Phase E grid
     join(c);
-#ifdef RS_WITH_NCCL
+    if (c.world > 1 && getenv("RS_DEBUG_E")) {      // per-rank Type-I work (balance diagnostics)
+        unsigned long long v[2];
+        CK(cudaMemcpyAsync(v, c.scal + rs::kScalNTri, sizeof(v), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        fprintf(stderr, "[rank %d] own [%lld, %lld) n_heavy %lld: triangles %llu probes %llu\n", c.rank,
+                (long long)c.head_lo, (long long)c.head_hi, (long long)c.e_nbig, v[0], v[1]);
+    }
     if (c.world > 1) {
         // Phase E is split by middle vertex: sum every head's Type-I limbs (and the
         // triangle/probe counters) over the ranks; integer sums, exact in any order
-        NK(NCCL.GroupStart());
-        NK(NCCL.AllReduce(c.acc1, c.acc1, (size_t)(3 * n), ncclUint64, ncclSum, c.comm, c.stream));
-        NK(NCCL.AllReduce(c.acc_hub, c.acc_hub, (size_t)(3 * rs::kHubStripes * c.n_hub), ncclUint64, ncclSum,
-                          c.comm, c.stream));
-        NK(NCCL.AllReduce(c.scal + rs::kScalNTri, c.scal + rs::kScalNTri, 2, ncclUint64, ncclSum, c.comm, c.stream));
-        NK(NCCL.GroupEnd());
+        XK(c.xp->allreduce_u64(c.acc1, (size_t)(3 * n), false, c.stream));
+        XK(c.xp->allreduce_u64(c.acc_hub, (size_t)(3 * rs::kHubStripes * c.n_hub), false, c.stream));
+        XK(c.xp->allreduce_u64(c.scal + rs::kScalNTri, 2, false, c.stream));
     }
-#endif
     CK(cudaEventRecord(c.ev_phase[3], c.stream));
     // multi-GPU: a rank writes only its heads' scores (scattered in original order)
     if (c.world > 1) CK(cudaMemsetAsync(c.score, 0, sizeof(double) * n, c.stream));
     // finalize: Type-II + Type-I sums, / omega_max / d(d-1), original order
     CK(rs::launch_finalize(c));
     CK(cudaEventRecord(c.ev_phase[4], c.stream));
-#ifdef RS_WITH_NCCL
     if (c.world > 1 && (flags & RS_GATHER_SCORES)) {
         // owned heads are a contiguous internal range, scattered in original order;
-        // every other entry is +0.0 on a rank, so a sum gathers the scores exactly
-        NK(NCCL.GroupStart());
-        NK(NCCL.AllReduce(c.score, c.score, (size_t)n, ncclFloat64, ncclSum, c.comm, c.stream));
-        NK(NCCL.GroupEnd());
+        // every other entry is +0.0 (all-zero bits) on a rank, so an integer sum of
+        // the bit patterns gathers the scores exactly
+        XK(c.xp->allreduce_u64((unsigned long long *)c.score, (size_t)n, false, c.stream));
     }
-#endif
     // zero the accumulators (and the dense B table) for the next rs_score on a side
     // stream: it overlaps whatever the caller does next (rs_topk, getters)
     {
@@ -676,8 +771,7 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         CK(rs::launch_topk_select(c, Kc, 0, c.n, ctx->cand_key, ctx->cand_id, nullptr, 0, 0));
         CK(rs::tk_sort_emit(c, ctx->cand_key, ctx->cand_id, Kc, Kc, ids_d, sc_d));
     } else {
-#ifdef RS_WITH_NCCL
-        // local top-K of the owned head range, padded with sentinels, allgathered,
+        // local top-K of the owned head range, padded with sentinels, all-gathered,
         // then the same deterministic merge on every rank
         const int64_t range = c.head_hi - c.head_lo;
         const int64_t Kl = std::min<int64_t>(Kc, range);
@@ -685,35 +779,33 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         int32_t *li = ctx->cand_id;
         s = ensure_stage(ctx, Kc);
         if (s != RS_OK) return s;
-        // pad: keys 0, ids INT_MAX sort last
+        const int64_t cnt = Kc * c.world;                 // gathered candidates
+        if (cnt > c.tk_gcap) {
+            CK(dalloc(&c.tk_gkey, (size_t)cnt));
+            CK(dalloc(&c.tk_gid, (size_t)cnt));
+            c.tk_gcap = cnt;
+        }
+        // pad: keys 0, ids INT32_MAX sort last
         CK(cudaMemsetAsync(lk, 0, sizeof(unsigned long long) * Kc, c.stream));
         CK(cudaMemsetAsync(li, 0x7f, sizeof(int32_t) * Kc, c.stream));
         if (Kl > 0) {
             // scores are in original order; keep the ids whose internal id is owned
             CK(rs::launch_topk_select(c, Kl, 0, c.n, lk, li, c.inv, c.head_lo, c.head_hi));
         }
-        unsigned long long *gk = (unsigned long long *)c.scratch;
-        int32_t *gi = (int32_t *)(gk + Kc * c.world * 3);
-        NK(NCCL.GroupStart());
-        NK(NCCL.AllGather(lk, gk, (size_t)Kc, ncclUint64, c.comm, c.stream));
-        NK(NCCL.AllGather(li, gi, (size_t)Kc, ncclInt32, c.comm, c.stream));
-        NK(NCCL.GroupEnd());
+        XK(c.xp->allgather(lk, c.tk_gkey, sizeof(unsigned long long) * Kc, c.stream));
+        XK(c.xp->allgather(li, c.tk_gid, sizeof(int32_t) * Kc, c.stream));
         // world * K candidates: merged on the host by the exported protocol function
-        const int64_t cnt = Kc * c.world;
         std::vector<uint64_t> hk(cnt);
         std::vector<int32_t> hi(cnt), hid(Kc);
         std::vector<double> hs(Kc);
-        CK(cudaMemcpyAsync(hk.data(), gk, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaMemcpyAsync(hi.data(), gi, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(hk.data(), c.tk_gkey, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(hi.data(), c.tk_gid, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
         int64_t got = 0;
         rs_merge_candidates(cnt, hk.data(), hi.data(), Kc, hid.data(), hs.data(), &got);
         CK(cudaMemcpyAsync(ids_d, hid.data(), sizeof(int32_t) * Kc, cudaMemcpyHostToDevice, c.stream));
         if (sc_d) CK(cudaMemcpyAsync(sc_d, hs.data(), sizeof(double) * Kc, cudaMemcpyHostToDevice, c.stream));
         CK(cudaStreamSynchronize(c.stream));
-#else
-        return fail(ctx, RS_ENCCL, "librs built without NCCL");
-#endif
     }
     if (!dev_ids) CK(cudaMemcpyAsync(ids_out, ids_d, sizeof(int32_t) * Kc, cudaMemcpyDeviceToHost, c.stream));
     if (scores_out && !dev_sc)
@@ -843,6 +935,28 @@ extern "C" rs_status rs_split_ranges(int64_t n, const int64_t *work_incl, int32_
     return RS_OK;
 }
 
+extern "C" rs_status rs_local_candidates(int64_t count, const double *scores, const int32_t *ids, int64_t K,
+                                         uint64_t *keys_out, int32_t *ids_out) {
+    if (count < 0 || K < 0 || (count > 0 && (!scores || !ids)) || (K > 0 && (!keys_out || !ids_out))) return RS_EINVAL;
+    std::vector<uint64_t> key(count);
+    for (int64_t i = 0; i < count; i++) {
+        uint64_t b;
+        memcpy(&b, &scores[i], sizeof(b));
+        key[i] = rs::score_key_bits(b);
+    }
+    std::vector<int64_t> ord(count);
+    for (int64_t i = 0; i < count; i++) ord[i] = i;
+    const int64_t take = std::min(K, count);
+    std::partial_sort(ord.begin(), ord.begin() + take, ord.end(), [&](int64_t a, int64_t b) {
+        return rs::cand_before(key[a], ids[a], key[b], ids[b]);
+    });
+    for (int64_t i = 0; i < K; i++) {
+        keys_out[i] = i < take ? key[ord[i]] : 0ull;
+        ids_out[i] = i < take ? ids[ord[i]] : INT32_MAX;
+    }
+    return RS_OK;
+}
+
 extern "C" rs_status rs_merge_candidates(int64_t count, const uint64_t *keys, const int32_t *ids, int64_t K,
                                          int32_t *ids_out, double *scores_out, int64_t *count_out) {
     if (count < 0 || K < 0 || (count > 0 && (!keys || !ids)) || (K > 0 && !ids_out)) return RS_EINVAL;
@@ -881,7 +995,9 @@ static cudaError_t ensure_parity_tables(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     if (c.parity_ok) return cudaSuccess;
     fork(c);
-    cudaError_t e = rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, true);
+    // every vertex (in the multi-GPU path too: the parity walk reads only the
+    // replicated CSR and labels)
+    cudaError_t e = rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, true, 0, c.n);
     join(c);
     if (e == cudaSuccess) c.parity_ok = true;
     return e;
@@ -966,6 +1082,7 @@ extern "C" rs_status rs_get_pred(rs_ctx *ctx, int64_t *pred_off_out, int32_t *pr
     Ctx &c = ctx->c;
     cudaSetDevice(c.device);
     if (!c.scored) return fail(ctx, RS_ESTATE, "rs_get_pred: call rs_score first");
+    if (c.world > 1) return fail(ctx, RS_ESTATE, "rs_get_pred: a rank holds only its own P lists (multi-GPU)");
     int64_t *off = nullptr;
     int32_t *pr = nullptr;
     int64_t ne = 0;
@@ -993,10 +1110,7 @@ extern "C" rs_status rs_get_triad_counts(rs_ctx *ctx, int64_t *type1_out, int64_
         // (kept off the timed rs_score path)
         CK(cudaMemsetAsync(c.n1, 0, sizeof(unsigned long long) * (size_t)c.n, c.stream));
         CK(rs::launch_triangle_counts(c));
-#ifdef RS_WITH_NCCL
-        if (c.world > 1)
-            NK(NCCL.AllReduce(c.n1, c.n1, (size_t)c.n, ncclUint64, ncclSum, c.comm, c.stream));
-#endif
+        if (c.world > 1) XK(c.xp->allreduce_u64(c.n1, (size_t)c.n, false, c.stream));
         CK(rs::launch_type1_export(c, tmp));
         rs_status s = out_copy(ctx, type1_out, tmp, (size_t)c.n);
         if (s) return s;

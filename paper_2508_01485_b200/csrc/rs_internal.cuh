@@ -45,6 +45,23 @@ struct NcclApi {
 const NcclApi *nccl_api(std::string *err);
 #endif
 
+// The multi-GPU exchange layer (rs_xport.cu): NCCL, or an in-process emulated
+// world of host threads on one GPU (rs_create_emulated). Collectives are
+// blocking with respect to the host only for the emulated transport.
+struct Xport {
+    std::string msg;   // last transport error
+    virtual ~Xport() {}
+    // every rank holds buf; rank r's segment is [off[r], off[r] + len[r]) bytes: copy all segments everywhere
+    virtual cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) = 0;
+    virtual cudaError_t allreduce_u64(unsigned long long *buf, size_t count, bool max, cudaStream_t s) = 0;
+    virtual cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+};
+struct EmuWorld;
+Xport *make_emu_xport(EmuWorld *w, int rank);
+#ifdef RS_WITH_NCCL
+Xport *make_nccl_xport(ncclComm_t comm, int world);
+#endif
+
 constexpr int kMaxK = 254;        // target columns (uint8 label 0xFF = "other")
 constexpr uint8_t kOther = 0xFF;  // community without its own 8-bit code
 constexpr int kNumBins = 8;       // degree classes (load time)
@@ -148,6 +165,13 @@ struct Ctx {
 #ifdef RS_WITH_NCCL
     ncclComm_t comm = nullptr;
 #endif
+    Xport *xp = nullptr;                       // world > 1: the exchange transport (owned)
+    int32_t *pk_id = nullptr;                  // world > 1: packed P+ runs of all ranks (ids, weights)
+    double *pk_w = nullptr;
+    int64_t pk_cap = 0;
+    unsigned long long *tk_gkey = nullptr;     // world > 1: gathered top-K candidates (world * K)
+    int32_t *tk_gid = nullptr;
+    int64_t tk_gcap = 0;
     int64_t head_lo = 0, head_hi = 0;          // owned vertex range [lo, hi)
     std::vector<int64_t> bounds;               // world+1 range boundaries
 
@@ -282,6 +306,8 @@ cudaError_t launch_awcc_degrees(Ctx &c, const int32_t *S_dev, int64_t nS, int64_
 cudaError_t launch_awcc_trial(Ctx &c, const int32_t *S_dev, int64_t nS, int mode, int step_pct, int J1, uint64_t st,
                               int32_t *zeta_dev, void *scratch, size_t scratch_bytes, int64_t cap);
 cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light);
+cudaError_t launch_plus_prefix(Ctx &c, int64_t *gpre);
+cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre, bool unpack);
 cudaError_t launch_triangle_counts(Ctx &c);
 cudaError_t launch_e_items(Ctx &c);
 cudaError_t launch_topk(Ctx &c, int64_t K, int32_t *ids_dev, double *scores_dev, int64_t lo, int64_t hi);

@@ -27,6 +27,10 @@ RS_HD int64_t split_point(const int64_t *incl, int64_t n, int world, int r) {
     return lo + 1 < n ? lo + 1 : n;
 }
 
+// the Step 4 order key of a non-negative score: its IEEE bits, -0.0 folded to
+// +0.0 (monotone as an unsigned integer)
+RS_HD uint64_t score_key_bits(uint64_t bits) { return bits == 0x8000000000000000ull ? 0ull : bits; }
+
 // the candidate order of Step 4: key descending, id ascending
 RS_HD bool cand_before(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
     return ka > kb || (ka == kb && ia < ib);

@@ -1,0 +1,171 @@
+// The exchange layer of the multi-GPU path: the
+// handful of collectives rs_score / rs_topk issue between the ranks, behind
+// one interface with two transports.
+//
+// * NcclXport: NCCL over NVLink (ncclAllReduce / ncclAllGather; a variable-size
+//   all-gather is a group of ncclBroadcast, one per root's segment).
+// * EmuXport: the ranks are host threads of ONE process on ONE GPU, each with
+//   its own context (rs_create_emulated); a collective is a host barrier, then
+//   device-to-device copies (or a summing kernel) reading the peers' buffers,
+//   then a barrier. No kernel ever waits on another: every rank synchronises
+//   its stream before the barrier. This runs rank r's whole pipeline -- its
+//   Phase A shard, the exchanges, its Phase D / finalize range and its
+//   filtered top-K select -- exactly as on a GPU of its own, so the tests can
+//   check that the merged world gives the single-GPU bits
+//   (tests/test_gpu_multirank.py); only the transport differs.
+#include "rs_internal.cuh"
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
+namespace rs {
+
+#ifdef RS_WITH_NCCL
+struct NcclXport : Xport {
+    ncclComm_t comm;
+    int world;
+    explicit NcclXport(ncclComm_t cm, int w) : comm(cm), world(w) {}
+    cudaError_t err(ncclResult_t r, const char *what) {
+        if (r == ncclSuccess) return cudaSuccess;
+        msg = std::string(what) + ": " + nccl_api(nullptr)->GetErrorString(r);
+        return cudaErrorUnknown;
+    }
+    cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) override {
+        const NcclApi &N = *nccl_api(nullptr);
+        ncclResult_t r = N.GroupStart();
+        for (int p = 0; p < world && r == ncclSuccess; p++)
+            if (len[p]) r = N.Broadcast((char *)buf + off[p], (char *)buf + off[p], len[p], ncclUint8, p, comm, s);
+        const ncclResult_t r2 = N.GroupEnd();
+        return err(r != ncclSuccess ? r : r2, "ncclBroadcast (all-gather of segments)");
+    }
+    cudaError_t allreduce_u64(unsigned long long *buf, size_t count, bool max, cudaStream_t s) override {
+        return err(nccl_api(nullptr)->AllReduce(buf, buf, count, ncclUint64, max ? ncclMax : ncclSum, comm, s),
+                   "ncclAllReduce");
+    }
+    cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
+        return err(nccl_api(nullptr)->AllGather(send, recv, bytes, ncclUint8, comm, s), "ncclAllGather");
+    }
+};
+Xport *make_nccl_xport(ncclComm_t comm, int world) { return new NcclXport(comm, world); }
+#endif
+
+// ---------------------------------------------------------------- emulated world
+struct EmuWorld {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long generation = 0;
+    std::vector<const void *> ptr;   // each rank's buffer of the current collective
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const unsigned long long gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            generation++;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
+constexpr int kEmuMaxWorld = 16;
+struct PtrPack {
+    const unsigned long long *p[kEmuMaxWorld];
+};
+
+__global__ void k_reduce_u64(PtrPack src, int world, size_t count, bool max, unsigned long long *out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long v = src.p[0][i];
+        for (int r = 1; r < world; r++) {
+            const unsigned long long x = src.p[r][i];
+            v = max ? (x > v ? x : v) : v + x;
+        }
+        out[i] = v;
+    }
+}
+
+struct EmuXport : Xport {
+    EmuWorld *W;
+    int rank;
+    unsigned long long *tmp = nullptr;
+    size_t tmp_count = 0;
+    EmuXport(EmuWorld *w, int r) : W(w), rank(r) {}
+    ~EmuXport() override {
+        if (tmp) cudaFree(tmp);
+    }
+    cudaError_t publish(const void *p, cudaStream_t s) {
+        const cudaError_t e = cudaStreamSynchronize(s);   // this rank's buffer is final
+        W->ptr[rank] = p;
+        W->barrier();
+        return e;
+    }
+    cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) override {
+        cudaError_t e = publish(buf, s);
+        for (int p = 0; p < W->world && e == cudaSuccess; p++)
+            if (p != rank && len[p])
+                e = cudaMemcpyAsync((char *)buf + off[p], (const char *)W->ptr[p] + off[p], len[p],
+                                    cudaMemcpyDeviceToDevice, s);
+        const cudaError_t e2 = cudaStreamSynchronize(s);
+        W->barrier();                                      // every peer done reading
+        return e != cudaSuccess ? e : e2;
+    }
+    cudaError_t allreduce_u64(unsigned long long *buf, size_t count, bool max, cudaStream_t s) override {
+        cudaError_t e = cudaSuccess;
+        if (count > tmp_count) {
+            if (tmp) cudaFree(tmp);
+            tmp = nullptr;
+            tmp_count = 0;
+            e = cudaMalloc(&tmp, sizeof(unsigned long long) * count);
+            if (e == cudaSuccess) tmp_count = count;
+        }
+        const cudaError_t ep = publish(buf, s);
+        if (e == cudaSuccess) e = ep;
+        if (e == cudaSuccess && count) {
+            PtrPack pk;
+            for (int r = 0; r < W->world; r++) pk.p[r] = (const unsigned long long *)W->ptr[r];
+            const unsigned blocks = (unsigned)std::min<size_t>((count + 255) / 256, 148 * 8);
+            k_reduce_u64<<<blocks, 256, 0, s>>>(pk, W->world, count, max, tmp);
+            e = cudaGetLastError();
+        }
+        const cudaError_t e2 = cudaStreamSynchronize(s);
+        W->barrier();                                      // every peer done reading
+        if (e == cudaSuccess) e = e2;
+        if (e == cudaSuccess && count)
+            e = cudaMemcpyAsync(buf, tmp, sizeof(unsigned long long) * count, cudaMemcpyDeviceToDevice, s);
+        return e;
+    }
+    cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
+        cudaError_t e = publish(send, s);
+        for (int p = 0; p < W->world && e == cudaSuccess; p++)
+            e = cudaMemcpyAsync((char *)recv + (size_t)p * bytes, W->ptr[p], bytes, cudaMemcpyDeviceToDevice, s);
+        const cudaError_t e2 = cudaStreamSynchronize(s);
+        W->barrier();
+        return e != cudaSuccess ? e : e2;
+    }
+};
+
+Xport *make_emu_xport(EmuWorld *w, int rank) { return new EmuXport(w, rank); }
+
+}  // namespace rs
+
+struct rs_emu_world {
+    rs::EmuWorld w;
+};
+
+namespace rs {
+EmuWorld *emu_world_of(rs_emu_world *w) { return w ? &w->w : nullptr; }
+int emu_world_size(EmuWorld *w) { return w->world; }
+}  // namespace rs
+
+extern "C" rs_status rs_emu_world_create(rs_emu_world **out, int32_t world) {
+    if (!out || world < 1 || world > rs::kEmuMaxWorld) return RS_EINVAL;
+    rs_emu_world *e = new rs_emu_world();
+    e->w.world = world;
+    e->w.ptr.assign(world, nullptr);
+    *out = e;
+    return RS_OK;
+}
+
+extern "C" void rs_emu_world_destroy(rs_emu_world *w) { delete w; }

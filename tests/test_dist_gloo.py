@@ -82,17 +82,13 @@ def case_split(rank, world, n, seed):
 
 
 def _local_candidates(scores, ids, K):
-    """rank-local top-K (key desc, id asc) padded with (0, INT32_MAX); the stand-in
-    for the GPU local select, which tests/test_gpu_parity.py checks on the GPU."""
+    """rank-local Step-4 candidates through librs's exported protocol function
+    (rs_local_candidates: key desc, id asc, padded (0, INT32_MAX)), the order
+    the GPU's filtered local select produces (checked against it by
+    tests/test_gpu_multirank.py)."""
     import paper_2508_01485_b200 as rsb
-    keys = rsb.score_keys(scores)
-    order = np.lexsort((ids, np.iinfo(np.uint64).max - keys))   # key desc, id asc
-    take = order[:K]
-    ck = np.zeros(K, dtype=np.uint64)
-    ci = np.full(K, INT32_MAX, dtype=np.int64)
-    ck[:take.size] = keys[take]
-    ci[:take.size] = ids[take]
-    return ck, ci
+    ck, ci = rsb.rs_local_candidates(scores, ids, K)
+    return ck, ci.astype(np.int64)
 
 
 def case_merge(rank, world, scores, K):
@@ -145,6 +141,13 @@ def test_topk_merge_ties_across_ranks():
     for ids, sc in out:
         assert ids == list(ids_o)
         assert np.array_equal(np.array(sc), np.asarray(sc_o))
+
+
+def test_local_candidates_order_and_padding():
+    import paper_2508_01485_b200 as rsb
+    ck, ci = rsb.rs_local_candidates(np.array([0.5, -0.0, 0.5, 0.25]), np.array([9, 3, 4, 1], np.int32), 6)
+    assert ci.tolist() == [4, 9, 1, 3, INT32_MAX, INT32_MAX]
+    assert ck.tolist()[:4] == rsb.score_keys(np.array([0.5, 0.5, 0.25, 0.0])).tolist() and ck.tolist()[4:] == [0, 0]
 
 
 def test_topk_merge_K_larger_than_candidates():

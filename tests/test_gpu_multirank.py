@@ -1,0 +1,119 @@
+"""The multi-GPU path on one GPU: `world` emulated
+ranks (rs_create_emulated -- host threads, one context each, collectives as
+host barriers + device-to-device copies) each run their whole pipeline: the
+Phase A shard of their own vertex range, the exchange of Phase A's outputs,
+their share of the Type-I middle vertices with the limb sum over the ranks,
+the Type-II pull and finalize of their own heads, and rs_topk's filtered
+local select + all-gather + merge. The merged world must give bitwise the
+single-GPU scores, top-K ids and scores, and the exact artefacts."""
+import threading
+
+import numpy as np
+import pytest
+
+import gen
+
+pytestmark = pytest.mark.gpu
+
+rsb = pytest.importorskip("paper_2508_01485_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rsb.load_library()
+
+
+def one_rank(s, g, k, K):
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, k)
+    R = np.empty(g.n)
+    st = s.score(scores_out=R, stats=True, gather=True)
+    ids, sc = s.topk(K)
+    t1, t2 = s.triad_counts()
+    f, T = s.counts()
+    w, wmax = s.weights()
+    return dict(R=R, ids=ids, sc=sc, t1=t1, t2=t2, f=f, T=T, w=w, wmax=wmax, bv=s.border(),
+                tri=st["n_triangles"], probes=st["n_probes"], omega_max=st["omega_max"])
+
+
+def run_world(g, k, K, world):
+    import torch
+    W = rsb.EmuWorld(world)
+    out, err = [None] * world, []
+
+    def main(r):
+        try:
+            stream = torch.cuda.Stream(device=0)
+            s = rsb.Scorer(0, stream.cuda_stream, rank=r, world=world, emu=W)
+            out[r] = one_rank(s, g, k, K)
+            s.close()
+        except Exception as e:  # reported by the main thread
+            err.append(f"rank {r}: {e!r}")
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    W.close()
+    assert not err, err
+    assert all(o is not None for o in out), "a rank did not finish"
+    return out
+
+
+CASES = [("orkut", 0.01, 5), ("lj", 0.004, 5), ("dblp", 0.05, 7)]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name,scale,k", CASES)
+def test_emulated_world_matches_single_gpu(name, scale, k, world):
+    g = gen.config_graph(name, scale=scale)
+    K = 50
+    s = rsb.Scorer(0)
+    ref = one_rank(s, g, k, K)
+    s.close()
+    out = run_world(g, k, K, world)
+    np.testing.assert_array_equal(sum(o["t2"] for o in out), ref["t2"])
+    for r, o in enumerate(out):
+        np.testing.assert_array_equal(o["t1"], ref["t1"])
+        assert o["omega_max"] == ref["omega_max"] and o["tri"] == ref["tri"] and o["probes"] == ref["probes"]
+        bad = np.nonzero(o["R"].view(np.uint64) != ref["R"].view(np.uint64))[0]
+        assert bad.size == 0, (f"rank {r}: {bad.size} scores differ, e.g. {bad[:8].tolist()} "
+                               f"{o['R'][bad[:4]].tolist()} vs {ref['R'][bad[:4]].tolist()}")
+        assert np.array_equal(o["ids"], ref["ids"]) and np.array_equal(o["sc"].view(np.uint64), ref["sc"].view(np.uint64))
+        assert o["omega_max"] == ref["omega_max"] and o["tri"] == ref["tri"] and o["probes"] == ref["probes"]
+        np.testing.assert_array_equal(o["t1"], ref["t1"])            # n_I: summed over the ranks
+        assert np.array_equal(o["f"], ref["f"]) and np.array_equal(o["T"], ref["T"])
+        assert np.array_equal(o["w"].view(np.uint64), ref["w"].view(np.uint64)) and o["wmax"] == ref["wmax"]
+        assert np.array_equal(o["bv"], ref["bv"])
+    # n_II: each rank reports its own heads (zeros elsewhere)
+    np.testing.assert_array_equal(sum(o["t2"] for o in out), ref["t2"])
+    # the GPU's filtered local select + merge equals the host protocol's merge of
+    # every rank's candidates (rs_local_candidates over the gathered scores)
+    n = g.n
+    ck, ci = rsb.rs_local_candidates(ref["R"], np.arange(n, dtype=np.int32), K)
+    mi, ms = rsb.rs_merge_candidates(ck, ci, min(K, n))
+    assert np.array_equal(mi, ref["ids"])
+
+
+def test_emulated_world_tiny_and_errors():
+    """karate with 8 ranks (ranges of a few vertices, some heads-free) and the
+    multi-GPU restrictions (k <= 8 explicit targets)."""
+    g, _ = gen.load_fixture("karate")
+    s = rsb.Scorer(0)
+    ref = one_rank(s, g, 2, 34)
+    s.close()
+    for o in run_world(g, 2, 34, 8):
+        assert np.array_equal(o["R"].view(np.uint64), ref["R"].view(np.uint64))
+        assert np.array_equal(o["ids"], ref["ids"])
+    W = rsb.EmuWorld(1)
+    s = rsb.Scorer(0, rank=0, world=1, emu=W)        # a world of one is the single-GPU path
+    o = one_rank(s, g, 2, 34)
+    s.close()
+    W.close()
+    assert np.array_equal(o["R"].view(np.uint64), ref["R"].view(np.uint64))
+    with pytest.raises(rsb.RsError):
+        rsb.EmuWorld(0)
