@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--k", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-mgpu", action="store_true", help="skip the emulated multi-GPU model leg")
     p.add_argument("--phases", action="store_true", help="print per-phase ms to stderr")
     return p.parse_args()
 
@@ -381,6 +382,10 @@ def main():
     if not a.no_awcc and world == 1:
         sparse = sparse_leg(a, rsb, dev, stream, sh, flush)
 
+    mgpu = None
+    if world == 1 and not a.no_mgpu:
+        mgpu = multigpu_model(a, g, rsb, st, ms_per_step, tk_ms[0])
+
     e2e = None
     if not a.no_e2e:
         e2e = measure_e2e(a, g, rsb, dev, stream, sh, rank, world, st)
@@ -412,6 +417,7 @@ def main():
             "next_literal_variants": variants,
             "next_shii": shii,
             "next_all_communities": sparse,
+            "multigpu_model": mgpu,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk_s, "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
         }
@@ -419,6 +425,80 @@ def main():
     sc.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+# NVLink figures measured on this pool's B200s (B200_PROFILING.md): 8-rank
+# all-reduce bus bandwidth at 1 GiB and a peer copy, per direction per GPU
+NVLINK_ALLREDUCE_BUSBW = 725e9
+NVLINK_PEER_BW = 770e9
+
+
+def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
+    """The multi-GPU path on this one GPU: N emulated
+    ranks (rs_create_emulated) in SERIAL mode -- inside rs_score the ranks take
+    turns between collectives, so each rank's kernels run alone on the GPU and
+    its rs_stats phase times are those of a GPU of its own. Per phase the max
+    over ranks is taken (ranks wait for each other at every exchange); the
+    exchanges are modelled from their exact byte counts at the measured NVLink
+    figures (NCCL all-reduce moves 2(N-1)/N of the buffer per rank, an
+    all-gather (N-1)/N of the gathered size). Not a multi-GPU measurement: the
+    box has one GPU."""
+    import threading
+    import torch
+    n, D, k = g.n, g.nnz, a.k
+    out = {"how": "per-rank phase times measured (serial emulated ranks, one GPU), max over ranks; "
+                  "exchange bytes exact, at 725 GB/s all-reduce bus bandwidth / 770 GB/s peer copy (measured, "
+                  "B200_PROFILING.md)", "N1_ms_per_step": round(ms1, 4)}
+    for N in worlds:
+        W = rsb.EmuWorld(N)
+        W.serial(True)
+        per, err, xb = [None] * N, [], [None] * N
+
+        def main(r):
+            try:
+                stream = torch.cuda.Stream(device=0)
+                s = rsb.Scorer(0, stream.cuda_stream, rank=r, world=N, emu=W)
+                s.load_csr(g.rowptr, g.col)
+                s.set_communities(g.comm, k)
+                s.score()
+                ph = []
+                for _ in range(reps):
+                    st_last = s.score(stats=True)
+                    ph.append(st_last["ms_phase"])
+                per[r] = np.median(np.array(ph), axis=0)
+                xb[r] = (st_last["xchg_allreduce_bytes"], st_last["xchg_allgather_bytes"])
+                s.close()
+            except Exception as e:  # reported below
+                err.append(repr(e))
+
+        th = [threading.Thread(target=main, args=(r,)) for r in range(N)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        W.close()
+        torch.cuda.empty_cache()
+        if err:
+            out[f"N={N}"] = {"error": err[0]}
+            continue
+        P = np.array(per)
+        A, ED, F = float(P[:, 0].max()), float(P[:, 2].max()), float(P[:, 3].max())
+        # the exchanges: exact byte counts reported by librs (rs_stats), at the
+        # measured NVLink figures; all-reduce buffers move 2(N-1)/N of their size
+        # per rank, an all-gather (N-1)/N of the gathered total
+        ar, ag = xb[0]
+        x1 = ar * 2 * (N - 1) / N / NVLINK_ALLREDUCE_BUSBW + ag * (N - 1) / N / NVLINK_PEER_BW
+        x2 = 0.0
+        tk = tk1                                       # top-K: local select + a K x 12 B all-gather
+        step = A + ED + F + 1e3 * (x1 + x2) + tk
+        out[f"N={N}"] = {"A_ms_max": round(A, 4), "ED_ms_max": round(ED, 4), "F_ms_max": round(F, 4),
+                         "A_ms_ranks": [round(float(x), 4) for x in P[:, 0]],
+                         "ED_ms_ranks": [round(float(x), 4) for x in P[:, 2]],
+                         "allreduce_MB": round(ar / 1e6, 1), "allgather_MB": round(ag / 1e6, 1),
+                         "exchange_ms": round(1e3 * x1, 4),
+                         "step_ms_model": round(step, 4), "GTEPS_model": round(g.m / (step * 1e-3) / 1e9, 3),
+                         "speedup_vs_N1": round(ms1 / step, 3)}
+    return out
 
 
 SPARSE_CFG = dict(base="lj", n_comm=10_000, zipf_s=0.8)

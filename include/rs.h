@@ -58,11 +58,20 @@ typedef struct {
     int64_t n_probes;         /* Phase E: P+ list entries probed (the Type-I
                                  intersection volume, bench roofline)           */
     double omega_max;         /* max weight over all cells (C-7)  */
-    float ms_phase[8];        /* [0] Phase A border/histogram/weights/G' lists
-                                 [1] Phase C B-table + orientation
+    float ms_phase[8];        /* CUDA-event times on the context stream:
+                                 [0] Phase A border/histogram/weights/G' lists,
+                                     orientation, B-table pushes
+                                 [1] multi-GPU: the exchange of Phase A's
+                                     outputs (0 on one GPU)
                                  [2] Phase E Type-I triangles, concurrent with
                                      Phase D Type-II pull
-                                 [3] finalize (sum, normalise) [4..7] reserved */
+                                 [3] finalize (sum, normalise)
+                                 [4] multi-GPU: the sum of the Type-I limbs
+                                     over the ranks [5..7] reserved */
+    int64_t xchg_allreduce_bytes; /* multi-GPU: bytes of the buffers all-reduced
+                                     in this rs_score (0 on one GPU)            */
+    int64_t xchg_allgather_bytes; /* multi-GPU: total bytes all-gathered (every
+                                     rank's segments together)                  */
 } rs_stats;
 
 /* Flags for rs_load_csr. */
@@ -126,6 +135,11 @@ typedef struct rs_emu_world rs_emu_world;
 rs_status rs_emu_world_create(rs_emu_world **out, int32_t world);
 void rs_emu_world_destroy(rs_emu_world *w);
 rs_status rs_create_emulated(rs_ctx **out, int device, void *cuda_stream, int rank, int world, rs_emu_world *w);
+/* Serial mode of an emulated world (on != 0): inside rs_score the ranks take
+ * turns, rank 0 first, between consecutive collectives, so that each rank's
+ * kernels run alone on the GPU and its rs_stats phase times are those of a GPU
+ * of its own (the multi-GPU model of bench.py). RS_EINVAL if w is NULL. */
+rs_status rs_emu_world_serial(rs_emu_world *w, int32_t on);
 
 /* Free every device buffer owned by ctx. NULL is a no-op. */
 void rs_destroy(rs_ctx *ctx);

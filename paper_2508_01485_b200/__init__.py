@@ -47,12 +47,14 @@ class RsError(RuntimeError):
 class rs_stats(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("n_border", ctypes.c_int64),
                 ("n_pred_entries", ctypes.c_int64), ("n_triangles", ctypes.c_int64),
-                ("n_probes", ctypes.c_int64), ("omega_max", ctypes.c_double), ("ms_phase", ctypes.c_float * 8)]
+                ("n_probes", ctypes.c_int64), ("omega_max", ctypes.c_double), ("ms_phase", ctypes.c_float * 8),
+                ("xchg_allreduce_bytes", ctypes.c_int64), ("xchg_allgather_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {"n": self.n, "m": self.m, "n_border": self.n_border, "n_pred_entries": self.n_pred_entries,
                 "n_triangles": self.n_triangles, "n_probes": self.n_probes, "omega_max": self.omega_max,
-                "ms_phase": [float(x) for x in self.ms_phase]}
+                "ms_phase": [float(x) for x in self.ms_phase],
+                "xchg_allreduce_bytes": self.xchg_allreduce_bytes, "xchg_allgather_bytes": self.xchg_allgather_bytes}
 
 
 _P = ctypes.c_void_p
@@ -85,6 +87,7 @@ SIGNATURES = [
     ("rs_emu_world_create", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32]),
     ("rs_emu_world_destroy", None, [_P]),
     ("rs_create_emulated", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, _P]),
+    ("rs_emu_world_serial", ctypes.c_int, [_P, ctypes.c_int32]),
     ("rs_local_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P]),
     ("rs_split_ranges", ctypes.c_int, [ctypes.c_int64, _P, ctypes.c_int32, _P]),
     ("rs_merge_candidates", ctypes.c_int, [ctypes.c_int64, _P, _P, ctypes.c_int64, _P, _P,
@@ -332,6 +335,10 @@ class EmuWorld:
         if st != RS_OK:
             raise RsError(st, "rs_emu_world_create: invalid world size")
         self.h, self.world = h, int(world)
+
+    def serial(self, on: bool = True):
+        """ranks take turns inside rs_score (each rank's phase times = a GPU of its own)"""
+        load_library().rs_emu_world_serial(self.h, 1 if on else 0)
 
     def close(self):
         if self.h is not None:

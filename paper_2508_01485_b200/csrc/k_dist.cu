@@ -1,31 +1,48 @@
 // Multi-GPU exchange helpers (SURVEY §8(e) option 2): every rank
 // runs Phase A on its own vertex range only, then the ranks exchange what the
-// other phases read of the 2-hop neighbourhood. Of the P lists, only the
-// oriented runs P+(x) travel (Phase E probes P+(x) of any predecessor x;
-// P-(y) and P(u) are read only for owned y, u): packed back to back in vertex
-// order at gpre[x] = sum of |P+| over the vertices before x, all-gathered by
-// segment, and unpacked into each vertex's CSR slot on the other ranks.
+// other phases read of the 2-hop neighbourhood, as compactly as the exact
+// results allow; everything derivable is rebuilt locally from replicated data
+// (the CSR, the labels) and the gathered cube-root rows:
+// * per vertex {|P|, |P+|, |P+_T|} (12 B): VRec and PRec are rebuilt from them
+//   (a_self = a_u(C(u)) from the gathered row; head / wide from d(u) and lab);
+// * the oriented runs P+(x): only their ids travel (4 B per entry), packed back
+//   to back in vertex order at gpre[x] = sum of |P+| over the vertices before x;
+//   the weight beside each entry, a_x(c_z), is re-read from x's gathered row;
+// * the P-(y) lists of the heavy middle vertices (degree >= 128; 4 B per
+//   entry): Phase E strides over their work items on every rank;
+// * the B table: only the pushed integer sums (8 B per cell, summed over the
+//   ranks); Q = a_w(c)^2 is recomputed from the gathered rows.
+// P(u) and the light P-(y) stay local: they are read only for a rank's own u, y.
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
 #include <cub/cub.cuh>
 
 namespace rs {
 
-__global__ void k_plus_count(const PRec *__restrict__ pc2, int64_t n, int64_t *cnt) {
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n; x += (int64_t)gridDim.x * blockDim.x)
-        cnt[x] = x < n ? (int64_t)pr_plus(pc2[x]) : 0;
+// MINUS = false: |P+(x)| for every x; true: |P-(y)| for the heavy y < n_heavy, else 0
+template <bool MINUS>
+__global__ void k_run_count(const PRec *__restrict__ pc2, int64_t n, int64_t n_heavy, int64_t *cnt) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n; x += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = 0;
+        if (x < n && (!MINUS || x < n_heavy)) {
+            const PRec r = pc2[x];
+            v = MINUS ? (int64_t)(r.y - pr_plus(r)) : (int64_t)pr_plus(r);
+        }
+        cnt[x] = v;
+    }
 }
 
-// gpre[0..n]: exclusive prefix of |P+(x)| (gpre in the context scratch, the
-// counts and the scan's temporary storage after it)
-cudaError_t launch_plus_prefix(Ctx &c, int64_t *gpre) {
+// gpre[0..n]: exclusive prefix of |P+(x)| (or, minus, of the heavy |P-(y)|) in
+// the context scratch, the counts and the scan's temporary storage after it
+cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus) {
     const int64_t n = c.n;
     int64_t *cnt = gpre + (n + 1);
     void *tmp = cnt + (n + 1);
     const size_t used = sizeof(int64_t) * 2 * (size_t)(n + 1);
     if (used > c.scratch_bytes) return cudaErrorMemoryAllocation;
     const size_t tmp_bytes = c.scratch_bytes - used;
-    k_plus_count<<<148 * 4, 256, 0, c.stream>>>(c.pc2, n, cnt);
+    if (minus) k_run_count<true><<<148 * 4, 256, 0, c.stream>>>(c.pc2, n, c.e_nbig, cnt);
+    else k_run_count<false><<<148 * 4, 256, 0, c.stream>>>(c.pc2, n, c.e_nbig, cnt);
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, gpre, (int)(n + 1), c.stream);
     if (need > tmp_bytes) return cudaErrorMemoryAllocation;
@@ -34,12 +51,14 @@ cudaError_t launch_plus_prefix(Ctx &c, int64_t *gpre) {
     return cudaGetLastError();
 }
 
-// a warp per vertex: pack the owned vertices' runs (UNPACK = false), or copy
-// every other vertex's run from the gathered buffer into its slot (true)
+// a warp per vertex: pack the owned vertices' P+ ids (UNPACK = false), or copy
+// every other vertex's run from the gathered buffer into its slot and set the
+// weight beside each entry, a_x(c_z) for a target z (0 otherwise), from x's row
 template <bool UNPACK>
 __global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gpre, int64_t n, int64_t lo,
                             int64_t hi, int32_t *__restrict__ pplus, double *__restrict__ wps,
-                            int32_t *__restrict__ pk_id, double *__restrict__ pk_w) {
+                            int32_t *__restrict__ pk_id, const uint8_t *__restrict__ lab,
+                            const double *__restrict__ amat, int k) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t first = UNPACK ? 0 : lo, last = UNPACK ? n : hi;
@@ -50,23 +69,120 @@ __global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restr
         const int64_t slot = pr_start(r), g = gpre[x];
         for (int i = lane; i < pp; i += 32) {
             if (UNPACK) {
-                pplus[slot + i] = pk_id[g + i];
-                wps[slot + i] = pk_w[g + i];
+                const int32_t z = pk_id[g + i];
+                const int lz = lab[z];
+                pplus[slot + i] = z;
+                wps[slot + i] = lz < k ? __ldg(amat + x * k + lz) : 0.0;
             } else {
                 pk_id[g + i] = pplus[slot + i];
-                pk_w[g + i] = wps[slot + i];
             }
         }
     }
 }
 
+// a warp per heavy vertex: pack the owned ones' P-(y) (the suffix of P(y) in its
+// slot), or copy every other heavy vertex's P-(y) into its slot
+template <bool UNPACK>
+__global__ void k_minus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gm, int64_t n_heavy, int64_t lo,
+                             int64_t hi, int32_t *__restrict__ pidx, int32_t *__restrict__ pk) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t first = UNPACK ? 0 : lo, last = UNPACK ? n_heavy : (hi < n_heavy ? hi : n_heavy);
+    for (int64_t y = first + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); y < last; y += nw) {
+        if (UNPACK && y >= lo && y < hi) continue;
+        const PRec r = pc2[y];
+        const int pp = pr_plus(r), pm = r.y - pp;
+        const int64_t at = pr_start(r) + pp, g = gm[y];
+        for (int i = lane; i < pm; i += 32) {
+            if (UNPACK) pidx[at + i] = pk[g + i];
+            else pk[g + i] = pidx[at + i];
+        }
+    }
+}
+cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm, bool unpack) {
+    if (unpack)
+        k_minus_pack<true><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gm, c.e_nbig, c.head_lo, c.head_hi, c.pidx, c.pk_m);
+    else
+        k_minus_pack<false><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gm, c.e_nbig, c.head_lo, c.head_hi, c.pidx, c.pk_m);
+    c.launches++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre, bool unpack) {
     if (unpack)
         k_plus_pack<true><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.wps,
-                                                        c.pk_id, c.pk_w);
+                                                        c.pk_id, c.lab, c.amat, c.k);
     else
         k_plus_pack<false><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.wps,
-                                                         c.pk_id, c.pk_w);
+                                                         c.pk_id, c.lab, c.amat, c.k);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+// {|P(u)|, |P+(u)|, |P+_T(u)|} of the owned vertices
+__global__ void k_vx_pack(const VRec *__restrict__ vrec, const PRec *__restrict__ pc2, int64_t lo, int64_t hi,
+                          int32_t *__restrict__ vx) {
+    for (int64_t u = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < hi; u += (int64_t)gridDim.x * blockDim.x) {
+        const PRec r = pc2[u];
+        vx[3 * u] = vrec[u].pcnt;
+        vx[3 * u + 1] = pr_plus(r);
+        vx[3 * u + 2] = pr_plus_t(r);
+    }
+}
+cudaError_t launch_vx_pack(Ctx &c) {
+    const int64_t m = std::max<int64_t>(c.head_hi - c.head_lo, 1);
+    k_vx_pack<<<(unsigned)std::min<int64_t>((m + 255) / 256, 148 * 8), 256, 0, c.stream>>>(c.vrec, c.pc2, c.head_lo,
+                                                                                         c.head_hi, c.vx);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+// VRec and PRec of every other vertex, as Phase A writes them (write_vrec, the
+// PRec of phase_a_vertex), from the exchanged counts and the gathered row
+__global__ void k_vx_unpack(const int32_t *__restrict__ vx, const int64_t *__restrict__ rowptr,
+                            const uint8_t *__restrict__ lab, const double *__restrict__ amat, int k, double wide_bound,
+                            int64_t n, int64_t lo, int64_t hi, VRec *__restrict__ vrec, PRec *__restrict__ pc2) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        if (u >= lo && u < hi) continue;
+        const uint32_t lu = lab[u];
+        const int64_t beg = rowptr[u], d = rowptr[u + 1] - beg;
+        VRec v;
+        v.a_self = lu < (uint32_t)k ? amat[u * k + lu] : 0.0;
+        v.pcnt = vx[3 * u];
+        v.lab = (uint8_t)lu;
+        v.head = (lu < (uint32_t)k && d >= 2) ? 1 : 0;
+        v.wide = ((double)d * (double)d >= wide_bound) ? 1 : 0;
+        v.pad = 0;
+        vrec[u] = v;
+        PRec r;
+        r.x = pr_pack(vx[3 * u + 1], lu);
+        r.y = vx[3 * u];
+        r.start = beg | ((long long)vx[3 * u + 2] << kPrShift);
+        pc2[u] = r;
+    }
+}
+cudaError_t launch_vx_unpack(Ctx &c) {
+    k_vx_unpack<<<148 * 8, 256, 0, c.stream>>>(c.vx, c.rowptr, c.lab, c.amat, c.k, wide_bound(c.k), c.n, c.head_lo,
+                                              c.head_hi, c.vrec, c.pc2);
+    c.launches++;
+    return cudaGetLastError();
+}
+
+// the B table of the Type-II pull: {B_w[c] (summed pushes), Q_w(c) = a_w(c)^2}
+__global__ void k_b_rebuild(const unsigned long long *__restrict__ bsum, const double *__restrict__ amat, int64_t n,
+                            int k, BQL *__restrict__ bql) {
+    const int64_t total = n * k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / n, w = i - c * n;       // column-major, like bql
+        const double a = amat[w * k + c];
+        BQL r;
+        r.b = bsum[i];
+        r.Q = a * a;
+        bql[i] = r;
+    }
+}
+cudaError_t launch_b_rebuild(Ctx &c) {
+    k_b_rebuild<<<148 * 8, 256, 0, c.stream>>>(c.bsum, c.amat, c.n, c.k, c.bql);
     c.launches++;
     return cudaGetLastError();
 }

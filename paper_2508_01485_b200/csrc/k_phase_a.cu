@@ -58,6 +58,8 @@ struct PhaseAArgs {
     VRec *__restrict__ vrec;
     int32_t *__restrict__ pidx;
     uint8_t *__restrict__ plab;         // label of each P(u) entry, beside it
+    unsigned long long *__restrict__ bsum;   // multi-GPU: the B pushes go here (k x n u64, summed over
+                                        // the ranks, then rebuilt into BQL with Q); nullptr on one GPU
     unsigned long long *scal;
 };
 
@@ -329,7 +331,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
                 a.f[u * k + c] = fc;
             } else {
                 a.amat[u * k + c] = ac;
-                a.bql[(int64_t)c * a.n + u].Q = ac * ac;
+                if (!a.bsum) a.bql[(int64_t)c * a.n + u].Q = ac * ac;
             }
             if (in_max(a, fc, L_all, c, (int)lu, pc)) wmax = w > wmax ? w : wmax;
         }
@@ -355,7 +357,10 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
     if (valid && g.lane == 0) write_vrec(a, u, lu < k ? aself : 0.0, pc, lu, d);
     // Step 3 inputs: B pushes and the P+ runs, reading P(u) back
     const unsigned long long qs = (valid && lu < k) ? bq_quantize(aself, a.bq) : 0ull;
-    BQL *bcol = a.bql + (int64_t)(qs ? lu : 0) * a.n;
+    // the pushes: into B_v's record, or (multi-GPU) the plain u64 sums
+    const int64_t col0 = (int64_t)(qs ? lu : 0) * a.n;
+    unsigned long long *bpush = a.bsum ? a.bsum + col0 : &a.bql[col0].b;
+    const int bstride = a.bsum ? 1 : 2;                 // u64 words per entry
     const int32_t *__restrict__ pin = a.pidx + beg;
     const uint8_t *__restrict__ lin = a.plab + beg;
     int ct = 0;
@@ -372,7 +377,7 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
 #ifndef RS_EXP_NO_BPUSH
 #pragma unroll
         for (int j = 0; j < U; j++)
-            if (qs && v[j] >= 0) atomicAdd(&bcol[v[j]].b, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
+            if (qs && v[j] >= 0) atomicAdd(bpush + (int64_t)v[j] * bstride, qs);   // u in P(v): a_u(c_u) into B_v[c_u]
 #endif
         bool t[U];
 #pragma unroll
@@ -634,6 +639,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.bq = c.bq;
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.plab = c.plab;
+    a.bsum = (c.world > 1 && !parity) ? c.bsum : nullptr;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8) launch_bins_a<false>(c, a, lo, hi);
     else launch_bins_a<true>(c, a, lo, hi);

@@ -706,10 +706,9 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     int32_t *off = cnt + (nh + 1);
     EItem *items = (EItem *)(((uintptr_t)(off + (nh + 1)) + 15) & ~(uintptr_t)15);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nh + 256) / 256, 148 * 4));
-    // multi-GPU: a rank takes the middle vertices of its own range (their P-(y)
-    // lists live only there); one GPU: all
-    const int64_t lo = c.world > 1 ? c.head_lo : 0, hi = c.world > 1 ? c.head_hi : c.n;
-    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, lo, hi, cnt);
+    // every heavy middle vertex (multi-GPU too: their P-(y) lists are exchanged,
+    // and the ranks stride over the items)
+    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, 0, c.n, cnt);
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
     if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
@@ -725,14 +724,23 @@ template <bool COUNT, bool SPARSE>
 static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     CdeArgs a = cde_args(c);
     int64_t ylo = 0, yhi = c.n;
+    CdeArgs ah;                                       // the heavy kernel's share of the items
     if (c.world > 1) {
-        // a rank takes the middle vertices of its own range (P-(y) is local); every
-        // head's terms are accumulated here and summed over the ranks afterwards
-        // (exact integer limbs)
+        // every head's terms are accumulated here and summed over the ranks
+        // afterwards (exact integer limbs). Light middle vertices: a rank's own
+        // range (P-(y) is local). Heavy ones (degree >= 128; the hubs hold most
+        // of the Type-I work, which a vertex-range split leaves on rank 0): the
+        // ranks stride over the items, heaviest first (P-(y) of every heavy y is
+        // exchanged after Phase A)
         a.head_lo = 0;
         a.head_hi = c.n;
         ylo = c.head_lo;
         yhi = c.head_hi;
+    }
+    ah = a;
+    if (c.world > 1) {
+        ah.e_rank = c.rank;
+        ah.e_world = c.world;
     }
     // test hook (RS_E_SHARES): the rank split run as sequential shares on one GPU
     const int shares = c.world > 1 ? 1 : std::max(1, c.e_shares);
@@ -753,8 +761,8 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     for (int s = 0; s < shares; s++) {
         if (shares > 1) {
-            a.e_rank = s;
-            a.e_world = shares;
+            a.e_rank = ah.e_rank = s;
+            a.e_world = ah.e_world = shares;
         }
         cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream);
         const int64_t l0 = std::max<int64_t>(n_heavy, ylo);
@@ -768,7 +776,7 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
             c.launches++;
         }
         if (n_heavy > 0) {
-            k_phase_e<COUNT, SPARSE><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(a, it, ctr);
+            k_phase_e<COUNT, SPARSE><<<std::max(1, per_sm) * sms, kWarpsE * 32, smem, c.stream>>>(ah, it, ctr);
             c.launches++;
         }
     }

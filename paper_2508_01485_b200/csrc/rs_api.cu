@@ -237,7 +237,9 @@ static void free_graph(rs_ctx *ctx) {
     dfree(c.acc1); dfree(c.acc_hub); dfree(c.t2); dfree(c.n1); dfree(c.score); dfree(c.f); dfree(c.omega); dfree(c.bql);
     dfree(c.cid); dfree(c.srec); dfree(c.ctk); dfree(c.ctb); dfree(c.pwr); dfree(c.prv); dfree(c.aself);
     dfree(c.xsum); dfree(c.n2s);
-    dfree(c.pk_id); dfree(c.pk_w); c.pk_cap = 0;
+    dfree(c.pk_id); c.pk_cap = 0;
+    dfree(c.pk_m); c.pkm_cap = 0;
+    dfree(c.bsum); dfree(c.vx); c.dist_cap = 0;
     c.sp_cap = 0;
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
     c.cap_n = c.cap_nnz = 0;
@@ -553,12 +555,13 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
 
 // ------------------------------------------------------------------ multi-GPU exchange
 // After each rank's Phase A shard (vertices [head_lo, head_hi)), every rank needs
-// for ALL vertices: omega_max (max), the B table (sums of every rank's pushes;
-// Q = a^2 is written by the owner only and the table is zeroed, so the same
-// integer sum copies it), the cube-root rows, vrec and pc2 (written by the
-// owner: all-gathered by segment), and the oriented runs P+(x) with their
-// weights (packed, all-gathered, unpacked into the slots). Exact: every value
-// is either copied bit for bit or an integer sum.
+// for ALL vertices what the other phases read of the 2-hop neighbourhood
+// (k_dist.cu): omega_max (max), the B sums (k x n u64, integer sum of every
+// rank's pushes), the cube-root rows (all-gather by segment), {|P|, |P+|,
+// |P+_T|} per vertex and the ids of the oriented runs P+(x) (all-gathered;
+// VRec, PRec, Q and the weights beside P+ entries are rebuilt from them and the
+// rows). Exact: every value is copied bit for bit, an integer sum, or
+// recomputed by the same operation Phase A uses. Bytes: DESIGN.md §7.
 static rs_status exchange_phase_a(rs_ctx *ctx) {
     Ctx &c = ctx->c;
     const int W = c.world;
@@ -570,17 +573,44 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
             len[r] = (size_t)(c.bounds[r + 1] - c.bounds[r]) * per;
         }
     };
+    c.xar_bytes = 8 + 8 * n * k;
+    c.xag_bytes = 0;
     XK(c.xp->allreduce_u64(c.scal + rs::kScalOmegaMaxBits, 1, true, c.stream));
-    XK(c.xp->allreduce_u64((unsigned long long *)c.bql, (size_t)(2 * n * k), false, c.stream));
+    XK(c.xp->allreduce_u64(c.bsum, (size_t)(n * k), false, c.stream));
     seg(sizeof(double) * k);
     XK(c.xp->allgatherv(c.amat, off.data(), len.data(), c.stream));
-    seg(sizeof(rs::VRec));
-    XK(c.xp->allgatherv(c.vrec, off.data(), len.data(), c.stream));
-    seg(sizeof(rs::PRec));
-    XK(c.xp->allgatherv(c.pc2, off.data(), len.data(), c.stream));
+    CK(rs::launch_vx_pack(c));
+    seg(3 * sizeof(int32_t));
+    c.xag_bytes += (8 * k + 12) * n;
+    XK(c.xp->allgatherv(c.vx, off.data(), len.data(), c.stream));
+    CK(rs::launch_vx_unpack(c));
+    CK(rs::launch_b_rebuild(c));
+    // the heavy P-(y) lists (Phase E's items stride over the ranks): gm = prefix of
+    // |P-(y)| over y < n_heavy in vertex order (every rank computes the same)
+    int64_t *gm = (int64_t *)c.scratch;
+    CK(rs::launch_run_prefix(c, gm, true));
+    {
+        std::vector<int64_t> hb(W + 1);
+        for (int r = 0; r <= W; r++)
+            CK(cudaMemcpyAsync(&hb[r], gm + std::min<int64_t>(c.bounds[r], c.e_nbig), sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        if (hb[W] > c.pkm_cap) {
+            CK(dalloc(&c.pk_m, (size_t)hb[W]));
+            c.pkm_cap = hb[W];
+        }
+        CK(rs::launch_minus_pack(c, gm, false));
+        for (int r = 0; r < W; r++) {
+            off[r] = (size_t)hb[r] * sizeof(int32_t);
+            len[r] = (size_t)(hb[r + 1] - hb[r]) * sizeof(int32_t);
+        }
+        XK(c.xp->allgatherv(c.pk_m, off.data(), len.data(), c.stream));
+        c.xag_bytes += 4 * hb[W];
+        CK(rs::launch_minus_pack(c, gm, true));
+    }
     // the P+ runs: gpre = prefix of |P+| in vertex order (every rank computes the same)
     int64_t *gpre = (int64_t *)c.scratch;
-    CK(rs::launch_plus_prefix(c, gpre));
+    CK(rs::launch_run_prefix(c, gpre, false));
     std::vector<int64_t> gb(W + 1);
     for (int r = 0; r <= W; r++)
         CK(cudaMemcpyAsync(&gb[r], gpre + c.bounds[r], sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
@@ -588,7 +618,6 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
     const int64_t total = gb[W];
     if (total > c.pk_cap) {
         CK(dalloc(&c.pk_id, (size_t)total));
-        CK(dalloc(&c.pk_w, (size_t)total));
         c.pk_cap = total;
     }
     CK(rs::launch_plus_pack(c, gpre, false));
@@ -597,11 +626,7 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
         len[r] = (size_t)(gb[r + 1] - gb[r]) * sizeof(int32_t);
     }
     XK(c.xp->allgatherv(c.pk_id, off.data(), len.data(), c.stream));
-    for (int r = 0; r < W; r++) {
-        off[r] = (size_t)gb[r] * sizeof(double);
-        len[r] = (size_t)(gb[r + 1] - gb[r]) * sizeof(double);
-    }
-    XK(c.xp->allgatherv(c.pk_w, off.data(), len.data(), c.stream));
+    c.xag_bytes += 4 * total;
     CK(rs::launch_plus_pack(c, gpre, true));
     return RS_OK;
 }
@@ -617,6 +642,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     c.variant = (int)((flags >> 16) & 7u);
     if (c.sparse && c.variant)
         return fail(ctx, RS_EINVAL, "rs_score: the NEXT-3 variant flags need explicit targets (k <= 254)");
+    if (c.xp) c.xp->score_begin();
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     // the accumulators (and the dense B table) were zeroed on a side stream at the
     // end of the previous rs_score, overlapping rs_topk; otherwise zero them here
@@ -640,7 +666,17 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(rs::launch_sparse_lists(c));
         join(c);
     } else {
-        if (!c.bql_zero) CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs
+        if (c.world > 1) {
+            // multi-GPU: the pushes go to plain u64 sums (exchanged, then rebuilt into BQL)
+            if (c.dist_cap < n * c.k) {
+                CK(dalloc(&c.bsum, (size_t)(n * c.k)));
+                CK(dalloc(&c.vx, (size_t)(3 * n)));
+                c.dist_cap = n * c.k;
+            }
+            CK(cudaMemsetAsync(c.bsum, 0, sizeof(unsigned long long) * (size_t)n * c.k, c.stream));
+        } else if (!c.bql_zero) {
+            CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs
+        }
         c.bql_zero = false;
         // Phase A: border + histogram + weights + P lists + omega_max partials, the
         // orientation of G' and the B-table pushes
@@ -670,23 +706,26 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         fprintf(stderr, "[rank %d] own [%lld, %lld) n_heavy %lld: triangles %llu probes %llu\n", c.rank,
                 (long long)c.head_lo, (long long)c.head_hi, (long long)c.e_nbig, v[0], v[1]);
     }
+    CK(cudaEventRecord(c.ev_phase[3], c.stream));
     if (c.world > 1) {
         // Phase E is split by middle vertex: sum every head's Type-I limbs (and the
         // triangle/probe counters) over the ranks; integer sums, exact in any order
+        c.xar_bytes += 8 * (3 * n + 3 * rs::kHubStripes * c.n_hub + 2);
         XK(c.xp->allreduce_u64(c.acc1, (size_t)(3 * n), false, c.stream));
         XK(c.xp->allreduce_u64(c.acc_hub, (size_t)(3 * rs::kHubStripes * c.n_hub), false, c.stream));
         XK(c.xp->allreduce_u64(c.scal + rs::kScalNTri, 2, false, c.stream));
     }
-    CK(cudaEventRecord(c.ev_phase[3], c.stream));
+    CK(cudaEventRecord(c.ev_phase[4], c.stream));
     // multi-GPU: a rank writes only its heads' scores (scattered in original order)
     if (c.world > 1) CK(cudaMemsetAsync(c.score, 0, sizeof(double) * n, c.stream));
     // finalize: Type-II + Type-I sums, / omega_max / d(d-1), original order
     CK(rs::launch_finalize(c));
-    CK(cudaEventRecord(c.ev_phase[4], c.stream));
+    CK(cudaEventRecord(c.ev_phase[5], c.stream));
     if (c.world > 1 && (flags & RS_GATHER_SCORES)) {
         // owned heads are a contiguous internal range, scattered in original order;
         // every other entry is +0.0 (all-zero bits) on a rank, so an integer sum of
         // the bit patterns gathers the scores exactly
+        c.xar_bytes += 8 * n;
         XK(c.xp->allreduce_u64((unsigned long long *)c.score, (size_t)n, false, c.stream));
     }
     // zero the accumulators (and the dense B table) for the next rs_score on a side
@@ -703,6 +742,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         if (!c.sparse) c.bql_zero = true;
     }
     c.scored = true;
+    if (c.xp) c.xp->score_end(c.stream);
     if (scores_out) {
         const bool dev = is_device_ptr(scores_out);
         CK(cudaMemcpyAsync(scores_out, c.score, sizeof(double) * n,
@@ -723,8 +763,15 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         unsigned long long wb = 0;
         CK(cudaMemcpy(&wb, c.scal + rs::kScalOmegaMaxBits, sizeof(wb), cudaMemcpyDeviceToHost));
         memcpy(&s.omega_max, &wb, sizeof(double));
-        for (int i = 0; i < 4; i++) CK(cudaEventElapsedTime(&s.ms_phase[i], c.ev_phase[i], c.ev_phase[i + 1]));
-        // ms_phase: [0] A (incl. zeroing) [1] - (no Phase C) [2] E (Type-I) || D (Type-II) [3] finalize
+        // ms_phase: [0] A (incl. zeroing) [1] the Phase A exchange (multi-GPU; else 0)
+        // [2] E (Type-I) || D (Type-II) [3] finalize [4] the limb sum over the ranks
+        CK(cudaEventElapsedTime(&s.ms_phase[0], c.ev_phase[0], c.ev_phase[1]));
+        CK(cudaEventElapsedTime(&s.ms_phase[1], c.ev_phase[1], c.ev_phase[2]));
+        CK(cudaEventElapsedTime(&s.ms_phase[2], c.ev_phase[2], c.ev_phase[3]));
+        CK(cudaEventElapsedTime(&s.ms_phase[3], c.ev_phase[4], c.ev_phase[5]));
+        CK(cudaEventElapsedTime(&s.ms_phase[4], c.ev_phase[3], c.ev_phase[4]));
+        s.xchg_allreduce_bytes = c.world > 1 ? c.xar_bytes : 0;
+        s.xchg_allgather_bytes = c.world > 1 ? c.xag_bytes : 0;
         *stats_out = s;
     }
     (void)flags;
@@ -807,6 +854,10 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         if (sc_d) CK(cudaMemcpyAsync(sc_d, hs.data(), sizeof(double) * Kc, cudaMemcpyHostToDevice, c.stream));
         CK(cudaStreamSynchronize(c.stream));
     }
+    // the accumulators zeroed for the next rs_score on a side stream (forked at the
+    // end of rs_score) overlap this call; the library stream waits for them here,
+    // so a step timed on it includes that work
+    if (c.acc_zero) CK(cudaStreamWaitEvent(c.stream, c.ev_zero, 0));
     if (!dev_ids) CK(cudaMemcpyAsync(ids_out, ids_d, sizeof(int32_t) * Kc, cudaMemcpyDeviceToHost, c.stream));
     if (scores_out && !dev_sc)
         CK(cudaMemcpyAsync(scores_out, sc_d, sizeof(double) * Kc, cudaMemcpyDeviceToHost, c.stream));

@@ -55,6 +55,10 @@ struct Xport {
     virtual cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) = 0;
     virtual cudaError_t allreduce_u64(unsigned long long *buf, size_t count, bool max, cudaStream_t s) = 0;
     virtual cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+    // rs_score brackets (the emulated world's serial mode times each rank's
+    // compute alone on the GPU: ranks take turns between collectives)
+    virtual void score_begin() {}
+    virtual void score_end(cudaStream_t) {}
 };
 struct EmuWorld;
 Xport *make_emu_xport(EmuWorld *w, int rank);
@@ -166,9 +170,14 @@ struct Ctx {
     ncclComm_t comm = nullptr;
 #endif
     Xport *xp = nullptr;                       // world > 1: the exchange transport (owned)
-    int32_t *pk_id = nullptr;                  // world > 1: packed P+ runs of all ranks (ids, weights)
-    double *pk_w = nullptr;
+    int32_t *pk_id = nullptr;                  // world > 1: packed P+ runs of all ranks (ids)
     int64_t pk_cap = 0;
+    int32_t *pk_m = nullptr;                   // world > 1: packed P- lists of the heavy vertices
+    int64_t pkm_cap = 0;
+    int64_t xar_bytes = 0, xag_bytes = 0;      // world > 1: bytes all-reduced / all-gathered in the last rs_score
+    unsigned long long *bsum = nullptr;        // world > 1: B pushes (k x n), summed over the ranks
+    int32_t *vx = nullptr;                     // world > 1: {|P|, |P+|, |P+_T|} per vertex, exchanged
+    int64_t dist_cap = 0;                      // n * k the two above were sized for
     unsigned long long *tk_gkey = nullptr;     // world > 1: gathered top-K candidates (world * K)
     int32_t *tk_gid = nullptr;
     int64_t tk_gcap = 0;
@@ -306,8 +315,12 @@ cudaError_t launch_awcc_degrees(Ctx &c, const int32_t *S_dev, int64_t nS, int64_
 cudaError_t launch_awcc_trial(Ctx &c, const int32_t *S_dev, int64_t nS, int mode, int step_pct, int J1, uint64_t st,
                               int32_t *zeta_dev, void *scratch, size_t scratch_bytes, int64_t cap);
 cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light);
-cudaError_t launch_plus_prefix(Ctx &c, int64_t *gpre);
+cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus);
 cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre, bool unpack);
+cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm, bool unpack);
+cudaError_t launch_vx_pack(Ctx &c);
+cudaError_t launch_vx_unpack(Ctx &c);
+cudaError_t launch_b_rebuild(Ctx &c);
 cudaError_t launch_triangle_counts(Ctx &c);
 cudaError_t launch_e_items(Ctx &c);
 cudaError_t launch_topk(Ctx &c, int64_t K, int32_t *ids_dev, double *scores_dev, int64_t lo, int64_t hi);

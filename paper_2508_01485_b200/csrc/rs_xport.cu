@@ -57,16 +57,31 @@ struct EmuWorld {
     int arrived = 0;
     unsigned long long generation = 0;
     std::vector<const void *> ptr;   // each rank's buffer of the current collective
+    // serial mode (rs_emu_world_serial): inside rs_score the ranks take turns,
+    // rank 0 first, between consecutive collectives, so each rank's kernels run
+    // alone on the GPU and its phase times are those of a GPU of its own
+    bool serial = false;
+    int token = 0;                   // the rank whose turn it is
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
         const unsigned long long gen = generation;
         if (++arrived == world) {
             arrived = 0;
             generation++;
+            token = 0;
             cv.notify_all();
         } else {
             cv.wait(lk, [&] { return generation != gen; });
         }
+    }
+    void turn_begin(int rank) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return token == rank; });
+    }
+    void turn_end(int rank) {
+        std::unique_lock<std::mutex> lk(mu);
+        if (token == rank) token = (rank + 1) % world;   // after the last rank: rank 0's next turn
+        cv.notify_all();
     }
 };
 
@@ -95,11 +110,27 @@ struct EmuXport : Xport {
     ~EmuXport() override {
         if (tmp) cudaFree(tmp);
     }
+    bool in_score = false;
+    void score_begin() override {
+        in_score = W->serial;
+        if (in_score) W->turn_begin(rank);
+    }
+    void score_end(cudaStream_t s) override {
+        if (!in_score) return;
+        cudaStreamSynchronize(s);
+        W->turn_end(rank);
+        in_score = false;
+    }
     cudaError_t publish(const void *p, cudaStream_t s) {
         const cudaError_t e = cudaStreamSynchronize(s);   // this rank's buffer is final
+        if (in_score) W->turn_end(rank);
         W->ptr[rank] = p;
         W->barrier();
         return e;
+    }
+    // the end of a collective: in serial mode wait for this rank's turn again
+    void resume() {
+        if (in_score) W->turn_begin(rank);
     }
     cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) override {
         cudaError_t e = publish(buf, s);
@@ -109,6 +140,7 @@ struct EmuXport : Xport {
                                     cudaMemcpyDeviceToDevice, s);
         const cudaError_t e2 = cudaStreamSynchronize(s);
         W->barrier();                                      // every peer done reading
+        resume();
         return e != cudaSuccess ? e : e2;
     }
     cudaError_t allreduce_u64(unsigned long long *buf, size_t count, bool max, cudaStream_t s) override {
@@ -134,6 +166,7 @@ struct EmuXport : Xport {
         if (e == cudaSuccess) e = e2;
         if (e == cudaSuccess && count)
             e = cudaMemcpyAsync(buf, tmp, sizeof(unsigned long long) * count, cudaMemcpyDeviceToDevice, s);
+        resume();
         return e;
     }
     cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
@@ -142,6 +175,7 @@ struct EmuXport : Xport {
             e = cudaMemcpyAsync((char *)recv + (size_t)p * bytes, W->ptr[p], bytes, cudaMemcpyDeviceToDevice, s);
         const cudaError_t e2 = cudaStreamSynchronize(s);
         W->barrier();
+        resume();
         return e != cudaSuccess ? e : e2;
     }
 };
@@ -169,3 +203,11 @@ extern "C" rs_status rs_emu_world_create(rs_emu_world **out, int32_t world) {
 }
 
 extern "C" void rs_emu_world_destroy(rs_emu_world *w) { delete w; }
+
+extern "C" rs_status rs_emu_world_serial(rs_emu_world *w, int32_t on) {
+    if (!w) return RS_EINVAL;
+    std::lock_guard<std::mutex> lk(w->w.mu);
+    w->w.serial = on != 0;
+    w->w.token = 0;
+    return RS_OK;
+}

@@ -117,3 +117,42 @@ def test_emulated_world_tiny_and_errors():
     assert np.array_equal(o["R"].view(np.uint64), ref["R"].view(np.uint64))
     with pytest.raises(rsb.RsError):
         rsb.EmuWorld(0)
+
+
+def test_emulated_world_serial_mode_repeats():
+    """serial mode (the multi-GPU model of bench.py): ranks take turns inside
+    rs_score, several calls in a row, same bits as the concurrent world"""
+    import torch
+    g = gen.config_graph("orkut", scale=0.004)
+    s = rsb.Scorer(0)
+    ref = one_rank(s, g, 5, 25)
+    s.close()
+    world = 4
+    W = rsb.EmuWorld(world)
+    W.serial(True)
+    out, err = [None] * world, []
+
+    def main(r):
+        try:
+            stream = torch.cuda.Stream(device=0)
+            sc = rsb.Scorer(0, stream.cuda_stream, rank=r, world=world, emu=W)
+            sc.load_csr(g.rowptr, g.col)
+            sc.set_communities(g.comm, 5)
+            for _ in range(3):
+                R = np.empty(g.n)
+                st = sc.score(scores_out=R, stats=True, gather=True)
+            out[r] = (R, st["ms_phase"])
+            sc.close()
+        except Exception as e:
+            err.append(repr(e))
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    W.close()
+    assert not err and all(o is not None for o in out), err
+    for R, ph in out:
+        assert np.array_equal(R.view(np.uint64), ref["R"].view(np.uint64))
+        assert ph[0] > 0 and ph[2] > 0
