@@ -44,12 +44,14 @@ constexpr int kBmWords = 128;    // 4096-bit membership filter of P+(y)
 constexpr int kPiece = 4;        // consecutive P+(x) entries one lane probes per round
 constexpr int kQCapE = 160;      // candidate queue (31 + 32 * kPiece < 160)
 constexpr int kPsWords = 128;    // piece-start bitmap: items of at most 4096 pieces (else binary search)
-constexpr int kSlotMaxHits = 4096;   // smem limbs of an x slot take at most this many terms
 constexpr int kWarpsE = 8;
 #ifndef RS_EXP_QBATCH
 #define RS_EXP_QBATCH 2
 #endif
 constexpr int kQBatch = RS_EXP_QBATCH;   // heavy work items per queue pop
+#ifndef RS_EXP_E_DEPTH
+#define RS_EXP_E_DEPTH 1                     // probe rounds in flight ahead of the one being filtered (1 or 2; 2: E||D +0.02 ms, spills)
+#endif
 
 // membership filter bit of z (top 12 bits of a multiplicative hash)
 __device__ __forceinline__ uint32_t bm_bit(int32_t z) {
@@ -149,8 +151,9 @@ __device__ __forceinline__ void cut_range(const int32_t *__restrict__ pplus, int
 
 // shared-memory per-item accumulator: four 20-bit limbs of q (< 2^80) added with
 // native 32-bit shared atomics (64-bit shared atomics are CAS loops); exact
-// while a slot receives fewer than 2^12 terms per item (x slots with longer
-// P+(x) go straight to the global limbs).
+// while a slot receives at most CdeArgs::slot_cap terms per item (the top limb
+// then cannot wrap; x slots with longer probed P+(x) go straight to the global
+// limbs).
 __device__ __forceinline__ void smem_red4(uint32_t *acc4, const U128 &q) {
     const uint32_t l0 = (uint32_t)(q.lo & 0xFFFFFull), l1 = (uint32_t)((q.lo >> 20) & 0xFFFFFull);
     const uint32_t l2 = (uint32_t)((q.lo >> 40) & 0xFFFFFull), l3 = (uint32_t)((q.lo >> 60) | (q.hi << 4));
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 #ifndef RS_EXP_NO_XRED
                             if (tx > 0.0) {
                                 const int lenx = S.xn[slot].x;
-                                if (lenx <= kSlotMaxHits) smem_red4(S.xa + 4 * slot, fx_quantize(tx));
+                                if (lenx <= a.slot_cap) smem_red4(S.xa + 4 * slot, fx_quantize(tx));
                                 else if (owned(a, x)) acc_add(a, x, fx_quantize(tx));
                             }
 #endif
@@ -439,16 +442,28 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             }
         };
 
-        // one piece per lane per round, the next round's loads in flight while this
-        // round is filtered; filter candidates packed by one warp scan
+        // one piece per lane per round, the next RS_EXP_E_DEPTH rounds' loads in flight
+        // while this round is filtered (profiled: with one round ahead, the wait for
+        // the piece was the top stall, 17% of the samples); filter candidates
+        // packed by one warp scan
         int32_t zc[kPiece];
         int tagc;
         fetch(0, zc, tagc);
+#if RS_EXP_E_DEPTH >= 2
+        int32_t zm[kPiece];
+        int tagm = 0;
+        if (32 < npieces) {
+            fetch(32, zm, tagm);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPiece; j++) zm[j] = -1;
+        }
+#endif
         for (int p0 = 0; p0 < npieces; p0 += 32) {
             int32_t zn[kPiece];
             int tagn = 0;
-            if (p0 + 32 < npieces) {
-                fetch(p0 + 32, zn, tagn);
+            if (p0 + 32 * RS_EXP_E_DEPTH < npieces) {
+                fetch(p0 + 32 * RS_EXP_E_DEPTH, zn, tagn);
             } else {
 #pragma unroll
                 for (int j = 0; j < kPiece; j++) zn[j] = -1;
@@ -476,9 +491,16 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 #endif
             __syncwarp();
             drain(32);
+#if RS_EXP_E_DEPTH >= 2
+#pragma unroll
+            for (int j = 0; j < kPiece; j++) { zc[j] = zm[j]; zm[j] = zn[j]; }
+            tagc = tagm;
+            tagm = tagn;
+#else
 #pragma unroll
             for (int j = 0; j < kPiece; j++) zc[j] = zn[j];
             tagc = tagn;
+#endif
         }
         drain(1);
         __syncwarp();
@@ -709,6 +731,8 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     // every heavy middle vertex (multi-GPU too: their P-(y) lists are exchanged,
     // and the ranks stride over the items)
     k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, 0, c.n, cnt);
+    // the prefix is CUB's device scan (a few microseconds; a one-CTA scan of our
+    // own measured 0.27 ms: one block cannot keep enough loads in flight)
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
     if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;

@@ -37,6 +37,7 @@ struct CdeArgs {
     const int64_t *__restrict__ prv;    // position of c_u in w's community table
     const unsigned long long *__restrict__ ctb;   // B_w[c] beside each column of w's table
     int bq;                             // B grid 2^-bq (BQL, ctb)
+    int slot_cap;                       // Phase E: an x slot's shared 20-bit limbs take at most this many terms
 };
 
 // VRec::wide by internal id: d(h)^2 >= wide_bound, d non-increasing in h
@@ -53,6 +54,15 @@ inline CdeArgs cde_args(Ctx &c) {
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
     a.e_rank = 0; a.e_world = 1;
     a.pwr = c.pwr; a.prv = c.prv; a.ctb = c.ctb; a.bq = c.bq;
+    {
+        // Phase E's per-item x slots (smem_red4): a grouped Type-I term is < 2 omega_max
+        // <= 2 k log2(k - 1) (wide_bound's weight bound), so one term adds < 32 k log2(k - 1) + 1
+        // to the top 32-bit limb (bits 60..91 of q = term * 2^64); the slot takes at most
+        // 2^32 / that many terms (4096 for every k <= 254; ~1000 at k = 10 000 communities)
+        const double wb = 2147483648.0 / (2.0 * wide_bound(c.k));
+        const double per = 32.0 * wb + 1.0;
+        a.slot_cap = (int)std::min(4096.0, std::floor(4294967295.0 / per));
+    }
     if (c.sparse) a.pplus = c.pidx;   // P+(u) is one ascending run: the prefix of P(u)
     return a;
 }
