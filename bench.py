@@ -262,21 +262,35 @@ def main():
 
     # top-k latency (rs_topk alone, device-resident scores -> device ids), for the
     # bench's K and SURVEY §8(d)'s K = 5 and K = 1000
-    def topk_ms(K):
-        ib = torch.empty(K, dtype=torch.int32, device=dev)
-        sb = torch.empty(K, dtype=torch.float64, device=dev)
+    def topk_ms(K, host=False):
+        # rs_topk from device-resident scores to HOST ids (pinned
+        # buffers; rs_topk returns once they are there: wall time); the device-
+        # output variant is timed with CUDA events on the library stream
+        if host:
+            ib = torch.empty(K, dtype=torch.int32).pin_memory()
+            sb = torch.empty(K, dtype=torch.float64).pin_memory()
+        else:
+            ib = torch.empty(K, dtype=torch.int32, device=dev)
+            sb = torch.empty(K, dtype=torch.float64, device=dev)
         sc.topk(K, ib, sb)
         out = []
-        for i in range(5):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            sc.topk(K, ib, sb)
-            e1.record(stream)
+        for i in range(7):
             torch.cuda.synchronize(dev)
-            out.append(e0.elapsed_time(e1))
+            if host:
+                t0 = time.perf_counter()
+                sc.topk(K, ib, sb)
+                out.append(1e3 * (time.perf_counter() - t0))
+            else:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                sc.topk(K, ib, sb)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                out.append(e0.elapsed_time(e1))
         return float(np.median(out))
     tk_ms = [topk_ms(a.K)]
     tk_more = {f"K={K}": round(topk_ms(K), 4) for K in (5, 1000)}
+    tk_more.update({f"K={K} to host ids": round(topk_ms(K, host=True), 4) for K in (5, a.K, 1000)})
     sc.topk(a.K, ids_d, sco_d)
 
     # per-phase split of one step (stats on), for the roofline of the dominant phase
