@@ -62,7 +62,8 @@ typedef struct {
                                  [0] Phase A border/histogram/weights/G' lists,
                                      orientation, B-table pushes
                                  [1] multi-GPU: the exchange of Phase A's
-                                     outputs (0 on one GPU)
+                                     outputs; one GPU: the B-table rebuild
+                                     when the pushes went to plain sums
                                  [2] Phase E Type-I triangles, concurrent with
                                      Phase D Type-II pull
                                  [3] finalize (sum, normalise)

@@ -168,17 +168,19 @@ cudaError_t launch_vx_unpack(Ctx &c) {
     return cudaGetLastError();
 }
 
-// the B table of the Type-II pull: {B_w[c] (summed pushes), Q_w(c) = a_w(c)^2}
+// the B table of the Type-II pull: {B_w[c] (summed pushes), Q_w(c) = a_w(c)^2};
+// a thread per w reads its cube-root row (coalesced across threads) and writes
+// its k records, one per column array (coalesced across threads per column)
 __global__ void k_b_rebuild(const unsigned long long *__restrict__ bsum, const double *__restrict__ amat, int64_t n,
                             int k, BQL *__restrict__ bql) {
-    const int64_t total = n * k;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = i / n, w = i - c * n;       // column-major, like bql
-        const double a = amat[w * k + c];
-        BQL r;
-        r.b = bsum[i];
-        r.Q = a * a;
-        bql[i] = r;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x) {
+        for (int c = 0; c < k; c++) {
+            const double a = __ldg(amat + w * k + c);
+            BQL r;
+            r.b = __ldg(bsum + (int64_t)c * n + w);
+            r.Q = a * a;
+            bql[(int64_t)c * n + w] = r;
+        }
     }
 }
 cudaError_t launch_b_rebuild(Ctx &c) {

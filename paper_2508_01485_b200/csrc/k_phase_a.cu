@@ -639,7 +639,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.bq = c.bq;
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.plab = c.plab;
-    a.bsum = (c.world > 1 && !parity) ? c.bsum : nullptr;
+    a.bsum = (c.bsum_mode && !parity) ? c.bsum : nullptr;
     a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8) launch_bins_a<false>(c, a, lo, hi);
     else launch_bins_a<true>(c, a, lo, hi);

@@ -57,6 +57,13 @@ __device__ __forceinline__ void phase_d_vertex(const CdeArgs &a, int64_t u, GR &
                     bq[j] = a.ctb[pv[j]];
                     Q[j] *= Q[j];
                 }
+            } else if (a.bsum) {
+                // the pushed sums and w's cube-root row, read directly (no BQL rebuild)
+                if (w[j] >= 0) {
+                    bq[j] = __ldg(a.bsum + (int64_t)cu * a.n + w[j]);
+                    const double aw = __ldg(a.amat + (int64_t)w[j] * a.k + cu);
+                    Q[j] = aw * aw;
+                }
             } else {
                 if (w[j] >= 0) {
                     const BQL r = bcol[w[j]];

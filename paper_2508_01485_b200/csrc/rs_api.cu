@@ -666,7 +666,21 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(rs::launch_sparse_lists(c));
         join(c);
     } else {
-        if (c.world > 1) {
+        {
+            // the B pushes go to a plain k x n u64 table (half the bytes of the BQL
+            // records, so the REDs hit L2 more often; Orkut shape: A 1.99 -> 1.84 ms)
+            // and a streaming pass rebuilds BQL: worth it when the pushes per cell
+            // (about D / (n k) x the foreign fraction) outweigh the rebuild's 32 B per
+            // cell -- measured: Orkut shape (D / nk = 15) step -0.07..-0.11 ms, LJ
+            // shape (3.5) +0.07 ms. Multi-GPU always (the sums are exchanged).
+            // RS_EXP_BSUM=0/1 forces it off/on; =2 lets Phase D read the sums and
+            // the rows directly instead of rebuilding (measured E||D +0.18 ms).
+            const char *ex = getenv("RS_EXP_BSUM");
+            const bool dense_enough = c.nnz >= 8 * n * (int64_t)c.k;
+            c.bsum_mode = c.world > 1 || (c.k <= 8 && (ex ? ex[0] != '0' : dense_enough));
+            c.bsum_direct = c.world == 1 && c.bsum_mode && ex && ex[0] == '2';
+        }
+        if (c.bsum_mode) {
             // multi-GPU: the pushes go to plain u64 sums (exchanged, then rebuilt into BQL)
             if (c.dist_cap < n * c.k) {
                 CK(dalloc(&c.bsum, (size_t)(n * c.k)));
@@ -690,6 +704,8 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         // other phases read of the 2-hop neighbourhood (ms_phase[1])
         rs_status st = exchange_phase_a(ctx);
         if (st != RS_OK) return st;
+    } else if (c.bsum_mode && !c.sparse && !c.bsum_direct) {
+        CK(rs::launch_b_rebuild(c));
     }
     CK(cudaEventRecord(c.ev_phase[2], c.stream));
     // Phase E (Type-I triangles) and Phase D (Type-II pull, which needs only

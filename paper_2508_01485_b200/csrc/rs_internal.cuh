@@ -178,6 +178,8 @@ struct Ctx {
     unsigned long long *bsum = nullptr;        // world > 1: B pushes (k x n), summed over the ranks
     int32_t *vx = nullptr;                     // world > 1: {|P|, |P+|, |P+_T|} per vertex, exchanged
     int64_t dist_cap = 0;                      // n * k the two above were sized for
+    bool bsum_mode = false;                    // this rs_score pushes into bsum (multi-GPU; RS_EXP_BSUM)
+    bool bsum_direct = false;                  // ... and Phase D reads bsum + amat directly (no BQL rebuild)
     unsigned long long *tk_gkey = nullptr;     // world > 1: gathered top-K candidates (world * K)
     int32_t *tk_gid = nullptr;
     int64_t tk_gcap = 0;

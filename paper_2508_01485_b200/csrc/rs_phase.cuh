@@ -20,6 +20,7 @@ struct CdeArgs {
     const double *__restrict__ wps;     // a_u(c_z) beside each z of P+(u)
     const PRec *__restrict__ pc2;       // {|P+(u)|, |P(u)|, rowptr[u] | |P+_T(u)| << 40}
     const BQL *__restrict__ bql;        // column-major: bql[c*n + w]
+    const unsigned long long *__restrict__ bsum;   // non-null: B sums read here, Q from amat (no BQL rebuild)
     unsigned long long *__restrict__ acc1;  // 3 limbs per vertex (Type-I)
     unsigned long long *__restrict__ acc_hub;  // striped limbs of vertices < n_hub
     int64_t n_hub;
@@ -48,7 +49,7 @@ inline CdeArgs cde_args(Ctx &c) {
     a.rowptr = c.rowptr; a.vlo = 0; a.nverts = 0; a.n = c.n; a.k = c.k;
     a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pc2 = c.pc2;
     a.pplus = c.pplus; a.wps = c.wps;
-    a.bql = c.bql; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.t2 = c.t2; a.score = c.score; a.scal = c.scal;
+    a.bql = c.bql; a.bsum = (c.bsum_direct && !c.sparse) ? c.bsum : nullptr; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.t2 = c.t2; a.score = c.score; a.scal = c.scal;
     a.perm = c.perm; a.lab = c.lab;
     a.n_wide = c.n_wide;
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
