@@ -455,8 +455,8 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
     over ranks is taken (ranks wait for each other at every exchange); the
     exchanges are modelled from their exact byte counts at the measured NVLink
     figures (NCCL all-reduce moves 2(N-1)/N of the buffer per rank, an
-    all-gather (N-1)/N of the gathered size). Not a multi-GPU measurement: the
-    box has one GPU."""
+    all-gather or reduce-scatter (N-1)/N of the total). Not a multi-GPU
+    measurement: the box has one GPU."""
     import threading
     import torch
     n, D, k = g.n, g.nnz, a.k
@@ -480,7 +480,8 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
                     st_last = s.score(stats=True)
                     ph.append(st_last["ms_phase"])
                 per[r] = np.median(np.array(ph), axis=0)
-                xb[r] = (st_last["xchg_allreduce_bytes"], st_last["xchg_allgather_bytes"])
+                xb[r] = (st_last["xchg_allreduce_bytes"], st_last["xchg_allgather_bytes"],
+                         st_last["xchg_reduce_scatter_bytes"])
                 s.close()
             except Exception as e:  # reported below
                 err.append(repr(e))
@@ -500,8 +501,9 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
         # the exchanges: exact byte counts reported by librs (rs_stats), at the
         # measured NVLink figures; all-reduce buffers move 2(N-1)/N of their size
         # per rank, an all-gather (N-1)/N of the gathered total
-        ar, ag = xb[0]
-        x1 = ar * 2 * (N - 1) / N / NVLINK_ALLREDUCE_BUSBW + ag * (N - 1) / N / NVLINK_PEER_BW
+        ar, ag, rsc = xb[0]
+        x1 = (ar * 2 * (N - 1) / N / NVLINK_ALLREDUCE_BUSBW + ag * (N - 1) / N / NVLINK_PEER_BW
+              + rsc * (N - 1) / N / NVLINK_PEER_BW)
         x2 = 0.0
         tk = tk1                                       # top-K: local select + a K x 12 B all-gather
         step = A + ED + F + 1e3 * (x1 + x2) + tk
@@ -509,6 +511,7 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
                          "A_ms_ranks": [round(float(x), 4) for x in P[:, 0]],
                          "ED_ms_ranks": [round(float(x), 4) for x in P[:, 2]],
                          "allreduce_MB": round(ar / 1e6, 1), "allgather_MB": round(ag / 1e6, 1),
+                         "reduce_scatter_MB": round(rsc / 1e6, 1),
                          "exchange_ms": round(1e3 * x1, 4),
                          "step_ms_model": round(step, 4), "GTEPS_model": round(g.m / (step * 1e-3) / 1e9, 3),
                          "speedup_vs_N1": round(ms1 / step, 3)}

@@ -73,6 +73,8 @@ typedef struct {
                                      in this rs_score (0 on one GPU)            */
     int64_t xchg_allgather_bytes; /* multi-GPU: total bytes all-gathered (every
                                      rank's segments together)                  */
+    int64_t xchg_reduce_scatter_bytes; /* multi-GPU: total bytes reduce-scattered
+                                     (every rank's segments together)           */
 } rs_stats;
 
 /* Flags for rs_load_csr. */

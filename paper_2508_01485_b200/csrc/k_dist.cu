@@ -189,4 +189,24 @@ cudaError_t launch_b_rebuild(Ctx &c) {
     return cudaGetLastError();
 }
 
+// multi-GPU, before the limb reduce-scatter: the kHubStripes copies of the
+// hub heads' limbs added into acc1 (limb by limb: both use the head's own
+// 2- or 3-limb format, so the sum is the one the REDs would have made)
+__global__ void k_fold_hubs(unsigned long long *__restrict__ acc1, const unsigned long long *__restrict__ hub,
+                            int64_t n_hub) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * n_hub; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long v = acc1[i];
+#pragma unroll
+        for (int s = 0; s < kHubStripes; s++) v += hub[(int64_t)s * 3 * n_hub + i];
+        acc1[i] = v;
+    }
+}
+cudaError_t launch_fold_hubs(Ctx &c) {
+    if (c.n_hub == 0) return cudaSuccess;
+    k_fold_hubs<<<148 * 2, 256, 0, c.stream>>>(c.acc1, c.acc_hub, c.n_hub);
+    c.launches++;
+    c.hubs_folded = true;
+    return cudaGetLastError();
+}
+
 }  // namespace rs

@@ -172,6 +172,7 @@ cudaError_t launch_phase_d(Ctx &c) { return c.sparse ? launch_phase_d_t<true>(c)
 
 cudaError_t launch_finalize(Ctx &c) {
     CdeArgs a = cde_args(c);
+    if (c.hubs_folded) a.n_hub = 0;   // multi-GPU: the stripes are already in acc1
     const int64_t m = c.head_hi - c.head_lo;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 8));
     k_finalize<<<(unsigned)blocks, 256, 0, c.stream>>>(a);

@@ -616,11 +616,18 @@ cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user
 
 namespace rs {
 // ---------------------------------------------------------------- multi-GPU partition
-// Contiguous head ranges balanced by the work estimate d(u) + 1 (prefix sum,
-// then the first vertex whose prefix reaches r/world of the total).
+// Contiguous vertex ranges balanced by the work estimate d(u) + kVertexWork
+// (prefix sum, then the first vertex whose prefix reaches r/world of the total).
+// a vertex's Phase A work ~ d(u) entries plus a fixed per-vertex part (weights,
+// records, the lists pass): worth about this many entries (from the per-rank
+// Phase A times of the emulated 8-rank world)
+#ifndef RS_EXP_VERTEX_WORK
+#define RS_EXP_VERTEX_WORK 16
+#endif
+constexpr int64_t kVertexWork = RS_EXP_VERTEX_WORK;
 __global__ void k_work(const int64_t *__restrict__ rowptr, int64_t n, int64_t *w) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
-        w[u] = rowptr[u + 1] - rowptr[u] + 1;
+        w[u] = rowptr[u + 1] - rowptr[u] + kVertexWork;
 }
 // boundaries of the head ranges (rs_protocol.h split_point, = rs_split_ranges)
 __global__ void k_split(const int64_t *__restrict__ incl, int64_t n, int world, int64_t *bounds) {

@@ -50,6 +50,7 @@ const rs::NcclApi *rs::nccl_api(std::string *err) {
             api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
             api.Broadcast = (decltype(api.Broadcast))sym("ncclBroadcast");
             api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+            api.Reduce = (decltype(api.Reduce))sym("ncclReduce");
             api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
             api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
@@ -575,6 +576,7 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
     };
     c.xar_bytes = 8 + 8 * n * k;
     c.xag_bytes = 0;
+    c.xrs_bytes = 0;
     XK(c.xp->allreduce_u64(c.scal + rs::kScalOmegaMaxBits, 1, true, c.stream));
     XK(c.xp->allreduce_u64(c.bsum, (size_t)(n * k), false, c.stream));
     seg(sizeof(double) * k);
@@ -643,6 +645,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (c.sparse && c.variant)
         return fail(ctx, RS_EINVAL, "rs_score: the NEXT-3 variant flags need explicit targets (k <= 254)");
     if (c.xp) c.xp->score_begin();
+    c.hubs_folded = false;
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     // the accumulators (and the dense B table) were zeroed on a side stream at the
     // end of the previous rs_score, overlapping rs_topk; otherwise zero them here
@@ -726,9 +729,18 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (c.world > 1) {
         // Phase E is split by middle vertex: sum every head's Type-I limbs (and the
         // triangle/probe counters) over the ranks; integer sums, exact in any order
-        c.xar_bytes += 8 * (3 * n + 3 * rs::kHubStripes * c.n_hub + 2);
-        XK(c.xp->allreduce_u64(c.acc1, (size_t)(3 * n), false, c.stream));
-        XK(c.xp->allreduce_u64(c.acc_hub, (size_t)(3 * rs::kHubStripes * c.n_hub), false, c.stream));
+        // the hub stripes are folded into the limbs first (exact integer adds), then
+        // each rank receives only its own heads' sums (a reduce-scatter: half the
+        // bytes an all-reduce moves)
+        CK(rs::launch_fold_hubs(c));
+        std::vector<size_t> off(c.world), len(c.world);
+        for (int r = 0; r < c.world; r++) {
+            off[r] = (size_t)(3 * c.bounds[r]);
+            len[r] = (size_t)(3 * (c.bounds[r + 1] - c.bounds[r]));
+        }
+        c.xrs_bytes = 8 * 3 * n;
+        c.xar_bytes += 16;
+        XK(c.xp->reduce_scatterv_u64(c.acc1, off.data(), len.data(), c.stream));
         XK(c.xp->allreduce_u64(c.scal + rs::kScalNTri, 2, false, c.stream));
     }
     CK(cudaEventRecord(c.ev_phase[4], c.stream));
@@ -788,6 +800,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(cudaEventElapsedTime(&s.ms_phase[4], c.ev_phase[3], c.ev_phase[4]));
         s.xchg_allreduce_bytes = c.world > 1 ? c.xar_bytes : 0;
         s.xchg_allgather_bytes = c.world > 1 ? c.xag_bytes : 0;
+        s.xchg_reduce_scatter_bytes = c.world > 1 ? c.xrs_bytes : 0;
         *stats_out = s;
     }
     (void)flags;

@@ -38,6 +38,7 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*GroupStart)();
     ncclResult_t (*GroupEnd)();
     const char *(*GetErrorString)(ncclResult_t);
@@ -55,6 +56,10 @@ struct Xport {
     virtual cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) = 0;
     virtual cudaError_t allreduce_u64(unsigned long long *buf, size_t count, bool max, cudaStream_t s) = 0;
     virtual cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+    // u64 sums of rank r's segment [off[r], off[r] + len[r]) (in u64 words) over
+    // all ranks, delivered to rank r only (the other segments are left as they are)
+    virtual cudaError_t reduce_scatterv_u64(unsigned long long *buf, const size_t *off, const size_t *len,
+                                            cudaStream_t s) = 0;
     // rs_score brackets (the emulated world's serial mode times each rank's
     // compute alone on the GPU: ranks take turns between collectives)
     virtual void score_begin() {}
@@ -175,6 +180,8 @@ struct Ctx {
     int32_t *pk_m = nullptr;                   // world > 1: packed P- lists of the heavy vertices
     int64_t pkm_cap = 0;
     int64_t xar_bytes = 0, xag_bytes = 0;      // world > 1: bytes all-reduced / all-gathered in the last rs_score
+    int64_t xrs_bytes = 0;                     //   and reduce-scattered
+    bool hubs_folded = false;                  // the hub stripes were folded into acc1 (multi-GPU)
     unsigned long long *bsum = nullptr;        // world > 1: B pushes (k x n), summed over the ranks
     int32_t *vx = nullptr;                     // world > 1: {|P|, |P+|, |P+_T|} per vertex, exchanged
     int64_t dist_cap = 0;                      // n * k the two above were sized for
@@ -323,6 +330,7 @@ cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm, bool unpack);
 cudaError_t launch_vx_pack(Ctx &c);
 cudaError_t launch_vx_unpack(Ctx &c);
 cudaError_t launch_b_rebuild(Ctx &c);
+cudaError_t launch_fold_hubs(Ctx &c);
 cudaError_t launch_triangle_counts(Ctx &c);
 cudaError_t launch_e_items(Ctx &c);
 cudaError_t launch_topk(Ctx &c, int64_t K, int32_t *ids_dev, double *scores_dev, int64_t lo, int64_t hi);

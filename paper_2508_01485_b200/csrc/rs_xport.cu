@@ -45,6 +45,16 @@ struct NcclXport : Xport {
     cudaError_t allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
         return err(nccl_api(nullptr)->AllGather(send, recv, bytes, ncclUint8, comm, s), "ncclAllGather");
     }
+    cudaError_t reduce_scatterv_u64(unsigned long long *buf, const size_t *off, const size_t *len,
+                                    cudaStream_t s) override {
+        // unequal segments: one ncclReduce per root, grouped
+        const NcclApi &N = *nccl_api(nullptr);
+        ncclResult_t r = N.GroupStart();
+        for (int p = 0; p < world && r == ncclSuccess; p++)
+            if (len[p]) r = N.Reduce(buf + off[p], buf + off[p], len[p], ncclUint64, ncclSum, p, comm, s);
+        const ncclResult_t r2 = N.GroupEnd();
+        return err(r != ncclSuccess ? r : r2, "ncclReduce (reduce-scatter of segments)");
+    }
 };
 Xport *make_nccl_xport(ncclComm_t comm, int world) { return new NcclXport(comm, world); }
 #endif
@@ -166,6 +176,34 @@ struct EmuXport : Xport {
         if (e == cudaSuccess) e = e2;
         if (e == cudaSuccess && count)
             e = cudaMemcpyAsync(buf, tmp, sizeof(unsigned long long) * count, cudaMemcpyDeviceToDevice, s);
+        resume();
+        return e;
+    }
+    cudaError_t reduce_scatterv_u64(unsigned long long *buf, const size_t *off, const size_t *len,
+                                    cudaStream_t s) override {
+        const size_t count = len[rank];
+        cudaError_t e = cudaSuccess;
+        if (count > tmp_count) {
+            if (tmp) cudaFree(tmp);
+            tmp = nullptr;
+            tmp_count = 0;
+            e = cudaMalloc(&tmp, sizeof(unsigned long long) * count);
+            if (e == cudaSuccess) tmp_count = count;
+        }
+        const cudaError_t ep = publish(buf, s);
+        if (e == cudaSuccess) e = ep;
+        if (e == cudaSuccess && count) {
+            PtrPack pk;
+            for (int r = 0; r < W->world; r++) pk.p[r] = (const unsigned long long *)W->ptr[r] + off[rank];
+            const unsigned blocks = (unsigned)std::min<size_t>((count + 255) / 256, 148 * 8);
+            k_reduce_u64<<<blocks, 256, 0, s>>>(pk, W->world, count, false, tmp);
+            e = cudaGetLastError();
+        }
+        const cudaError_t e2 = cudaStreamSynchronize(s);
+        W->barrier();                                      // every peer done reading
+        if (e == cudaSuccess) e = e2;
+        if (e == cudaSuccess && count)
+            e = cudaMemcpyAsync(buf + off[rank], tmp, sizeof(unsigned long long) * count, cudaMemcpyDeviceToDevice, s);
         resume();
         return e;
     }
