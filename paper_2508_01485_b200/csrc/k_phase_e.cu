@@ -35,6 +35,7 @@
 // pairs instead.
 #include "rs_phase.cuh"
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 namespace rs {
 
@@ -781,6 +782,10 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     cudaFuncSetAttribute(k_phase_e<COUNT, SPARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase_e<COUNT, SPARSE>, kWarpsE * 32, smem);
+    if (const char *ev = getenv("RS_EXP_E_BLOCKS")) {   // experiment: heavy-grid blocks per SM
+        const int v = atoi(ev);
+        if (v >= 1 && v < per_sm) per_sm = v;
+    }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     for (int s = 0; s < shares; s++) {
