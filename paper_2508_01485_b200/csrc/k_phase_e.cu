@@ -47,9 +47,12 @@ constexpr int kQCapE = 160;      // candidate queue (31 + 32 * kPiece < 160)
 constexpr int kPsWords = 128;    // piece-start bitmap: items of at most 4096 pieces (else binary search)
 constexpr int kWarpsE = 8;
 #ifndef RS_EXP_QBATCH
-#define RS_EXP_QBATCH 2
+#define RS_EXP_QBATCH 4
 #endif
 constexpr int kQBatch = RS_EXP_QBATCH;   // heavy work items per queue pop
+#ifndef RS_EXP_E_REUSE
+#define RS_EXP_E_REUSE 1                     // reuse the filter / P+(y) copy when consecutive items share y
+#endif
 #ifndef RS_EXP_E_DEPTH
 #define RS_EXP_E_DEPTH 1                     // probe rounds in flight ahead of the one being filtered (1 or 2; 2: E||D +0.02 ms, spills)
 #endif
@@ -226,6 +229,10 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
     unsigned long long qbase = __shfl_sync(0xffffffffu, qnext, 0);
     unsigned long long qi = qbase;
     int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
+    // the items of one y are consecutive (a batch pop often brings two of them):
+    // the filter, the sorted copy of P+(y) and y's weights built for the previous
+    // item are reused when y repeats
+    int32_t prev_y = -1;
     for (;;) {
         if (qi >= n_items) break;
         const bool last_of_batch = qi - qbase == (unsigned long long)(kQBatch - 1);
@@ -253,8 +260,9 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
         // i-th entry of P+(y) in ascending order within its run (the target run is
         // stored descending, the other run ascending after it)
         auto py_at = [&](int i) -> int64_t { return SPARSE ? by + i : (i < pyt ? by + pyt - 1 - i : by + i); };
-        const int32_t z0 = lane < py ? __ldg(a.pplus + py_at(lane)) : -1;
-        const double ay0 = (!SPARSE && lane < k) ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
+        const bool fresh = !RS_EXP_E_REUSE || y != prev_y;   // warp-uniform
+        const int32_t z0 = (fresh && lane < py) ? __ldg(a.pplus + py_at(lane)) : -1;
+        const double ay0 = (fresh && !SPARSE && lane < k) ? __ldg(a.amat + (int64_t)y * k + lane) : 0.0;
         // x's record and label; its weight a_x(c_y) (and, all-communities mode,
         // a_y(c_x)) is gathered only by the lanes that verify a triangle (most
         // (y, x) pairs close none), from x's position kept in S.xn[slot].y
@@ -265,19 +273,23 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
             pcx[h] = xv[h] >= 0 ? a.pc2[xv[h]] : PRec{(int)0xFF000000, 0, 0};
             lxv[h] = pr_lab(pcx[h]);                      // the label rides in the record
         }
-        for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
-        if constexpr (!SPARSE) {
-            if (lane < k) Ay[lane] = ay0;
-            for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
-        }
-        __syncwarp();
-        for (int i = lane; i < py; i += 32) {
-            const int32_t z = i == lane ? z0 : __ldg(a.pplus + py_at(i));
-            const uint32_t b = bm_bit(z);
-            atomicOr(&S.bm[b >> 5], 1u << (b & 31));
-            if (local) {
-                S.py[i] = z;
+        if (fresh) {
+            __syncwarp();                                   // the previous item's readers are done
+            for (int w = lane; w < kBmWords; w += 32) S.bm[w] = 0u;
+            if constexpr (!SPARSE) {
+                if (lane < k) Ay[lane] = ay0;
+                for (int c = lane + 32; c < k; c += 32) Ay[c] = __ldg(a.amat + (int64_t)y * k + c);
             }
+            __syncwarp();
+            for (int i = lane; i < py; i += 32) {
+                const int32_t z = i == lane ? z0 : __ldg(a.pplus + py_at(i));
+                const uint32_t b = bm_bit(z);
+                atomicOr(&S.bm[b >> 5], 1u << (b & 31));
+                if (local) {
+                    S.py[i] = z;
+                }
+            }
+            prev_y = y;
         }
         // the next item's record, in flight during this item
         if (last_of_batch) {
