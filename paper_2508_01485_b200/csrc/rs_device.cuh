@@ -214,6 +214,14 @@ struct LockGroup {
         for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
         return v;
     }
+    __device__ __forceinline__ U128 sum(U128 v) const {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            U128 w{__shfl_xor_sync(0xffffffffu, v.lo, o, G), __shfl_xor_sync(0xffffffffu, v.hi, o, G)};
+            v = u128_add(v, w);
+        }
+        return v;
+    }
     // v of the group's lane src (src may differ per lane)
     template <class T>
     __device__ __forceinline__ T from(T v, int src) const { return __shfl_sync(0xffffffffu, v, (int)shift + src); }
