@@ -501,7 +501,10 @@ __device__ __forceinline__ void block_max_to_scal(double v, unsigned long long *
 }
 
 template <int G, int U, bool SMEM>
-__global__ void __launch_bounds__(256, 4) k_phase_a_warp(PhaseAArgs a) {
+#ifndef RS_EXP_A_MINB
+#define RS_EXP_A_MINB 5      // warp kernels: resident blocks of 256 per SM (5: 51 registers, no spill; 6 spills)
+#endif
+__global__ void __launch_bounds__(256, RS_EXP_A_MINB) k_phase_a_warp(PhaseAArgs a) {
     __shared__ int hist[SMEM ? 8 * 256 : 1];
     double wmax = 0.0;
     if constexpr (SMEM) {
