@@ -113,8 +113,11 @@ __global__ void __launch_bounds__(256) k_finalize(CdeArgs a) {
     }
 }
 
+#ifndef RS_EXP_D_MINB
+#define RS_EXP_D_MINB 6
+#endif
 template <int G, int U, bool SPARSE>
-__global__ void __launch_bounds__(256) k_phase_d_warp(CdeArgs a) {
+__global__ void __launch_bounds__(256, RS_EXP_D_MINB) k_phase_d_warp(CdeArgs a) {
     WarpGroup<G> g;
     const int64_t gpb = blockDim.x / G;
     for (int64_t i = blockIdx.x * gpb + threadIdx.x / G; i < a.nverts; i += (int64_t)gridDim.x * gpb)

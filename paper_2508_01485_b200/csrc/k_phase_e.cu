@@ -557,7 +557,10 @@ __global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems i
 // (short, L1-resident), so the work per lane is uniform whatever the list
 // lengths. Terms go to the heads with one RED each.
 template <bool COUNT, bool SPARSE>
-__global__ void __launch_bounds__(256) k_phase_e_light(CdeArgs a, int64_t ylo, int64_t yhi) {
+#ifndef RS_EXP_LIGHT_MINB
+#define RS_EXP_LIGHT_MINB 5
+#endif
+__global__ void __launch_bounds__(256, RS_EXP_LIGHT_MINB) k_phase_e_light(CdeArgs a, int64_t ylo, int64_t yhi) {
     const int k = a.k;
     const int lane = threadIdx.x & 31;
     unsigned long long ntri = 0, nprobe = 0;   // nprobe: warp-uniform
