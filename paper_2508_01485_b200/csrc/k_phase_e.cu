@@ -40,11 +40,20 @@
 namespace rs {
 
 constexpr int kChunkE = 64;      // positions of P(y) per work item
-constexpr int kPyCap = 256;      // P+(y) kept in shared memory (sorted copy + labels)
+#ifndef RS_EXP_PYCAP
+#define RS_EXP_PYCAP 128
+#endif
+#ifndef RS_EXP_E_MINB
+#define RS_EXP_E_MINB 4
+#endif
+constexpr int kPyCap = RS_EXP_PYCAP;   // P+(y) kept in shared memory (sorted copy + labels)
 constexpr int kBmWords = 128;    // 4096-bit membership filter of P+(y)
 constexpr int kPiece = 4;        // consecutive P+(x) entries one lane probes per round
 constexpr int kQCapE = 160;      // candidate queue (31 + 32 * kPiece < 160)
-constexpr int kPsWords = 128;    // piece-start bitmap: items of at most 4096 pieces (else binary search)
+#ifndef RS_EXP_PSWORDS
+#define RS_EXP_PSWORDS 128
+#endif
+constexpr int kPsWords = RS_EXP_PSWORDS;    // piece-start bitmap: items of at most 4096 pieces (else binary search)
 constexpr int kWarpsE = 8;
 #ifndef RS_EXP_QBATCH
 #define RS_EXP_QBATCH 4
@@ -206,7 +215,7 @@ __host__ __device__ constexpr size_t e_stride_bytes(int k) {
 // is one ascending run in pidx, and the weights come from beside the list
 // entries (wps: a_u(c_w), pwr: a_w(c_u)) instead of the dense rows.
 template <bool COUNT, bool SPARSE>
-__global__ void __launch_bounds__(kWarpsE * 32, 4) k_phase_e(CdeArgs a, EItems it, unsigned long long *queue_ctr) {
+__global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs a, EItems it, unsigned long long *queue_ctr) {
     extern __shared__ __align__(16) unsigned char e_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k;
