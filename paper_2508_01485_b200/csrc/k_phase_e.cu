@@ -705,11 +705,15 @@ __global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t
         cnt[y] = c;
     }
 }
+// a thread per heavy y writes its first 8 items; the rare y with more (hubs:
+// up to hundreds of chunks) hand the rest to a warp each (second loop), so no
+// thread serialises a hub's whole item list
 __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
                             const PRec *__restrict__ pc2, const int64_t *__restrict__ rowptr,
                             const uint8_t *__restrict__ lab, int64_t n_heavy,
                             EItem *items) {
-    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += stride) {
         const int c = cnt[y], o = off[y];
         if (c == 0) continue;
         const PRec p = pc2[y];
@@ -720,7 +724,26 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         e.pm = p.y - pr_plus(p);
         e.pyt = pr_plus_t(p);
         e.pad = 0;
-        for (int j = 0; j < c; j++) {
+        for (int j = 0; j < c && j < 8; j++) {
+            e.chunk = j;
+            items[o + j] = e;
+        }
+    }
+    // a warp per y with more than 8 chunks
+    const int lane = threadIdx.x & 31;
+    for (int64_t y = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; y < n_heavy; y += stride >> 5) {
+        const int c = cnt[y];
+        if (c <= 8) continue;
+        const int o = off[y];
+        const PRec p = pc2[y];
+        EItem e;
+        e.by = rowptr[y];
+        e.y = (int32_t)y;
+        e.pyl = p.x;
+        e.pm = p.y - pr_plus(p);
+        e.pyt = pr_plus_t(p);
+        e.pad = 0;
+        for (int j = 8 + lane; j < c; j += 32) {
             e.chunk = j;
             items[o + j] = e;
         }

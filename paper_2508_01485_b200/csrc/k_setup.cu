@@ -594,6 +594,7 @@ void launch_comm_hist(Ctx &c, int64_t nbins) {
 }
 void launch_nwide(Ctx &c, double bound) {
     k_nwide<<<1, 1, 0, c.stream>>>(c.rowptr, c.n, bound, c.scal + kScalNWide);
+    c.nwide_k = -1;                                  // the dense path's cached n_wide is gone
     c.launches++;
 }
 
@@ -607,8 +608,13 @@ cudaError_t launch_set_communities(Ctx &c, int64_t max_comm, const int32_t *user
     k_select<<<1, kSelThreads, 0, c.stream>>>(c.chist, nbins, c.k, user_targets, c.targets, c.ccode, c.scal);
     c.launches++;
     k_labels<<<blocks, 256, 0, c.stream>>>(c.comm_in, c.perm, c.ccode, c.n, c.comm_id, c.lab);
-    k_nwide<<<1, 1, 0, c.stream>>>(c.rowptr, c.n, wide_bound(c.k), c.scal + kScalNWide);
-    c.launches += 2;
+    // n_wide depends only on the graph and k: recomputed when either changed
+    if (c.nwide_k != c.k) {
+        k_nwide<<<1, 1, 0, c.stream>>>(c.rowptr, c.n, wide_bound(c.k), c.scal + kScalNWide);
+        c.nwide_k = c.k;
+        c.launches++;
+    }
+    c.launches++;
     return cudaGetLastError();
 }
 

@@ -302,6 +302,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     if (!fits) free_graph(ctx);
     c.loaded = c.has_comm = c.scored = false;
     c.acc_zero = c.bql_zero = false;
+    c.nwide_k = 0;
     c.n = n;
     c.nnz = nnz;
     // arena: host-input staging + relabel temporaries (grow-only)

@@ -255,6 +255,7 @@ struct Ctx {
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQL *bql = nullptr;          // k*n, column-major: bql[c*n + w]
     int64_t n_wide = 0;          // vertices [0, n_wide) (degree^2 >= wide_bound) use 3 Type-I limbs
+    int32_t nwide_k = 0;         // the k scal[kScalNWide] was computed for (0: none; reset by rs_load_csr)
     int bq = 40;                 // fraction bits of the B table's integer sums (BQL)
     unsigned long long *acc1 = nullptr;  // 3*n fixed-point limbs of the Type-I sum (2 used unless wide)
     unsigned long long *acc_hub = nullptr;  // kHubStripes copies of the limbs of the first n_hub vertices
