@@ -460,9 +460,10 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
     import threading
     import torch
     n, D, k = g.n, g.nnz, a.k
-    out = {"how": "per-rank phase times measured (serial emulated ranks, one GPU), max over ranks; "
-                  "exchange bytes exact, at 725 GB/s all-reduce bus bandwidth / 770 GB/s peer copy (measured, "
-                  "B200_PROFILING.md)", "N1_ms_per_step": round(ms1, 4)}
+    out = {"how": "per-rank phase times measured (serial emulated ranks, one GPU; the exchange phases' own "
+                  "kernels included, their waits excluded), max over ranks; exchange bytes exact, at 725 GB/s "
+                  "all-reduce bus bandwidth / 770 GB/s peer copy (measured, B200_PROFILING.md)",
+           "N1_ms_per_step": round(ms1, 4)}
     for N in worlds:
         W = rsb.EmuWorld(N)
         W.serial(True)
@@ -478,7 +479,9 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
                 ph = []
                 for _ in range(reps):
                     st_last = s.score(stats=True)
-                    ph.append(st_last["ms_phase"])
+                    # the rank's own kernel time per phase: the collectives' waits
+                    # (peers' turns, the emulated copies) taken out
+                    ph.append(np.array(st_last["ms_phase"]) - np.array(st_last["ms_xwait"]))
                 per[r] = np.median(np.array(ph), axis=0)
                 xb[r] = (st_last["xchg_allreduce_bytes"], st_last["xchg_allgather_bytes"],
                          st_last["xchg_reduce_scatter_bytes"])
@@ -498,6 +501,8 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
             continue
         P = np.array(per)
         A, ED, F = float(P[:, 0].max()), float(P[:, 2].max()), float(P[:, 3].max())
+        # the local kernels of the exchange phases (packing, unpacking, the hub fold)
+        XL, LL = float(P[:, 1].max()), float(P[:, 4].max())
         # the exchanges: exact byte counts reported by librs (rs_stats), at the
         # measured NVLink figures; all-reduce buffers move 2(N-1)/N of their size
         # per rank, an all-gather (N-1)/N of the gathered total
@@ -506,8 +511,9 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
               + rsc * (N - 1) / N / NVLINK_PEER_BW)
         x2 = 0.0
         tk = tk1                                       # top-K: local select + a K x 12 B all-gather
-        step = A + ED + F + 1e3 * (x1 + x2) + tk
+        step = A + XL + ED + LL + F + 1e3 * (x1 + x2) + tk
         out[f"N={N}"] = {"A_ms_max": round(A, 4), "ED_ms_max": round(ED, 4), "F_ms_max": round(F, 4),
+                         "xchg_local_ms_max": round(XL, 4), "limb_local_ms_max": round(LL, 4),
                          "A_ms_ranks": [round(float(x), 4) for x in P[:, 0]],
                          "ED_ms_ranks": [round(float(x), 4) for x in P[:, 2]],
                          "allreduce_MB": round(ar / 1e6, 1), "allgather_MB": round(ag / 1e6, 1),

@@ -75,6 +75,11 @@ typedef struct {
                                      rank's segments together)                  */
     int64_t xchg_reduce_scatter_bytes; /* multi-GPU: total bytes reduce-scattered
                                      (every rank's segments together)           */
+    float ms_xwait[8];        /* emulated world (rs_create_emulated): the part of
+                                 ms_phase[i] this rank's stream spent inside
+                                 collectives (waiting for the peers, the device
+                                 copies); ms_phase[i] - ms_xwait[i] is its own
+                                 kernel time. 0 elsewhere                       */
 } rs_stats;
 
 /* Flags for rs_load_csr. */

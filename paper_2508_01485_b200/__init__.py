@@ -49,14 +49,15 @@ class rs_stats(ctypes.Structure):
                 ("n_pred_entries", ctypes.c_int64), ("n_triangles", ctypes.c_int64),
                 ("n_probes", ctypes.c_int64), ("omega_max", ctypes.c_double), ("ms_phase", ctypes.c_float * 8),
                 ("xchg_allreduce_bytes", ctypes.c_int64), ("xchg_allgather_bytes", ctypes.c_int64),
-                ("xchg_reduce_scatter_bytes", ctypes.c_int64)]
+                ("xchg_reduce_scatter_bytes", ctypes.c_int64), ("ms_xwait", ctypes.c_float * 8)]
 
     def as_dict(self):
         return {"n": self.n, "m": self.m, "n_border": self.n_border, "n_pred_entries": self.n_pred_entries,
                 "n_triangles": self.n_triangles, "n_probes": self.n_probes, "omega_max": self.omega_max,
                 "ms_phase": [float(x) for x in self.ms_phase],
                 "xchg_allreduce_bytes": self.xchg_allreduce_bytes, "xchg_allgather_bytes": self.xchg_allgather_bytes,
-                "xchg_reduce_scatter_bytes": self.xchg_reduce_scatter_bytes}
+                "xchg_reduce_scatter_bytes": self.xchg_reduce_scatter_bytes,
+                "ms_xwait": [float(x) for x in self.ms_xwait]}
 
 
 _P = ctypes.c_void_p

@@ -6,12 +6,13 @@
 // * per vertex {|P|, |P+|, |P+_T|} (12 B): VRec and PRec are rebuilt from them
 //   (a_self = a_u(C(u)) from the gathered row; head / wide from d(u) and lab);
 // * the oriented runs P+(x): only their ids travel (4 B per entry), packed back
-//   to back in vertex order at gpre[x] = sum of |P+| over the vertices before x;
-//   the weight beside each entry, a_x(c_z), is re-read from x's gathered row;
+//   to back in vertex order at gpre[x] = sum of |P+| over the vertices before x
+//   (Phase E reads the weights a_x(c_z) from the gathered rows);
 // * the P-(y) lists of the heavy middle vertices (degree >= 128; 4 B per
 //   entry): Phase E strides over their work items on every rank;
 // * the B table: only the pushed integer sums (8 B per cell, summed over the
-//   ranks); Q = a_w(c)^2 is recomputed from the gathered rows.
+//   ranks); Phase D reads them with a_w(c) from the gathered rows (no rebuild
+//   pass over the n k cells on every rank).
 // P(u) and the light P-(y) stay local: they are read only for a rank's own u, y.
 #include "rs_internal.cuh"
 #include "rs_device.cuh"
@@ -33,12 +34,13 @@ __global__ void k_run_count(const PRec *__restrict__ pc2, int64_t n, int64_t n_h
 }
 
 // gpre[0..n]: exclusive prefix of |P+(x)| (or, minus, of the heavy |P-(y)|) in
-// the context scratch, the counts and the scan's temporary storage after it
+// the context scratch (gpre inside it), the counts and the scan's temporary
+// storage after it
 cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus) {
     const int64_t n = c.n;
     int64_t *cnt = gpre + (n + 1);
     void *tmp = cnt + (n + 1);
-    const size_t used = sizeof(int64_t) * 2 * (size_t)(n + 1);
+    const size_t used = (size_t)((char *)tmp - (char *)c.scratch);
     if (used > c.scratch_bytes) return cudaErrorMemoryAllocation;
     const size_t tmp_bytes = c.scratch_bytes - used;
     if (minus) k_run_count<true><<<148 * 4, 256, 0, c.stream>>>(c.pc2, n, c.e_nbig, cnt);
@@ -51,30 +53,52 @@ cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus) {
     return cudaGetLastError();
 }
 
-// a warp per vertex: pack the owned vertices' P+ ids (UNPACK = false), or copy
-// every other vertex's run from the gathered buffer into its slot and set the
-// weight beside each entry, a_x(c_z) for a target z (0 otherwise), from x's row
+// pack the owned vertices' P+ ids (UNPACK = false), or copy every other
+// vertex's run from the gathered buffer into its slot. A warp takes 32
+// consecutive vertices and deals their entries to the lanes 32 at a time (a
+// warp scan of the run lengths; most runs are a few entries, so a warp per
+// vertex would leave most lanes idle): the gathered ids are read coalesced
 template <bool UNPACK>
 __global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gpre, int64_t n, int64_t lo,
-                            int64_t hi, int32_t *__restrict__ pplus, double *__restrict__ wps,
-                            int32_t *__restrict__ pk_id, const uint8_t *__restrict__ lab,
-                            const double *__restrict__ amat, int k) {
+                            int64_t hi, int32_t *__restrict__ pplus, int32_t *__restrict__ pk_id) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t first = UNPACK ? 0 : lo, last = UNPACK ? n : hi;
-    for (int64_t x = first + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); x < last; x += nw) {
-        if (UNPACK && x >= lo && x < hi) continue;
-        const PRec r = pc2[x];
-        const int pp = pr_plus(r);
-        const int64_t slot = pr_start(r), g = gpre[x];
-        for (int i = lane; i < pp; i += 32) {
+    for (int64_t x0 = first + 32 * ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); x0 < last; x0 += 32 * nw) {
+        const int64_t x = x0 + lane;
+        int cnt = 0;
+        int64_t slot = 0;
+        if (x < last && !(UNPACK && x >= lo && x < hi)) {
+            const PRec r = pc2[x];
+            cnt = pr_plus(r);
+            slot = pr_start(r);
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t g0 = (!UNPACK && total) ? gpre[x0] : 0;   // the first vertex's packed offset
+        for (int q0 = 0; q0 < total; q0 += 32) {
+            const int q = q0 + lane;
+            int j = 0;                                    // the first lane whose inclusive count exceeds q
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, j + s - 1);
+                if (v <= q) j += s;
+            }
+            const int i = q - (__shfl_sync(0xffffffffu, incl, j) - __shfl_sync(0xffffffffu, cnt, j));
+            const int64_t sj = __shfl_sync(0xffffffffu, (long long)slot, j);
+            if (q >= total) continue;
             if (UNPACK) {
-                const int32_t z = pk_id[g + i];
-                const int lz = lab[z];
-                pplus[slot + i] = z;
-                wps[slot + i] = lz < k ? __ldg(amat + x * k + lz) : 0.0;
+                // packed offset of x0 + j: gpre is in vertex order, and the owned
+                // vertices (skipped, count 0 here) have their entries in between
+                const int64_t gj = gpre[x0 + j] + i;
+                pplus[sj + i] = pk_id[gj];
             } else {
-                pk_id[g + i] = pplus[slot + i];
+                pk_id[g0 + q] = pplus[sj + i];            // owned range: contiguous in the packed buffer
             }
         }
     }
@@ -110,11 +134,9 @@ cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm, bool unpack) {
 
 cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre, bool unpack) {
     if (unpack)
-        k_plus_pack<true><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.wps,
-                                                        c.pk_id, c.lab, c.amat, c.k);
+        k_plus_pack<true><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.pk_id);
     else
-        k_plus_pack<false><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.wps,
-                                                         c.pk_id, c.lab, c.amat, c.k);
+        k_plus_pack<false><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.pk_id);
     c.launches++;
     return cudaGetLastError();
 }

@@ -13,7 +13,7 @@
 //   Step 2c omega_max partial maxima,
 // and, once u's weights are known, the inputs of Step 3: the orientation of G'
 // by internal id (P+(u) = the prefix of P(u) below u, split into its target run
-// and the rest, with a_u(c_z) beside each z) and u's pushes of a_u(c_u) into
+// and the rest) and u's pushes of a_u(c_u) into
 // B_w[c_u] for every w in P(u) (v in P(w) iff w in P(v)), exact integer REDs.
 //
 // The row walk is the only per-neighbour work: one coalesced column load, one
@@ -47,7 +47,6 @@ struct PhaseAArgs {
     int bq;                             // B table grid: 2^-bq
     int64_t n;
     int32_t *__restrict__ pplus;
-    double *__restrict__ wps;
     PRec *__restrict__ pc2;
     BQL *__restrict__ bql;
     const double *__restrict__ l2t;     // log2 of small integers
@@ -157,7 +156,7 @@ __device__ __forceinline__ void walk_row(const PhaseAArgs &a, int64_t u, int64_t
 }
 
 // Step 3 inputs of u (after its weights are known; au(c) = a_u(c)): B pushes
-// and the P+ runs with a_u(c_z), reading P(u) and its labels back from this
+// and the P+ runs, reading P(u) and its labels back from this
 // group's writes (k > 8 path). P+(u) is written as its
 // target run DESCENDING at [0, pt) followed by the other run ascending at
 // [pt, pp): an entry i of the prefix P+ has i predecessors in it, so its rank in
@@ -204,7 +203,6 @@ __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, GR &g, int64_
                     const int tb = ct + rt[j];                // target entries before i
                     const int64_t at = t[j] ? beg + pt - 1 - tb : beg + pt + (i - tb);
                     a.pplus[at] = v[j];
-                    a.wps[at] = t[j] ? au(lv[j]) : 0.0;
                 }
                 ct += tt[j];
             }
@@ -395,7 +393,6 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
                 const int tb = ct + rt[j];                // target entries of P+ before i
                 const int64_t at = t[j] ? beg + pt - 1 - tb : beg + pt + (i - tb);
                 a.pplus[at] = v[j];
-                a.wps[at] = t[j] ? aw : 0.0;
             }
             ct += tt[j];
         }
@@ -643,7 +640,7 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.f = c.f; a.omega = c.omega; a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.scal = c.scal;
     a.plab = c.plab;
     a.bsum = (c.bsum_mode && !parity) ? c.bsum : nullptr;
-    a.n = c.n; a.pplus = c.pplus; a.wps = c.wps; a.pc2 = c.pc2; a.bql = c.bql;
+    a.n = c.n; a.pplus = c.pplus; a.pc2 = c.pc2; a.bql = c.bql;
     if (c.k <= 8) launch_bins_a<false>(c, a, lo, hi);
     else launch_bins_a<true>(c, a, lo, hi);
     return cudaGetLastError();

@@ -211,6 +211,33 @@ __host__ __device__ constexpr size_t e_stride_bytes(int k) {
     return ((sizeof(ESmem) + 15) / 16) * 16 + ((8 * (size_t)k + 15) / 16) * 16;
 }
 
+// multi-GPU: the heavy items are dealt to the ranks in blocks of e_blk
+// consecutive items, block b to rank b mod world. Measured (8 emulated ranks,
+// Orkut shape, E || D max / mean over ranks): e_blk 1 1.07 / 0.85 ms, 4 1.38 /
+// 1.22, 32 1.36 / 1.21, 256 1.38 / 1.21 -- keeping a y's items together on one
+// rank (filter reuse) loses to spreading them, so 1 is the default
+__device__ __forceinline__ unsigned long long e_item(unsigned long long qi, int r, int world, int blk) {
+    const unsigned long long B = (unsigned long long)blk;
+    return ((qi / B) * (unsigned long long)world + (unsigned long long)r) * B + qi % B;
+}
+// within each group of kQBatch * P items, batch b takes items b, b + P,
+// b + 2P, ... (a P x kQBatch transpose of the heaviest-first order)
+__device__ __forceinline__ unsigned long long e_perm_map(unsigned long long g, int P, unsigned long long n_all) {
+    if (P <= 1) return g;
+    const unsigned long long G = (unsigned long long)P * kQBatch, base = g - g % G, o = g % G;
+    if (base + G > n_all) return g;
+    return base + (o / kQBatch) + (unsigned long long)P * (o % kQBatch);
+}
+__device__ __forceinline__ unsigned long long e_rank_items(unsigned long long n_all, int r, int world, int blk) {
+    const unsigned long long B = (unsigned long long)blk;
+    const unsigned long long nb = (n_all + B - 1) / B, W = (unsigned long long)world, R = (unsigned long long)r;
+    if (nb <= R) return 0ull;
+    const unsigned long long mine = (nb - R + W - 1) / W;           // blocks r, r + W, ... < nb
+    unsigned long long cnt = mine * B;
+    if ((nb - 1) % W == R) cnt -= nb * B - n_all;                   // the last, partial block is this rank's
+    return cnt;
+}
+
 // SPARSE (all-communities mode, k_sparse.cu): every vertex is a target, P+(u)
 // is one ascending run in pidx, and the weights come from beside the list
 // entries (wps: a_u(c_w), pwr: a_w(c_u)) instead of the dense rows.
@@ -223,10 +250,10 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
     ESmem &S = *reinterpret_cast<ESmem *>(base);
     double *Ay = (double *)(base + ((sizeof(ESmem) + 15) / 16) * 16);
     unsigned long long ntri = 0, nprobe = 0;
-    // multi-GPU: rank r takes items r, r + world, ... (heaviest first on every rank)
+    // multi-GPU: rank r takes the blocks of e_blk items b = r, r + world, ...
+    // (heaviest first on every rank; e_item maps its queue index to the item)
     const unsigned long long n_all = (unsigned long long)*it.total;
-    const unsigned long long n_items = n_all > (unsigned long long)a.e_rank
-                                           ? (n_all - a.e_rank + a.e_world - 1) / a.e_world : 0ull;
+    const unsigned long long n_items = e_rank_items(n_all, a.e_rank, a.e_world, a.e_blk);
 
     // the next item's index and its 32-byte record (word `lane` of it in lanes
     // 0-7) are fetched while the current item is processed
@@ -237,7 +264,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
     if (lane == 0) qnext = atomicAdd(queue_ctr, (unsigned long long)kQBatch);
     unsigned long long qbase = __shfl_sync(0xffffffffu, qnext, 0);
     unsigned long long qi = qbase;
-    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
+    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * e_perm_map(e_item(qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, n_all) + lane) : 0;
     // the items of one y are consecutive (a batch pop often brings two of them):
     // the filter, the sorted copy of P+(y) and y's weights built for the previous
     // item are reused when y repeats
@@ -255,7 +282,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         const int ipm = __shfl_sync(0xffffffffu, rec, 5);
         const int pyt = __shfl_sync(0xffffffffu, rec, 6);
         const int py = pyl & 0xFFFFFF, ly = (int)((uint32_t)pyl >> 24);
-        const int start = chunk * kChunkE, end = min(ipm, start + kChunkE);
+        const int start = chunk * a.e_chunk, end = min(ipm, start + a.e_chunk);
         const bool ty = ly < k;
         const bool local = py <= kPyCap;            // sorted copy of P+(y) in smem
         // setup: the loads of P-(y) (x list), P+(y) (filter) and y's weights are
@@ -307,7 +334,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         } else {
             qi++;
         }
-        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (qi * a.e_world + a.e_rank) + lane) : 0;
+        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * e_perm_map(e_item(qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, n_all) + lane) : 0;
         // the item's predecessors x. A triangle carries a term only if two of its
         // vertices are targets: with both x and y targets every z < y of P+(x) is
         // probed, with one of them only those of the target run, with neither
@@ -432,7 +459,11 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
                             if (tz && (tx + ty) && owned(a, z)) atomicAdd(a.n1 + z, (unsigned long long)(tx + ty));
                             cnty += ty ? (unsigned long long)(tx + tz) : 0ull;
                         } else {
-                            const double Axlz = __ldg(a.wps + xe.x + off);  // a_x(c_z), stored by Phase A
+                            // a_x(c_z) and a_y(c_z): 0 unless z is a target (its run of
+                            // P+(x)); else x's row at lab(z) and y's row in shared memory
+                            const int lz = (!SPARSE && zt) ? (int)__ldg(a.lab + z) : 0;
+                            const double Axlz = SPARSE ? __ldg(a.wps + xe.x + off)
+                                                       : (zt ? __ldg(a.amat + (int64_t)x * k + lz) : 0.0);
                             // a_x(c_y) (and, all-communities mode, a_y(c_x)) gathered per
                             // verified triangle rather than per (y, x) pair: most pairs close none
                             const int64_t xq = by + py + S.xn[slot].y;
@@ -440,7 +471,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
                             const double Aylx = SPARSE ? __ldg(a.wps + xq) : (lx < k ? Ay[lx] : 0.0);
                             // a_y(c_z), beside z in y's slot (the other run holds 0)
                             const int64_t ypos = by + (!zt ? pyt + iz : ((local && !SPARSE) ? pyt - 1 - iz : iz));
-                            const double Aylz = __ldg(a.wps + ypos);
+                            const double Aylz = SPARSE ? __ldg(a.wps + ypos) : (zt ? Ay[lz] : 0.0);
                             const double Azlx = SPARSE ? __ldg(a.pwr + xe.x + off) : amat_at(a, z, lx);
                             const double Azly = SPARSE ? __ldg(a.pwr + ypos) : amat_at(a, z, ly);
                             const double tx = Aylx * Azlx * (Azly + Aylz);
@@ -673,7 +704,10 @@ __global__ void __launch_bounds__(256, RS_EXP_LIGHT_MINB) k_phase_e_light(CdeArg
                 } else {
                     const double Axlyp = SPARSE ? __ldg(a.pwr + qp) : amat_at(a, xp, lyp);
                     const double Aylxp = txp ? (SPARSE ? __ldg(a.wps + qp) : __ldg(a.amat + (int64_t)y * k + lxp)) : 0.0;
-                    const double Axlz = __ldg(a.wps + pos), Aylz = __ldg(a.wps + ypos);
+                    // a_x(c_z), a_y(c_z): 0 unless z is a target (its run), else the rows at lab(z)
+                    const int lz = (!SPARSE && zt) ? (int)__ldg(a.lab + z) : 0;
+                    const double Axlz = SPARSE ? __ldg(a.wps + pos) : (zt ? __ldg(a.amat + (int64_t)xp * k + lz) : 0.0);
+                    const double Aylz = SPARSE ? __ldg(a.wps + ypos) : (zt ? __ldg(a.amat + (int64_t)y * k + lz) : 0.0);
                     const double Azlx = SPARSE ? __ldg(a.pwr + pos) : amat_at(a, z, lxp);
                     const double Azly = SPARSE ? __ldg(a.pwr + ypos) : amat_at(a, z, lyp);
                     const double ttx = Aylxp * Azlx * (Azly + Aylz);
@@ -692,15 +726,20 @@ __global__ void __launch_bounds__(256, RS_EXP_LIGHT_MINB) k_phase_e_light(CdeArg
 }
 
 // ---------------------------------------------------------------- work items (per step)
-// Heavy middle vertices (degree >= 128) are cut into chunks of kChunkE
+// Heavy middle vertices (degree >= 128) are cut into chunks of e_chunk
 // positions of P(y); the chunk counts depend on the communities, so the item
 // list is rebuilt every step (count, scan, scatter), heaviest vertices first.
-__global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t lo, int64_t hi, int32_t *cnt) {
+// One GPU: chunks of kChunkE = 64 positions. Multi-GPU: shorter ones -- a
+// rank's share of the probes is 1/N, and a 64-position item can take ~16 K
+// probes (Orkut shape), about a whole warp's share at N = 8, so the last items
+// would set the kernel's length
+__global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t lo, int64_t hi, int chunk,
+                          int32_t *cnt) {
     for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
         int c = 0;
         if (y < n_heavy && y >= lo && y < hi) {   // multi-GPU: this rank's middle vertices only
             const PRec p = pc2[y];
-            if (pr_plus(p) > 0 && p.y > pr_plus(p)) c = (p.y - pr_plus(p) + kChunkE - 1) / kChunkE;   // chunks of P-(y)
+            if (pr_plus(p) > 0 && p.y > pr_plus(p)) c = (p.y - pr_plus(p) + chunk - 1) / chunk;   // chunks of P-(y)
         }
         cnt[y] = c;
     }
@@ -758,7 +797,12 @@ cudaError_t launch_e_items(Ctx &c) {
 #endif
     const int64_t nh = c.bins.offset[RS_EXP_HEAVY_CLS];   // degree classes 5-7
     c.e_nbig = nh;
-    c.e_extra = nh + c.nnz / kChunkE + 1;         // item capacity
+    // measured, emulated ranks of the Orkut shape (E || D max over ranks): N = 8
+    // 1.07 / 0.85 / 0.78 ms at 64 / 32 / 16 positions, N = 4 1.30 / 1.22 at 16 /
+    // 32; one GPU: 64 (32: +0.33 ms)
+    c.e_chunk = c.world >= 5 ? 16 : c.world >= 2 ? 32 : kChunkE;
+    if (const char *ev = getenv("RS_EXP_ECHUNK")) c.e_chunk = std::min(kChunkE, std::max(1, atoi(ev)));
+    c.e_extra = nh + c.nnz / c.e_chunk + 1;       // item capacity
     // layout: cnt[nh+1] | off[nh+1] | items[cap] (EItem)
     const size_t bytes = sizeof(int32_t) * 2 * (size_t)(nh + 1) + sizeof(EItem) * (size_t)c.e_extra + 16;
     if (bytes <= c.e_bytes) return cudaSuccess;
@@ -778,7 +822,7 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nh + 256) / 256, 148 * 4));
     // every heavy middle vertex (multi-GPU too: their P-(y) lists are exchanged,
     // and the ranks stride over the items)
-    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, 0, c.n, cnt);
+    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, 0, c.n, c.e_chunk, cnt);
     // the prefix is CUB's device scan (a few microseconds; a one-CTA scan of our
     // own measured 0.27 ms: one block cannot keep enough loads in flight)
     size_t need = 0;
@@ -813,7 +857,14 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     if (c.world > 1) {
         ah.e_rank = c.rank;
         ah.e_world = c.world;
+        const char *eb = getenv("RS_EXP_EBLK");
+        ah.e_blk = eb ? std::max(1, atoi(eb)) : 1;
     }
+    // one GPU: the queue order interleaved over 2 batches (measured on the Orkut
+    // shape: E || D 2.88-3.01 -> 2.80 ms; P = 4 / 8 / 16 2.81 / 2.82 / 2.83; LJ
+    // shape unchanged). Multi-GPU: the items are already dealt one by one
+    ah.e_perm = c.world > 1 ? 1 : 2;
+    if (const char *ep = getenv("RS_EXP_EPERM")) ah.e_perm = std::max(1, atoi(ep));
     // test hook (RS_E_SHARES): the rank split run as sequential shares on one GPU
     const int shares = c.world > 1 ? 1 : std::max(1, c.e_shares);
     unsigned long long *ctr = c.scal + kScalCnt0;

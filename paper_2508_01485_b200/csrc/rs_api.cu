@@ -301,7 +301,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     const bool fits = c.cap_n >= n && c.cap_nnz >= nnz;
     if (!fits) free_graph(ctx);
     c.loaded = c.has_comm = c.scored = false;
-    c.acc_zero = c.bql_zero = false;
+    c.acc_zero = c.bql_zero = c.bsum_zero = false;
     c.nwide_k = 0;
     c.n = n;
     c.nnz = nnz;
@@ -367,7 +367,6 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
         CK(dalloc(&c.pidx, nnz));
         CK(dalloc(&c.plab, nnz));
         CK(dalloc(&c.pplus, nnz + 4));   // + 4: aligned 16-byte probes may read past the end
-        CK(dalloc(&c.wps, nnz));
         CK(dalloc(&c.pc2, n));
         CK(dalloc(&c.acc1, 3 * n));
         c.n_hub = std::min<int64_t>(n, rs::kHubMax);
@@ -445,7 +444,7 @@ static rs_status set_communities_all(rs_ctx *ctx, int64_t mx) {
         CK(dalloc(&c.cid, n)); CK(dalloc(&c.srec, n)); CK(dalloc(&c.aself, n)); CK(dalloc(&c.xsum, n));
         CK(dalloc(&c.n2s, n));
         CK(dalloc(&c.ctk, nnz)); CK(dalloc(&c.ctb, nnz));
-        CK(dalloc(&c.pwr, nnz)); CK(dalloc(&c.prv, nnz));
+        CK(dalloc(&c.pwr, nnz)); CK(dalloc(&c.prv, nnz)); CK(dalloc(&c.wps, nnz));
         c.sp_cap = c.cap_nnz;
     }
     int64_t nc = 0;
@@ -561,8 +560,8 @@ extern "C" rs_status rs_set_communities(rs_ctx *ctx, const int32_t *community_of
 // (k_dist.cu): omega_max (max), the B sums (k x n u64, integer sum of every
 // rank's pushes), the cube-root rows (all-gather by segment), {|P|, |P+|,
 // |P+_T|} per vertex and the ids of the oriented runs P+(x) (all-gathered;
-// VRec, PRec, Q and the weights beside P+ entries are rebuilt from them and the
-// rows). Exact: every value is copied bit for bit, an integer sum, or
+// VRec, PRec and the weights beside P+ entries are rebuilt from them and the
+// rows; Phase D reads the summed B pushes and the rows directly). Exact: every value is copied bit for bit, an integer sum, or
 // recomputed by the same operation Phase A uses. Bytes: DESIGN.md §7.
 static rs_status exchange_phase_a(rs_ctx *ctx) {
     Ctx &c = ctx->c;
@@ -587,37 +586,34 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
     c.xag_bytes += (8 * k + 12) * n;
     XK(c.xp->allgatherv(c.vx, off.data(), len.data(), c.stream));
     CK(rs::launch_vx_unpack(c));
-    CK(rs::launch_b_rebuild(c));
-    // the heavy P-(y) lists (Phase E's items stride over the ranks): gm = prefix of
-    // |P-(y)| over y < n_heavy in vertex order (every rank computes the same)
+    if (!c.bsum_direct) CK(rs::launch_b_rebuild(c));
+    // the heavy P-(y) lists (Phase E's items are dealt over the ranks): gm = prefix
+    // of |P-(y)| over y < n_heavy in vertex order; the P+ runs: gpre = prefix of
+    // |P+| in vertex order (every rank computes the same); one host read of the
+    // segment bounds for both
     int64_t *gm = (int64_t *)c.scratch;
+    int64_t *gpre = gm + (n + 1);
     CK(rs::launch_run_prefix(c, gm, true));
-    {
-        std::vector<int64_t> hb(W + 1);
-        for (int r = 0; r <= W; r++)
-            CK(cudaMemcpyAsync(&hb[r], gm + std::min<int64_t>(c.bounds[r], c.e_nbig), sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaStreamSynchronize(c.stream));
-        if (hb[W] > c.pkm_cap) {
-            CK(dalloc(&c.pk_m, (size_t)hb[W]));
-            c.pkm_cap = hb[W];
-        }
-        CK(rs::launch_minus_pack(c, gm, false));
-        for (int r = 0; r < W; r++) {
-            off[r] = (size_t)hb[r] * sizeof(int32_t);
-            len[r] = (size_t)(hb[r + 1] - hb[r]) * sizeof(int32_t);
-        }
-        XK(c.xp->allgatherv(c.pk_m, off.data(), len.data(), c.stream));
-        c.xag_bytes += 4 * hb[W];
-        CK(rs::launch_minus_pack(c, gm, true));
-    }
-    // the P+ runs: gpre = prefix of |P+| in vertex order (every rank computes the same)
-    int64_t *gpre = (int64_t *)c.scratch;
     CK(rs::launch_run_prefix(c, gpre, false));
-    std::vector<int64_t> gb(W + 1);
-    for (int r = 0; r <= W; r++)
+    std::vector<int64_t> hb(W + 1), gb(W + 1);
+    for (int r = 0; r <= W; r++) {
+        CK(cudaMemcpyAsync(&hb[r], gm + std::min<int64_t>(c.bounds[r], c.e_nbig), sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, c.stream));
         CK(cudaMemcpyAsync(&gb[r], gpre + c.bounds[r], sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    }
     CK(cudaStreamSynchronize(c.stream));
+    if (hb[W] > c.pkm_cap) {
+        CK(dalloc(&c.pk_m, (size_t)hb[W]));
+        c.pkm_cap = hb[W];
+    }
+    CK(rs::launch_minus_pack(c, gm, false));
+    for (int r = 0; r < W; r++) {
+        off[r] = (size_t)hb[r] * sizeof(int32_t);
+        len[r] = (size_t)(hb[r + 1] - hb[r]) * sizeof(int32_t);
+    }
+    XK(c.xp->allgatherv(c.pk_m, off.data(), len.data(), c.stream));
+    c.xag_bytes += 4 * hb[W];
+    CK(rs::launch_minus_pack(c, gm, true));
     const int64_t total = gb[W];
     if (total > c.pk_cap) {
         CK(dalloc(&c.pk_id, (size_t)total));
@@ -650,7 +646,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     // the accumulators (and the dense B table) were zeroed on a side stream at the
     // end of the previous rs_score, overlapping rs_topk; otherwise zero them here
-    if (c.acc_zero || (!c.sparse && c.bql_zero)) CK(cudaStreamWaitEvent(c.stream, c.ev_zero, 0));
+    if (c.acc_zero || (!c.sparse && (c.bql_zero || c.bsum_zero))) CK(cudaStreamWaitEvent(c.stream, c.ev_zero, 0));
     if (!c.acc_zero) {
         CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, c.stream));
         CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, c.stream));
@@ -682,20 +678,22 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
             const char *ex = getenv("RS_EXP_BSUM");
             const bool dense_enough = c.nnz >= 8 * n * (int64_t)c.k;
             c.bsum_mode = c.world > 1 || (c.k <= 8 && (ex ? ex[0] != '0' : dense_enough));
-            c.bsum_direct = c.world == 1 && c.bsum_mode && ex && ex[0] == '2';
+            // multi-GPU: Phase D reads the summed pushes and the gathered rows directly
+            // (the rebuild would be a pass over all n k cells on every rank)
+            c.bsum_direct = c.bsum_mode && (c.world > 1 || (ex && ex[0] == '2'));
         }
         if (c.bsum_mode) {
-            // multi-GPU: the pushes go to plain u64 sums (exchanged, then rebuilt into BQL)
             if (c.dist_cap < n * c.k) {
                 CK(dalloc(&c.bsum, (size_t)(n * c.k)));
                 CK(dalloc(&c.vx, (size_t)(3 * n)));
                 c.dist_cap = n * c.k;
+                c.bsum_zero = false;
             }
-            CK(cudaMemsetAsync(c.bsum, 0, sizeof(unsigned long long) * (size_t)n * c.k, c.stream));
+            if (!c.bsum_zero) CK(cudaMemsetAsync(c.bsum, 0, sizeof(unsigned long long) * (size_t)n * c.k, c.stream));
         } else if (!c.bql_zero) {
             CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, c.stream));   // B limbs
         }
-        c.bql_zero = false;
+        c.bql_zero = c.bsum_zero = false;
         // Phase A: border + histogram + weights + P lists + omega_max partials, the
         // orientation of G' and the B-table pushes
         fork(c);
@@ -706,6 +704,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (c.world > 1) {
         // multi-GPU: Phase A ran on this rank's vertices only; exchange what the
         // other phases read of the 2-hop neighbourhood (ms_phase[1])
+        c.xp->tag = 1;
         rs_status st = exchange_phase_a(ctx);
         if (st != RS_OK) return st;
     } else if (c.bsum_mode && !c.sparse && !c.bsum_direct) {
@@ -741,6 +740,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         }
         c.xrs_bytes = 8 * 3 * n;
         c.xar_bytes += 16;
+        c.xp->tag = 4;
         XK(c.xp->reduce_scatterv_u64(c.acc1, off.data(), len.data(), c.stream));
         XK(c.xp->allreduce_u64(c.scal + rs::kScalNTri, 2, false, c.stream));
     }
@@ -755,6 +755,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         // every other entry is +0.0 (all-zero bits) on a rank, so an integer sum of
         // the bit patterns gathers the scores exactly
         c.xar_bytes += 8 * n;
+        c.xp->tag = 6;
         XK(c.xp->allreduce_u64((unsigned long long *)c.score, (size_t)n, false, c.stream));
     }
     // zero the accumulators (and the dense B table) for the next rs_score on a side
@@ -765,10 +766,17 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         CK(cudaStreamWaitEvent(zs, c.ev_fork, 0));
         CK(cudaMemsetAsync(c.acc1, 0, sizeof(unsigned long long) * 3 * n, zs));
         CK(cudaMemsetAsync(c.acc_hub, 0, sizeof(unsigned long long) * 3 * rs::kHubStripes * c.n_hub, zs));
-        if (!c.sparse) CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, zs));
+        // the table the next pushes go to: the plain sums (bsum mode: BQL is
+        // rewritten whole by the rebuild) or the BQL limbs
+        if (!c.sparse && c.bsum_mode) {
+            CK(cudaMemsetAsync(c.bsum, 0, sizeof(unsigned long long) * (size_t)n * c.k, zs));
+            c.bsum_zero = true;
+        } else if (!c.sparse) {
+            CK(cudaMemsetAsync(c.bql, 0, sizeof(rs::BQL) * (size_t)n * c.k, zs));
+            c.bql_zero = true;
+        }
         CK(cudaEventRecord(c.ev_zero, zs));
         c.acc_zero = true;
-        if (!c.sparse) c.bql_zero = true;
     }
     c.scored = true;
     if (c.xp) c.xp->score_end(c.stream);
@@ -802,6 +810,8 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         s.xchg_allreduce_bytes = c.world > 1 ? c.xar_bytes : 0;
         s.xchg_allgather_bytes = c.world > 1 ? c.xag_bytes : 0;
         s.xchg_reduce_scatter_bytes = c.world > 1 ? c.xrs_bytes : 0;
+        if (c.xp)
+            for (int i = 0; i < 8; i++) s.ms_xwait[i] = c.xp->wait_ms(i);
         *stats_out = s;
     }
     (void)flags;

@@ -64,6 +64,11 @@ struct Xport {
     // compute alone on the GPU: ranks take turns between collectives)
     virtual void score_begin() {}
     virtual void score_end(cudaStream_t) {}
+    // the phase (rs_stats.ms_phase index) the next collectives belong to, and the
+    // stream time this rank spent inside that phase's collectives (emulated
+    // world: waiting for the peers, the device copies; 0 where not measured)
+    int tag = 0;
+    virtual float wait_ms(int) { return 0.f; }
 };
 struct EmuWorld;
 Xport *make_emu_xport(EmuWorld *w, int rank);
@@ -99,8 +104,10 @@ struct __align__(16) VRec {
 // suffix. Phase A also copies P+(u) to pplus at the same offset as two runs:
 // the entries in a target community in DESCENDING order at [0, t), the others
 // ascending at [t, |P+|), so the entries below any y form one contiguous range
-// around t; wps holds a_u(c_z) beside each entry. (All-communities mode: pplus
-// is pidx itself, one ascending run, t = |P+|.)
+// around t. Phase E reads a_u(c_z) from u's row at lab(z) (0 for the other
+// run); round 2 dropped the copy Phase A wrote beside each entry (Orkut shape:
+// Phase A 1.78 -> 1.60 ms, E unchanged). (All-communities mode: pplus is pidx
+// itself, one ascending run, t = |P+|; wps holds a_u(c_w) beside each w.)
 // t = |P+_T(u)| is packed above bit 40 of `start` (offsets < 2^40).
 // x also carries u's 8-bit label above bit 24, so Phase E gets a predecessor's
 // label with the record it gathers anyway (one random 1-byte gather less per
@@ -165,6 +172,7 @@ struct Ctx {
     cudaEvent_t ev_zero = nullptr;   // accumulators zeroed for the next rs_score (side stream)
     bool acc_zero = false;           // acc1 / acc_hub are zero once ev_zero completes
     bool bql_zero = false;           // the dense B table's limbs are zero once ev_zero completes
+    bool bsum_zero = false;          // the plain B sums (bsum mode) are zero once ev_zero completes
     bool parity_ok = false;          // f / omega written for the last rs_score (getters)
     std::string err;
     int64_t launches = 0;
@@ -208,6 +216,7 @@ struct Ctx {
     int64_t d_max = 0;
     int64_t *e_pre = nullptr;    // Phase E work items: prefix of extra chunks of the e_nbig largest rows
     int64_t e_nbig = 0, e_extra = 0;
+    int e_chunk = 64;            // Phase E: positions of P-(y) per heavy work item (<= kChunkE)
     size_t e_bytes = 0;
     bool loaded = false;
 
@@ -250,7 +259,7 @@ struct Ctx {
     int32_t *pidx = nullptr;     // nnz, P(u) ascending at rowptr[u] (P+(u) its prefix, see PRec)
     uint8_t *plab = nullptr;     // nnz, the 8-bit label of each P(u) entry, beside it (Phase A)
     int32_t *pplus = nullptr;    // nnz, P+(u) at rowptr[u] as a target run and the other run
-    double *wps = nullptr;       // nnz, a_u(c_z) beside each z of P+(u)
+    double *wps = nullptr;       // nnz, all-communities mode only: a_u(c_w) beside each w of P(u)
     PRec *pc2 = nullptr;         // n: {|P+(u)|, |P(u)|, rowptr[u] | |P+_T(u)| << 40}
     double *amat = nullptr;      // n*k cube roots a_u(C_i) = omega_u(C_i)^(1/3)
     BQL *bql = nullptr;          // k*n, column-major: bql[c*n + w]

@@ -1,6 +1,7 @@
 // Shared argument block of the P-list phases (D, E) and the finalize pass.
 #pragma once
 #include "rs_internal.cuh"
+
 #include "rs_device.cuh"
 #include <algorithm>
 #include <cmath>
@@ -17,7 +18,7 @@ struct CdeArgs {
     const VRec *__restrict__ vrec;
     const int32_t *__restrict__ pidx;   // P(u) ascending at rowptr[u]: P+(u) prefix, P-(u) suffix
     const int32_t *__restrict__ pplus;  // P+(u) at rowptr[u]: target run + other run (see PRec)
-    const double *__restrict__ wps;     // a_u(c_z) beside each z of P+(u)
+    const double *__restrict__ wps;     // all-communities mode: a_u(c_w) beside each w of P(u)
     const PRec *__restrict__ pc2;       // {|P+(u)|, |P(u)|, rowptr[u] | |P+_T(u)| << 40}
     const BQL *__restrict__ bql;        // column-major: bql[c*n + w]
     const unsigned long long *__restrict__ bsum;   // non-null: B sums read here, Q from amat (no BQL rebuild)
@@ -32,6 +33,9 @@ struct CdeArgs {
     unsigned long long *scal;
     int64_t head_lo, head_hi;           // owned head range (multi-GPU); [0, n) on one GPU
     int32_t e_rank, e_world;            // Phase E: this rank's share of the middle vertices
+    int32_t e_blk;                      // Phase E: heavy items dealt to the ranks in blocks of e_blk
+    int32_t e_perm;                     // Phase E: the queue order interleaved over e_perm batches
+    int32_t e_chunk;                    // Phase E: positions of P-(y) per heavy work item
     int64_t n_wide;                     // heads [0, n_wide) use the 3-limb Type-I accumulator
     // all-communities mode (k_sparse.cu): weights per G' edge instead of dense rows
     const double *__restrict__ pwr;     // a_w(c_u) beside each w of P(u) (wps: a_u(c_w))
@@ -53,7 +57,7 @@ inline CdeArgs cde_args(Ctx &c) {
     a.perm = c.perm; a.lab = c.lab;
     a.n_wide = c.n_wide;
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
-    a.e_rank = 0; a.e_world = 1;
+    a.e_rank = 0; a.e_world = 1; a.e_blk = 1; a.e_perm = 1; a.e_chunk = c.e_chunk;
     a.pwr = c.pwr; a.prv = c.prv; a.ctb = c.ctb; a.bq = c.bq;
     {
         // Phase E's per-item x slots (smem_red4): a grouped Type-I term is < 2 omega_max

@@ -119,11 +119,36 @@ struct EmuXport : Xport {
     EmuXport(EmuWorld *w, int r) : W(w), rank(r) {}
     ~EmuXport() override {
         if (tmp) cudaFree(tmp);
+        for (Wait &x : waits) {
+            cudaEventDestroy(x.e0);
+            cudaEventDestroy(x.e1);
+        }
     }
+    // each collective of an rs_score: events on the rank's stream when it enters
+    // (its buffer final) and when it resumes (the copies done, its turn again)
+    struct Wait {
+        cudaEvent_t e0, e1;
+        int tag;
+    };
+    std::vector<Wait> waits;
+    size_t nwait = 0;
+    cudaStream_t wait_stream = nullptr;
     bool in_score = false;
     void score_begin() override {
+        nwait = 0;
         in_score = W->serial;
         if (in_score) W->turn_begin(rank);
+    }
+    float wait_ms(int t) override {
+        float sum = 0.f;
+        for (size_t i = 0; i < nwait; i++) {
+            if (waits[i].tag != t) continue;
+            float ms = 0.f;
+            if (cudaEventSynchronize(waits[i].e1) == cudaSuccess &&
+                cudaEventElapsedTime(&ms, waits[i].e0, waits[i].e1) == cudaSuccess)
+                sum += ms;
+        }
+        return sum;
     }
     void score_end(cudaStream_t s) override {
         if (!in_score) return;
@@ -133,6 +158,16 @@ struct EmuXport : Xport {
     }
     cudaError_t publish(const void *p, cudaStream_t s) {
         const cudaError_t e = cudaStreamSynchronize(s);   // this rank's buffer is final
+        if (nwait == 64) nwait = 63;                      // collectives outside rs_score: keep the last
+        if (nwait == waits.size()) {
+            Wait x{nullptr, nullptr, 0};
+            cudaEventCreate(&x.e0);
+            cudaEventCreate(&x.e1);
+            waits.push_back(x);
+        }
+        waits[nwait].tag = tag;
+        cudaEventRecord(waits[nwait].e0, s);
+        wait_stream = s;
         if (in_score) W->turn_end(rank);
         W->ptr[rank] = p;
         W->barrier();
@@ -141,6 +176,8 @@ struct EmuXport : Xport {
     // the end of a collective: in serial mode wait for this rank's turn again
     void resume() {
         if (in_score) W->turn_begin(rank);
+        cudaEventRecord(waits[nwait].e1, wait_stream);
+        nwait++;
     }
     cudaError_t allgatherv(void *buf, const size_t *off, const size_t *len, cudaStream_t s) override {
         cudaError_t e = publish(buf, s);
