@@ -6,10 +6,11 @@
 // * per vertex {|P|, |P+|, |P+_T|} (12 B): VRec and PRec are rebuilt from them
 //   (a_self = a_u(C(u)) from the gathered row; head / wide from d(u) and lab);
 // * the oriented runs P+(x): only their ids travel (4 B per entry), packed back
-//   to back in vertex order at gpre[x] = sum of |P+| over the vertices before x
-//   (Phase E reads the weights a_x(c_z) from the gathered rows);
+//   to back in vertex order at gpre[x] = sum of |P+| over the vertices before x;
+//   Phase E reads them there (PRec start rebased to gpre[x]) and the weights
+//   a_x(c_z) from the gathered rows: nothing is copied back into slots;
 // * the P-(y) lists of the heavy middle vertices (degree >= 128; 4 B per
-//   entry): Phase E strides over their work items on every rank;
+//   entry), packed at gm[y]: Phase E deals their work items over the ranks;
 // * the B table: only the pushed integer sums (8 B per cell, summed over the
 //   ranks); Phase D reads them with a_w(c) from the gathered rows (no rebuild
 //   pass over the n k cells on every rank).
@@ -33,14 +34,13 @@ __global__ void k_run_count(const PRec *__restrict__ pc2, int64_t n, int64_t n_h
     }
 }
 
-// gpre[0..n]: exclusive prefix of |P+(x)| (or, minus, of the heavy |P-(y)|) in
-// the context scratch (gpre inside it), the counts and the scan's temporary
-// storage after it
+// gpre[0..n]: exclusive prefix of |P+(x)| (or, minus, of the heavy |P-(y)|);
+// the counts and the scan's temporary storage in the context scratch
 cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus) {
     const int64_t n = c.n;
-    int64_t *cnt = gpre + (n + 1);
+    int64_t *cnt = (int64_t *)c.scratch;
     void *tmp = cnt + (n + 1);
-    const size_t used = (size_t)((char *)tmp - (char *)c.scratch);
+    const size_t used = sizeof(int64_t) * (size_t)(n + 1);
     if (used > c.scratch_bytes) return cudaErrorMemoryAllocation;
     const size_t tmp_bytes = c.scratch_bytes - used;
     if (minus) k_run_count<true><<<148 * 4, 256, 0, c.stream>>>(c.pc2, n, c.e_nbig, cnt);
@@ -53,22 +53,21 @@ cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus) {
     return cudaGetLastError();
 }
 
-// pack the owned vertices' P+ ids (UNPACK = false), or copy every other
-// vertex's run from the gathered buffer into its slot. A warp takes 32
-// consecutive vertices and deals their entries to the lanes 32 at a time (a
-// warp scan of the run lengths; most runs are a few entries, so a warp per
-// vertex would leave most lanes idle): the gathered ids are read coalesced
-template <bool UNPACK>
-__global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gpre, int64_t n, int64_t lo,
-                            int64_t hi, int32_t *__restrict__ pplus, int32_t *__restrict__ pk_id) {
+// pack the owned vertices' P+ runs (two runs each, as Phase A wrote them in
+// their slots) back to back at gpre[x]. A warp takes 32 consecutive vertices
+// and deals their entries to the lanes 32 at a time (a warp scan of the run
+// lengths; most runs are a few entries): the packed writes are coalesced.
+// After the all-gather every rank holds all runs packed, and Phase E reads
+// them there (PRec start rebased to gpre[x], k_rebase): no copy back into slots
+__global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gpre, int64_t lo, int64_t hi,
+                            const int32_t *__restrict__ pplus, int32_t *__restrict__ pk_id) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t first = UNPACK ? 0 : lo, last = UNPACK ? n : hi;
-    for (int64_t x0 = first + 32 * ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); x0 < last; x0 += 32 * nw) {
+    for (int64_t x0 = lo + 32 * ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); x0 < hi; x0 += 32 * nw) {
         const int64_t x = x0 + lane;
         int cnt = 0;
         int64_t slot = 0;
-        if (x < last && !(UNPACK && x >= lo && x < hi)) {
+        if (x < hi) {
             const PRec r = pc2[x];
             cnt = pr_plus(r);
             slot = pr_start(r);
@@ -80,7 +79,7 @@ __global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restr
             if (lane >= o) incl += t;
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int64_t g0 = (!UNPACK && total) ? gpre[x0] : 0;   // the first vertex's packed offset
+        const int64_t g0 = total ? gpre[x0] : 0;       // the first vertex's packed offset
         for (int q0 = 0; q0 < total; q0 += 32) {
             const int q = q0 + lane;
             int j = 0;                                    // the first lane whose inclusive count exceeds q
@@ -91,52 +90,47 @@ __global__ void k_plus_pack(const PRec *__restrict__ pc2, const int64_t *__restr
             }
             const int i = q - (__shfl_sync(0xffffffffu, incl, j) - __shfl_sync(0xffffffffu, cnt, j));
             const int64_t sj = __shfl_sync(0xffffffffu, (long long)slot, j);
-            if (q >= total) continue;
-            if (UNPACK) {
-                // packed offset of x0 + j: gpre is in vertex order, and the owned
-                // vertices (skipped, count 0 here) have their entries in between
-                const int64_t gj = gpre[x0 + j] + i;
-                pplus[sj + i] = pk_id[gj];
-            } else {
-                pk_id[g0 + q] = pplus[sj + i];            // owned range: contiguous in the packed buffer
-            }
+            if (q < total) pk_id[g0 + q] = pplus[sj + i];
         }
     }
 }
 
-// a warp per heavy vertex: pack the owned ones' P-(y) (the suffix of P(y) in its
-// slot), or copy every other heavy vertex's P-(y) into its slot
-template <bool UNPACK>
-__global__ void k_minus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gm, int64_t n_heavy, int64_t lo,
-                             int64_t hi, int32_t *__restrict__ pidx, int32_t *__restrict__ pk) {
+// a warp per owned heavy vertex: its P-(y) (the suffix of P(y) in its slot) at gm[y]
+__global__ void k_minus_pack(const PRec *__restrict__ pc2, const int64_t *__restrict__ gm, int64_t lo, int64_t hi,
+                             const int32_t *__restrict__ pidx, int32_t *__restrict__ pk) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t first = UNPACK ? 0 : lo, last = UNPACK ? n_heavy : (hi < n_heavy ? hi : n_heavy);
-    for (int64_t y = first + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); y < last; y += nw) {
-        if (UNPACK && y >= lo && y < hi) continue;
+    for (int64_t y = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); y < hi; y += nw) {
         const PRec r = pc2[y];
         const int pp = pr_plus(r), pm = r.y - pp;
         const int64_t at = pr_start(r) + pp, g = gm[y];
-        for (int i = lane; i < pm; i += 32) {
-            if (UNPACK) pidx[at + i] = pk[g + i];
-            else pk[g + i] = pidx[at + i];
-        }
+        for (int i = lane; i < pm; i += 32) pk[g + i] = pidx[at + i];
     }
 }
-cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm, bool unpack) {
-    if (unpack)
-        k_minus_pack<true><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gm, c.e_nbig, c.head_lo, c.head_hi, c.pidx, c.pk_m);
-    else
-        k_minus_pack<false><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gm, c.e_nbig, c.head_lo, c.head_hi, c.pidx, c.pk_m);
+cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm) {
+    const int64_t hi = std::min(c.head_hi, c.e_nbig);
+    if (c.head_lo < hi) {
+        k_minus_pack<<<148 * 8, 256, 0, c.stream>>>(c.pc2, gm, c.head_lo, hi, c.pidx, c.pk_m);
+        c.launches++;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre) {
+    k_plus_pack<<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.head_lo, c.head_hi, c.pplus, c.pk_id);
     c.launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre, bool unpack) {
-    if (unpack)
-        k_plus_pack<true><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.pk_id);
-    else
-        k_plus_pack<false><<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n, c.head_lo, c.head_hi, c.pplus, c.pk_id);
+// every vertex's PRec start -> its packed offset gpre[x] (|P+_T| kept above the offset bits)
+__global__ void k_rebase(PRec *__restrict__ pc2, const int64_t *__restrict__ gpre, int64_t n) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const long long s = pc2[x].start;
+        pc2[x].start = (s & ~((1ll << kPrShift) - 1)) | gpre[x];
+    }
+}
+cudaError_t launch_rebase(Ctx &c, const int64_t *gpre) {
+    k_rebase<<<148 * 8, 256, 0, c.stream>>>(c.pc2, gpre, c.n);
     c.launches++;
     return cudaGetLastError();
 }

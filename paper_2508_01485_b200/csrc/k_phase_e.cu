@@ -186,10 +186,12 @@ __device__ __forceinline__ U128 from4(const uint32_t *acc4) {
 // a work item: positions [64 chunk, 64 chunk + 64) of P-(y), with y's record
 struct __align__(16) EItem {
     int64_t by;            // start of y's slot (rowptr[y]): P(y) in pidx, P+(y) runs in pplus
+                           // (multi-GPU: the packed offset of P+(y))
     int32_t y, chunk;
     int32_t pyl;           // |P+(y)| | lab(y) << 24
     int32_t pm;            // |P-(y)|
-    int32_t pyt, pad;      // |P+_T(y)|
+    int32_t pyt;           // |P+_T(y)|
+    uint32_t mbase;        // multi-GPU: offset of P-(y) in the packed heavy lists
 };
 struct EItems {
     const EItem *items;    // work items of the heavy middle vertices, heaviest first
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         const int pyl = __shfl_sync(0xffffffffu, rec, 4);
         const int ipm = __shfl_sync(0xffffffffu, rec, 5);
         const int pyt = __shfl_sync(0xffffffffu, rec, 6);
+        const uint32_t mb = (uint32_t)__shfl_sync(0xffffffffu, rec, 7);
         const int py = pyl & 0xFFFFFF, ly = (int)((uint32_t)pyl >> 24);
         const int start = chunk * a.e_chunk, end = min(ipm, start + a.e_chunk);
         const bool ty = ly < k;
@@ -291,7 +294,8 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int i = start + 32 * h + lane;
-            xv[h] = i < end ? __ldg(a.pidx + by + py + i) : -1;   // x in P-(y) (suffix of P(y)): x > y
+            // x in P-(y) (the suffix of P(y) in its slot; multi-GPU: packed): x > y
+            xv[h] = i < end ? __ldg(a.pidx + (a.mg ? (int64_t)mb : by + py) + i) : -1;
         }
         // i-th entry of P+(y) in ascending order within its run (the target run is
         // stored descending, the other run ascending after it)
@@ -623,7 +627,9 @@ __global__ void __launch_bounds__(256, RS_EXP_LIGHT_MINB) k_phase_e_light(CdeArg
         PRec pcl{(int)0xFF000000, 0, 0};
         if (yl < yhi) pcl = a.pc2[yl];
         const int lyl = pr_lab(pcl);
-        const int64_t rpl = pr_start(pcl);                 // rowptr[y]
+        // P-(y): the suffix of P(y) in y's slot (multi-GPU: P+ runs are packed, the
+        // light P-(y) of a rank's own y stay in their slots)
+        const int64_t rpl = a.mg ? (yl < yhi ? __ldg(a.rowptr + yl) : 0) : pr_start(pcl);
         const int cnt = pr_plus(pcl) > 0 ? pcl.y - pr_plus(pcl) : 0;   // pairs of this y: |P-(y)| if P+(y) is non-empty
         int incl = cnt;
 #pragma unroll
@@ -747,9 +753,10 @@ __global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t
 // a thread per heavy y writes its first 8 items; the rare y with more (hubs:
 // up to hundreds of chunks) hand the rest to a warp each (second loop), so no
 // thread serialises a hub's whole item list
+// (multi-GPU, gpre / gm non-null: y's runs are read packed)
 __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
                             const PRec *__restrict__ pc2, const int64_t *__restrict__ rowptr,
-                            const uint8_t *__restrict__ lab, int64_t n_heavy,
+                            const int64_t *__restrict__ gpre, const int64_t *__restrict__ gm, int64_t n_heavy,
                             EItem *items) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += stride) {
@@ -757,12 +764,12 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         if (c == 0) continue;
         const PRec p = pc2[y];
         EItem e;
-        e.by = rowptr[y];
+        e.by = gpre ? gpre[y] : rowptr[y];
         e.y = (int32_t)y;
         e.pyl = p.x;                                  // |P+(y)| | lab(y) << 24
         e.pm = p.y - pr_plus(p);
         e.pyt = pr_plus_t(p);
-        e.pad = 0;
+        e.mbase = gm ? (uint32_t)gm[y] : 0u;
         for (int j = 0; j < c && j < 8; j++) {
             e.chunk = j;
             items[o + j] = e;
@@ -776,12 +783,12 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         const int o = off[y];
         const PRec p = pc2[y];
         EItem e;
-        e.by = rowptr[y];
+        e.by = gpre ? gpre[y] : rowptr[y];
         e.y = (int32_t)y;
         e.pyl = p.x;
         e.pm = p.y - pr_plus(p);
         e.pyt = pr_plus_t(p);
-        e.pad = 0;
+        e.mbase = gm ? (uint32_t)gm[y] : 0u;
         for (int j = 8 + lane; j < c; j += 32) {
             e.chunk = j;
             items[o + j] = e;
@@ -829,7 +836,8 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
     if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
     cub::DeviceScan::ExclusiveSum(c.scratch, need, cnt, off, (int)(nh + 1), c.stream);
-    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, c.pc2, c.rowptr, c.lab, nh, items);
+    const int64_t *gm = c.mg_packed ? c.xg : nullptr, *gpre = c.mg_packed ? c.xg + (c.n + 1) : nullptr;
+    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, c.pc2, c.rowptr, gpre, gm, nh, items);
     c.launches += 3;
     it.items = items;
     it.total = off + nh;
@@ -857,6 +865,7 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     if (c.world > 1) {
         ah.e_rank = c.rank;
         ah.e_world = c.world;
+        if (c.mg_packed) ah.pidx = c.pk_m;            // the heavy P-(y), packed
         const char *eb = getenv("RS_EXP_EBLK");
         ah.e_blk = eb ? std::max(1, atoi(eb)) : 1;
     }

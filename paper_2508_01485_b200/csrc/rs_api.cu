@@ -240,6 +240,7 @@ static void free_graph(rs_ctx *ctx) {
     dfree(c.xsum); dfree(c.n2s);
     dfree(c.pk_id); c.pk_cap = 0;
     dfree(c.pk_m); c.pkm_cap = 0;
+    dfree(c.xg); c.xg_cap = 0;
     dfree(c.bsum); dfree(c.vx); c.dist_cap = 0;
     c.sp_cap = 0;
     c.k_alloc = 0; c.scratch_bytes = 0; c.loaded = c.has_comm = c.scored = false;
@@ -590,9 +591,13 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
     // the heavy P-(y) lists (Phase E's items are dealt over the ranks): gm = prefix
     // of |P-(y)| over y < n_heavy in vertex order; the P+ runs: gpre = prefix of
     // |P+| in vertex order (every rank computes the same); one host read of the
-    // segment bounds for both
-    int64_t *gm = (int64_t *)c.scratch;
-    int64_t *gpre = gm + (n + 1);
+    // segment bounds for both. Both travel packed and Phase E reads them packed
+    if (c.xg_cap < n) {
+        CK(dalloc(&c.xg, 2 * (size_t)(n + 1)));
+        c.xg_cap = n;
+    }
+    int64_t *gm = c.xg;
+    int64_t *gpre = c.xg + (n + 1);
     CK(rs::launch_run_prefix(c, gm, true));
     CK(rs::launch_run_prefix(c, gpre, false));
     std::vector<int64_t> hb(W + 1), gb(W + 1);
@@ -606,27 +611,29 @@ static rs_status exchange_phase_a(rs_ctx *ctx) {
         CK(dalloc(&c.pk_m, (size_t)hb[W]));
         c.pkm_cap = hb[W];
     }
-    CK(rs::launch_minus_pack(c, gm, false));
+    CK(rs::launch_minus_pack(c, gm));
     for (int r = 0; r < W; r++) {
         off[r] = (size_t)hb[r] * sizeof(int32_t);
         len[r] = (size_t)(hb[r + 1] - hb[r]) * sizeof(int32_t);
     }
     XK(c.xp->allgatherv(c.pk_m, off.data(), len.data(), c.stream));
     c.xag_bytes += 4 * hb[W];
-    CK(rs::launch_minus_pack(c, gm, true));
     const int64_t total = gb[W];
-    if (total > c.pk_cap) {
-        CK(dalloc(&c.pk_id, (size_t)total));
-        c.pk_cap = total;
+    if (total + 4 > c.pk_cap) {                           // + 4: aligned 16-byte probes may read past the end
+        CK(dalloc(&c.pk_id, (size_t)total + 4));
+        c.pk_cap = total + 4;
     }
-    CK(rs::launch_plus_pack(c, gpre, false));
+    CK(rs::launch_plus_pack(c, gpre));
     for (int r = 0; r < W; r++) {
         off[r] = (size_t)gb[r] * sizeof(int32_t);
         len[r] = (size_t)(gb[r + 1] - gb[r]) * sizeof(int32_t);
     }
     XK(c.xp->allgatherv(c.pk_id, off.data(), len.data(), c.stream));
     c.xag_bytes += 4 * total;
-    CK(rs::launch_plus_pack(c, gpre, true));
+    // Phase E reads every P+ run packed: PRec start -> gpre[x] (after the pack,
+    // which read the owned runs from their slots)
+    CK(rs::launch_rebase(c, gpre));
+    c.mg_packed = true;
     return RS_OK;
 }
 
@@ -643,6 +650,7 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         return fail(ctx, RS_EINVAL, "rs_score: the NEXT-3 variant flags need explicit targets (k <= 254)");
     if (c.xp) c.xp->score_begin();
     c.hubs_folded = false;
+    c.mg_packed = false;
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
     // the accumulators (and the dense B table) were zeroed on a side stream at the
     // end of the previous rs_score, overlapping rs_topk; otherwise zero them here

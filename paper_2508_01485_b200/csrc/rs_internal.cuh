@@ -183,10 +183,13 @@ struct Ctx {
     ncclComm_t comm = nullptr;
 #endif
     Xport *xp = nullptr;                       // world > 1: the exchange transport (owned)
-    int32_t *pk_id = nullptr;                  // world > 1: packed P+ runs of all ranks (ids)
+    int32_t *pk_id = nullptr;                  // world > 1: packed P+ runs of all ranks (ids), at gpre[x]
     int64_t pk_cap = 0;
-    int32_t *pk_m = nullptr;                   // world > 1: packed P- lists of the heavy vertices
+    int32_t *pk_m = nullptr;                   // world > 1: packed P- lists of the heavy vertices, at gm[y]
     int64_t pkm_cap = 0;
+    int64_t *xg = nullptr;                     // world > 1: gm[0..n] | gpre[0..n] (exclusive prefixes)
+    int64_t xg_cap = 0;
+    bool mg_packed = false;                    // Phase E reads the packed runs (PRec start = gpre[x])
     int64_t xar_bytes = 0, xag_bytes = 0;      // world > 1: bytes all-reduced / all-gathered in the last rs_score
     int64_t xrs_bytes = 0;                     //   and reduce-scattered
     bool hubs_folded = false;                  // the hub stripes were folded into acc1 (multi-GPU)
@@ -335,8 +338,9 @@ cudaError_t launch_awcc_trial(Ctx &c, const int32_t *S_dev, int64_t nS, int mode
                               int32_t *zeta_dev, void *scratch, size_t scratch_bytes, int64_t cap);
 cudaError_t launch_phase_e_on(Ctx &c, cudaStream_t light);
 cudaError_t launch_run_prefix(Ctx &c, int64_t *gpre, bool minus);
-cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre, bool unpack);
-cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm, bool unpack);
+cudaError_t launch_plus_pack(Ctx &c, const int64_t *gpre);
+cudaError_t launch_minus_pack(Ctx &c, const int64_t *gm);
+cudaError_t launch_rebase(Ctx &c, const int64_t *gpre);
 cudaError_t launch_vx_pack(Ctx &c);
 cudaError_t launch_vx_unpack(Ctx &c);
 cudaError_t launch_b_rebuild(Ctx &c);

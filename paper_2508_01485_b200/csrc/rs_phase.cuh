@@ -36,6 +36,8 @@ struct CdeArgs {
     int32_t e_blk;                      // Phase E: heavy items dealt to the ranks in blocks of e_blk
     int32_t e_perm;                     // Phase E: the queue order interleaved over e_perm batches
     int32_t e_chunk;                    // Phase E: positions of P-(y) per heavy work item
+    int32_t mg;                         // multi-GPU: P+ runs packed (pplus = the gathered runs, PRec start
+                                        // = packed offset); heavy P-(y) at item.mbase of pidx (packed)
     int64_t n_wide;                     // heads [0, n_wide) use the 3-limb Type-I accumulator
     // all-communities mode (k_sparse.cu): weights per G' edge instead of dense rows
     const double *__restrict__ pwr;     // a_w(c_u) beside each w of P(u) (wps: a_u(c_w))
@@ -52,7 +54,7 @@ inline CdeArgs cde_args(Ctx &c) {
     CdeArgs a;
     a.rowptr = c.rowptr; a.vlo = 0; a.nverts = 0; a.n = c.n; a.k = c.k;
     a.amat = c.amat; a.vrec = c.vrec; a.pidx = c.pidx; a.pc2 = c.pc2;
-    a.pplus = c.pplus; a.wps = c.wps;
+    a.pplus = c.mg_packed ? c.pk_id : c.pplus; a.wps = c.wps; a.mg = c.mg_packed ? 1 : 0;
     a.bql = c.bql; a.bsum = (c.bsum_direct && !c.sparse) ? c.bsum : nullptr; a.acc1 = c.acc1; a.acc_hub = c.acc_hub; a.n_hub = c.n_hub; a.n1 = c.n1; a.t2 = c.t2; a.score = c.score; a.scal = c.scal;
     a.perm = c.perm; a.lab = c.lab;
     a.n_wide = c.n_wide;
