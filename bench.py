@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-mgpu", action="store_true", help="skip the emulated multi-GPU model leg")
     p.add_argument("--phases", action="store_true", help="print per-phase ms to stderr")
+    p.add_argument("--mg-mode", default="sharded", choices=["sharded", "replicated"],
+                   help="N > 1: Phase A sharded + exchanged, or replicated on every rank (RS_REPLICATE_A)")
     return p.parse_args()
 
 
@@ -220,17 +222,18 @@ def main():
     sco_d = torch.empty(a.K, dtype=torch.float64, device=dev)
     sc.load_csr(rp_d, col_d, validate=False)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    mgf = rsb.RS_REPLICATE_A if (world > 1 and a.mg_mode == "replicated") else 0
 
     def step():
         sc.set_communities(comm_d, a.k)
-        sc.score(gather=False)
+        sc.score(gather=False, flags=mgf)
         sc.topk(a.K, ids_d, sco_d)
 
     # warm-up (also sizes every buffer)
     for _ in range(max(a.warmup, 0)):
         step()
     torch.cuda.synchronize(dev)
-    st = sc.score(stats=True)
+    st = sc.score(stats=True, flags=mgf)
     torch.cuda.synchronize(dev)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
@@ -245,7 +248,7 @@ def main():
                 flush.fill_(i & 0xFF)            # L2 flush outside the timed events
             ev[i][0].record(stream)
             sc.set_communities(comm_d, a.k)
-            s = sc.score(stats=a.phases)
+            s = sc.score(stats=a.phases, flags=mgf)
             sc.topk(a.K, ids_d, sco_d)
             ev[i][1].record(stream)
             if a.phases:
@@ -418,7 +421,7 @@ def main():
                        "k_targets": a.k, "K": a.K, "seed": gen.CONFIGS.get(a.config, {}).get("seed"),
                        "n_border": nb, "pred_entries": Db, "triangles": ntri, "probes": nprobe, "omega_max": st["omega_max"],
                        "l2": "flushed between timed steps (512 MiB write)", "gen_s": round(gen_s, 1),
-                       "parallelism": f"head-range x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"head-range x{world} (Phase A {a.mg_mode})" if world > 1 else "single GPU"},
             "roofline": roof,
             "topk_latency_ms": round(float(np.median(tk_ms)), 4),
             "topk_latency_ms_more": tk_more,
@@ -448,6 +451,27 @@ NVLINK_PEER_BW = 770e9
 
 
 def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
+    """Both multi-GPU modes: Phase A sharded + exchanged, and Phase A
+    replicated on every rank (RS_REPLICATE_A, the north_star's replicated CSR and
+    labels: only the Type-I limbs are exchanged); per N the faster is the
+    modelled step."""
+    sh = multigpu_model_mode(a, g, rsb, st1, ms1, tk1, worlds, reps, 0)
+    rep = multigpu_model_mode(a, g, rsb, st1, ms1, tk1, worlds, reps, rsb.RS_REPLICATE_A)
+    out = {"how": sh.pop("how"), "N1_ms_per_step": sh.pop("N1_ms_per_step")}
+    rep.pop("how"), rep.pop("N1_ms_per_step")
+    for N in worlds:
+        key = f"N={N}"
+        a_, b_ = sh.get(key, {}), rep.get(key, {})
+        best = min((x for x in (("sharded", a_), ("replicated", b_)) if "step_ms_model" in x[1]),
+                   key=lambda x: x[1]["step_ms_model"], default=None)
+        out[key] = {"mode": best[0], "step_ms_model": best[1]["step_ms_model"],
+                    "GTEPS_model": best[1]["GTEPS_model"], "speedup_vs_N1": best[1]["speedup_vs_N1"]} if best else {}
+    out["sharded"] = sh
+    out["replicated"] = rep
+    return out
+
+
+def multigpu_model_mode(a, g, rsb, st1, ms1, tk1, worlds, reps, flags):
     """The multi-GPU path on this one GPU: N emulated
     ranks (rs_create_emulated) in SERIAL mode -- inside rs_score the ranks take
     turns between collectives, so each rank's kernels run alone on the GPU and
@@ -475,10 +499,10 @@ def multigpu_model(a, g, rsb, st1, ms1, tk1, worlds=(2, 4, 8), reps=3):
                 s = rsb.Scorer(0, stream.cuda_stream, rank=r, world=N, emu=W)
                 s.load_csr(g.rowptr, g.col)
                 s.set_communities(g.comm, k)
-                s.score()
+                s.score(flags=flags)
                 ph = []
                 for _ in range(reps):
-                    st_last = s.score(stats=True)
+                    st_last = s.score(stats=True, flags=flags)
                     # the rank's own kernel time per phase: the collectives' waits
                     # (peers' turns, the emulated copies) taken out
                     ph.append(np.array(st_last["ms_phase"]) - np.array(st_last["ms_xwait"]))

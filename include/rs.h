@@ -98,6 +98,12 @@ typedef struct {
  * split by middle vertex (s = 2..255) on one GPU; results must not change. */
 #define RS_E_SHARES(s)    (((uint32_t)(s) & 0xFFu) << 8)
 #define RS_E_SHARES_OF(f) (((f) >> 8) & 0xFFu)
+/* Multi-GPU: every rank runs Phase A (Steps 1-2d and the B table) over ALL
+ * vertices from its replicated CSR and labels instead of its own range, so the
+ * Phase A exchange disappears and the only collectives are the Type-I limb
+ * reduce-scatter, the counters and the top-K merge. Results are
+ * bitwise those of the sharded path and of one GPU. Ignored on one GPU. */
+#define RS_REPLICATE_A (1u << 20)
 /* NEXT-3 literal variants of the paper (DESIGN reading C-30; default = the
  * adopted readings C-3, C-4, C-7): */
 #define RS_LITERAL_L (1u << 16) /* |L(u,v)| as Eq. 2 defines L: communities of

@@ -24,6 +24,7 @@ RS_VALIDATE = 1
 RS_GATHER_SCORES = 1
 RS_REMOVE_EDGES, RS_REMOVE_NODES = 0, 1
 RS_LITERAL_L, RS_GATE_L, RS_WMAX_EB = 1 << 16, 1 << 17, 1 << 18   # NEXT-3 variants (rs_score flags)
+RS_REPLICATE_A = 1 << 20   # multi-GPU: Phase A on every rank over all vertices, no Phase A exchange
 RS_ALL_COMMUNITIES = -1   # rs_set_communities k: every community a target (NEXT-2 sparse mode)
 
 

@@ -29,6 +29,7 @@
 #include "rs_device.cuh"
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 namespace rs {
 
@@ -60,6 +61,7 @@ struct PhaseAArgs {
     unsigned long long *__restrict__ bsum;   // multi-GPU: the B pushes go here (k x n u64, summed over
                                         // the ranks, then rebuilt into BQL with Q); nullptr on one GPU
     unsigned long long *scal;
+    int32_t hc;                         // vec walk: labels of vertices [0, hc) cached in shared memory
 };
 
 __device__ __forceinline__ double lg2(const PhaseAArgs &a, int64_t x) {
@@ -210,27 +212,15 @@ __device__ __forceinline__ void phase_a_lists(const PhaseAArgs &a, GR &g, int64_
     }
 }
 
-// k <= 8: Steps 1, 2a-2d and the Step 3 inputs of u, in lockstep over the
-// groups of a warp (LockGroup: warp-uniform loop bounds; u < 0 = no vertex).
-// The row walk keeps per-lane packed 16-bit histograms and P+ counts; one
-// ballot per neighbour compacts P(u). The lists pass reads P(u) and its labels
-// back (L2) and takes a_u(c) from the lane that computed it (shuffle).
+// The row walk of the k <= 8 path, scalar form (CTA groups, and the fallback):
+// lane i of the group takes entries base + j G + i, U loads in flight, per-lane
+// packed 16-bit histograms, one ballot per entry compacts P(u).
 template <int U, class GR>
-__device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
+__device__ __forceinline__ void walk_scalar(const PhaseAArgs &a, int64_t u, int64_t beg, int d, uint32_t lu,
+                                            int32_t cfull, bool wr, GR &g, int &pc_out, int &pp_out, int &pt_out,
+                                            int (&cnt)[8]) {
     const uint32_t k = (uint32_t)a.k;
-    const bool valid = u >= 0;
-    int64_t beg = 0;
-    int d = 0;
-    uint32_t lu = kOther;
-    int32_t cfull = 0;
-    if (valid) {
-        beg = a.rowptr[u];
-        d = (int)(a.rowptr[u + 1] - beg);
-        lu = a.lab[u];
-        if (lu == kOther) cfull = a.comm[u];
-    }
     const bool other = lu == kOther;                 // compare kOther neighbours by full id
-    const bool wr = valid && !a.parity;
     int32_t *__restrict__ pout = a.pidx + beg;
     uint8_t *__restrict__ lout = a.plab + beg;
     unsigned long long h0 = 0ull, h1 = 0ull;
@@ -270,8 +260,9 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
             pc += tot[j];
         }
     }
-    const int pp = g.sum(ppl), pt = g.sum(ptl);
-    int cnt[8];
+    pp_out = g.sum(ppl);
+    pt_out = g.sum(ptl);
+    pc_out = pc;
     if (dw < 65536) {         // group totals still fit the 16-bit fields
         h0 = g.sum(h0);
         h1 = g.sum(h1);
@@ -286,6 +277,167 @@ __device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u,
             cnt[c] = g.sum((int)((h0 >> (16 * c)) & 0xFFFFull));
             cnt[c + 4] = g.sum((int)((h1 >> (16 * c)) & 0xFFFFull));
         }
+    }
+}
+
+// The row walk, vectorised (lockstep groups of G <= 32 lanes): the group reads
+// its row as aligned 16-byte pieces of col (one LDG.128 per lane per piece,
+// 16 G contiguous bytes per group; entries of the first and last piece outside
+// the row are masked), so a lane holds 4 consecutive entries of each of its V
+// pieces; the 4 V label gathers are independent. Branch-free per entry:
+// histogram counts in packed fields (8-bit while a lane's share of the row
+// cannot reach 256, PACK8; else 16-bit), P(u) compacted by ONE group scan of
+// the per-lane foreign counts per piece (ascending order: piece, lane, slot).
+// OTHER (warp-uniform): some group's vertex has no 8-bit code of its own.
+extern __shared__ __align__(16) uint8_t s_lab[];   // vec walk: labels of vertices [0, PhaseAArgs::hc)
+
+template <int V, bool PACK8, bool OTHER, int G>
+__device__ __forceinline__ void walk_vec(const PhaseAArgs &a, int64_t u, int64_t beg, int d, uint32_t lu,
+                                         int32_t cfull, bool wr, LockGroup<G> &g, int &pc_out, int &pp_out,
+                                         int &pt_out, int (&cnt)[8]) {
+    const uint32_t k = (uint32_t)a.k;
+    const int head = (int)(beg & 3);                // entries of the first piece before the row
+    const int hi = d > 0 ? d + head : 0;            // the row is window positions [head, hi)
+    const int4 *__restrict__ wp = reinterpret_cast<const int4 *>(a.col + (beg - head));
+    int32_t *__restrict__ pout = a.pidx + beg;
+    uint8_t *__restrict__ lout = a.plab + beg;
+    typedef typename std::conditional<PACK8, uint32_t, unsigned long long>::type H;
+    H h0 = 0, h1 = 0;
+    int pc = 0, ppl = 0, ptl = 0;
+    const int dw = g.umax(hi);
+    const int32_t u32 = (int32_t)u;
+    for (int base = 0; base < dw; base += 4 * G * V) {
+        int32_t x[V][4];
+        uint32_t l[V][4];
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            const int w0 = base + 4 * (v * G + (int)g.lane);
+            int4 q = make_int4(-1, -1, -1, -1);
+            if (w0 < hi) q = __ldcs(wp + (w0 >> 2));
+            x[v][0] = (w0 >= head && w0 < hi) ? q.x : -1;
+            x[v][1] = (w0 + 1 >= head && w0 + 1 < hi) ? q.y : -1;
+            x[v][2] = (w0 + 2 >= head && w0 + 2 < hi) ? q.z : -1;
+            x[v][3] = (w0 + 3 < hi) ? q.w : -1;
+        }
+#pragma unroll
+        for (int v = 0; v < V; v++)
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                const int32_t xs = x[v][s];
+                // the highest-degree vertices (the first ids) are most of the references:
+                // their labels come from the block's shared copy (a random byte gather
+                // from shared memory costs a few bank wavefronts, from L1 one per lane)
+                l[v][s] = xs < 0 ? (uint32_t)kOther : xs < a.hc ? (uint32_t)s_lab[xs] : (uint32_t)__ldg(a.lab + xs);
+            }
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            unsigned fm = 0u;
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                const int32_t xs = x[v][s];
+                const uint32_t ls = l[v][s];
+                bool f = xs >= 0 && ls != lu;
+                if (OTHER && xs >= 0 && ls == kOther && lu == kOther) f = __ldg(a.comm + xs) != cfull;
+                fm |= f ? (1u << s) : 0u;
+                const bool tg = ls < k;                                  // invalid entries: kOther, never < k
+                if constexpr (PACK8) {
+                    const uint32_t inc = 1u << ((ls & 3u) * 8u);
+                    h0 += (tg && ls < 4u) ? inc : 0u;
+                    h1 += (tg && ls >= 4u) ? inc : 0u;
+                } else {
+                    const unsigned long long inc = 1ull << ((ls & 3u) * 16u);
+                    h0 += (tg && ls < 4u) ? inc : 0ull;
+                    h1 += (tg && ls >= 4u) ? inc : 0ull;
+                }
+                const bool below = f && xs < u32;                        // P+(u): foreign and above u
+                ppl += below ? 1 : 0;
+                ptl += (below && tg) ? 1 : 0;
+            }
+            // exclusive rank of this lane's first foreign entry in the piece round
+            const int c = __popc(fm);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o, G);
+                if ((int)g.lane >= o) incl += t;
+            }
+            const int tot = __shfl_sync(0xffffffffu, incl, G - 1, G);
+            int r = pc + incl - c;
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                const bool f = (fm >> s) & 1u;
+                if (f && wr) {
+                    pout[r] = x[v][s];
+                    lout[r] = (uint8_t)l[v][s];
+                }
+                r += f ? 1 : 0;
+            }
+            pc += tot;
+        }
+    }
+    pp_out = g.sum(ppl);
+    pt_out = g.sum(ptl);
+    pc_out = pc;
+    if constexpr (PACK8) {
+        // 8-bit lane fields -> 16-bit fields (even / odd columns), then group sums
+        // (a row has < 65536 entries on this path)
+        const uint32_t a0 = g.sum(h0 & 0x00FF00FFu), a1 = g.sum((h0 >> 8) & 0x00FF00FFu);
+        const uint32_t b0 = g.sum(h1 & 0x00FF00FFu), b1 = g.sum((h1 >> 8) & 0x00FF00FFu);
+        cnt[0] = (int)(a0 & 0xFFFFu); cnt[2] = (int)(a0 >> 16);
+        cnt[1] = (int)(a1 & 0xFFFFu); cnt[3] = (int)(a1 >> 16);
+        cnt[4] = (int)(b0 & 0xFFFFu); cnt[6] = (int)(b0 >> 16);
+        cnt[5] = (int)(b1 & 0xFFFFu); cnt[7] = (int)(b1 >> 16);
+    } else if (dw < 65536) {
+        h0 = g.sum(h0);
+        h1 = g.sum(h1);
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            cnt[c] = (int)((h0 >> (16 * c)) & 0xFFFFull);
+            cnt[c + 4] = (int)((h1 >> (16 * c)) & 0xFFFFull);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            cnt[c] = g.sum((int)((h0 >> (16 * c)) & 0xFFFFull));
+            cnt[c + 4] = g.sum((int)((h1 >> (16 * c)) & 0xFFFFull));
+        }
+    }
+}
+
+template <class GR> struct IsLock { static constexpr bool value = false; };
+template <int G> struct IsLock<LockGroup<G>> { static constexpr bool value = true; };
+
+// k <= 8: Steps 1, 2a-2d and the Step 3 inputs of u, in lockstep over the
+// groups of a warp (LockGroup: warp-uniform loop bounds; u < 0 = no vertex).
+// The row walk (walk_vec for lockstep groups, VEC pieces per lane per round;
+// walk_scalar for CTAs) gives |P(u)|, |P+(u)|, |P+_T(u)| and the histogram. The
+// lists pass reads P(u) and its labels back (L2) and takes a_u(c) from the lane
+// that computed it (shuffle).
+template <int U, class GR, int VEC = 0, bool PACK8 = false>
+__device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
+    const uint32_t k = (uint32_t)a.k;
+    const bool valid = u >= 0;
+    int64_t beg = 0;
+    int d = 0;
+    uint32_t lu = kOther;
+    int32_t cfull = 0;
+    if (valid) {
+        beg = a.rowptr[u];
+        d = (int)(a.rowptr[u + 1] - beg);
+        lu = a.lab[u];
+        if (lu == kOther) cfull = a.comm[u];
+    }
+    const bool wr = valid && !a.parity;
+    int pc, pp, pt;
+    int cnt[8];
+    if constexpr (VEC > 0 && IsLock<GR>::value) {
+        // warp-uniform: the full-id comparison only where some group needs it
+        if (__any_sync(0xffffffffu, lu == kOther))
+            walk_vec<VEC, PACK8, true>(a, u, beg, d, lu, cfull, wr, g, pc, pp, pt, cnt);
+        else
+            walk_vec<VEC, PACK8, false>(a, u, beg, d, lu, cfull, wr, g, pc, pp, pt, cnt);
+    } else {
+        walk_scalar<U>(a, u, beg, d, lu, cfull, wr, g, pc, pp, pt, cnt);
     }
     int T = 0, L_all = 0;
 #pragma unroll
@@ -497,7 +649,7 @@ __device__ __forceinline__ void block_max_to_scal(double v, unsigned long long *
     }
 }
 
-template <int G, int U, bool SMEM>
+template <int G, int U, bool SMEM, int VEC = 0, bool PACK8 = false>
 #ifndef RS_EXP_A_MINB
 #define RS_EXP_A_MINB 5      // warp kernels: resident blocks of 256 per SM (5: 51 registers, no spill; 6 spills)
 #endif
@@ -517,13 +669,19 @@ __global__ void __launch_bounds__(256, RS_EXP_A_MINB) k_phase_a_warp(PhaseAArgs 
         // lockstep: a warp takes 32 / G consecutive vertices per step, all its
         // lanes iterate together (a group past the end takes no vertex)
         LockGroup<G> g;
+        if constexpr (VEC > 0) {
+            // the label cache: a.hc bytes (a multiple of 16), 16-byte loads
+            for (int i = threadIdx.x; i < (a.hc >> 4); i += blockDim.x)
+                reinterpret_cast<int4 *>(s_lab)[i] = __ldg(reinterpret_cast<const int4 *>(a.lab) + i);
+            __syncthreads();
+        }
         constexpr int gpw = 32 / G;
         const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
         const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
         const int gi = (int)((threadIdx.x & 31u) / G);
         for (int64_t i0 = warp * gpw; i0 < a.nverts; i0 += nwarps * gpw) {
             const int64_t i = i0 + gi;
-            const double w = phase_a_vertex<U>(a, i < a.nverts ? a.vlo + i : -1, g);
+            const double w = phase_a_vertex<U, LockGroup<G>, VEC, PACK8>(a, i < a.nverts ? a.vlo + i : -1, g);
             wmax = w > wmax ? w : wmax;
         }
     }
@@ -550,14 +708,39 @@ __global__ void __launch_bounds__(kCtaThreads) k_phase_a_cta(PhaseAArgs a) {
 #ifndef RS_EXP_A_BLK
 #define RS_EXP_A_BLK 16   // warp-class grids: 148 x RS_EXP_A_BLK blocks of 8 warps (grid-stride)
 #endif
-template <int G, int U, bool SMEM>
+template <int G, int U, bool SMEM, int VEC = 0, bool PACK8 = false>
 static void launch_warp_bin(Ctx &c, PhaseAArgs a, cudaStream_t s) {
     const int64_t gpb = 256 / G;
     int64_t blocks = (a.nverts + gpb - 1) / gpb;
     blocks = std::min<int64_t>(blocks, 148 * RS_EXP_A_BLK);
     if (blocks < 1) return;
-    k_phase_a_warp<G, U, SMEM><<<(unsigned)blocks, 256, 0, s>>>(a);
+    const size_t dyn = VEC > 0 ? (size_t)a.hc : 0;
+    if (dyn > 48 * 1024)
+        cudaFuncSetAttribute(k_phase_a_warp<G, U, SMEM, VEC, PACK8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    k_phase_a_warp<G, U, SMEM, VEC, PACK8><<<(unsigned)blocks, 256, dyn, s>>>(a);
     c.launches++;
+}
+
+// the vectorised walk (walk_vec): V 16-byte pieces per lane per round; 8-bit
+// histogram fields when a lane's share of the class's longest row stays < 256
+template <int G>
+static void launch_vec_bin(Ctx &c, PhaseAArgs a, cudaStream_t s, int V, int64_t dhi) {
+    const bool p8 = (dhi + 3) / G + 4 * V < 256;
+    if (V >= 2) {
+        if (p8) launch_warp_bin<G, 4, false, 2, true>(c, a, s);
+        else launch_warp_bin<G, 4, false, 2, false>(c, a, s);
+    } else {
+        if (p8) launch_warp_bin<G, 4, false, 1, true>(c, a, s);
+        else launch_warp_bin<G, 4, false, 1, false>(c, a, s);
+    }
+}
+static int a_vec() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("RS_A_VEC");   // 0: the scalar walk; 1 / 2: pieces per lane per round
+        v = e ? std::max(0, std::min(2, atoi(e))) : 1;
+    }
+    return v;
 }
 
 #ifndef RS_EXP_A_CTA_CLS
@@ -609,6 +792,17 @@ static void launch_bins_a(Ctx &c, PhaseAArgs base, int64_t lo, int64_t hi) {
         } else {
             int G, U;
             a_config(cls, &G, &U);
+            const int V = a_vec();
+            const int64_t dhi = bin_lo(cls + 1) - 1;
+            if (V > 0) {
+                switch (G) {
+                    case 4: launch_vec_bin<4>(c, a, s, V, dhi); break;
+                    case 8: launch_vec_bin<8>(c, a, s, V, dhi); break;
+                    case 16: launch_vec_bin<16>(c, a, s, V, dhi); break;
+                    default: launch_vec_bin<32>(c, a, s, V, dhi); break;
+                }
+                continue;
+            }
             const int key = G * 10 + U;
             switch (key) {
                 case 42: launch_warp_bin<4, 2, false>(c, a, s); break;
@@ -641,6 +835,16 @@ cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool par
     a.plab = c.plab;
     a.bsum = (c.bsum_mode && !parity) ? c.bsum : nullptr;
     a.n = c.n; a.pplus = c.pplus; a.pc2 = c.pc2; a.bql = c.bql;
+    {
+        // label cache of the vec walk: the first hc vertex ids (highest degrees),
+        // RS_A_HC bytes per block (default 0: off)
+        static int hc_env = -1;
+        if (hc_env < 0) {
+            const char *e = getenv("RS_A_HC");
+            hc_env = e ? std::max(0, std::min(200 * 1024, atoi(e))) : 0;   // measured: 16 / 32 / 40 KB cost A +0.08 / +0.23 / +0.73 ms (the L1 it takes caches the hub labels already)
+        }
+        a.hc = (int32_t)(std::min<int64_t>(hc_env, c.n) & ~15ll);   // whole 16-byte pieces of lab
+    }
     if (c.k <= 8) launch_bins_a<false>(c, a, lo, hi);
     else launch_bins_a<true>(c, a, lo, hi);
     return cudaGetLastError();

@@ -355,7 +355,7 @@ extern "C" rs_status rs_load_csr(rs_ctx *ctx, int64_t n, const int64_t *row_offs
     }
     if (!fits) {
         CK(dalloc(&c.rowptr, n + 1));
-        CK(dalloc(&c.col, nnz));
+        CK(dalloc(&c.col, nnz + 4));    // + 4: Phase A reads rows as aligned 16-byte pieces
         CK(dalloc(&c.perm, n));
         CK(dalloc(&c.inv, n));
         const size_t scratch = 24 * (size_t)(n + 1) + (64u << 20);
@@ -649,6 +649,12 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
     if (c.sparse && c.variant)
         return fail(ctx, RS_EINVAL, "rs_score: the NEXT-3 variant flags need explicit targets (k <= 254)");
     if (c.xp) c.xp->score_begin();
+    // multi-GPU, RS_REPLICATE_A: every rank runs Phase A over all vertices (the
+    // replicated CSR and labels of the north_star's layout), so the only exchange
+    // is the Type-I limb reduce-scatter; otherwise Phase A is sharded by range and
+    // its outputs exchanged
+    c.rep_a = c.world > 1 && (flags & RS_REPLICATE_A);
+    const bool shard_a = c.world > 1 && !c.rep_a;
     c.hubs_folded = false;
     c.mg_packed = false;
     CK(cudaEventRecord(c.ev_phase[0], c.stream));
@@ -685,10 +691,10 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
             // the rows directly instead of rebuilding (measured E||D +0.18 ms).
             const char *ex = getenv("RS_EXP_BSUM");
             const bool dense_enough = c.nnz >= 8 * n * (int64_t)c.k;
-            c.bsum_mode = c.world > 1 || (c.k <= 8 && (ex ? ex[0] != '0' : dense_enough));
+            c.bsum_mode = shard_a || (c.k <= 8 && (ex ? ex[0] != '0' : dense_enough));
             // multi-GPU: Phase D reads the summed pushes and the gathered rows directly
             // (the rebuild would be a pass over all n k cells on every rank)
-            c.bsum_direct = c.bsum_mode && (c.world > 1 || (ex && ex[0] == '2'));
+            c.bsum_direct = c.bsum_mode && (shard_a || (ex && ex[0] == '2'));
         }
         if (c.bsum_mode) {
             if (c.dist_cap < n * c.k) {
@@ -705,11 +711,13 @@ extern "C" rs_status rs_score(rs_ctx *ctx, double *scores_out, rs_stats *stats_o
         // Phase A: border + histogram + weights + P lists + omega_max partials, the
         // orientation of G' and the B-table pushes
         fork(c);
-        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, false, c.head_lo, c.head_hi));   // own range
+        CK(rs::launch_phase_a_impl(c, ctx->l2t, ctx->l2n, false, shard_a ? c.head_lo : 0,
+                                   shard_a ? c.head_hi : n));   // own range (sharded) or all
         join(c);
     }
     CK(cudaEventRecord(c.ev_phase[1], c.stream));
-    if (c.world > 1) {
+    c.xar_bytes = c.xag_bytes = c.xrs_bytes = 0;
+    if (shard_a) {
         // multi-GPU: Phase A ran on this rank's vertices only; exchange what the
         // other phases read of the 2-hop neighbourhood (ms_phase[1])
         c.xp->tag = 1;

@@ -189,6 +189,7 @@ struct Ctx {
     int64_t pkm_cap = 0;
     int64_t *xg = nullptr;                     // world > 1: gm[0..n] | gpre[0..n] (exclusive prefixes)
     int64_t xg_cap = 0;
+    bool rep_a = false;                        // multi-GPU: Phase A replicated on every rank (RS_REPLICATE_A)
     bool mg_packed = false;                    // Phase E reads the packed runs (PRec start = gpre[x])
     int64_t xar_bytes = 0, xag_bytes = 0;      // world > 1: bytes all-reduced / all-gathered in the last rs_score
     int64_t xrs_bytes = 0;                     //   and reduce-scattered

@@ -26,11 +26,11 @@ def _cuda():
     rsb.load_library()
 
 
-def one_rank(s, g, k, K):
+def one_rank(s, g, k, K, flags=0):
     s.load_csr(g.rowptr, g.col)
     s.set_communities(g.comm, k)
     R = np.empty(g.n)
-    st = s.score(scores_out=R, stats=True, gather=True)
+    st = s.score(scores_out=R, stats=True, gather=True, flags=flags)
     ids, sc = s.topk(K)
     t1, t2 = s.triad_counts()
     f, T = s.counts()
@@ -39,7 +39,7 @@ def one_rank(s, g, k, K):
                 tri=st["n_triangles"], probes=st["n_probes"], omega_max=st["omega_max"])
 
 
-def run_world(g, k, K, world):
+def run_world(g, k, K, world, flags=0):
     import torch
     W = rsb.EmuWorld(world)
     out, err = [None] * world, []
@@ -48,7 +48,7 @@ def run_world(g, k, K, world):
         try:
             stream = torch.cuda.Stream(device=0)
             s = rsb.Scorer(0, stream.cuda_stream, rank=r, world=world, emu=W)
-            out[r] = one_rank(s, g, k, K)
+            out[r] = one_rank(s, g, k, K, flags)
             s.close()
         except Exception as e:  # reported by the main thread
             err.append(f"rank {r}: {e!r}")
@@ -69,13 +69,13 @@ CASES = [("orkut", 0.01, 5), ("lj", 0.004, 5), ("dblp", 0.05, 7)]
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("name,scale,k", CASES)
-def test_emulated_world_matches_single_gpu(name, scale, k, world):
+def test_emulated_world_matches_single_gpu(name, scale, k, world, flags=0):
     g = gen.config_graph(name, scale=scale)
     K = 50
     s = rsb.Scorer(0)
     ref = one_rank(s, g, k, K)
     s.close()
-    out = run_world(g, k, K, world)
+    out = run_world(g, k, K, world, flags)
     np.testing.assert_array_equal(sum(o["t2"] for o in out), ref["t2"])
     for r, o in enumerate(out):
         np.testing.assert_array_equal(o["t1"], ref["t1"])
@@ -97,6 +97,41 @@ def test_emulated_world_matches_single_gpu(name, scale, k, world):
     ck, ci = rsb.rs_local_candidates(ref["R"], np.arange(n, dtype=np.int32), K)
     mi, ms = rsb.rs_merge_candidates(ck, ci, min(K, n))
     assert np.array_equal(mi, ref["ids"])
+
+
+@pytest.mark.parametrize("world", [2, 8])
+@pytest.mark.parametrize("name,scale,k", CASES[:2])
+def test_emulated_world_replicated_phase_a(name, scale, k, world):
+    """RS_REPLICATE_A (the north_star's replicated CSR + labels): every rank runs
+    Phase A over all vertices, no Phase A exchange; bitwise the single GPU's
+    results, and the only exchanged bytes are the limb reduce-scatter (+ the
+    counters and the optional score gather)"""
+    test_emulated_world_matches_single_gpu(name, scale, k, world, flags=rsb.RS_REPLICATE_A)
+    g = gen.config_graph(name, scale=scale)
+    import torch
+    W = rsb.EmuWorld(world)
+    xb, err = [None] * world, []
+
+    def main(r):
+        try:
+            s = rsb.Scorer(0, torch.cuda.Stream(device=0).cuda_stream, rank=r, world=world, emu=W)
+            s.load_csr(g.rowptr, g.col)
+            s.set_communities(g.comm, k)
+            st = s.score(stats=True, flags=rsb.RS_REPLICATE_A)
+            xb[r] = (st["xchg_allreduce_bytes"], st["xchg_allgather_bytes"], st["xchg_reduce_scatter_bytes"])
+            s.close()
+        except Exception as e:
+            err.append(repr(e))
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    W.close()
+    assert not err, err
+    for ar, ag, rsc in xb:
+        assert ag == 0 and ar == 16 and rsc == 24 * g.n
 
 
 def test_emulated_world_tiny_and_errors():
