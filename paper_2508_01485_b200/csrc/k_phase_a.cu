@@ -413,19 +413,34 @@ template <int G> struct IsLock<LockGroup<G>> { static constexpr bool value = tru
 // walk_scalar for CTAs) gives |P(u)|, |P+(u)|, |P+_T(u)| and the histogram. The
 // lists pass reads P(u) and its labels back (L2) and takes a_u(c) from the lane
 // that computed it (shuffle).
+#ifndef RS_EXP_A_PF
+#define RS_EXP_A_PF 0        // vec walk: prefetch the group's next row into L2 while this vertex runs (measured: no gain, off)
+#endif
 template <int U, class GR, int VEC = 0, bool PACK8 = false>
-__device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g) {
+__device__ __forceinline__ double phase_a_vertex(const PhaseAArgs &a, int64_t u, GR &g, int64_t unext = -1) {
     const uint32_t k = (uint32_t)a.k;
     const bool valid = u >= 0;
     int64_t beg = 0;
     int d = 0;
     uint32_t lu = kOther;
     int32_t cfull = 0;
+    int64_t nb = -1, ne = 0;
+    if (RS_EXP_A_PF && VEC > 0 && unext >= 0) {     // issued with this vertex's own loads
+        nb = __ldg(a.rowptr + unext);
+        ne = __ldg(a.rowptr + unext + 1);
+    }
     if (valid) {
         beg = a.rowptr[u];
         d = (int)(a.rowptr[u + 1] - beg);
         lu = a.lab[u];
         if (lu == kOther) cfull = a.comm[u];
+    }
+    if (RS_EXP_A_PF && VEC > 0 && nb >= 0) {
+        // the next vertex's first two rounds of 16-byte pieces (a DRAM stream
+        // otherwise first touched after this vertex's whole dependent chain)
+        const int64_t p0 = (nb & ~3ll) + 4 * (int64_t)g.lane;
+        if (p0 < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.col + p0));
+        if (p0 + 4 * GR::size < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.col + p0 + 4 * GR::size));
     }
     const bool wr = valid && !a.parity;
     int pc, pp, pt;
@@ -681,7 +696,9 @@ __global__ void __launch_bounds__(256, RS_EXP_A_MINB) k_phase_a_warp(PhaseAArgs 
         const int gi = (int)((threadIdx.x & 31u) / G);
         for (int64_t i0 = warp * gpw; i0 < a.nverts; i0 += nwarps * gpw) {
             const int64_t i = i0 + gi;
-            const double w = phase_a_vertex<U, LockGroup<G>, VEC, PACK8>(a, i < a.nverts ? a.vlo + i : -1, g);
+            const int64_t inx = i + nwarps * gpw;          // this group's next vertex
+            const double w = phase_a_vertex<U, LockGroup<G>, VEC, PACK8>(a, i < a.nverts ? a.vlo + i : -1, g,
+                                                                         inx < a.nverts ? a.vlo + inx : -1);
             wmax = w > wmax ? w : wmax;
         }
     }

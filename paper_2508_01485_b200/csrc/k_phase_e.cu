@@ -218,17 +218,27 @@ __host__ __device__ constexpr size_t e_stride_bytes(int k) {
 // Orkut shape, E || D max / mean over ranks): e_blk 1 1.07 / 0.85 ms, 4 1.38 /
 // 1.22, 32 1.36 / 1.21, 256 1.38 / 1.21 -- keeping a y's items together on one
 // rank (filter reuse) loses to spreading them, so 1 is the default
-__device__ __forceinline__ unsigned long long e_item(unsigned long long qi, int r, int world, int blk) {
-    const unsigned long long B = (unsigned long long)blk;
-    return ((qi / B) * (unsigned long long)world + (unsigned long long)r) * B + qi % B;
+// (32-bit: item counts stay below 2^32; the common one-GPU / e_blk = 1 case is
+// a multiply-add, the default e_perm = 2 constant shifts -- profiled: the 64-bit
+// divisions of the general form were 2 % of the kernel's instructions)
+__device__ __forceinline__ unsigned e_item(unsigned qi, int r, int world, int blk) {
+    if (blk == 1) return qi * (unsigned)world + (unsigned)r;
+    const unsigned B = (unsigned)blk;
+    return ((qi / B) * (unsigned)world + (unsigned)r) * B + qi % B;
 }
 // within each group of kQBatch * P items, batch b takes items b, b + P,
 // b + 2P, ... (a P x kQBatch transpose of the heaviest-first order)
-__device__ __forceinline__ unsigned long long e_perm_map(unsigned long long g, int P, unsigned long long n_all) {
+__device__ __forceinline__ unsigned e_perm_map(unsigned g, int P, unsigned n_all) {
     if (P <= 1) return g;
-    const unsigned long long G = (unsigned long long)P * kQBatch, base = g - g % G, o = g % G;
+    if (P == 2) {
+        constexpr unsigned G2 = 2u * kQBatch;
+        const unsigned base = g - g % G2, o = g % G2;
+        if (base + G2 > n_all) return g;
+        return base + (o / kQBatch) + 2u * (o % kQBatch);
+    }
+    const unsigned G = (unsigned)P * kQBatch, base = g - g % G, o = g % G;
     if (base + G > n_all) return g;
-    return base + (o / kQBatch) + (unsigned long long)P * (o % kQBatch);
+    return base + (o / kQBatch) + (unsigned)P * (o % kQBatch);
 }
 __device__ __forceinline__ unsigned long long e_rank_items(unsigned long long n_all, int r, int world, int blk) {
     const unsigned long long B = (unsigned long long)blk;
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
     if (lane == 0) qnext = atomicAdd(queue_ctr, (unsigned long long)kQBatch);
     unsigned long long qbase = __shfl_sync(0xffffffffu, qnext, 0);
     unsigned long long qi = qbase;
-    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * e_perm_map(e_item(qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, n_all) + lane) : 0;
+    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (size_t)e_perm_map(e_item((unsigned)qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, (unsigned)n_all) + lane) : 0;
     // the items of one y are consecutive (a batch pop often brings two of them):
     // the filter, the sorted copy of P+(y) and y's weights built for the previous
     // item are reused when y repeats
@@ -338,7 +348,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         } else {
             qi++;
         }
-        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * e_perm_map(e_item(qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, n_all) + lane) : 0;
+        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (size_t)e_perm_map(e_item((unsigned)qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, (unsigned)n_all) + lane) : 0;
         // the item's predecessors x. A triangle carries a term only if two of its
         // vertices are targets: with both x and y targets every z < y of P+(x) is
         // probed, with one of them only those of the target run, with neither
@@ -860,6 +870,14 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
         a.head_hi = c.n;
         ylo = c.head_lo;
         yhi = c.head_hi;
+        if (c.rep_a) {
+            // Phase A replicated: every P-(y) is local, so the light warp tasks stride
+            // over ALL light y (balanced; a vertex range holds very unequal work)
+            ylo = 0;
+            yhi = c.n;
+            a.e_rank = c.rank;
+            a.e_world = c.world;
+        }
     }
     ah = a;
     if (c.world > 1) {

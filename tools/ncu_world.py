@@ -19,10 +19,12 @@ def main():
     p.add_argument("--config", default="orkut")
     p.add_argument("--world", type=int, default=8)
     p.add_argument("--k", type=int, default=5)
+    p.add_argument("--replicated", action="store_true", help="RS_REPLICATE_A (Phase A on every rank)")
     a = p.parse_args()
     import torch
     g = gen.config_graph(a.config)
     N = a.world
+    fl = rsb.RS_REPLICATE_A if a.replicated else 0
     W = rsb.EmuWorld(N)
     W.serial(True)
     bar = threading.Barrier(N)
@@ -35,13 +37,13 @@ def main():
             s.load_csr(g.rowptr, g.col)
             s.set_communities(g.comm, a.k)
             for _ in range(2):
-                s.score()
+                s.score(flags=fl)
             torch.cuda.synchronize()
             bar.wait()
             if r == 0:
                 torch.cuda.profiler.start()
             bar.wait()
-            st = s.score(stats=True)
+            st = s.score(stats=True, flags=fl)
             torch.cuda.synchronize()
             bar.wait()
             if r == 0:
