@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
     if (lane == 0) qnext = atomicAdd(queue_ctr, (unsigned long long)kQBatch);
     unsigned long long qbase = __shfl_sync(0xffffffffu, qnext, 0);
     unsigned long long qi = qbase;
-    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (size_t)e_perm_map(e_item((unsigned)qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, (unsigned)n_all) + lane) : 0;
+    int32_t rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (size_t)(a.e_local ? (unsigned)qi : e_perm_map(e_item((unsigned)qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, (unsigned)n_all)) + lane) : 0;
     // the items of one y are consecutive (a batch pop often brings two of them):
     // the filter, the sorted copy of P+(y) and y's weights built for the previous
     // item are reused when y repeats
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         } else {
             qi++;
         }
-        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (size_t)e_perm_map(e_item((unsigned)qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, (unsigned)n_all) + lane) : 0;
+        rec = (qi < n_items && lane < 8) ? __ldg(items_w + 8 * (size_t)(a.e_local ? (unsigned)qi : e_perm_map(e_item((unsigned)qi, a.e_rank, a.e_world, a.e_blk), a.e_perm, (unsigned)n_all)) + lane) : 0;
         // the item's predecessors x. A triangle carries a term only if two of its
         // vertices are targets: with both x and y targets every z < y of P+(x) is
         // probed, with one of them only those of the target run, with neither
@@ -764,10 +764,16 @@ __global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t
 // up to hundreds of chunks) hand the rest to a warp each (second loop), so no
 // thread serialises a hub's whole item list
 // (multi-GPU, gpre / gm non-null: y's runs are read packed)
+// multi-GPU (world > 1, items dealt one by one): only this rank's items g = rank
+// mod world are written, at g / world (the rank's heavy kernel reads them in order)
+__device__ __forceinline__ void e_put(EItem *items, int g, const EItem &e, int rank, int world) {
+    if (world == 1) items[g] = e;
+    else if (g % world == rank) items[g / world] = e;
+}
 __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
                             const PRec *__restrict__ pc2, const int64_t *__restrict__ rowptr,
                             const int64_t *__restrict__ gpre, const int64_t *__restrict__ gm, int64_t n_heavy,
-                            EItem *items) {
+                            EItem *items, int rank, int world) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += stride) {
         const int c = cnt[y], o = off[y];
@@ -782,7 +788,7 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         e.mbase = gm ? (uint32_t)gm[y] : 0u;
         for (int j = 0; j < c && j < 8; j++) {
             e.chunk = j;
-            items[o + j] = e;
+            e_put(items, o + j, e, rank, world);
         }
     }
     // a warp per y with more than 8 chunks
@@ -801,7 +807,7 @@ __global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__re
         e.mbase = gm ? (uint32_t)gm[y] : 0u;
         for (int j = 8 + lane; j < c; j += 32) {
             e.chunk = j;
-            items[o + j] = e;
+            e_put(items, o + j, e, rank, world);
         }
     }
 }
@@ -831,7 +837,7 @@ cudaError_t launch_e_items(Ctx &c) {
     return cudaSuccess;
 }
 
-static cudaError_t build_e_items(Ctx &c, EItems &it) {
+static cudaError_t build_e_items(Ctx &c, EItems &it, int deal_rank, int deal_world) {
     const int64_t nh = c.e_nbig;
     int32_t *cnt = (int32_t *)c.e_pre;
     int32_t *off = cnt + (nh + 1);
@@ -847,7 +853,7 @@ static cudaError_t build_e_items(Ctx &c, EItems &it) {
     if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
     cub::DeviceScan::ExclusiveSum(c.scratch, need, cnt, off, (int)(nh + 1), c.stream);
     const int64_t *gm = c.mg_packed ? c.xg : nullptr, *gpre = c.mg_packed ? c.xg + (c.n + 1) : nullptr;
-    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, c.pc2, c.rowptr, gpre, gm, nh, items);
+    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, c.pc2, c.rowptr, gpre, gm, nh, items, deal_rank, deal_world);
     c.launches += 3;
     it.items = items;
     it.total = off + nh;
@@ -897,8 +903,12 @@ static cudaError_t launch_e(Ctx &c, cudaStream_t light) {
     unsigned long long *ctr = c.scal + kScalCnt0;
     const int64_t n_heavy = c.e_nbig;                 // degree classes 5-7 (d >= 128)
     EItems it{nullptr, nullptr};
+    // multi-GPU with items dealt one by one: the build writes only this rank's
+    // (a scatter of all heavy items on every rank was ~40 us per rank at N = 8)
+    const bool deal = c.world > 1 && ah.e_blk == 1;
+    if (deal) ah.e_local = 1;
     if (n_heavy > 0) {
-        cudaError_t e = build_e_items(c, it);
+        cudaError_t e = build_e_items(c, it, deal ? c.rank : 0, deal ? c.world : 1);
         if (e != cudaSuccess) return e;
     }
     const size_t smem = (size_t)kWarpsE * e_stride_bytes(c.sparse ? 0 : c.k);

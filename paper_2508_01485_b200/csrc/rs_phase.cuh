@@ -36,6 +36,7 @@ struct CdeArgs {
     int32_t e_blk;                      // Phase E: heavy items dealt to the ranks in blocks of e_blk
     int32_t e_perm;                     // Phase E: the queue order interleaved over e_perm batches
     int32_t e_chunk;                    // Phase E: positions of P-(y) per heavy work item
+    int32_t e_local;                    // Phase E: the item list holds only this rank's items (dealt at build)
     int32_t mg;                         // multi-GPU: P+ runs packed (pplus = the gathered runs, PRec start
                                         // = packed offset); heavy P-(y) at item.mbase of pidx (packed)
     int64_t n_wide;                     // heads [0, n_wide) use the 3-limb Type-I accumulator
@@ -59,7 +60,7 @@ inline CdeArgs cde_args(Ctx &c) {
     a.perm = c.perm; a.lab = c.lab;
     a.n_wide = c.n_wide;
     a.head_lo = c.head_lo; a.head_hi = c.head_hi;
-    a.e_rank = 0; a.e_world = 1; a.e_blk = 1; a.e_perm = 1; a.e_chunk = c.e_chunk;
+    a.e_rank = 0; a.e_world = 1; a.e_blk = 1; a.e_perm = 1; a.e_chunk = c.e_chunk; a.e_local = 0;
     a.pwr = c.pwr; a.prv = c.prv; a.ctb = c.ctb; a.bq = c.bq;
     {
         // Phase E's per-item x slots (smem_red4): a grouped Type-I term is < 2 omega_max
