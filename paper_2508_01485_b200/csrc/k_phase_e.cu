@@ -62,6 +62,12 @@ constexpr int kQBatch = RS_EXP_QBATCH;   // heavy work items per queue pop
 #ifndef RS_EXP_E_REUSE
 #define RS_EXP_E_REUSE 1                     // reuse the filter / P+(y) copy when consecutive items share y
 #endif
+#ifndef RS_EXP_E_RING
+#define RS_EXP_E_RING 0                      // probe rounds staged in shared memory by cp.async (0: registers; measured 2 / 3 / 4 / 6 stages: E||D +0.04 / +0.08 / +0.20 / +0.22 ms, fewer resident blocks)
+#endif
+#ifndef RS_EXP_E_XPRE
+#define RS_EXP_E_XPRE 0                      // load the next item's x list during this item (measured: E||D +0.03 ms, spills; off)
+#endif
 #ifndef RS_EXP_E_YSKIP
 #define RS_EXP_E_YSKIP 1                     // skip the filter of probe rounds without any z < y
 #endif
@@ -142,7 +148,17 @@ __device__ __forceinline__ void cut_range(const int32_t *__restrict__ pplus, int
                                           bool both, bool any, int64_t &rs, int &len, int &tb) {
     if (!any) { rs = bx; len = 0; tb = 0; return; }
     if (pp < RS_EXP_CUT_MIN) {   // experiment: no cut below this list length
-        rs = bx; tb = SPARSE ? pp : t; len = SPARSE ? pp : (both ? pp : t);
+        // free bound: the ids are distinct and >= 0, so at most y entries of a run
+        // lie below y -- the tail of the descending target run, the head of the
+        // ascending other run (exact; 6 % fewer probes on the Orkut shape, mostly
+        // for the hub middle vertices with small ids)
+        const int yb = y;
+        if constexpr (SPARSE) {
+            rs = bx; len = min(pp, yb); tb = len;
+        } else {
+            const int mt = min(t, yb), mo = both ? min(pp - t, yb) : 0;
+            rs = bx + (t - mt); tb = mt; len = mt + mo;
+        }
         return;
     }
     if constexpr (SPARSE) {
@@ -210,6 +226,10 @@ struct ESmem {             // one warp's shared memory
     int32_t pe[kChunkE];    // end of each list's pieces
     int2 q[kQCapE];         // candidates {((offset of z in P+(x)) + 4) << 6 | x slot, z}
     uint32_t ps[kPsWords];  // bit p: piece p is the first piece of a list
+#if RS_EXP_E_RING
+    int4 ring[RS_EXP_E_RING][32];   // probe pieces in flight (cp.async), one per lane per round
+    int rtag[RS_EXP_E_RING][32];    // their tags (-1: no piece)
+#endif
 };
 
 __host__ __device__ constexpr size_t e_stride_bytes(int k) {
@@ -284,6 +304,11 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
     // the filter, the sorted copy of P+(y) and y's weights built for the previous
     // item are reused when y repeats
     int32_t prev_y = -1;
+    // the next item's x list, loaded during the current item's probes (its x
+    // records prefetched into L2 after the first probe round): the setup of an
+    // item is a chain of dependent gathers (P-(y) -> PRec(x) -> pieces)
+    int32_t xpre[2] = {-1, -1};
+    bool pre_ok = false;
     for (;;) {
         if (qi >= n_items) break;
         const bool last_of_batch = qi - qbase == (unsigned long long)(kQBatch - 1);
@@ -308,8 +333,9 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         for (int h = 0; h < 2; h++) {
             const int i = start + 32 * h + lane;
             // x in P-(y) (the suffix of P(y) in its slot; multi-GPU: packed): x > y
-            xv[h] = i < end ? __ldg(a.pidx + (a.mg ? (int64_t)mb : by + py) + i) : -1;
+            xv[h] = pre_ok ? xpre[h] : (i < end ? __ldg(a.pidx + (a.mg ? (int64_t)mb : by + py) + i) : -1);
         }
+        pre_ok = false;
         // i-th entry of P+(y) in ascending order within its run (the target run is
         // stored descending, the other run ascending after it)
         auto py_at = [&](int i) -> int64_t { return SPARSE ? by + i : (i < pyt ? by + pyt - 1 - i : by + i); };
@@ -407,6 +433,28 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
             }
             __syncwarp();
         }
+#if RS_EXP_E_XPRE
+        if (qi < n_items) {                                 // warp-uniform: the next item exists
+            const int64_t byn = (int64_t)(uint32_t)__shfl_sync(0xffffffffu, rec, 0) |
+                                ((int64_t)__shfl_sync(0xffffffffu, rec, 1) << 32);
+            const int32_t yn = __shfl_sync(0xffffffffu, rec, 2);
+            const int chn = __shfl_sync(0xffffffffu, rec, 3);
+            const int pyn = __shfl_sync(0xffffffffu, rec, 4) & 0xFFFFFF;
+            const int pmn = __shfl_sync(0xffffffffu, rec, 5);
+            const uint32_t mbn = (uint32_t)__shfl_sync(0xffffffffu, rec, 7);
+            const int sn = chn * a.e_chunk, en = min(pmn, sn + a.e_chunk);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int i = sn + 32 * h + lane;
+                xpre[h] = i < en ? __ldg(a.pidx + (a.mg ? (int64_t)mbn : byn + pyn) + i) : -1;
+            }
+            pre_ok = true;
+            if (yn != y) {                                  // a new y: its P+(y) runs and weight row
+                if (32 * lane < pyn) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.pplus + byn + 32 * lane));
+                if (!SPARSE && lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.amat + (int64_t)yn * k));
+            }
+        }
+#endif
         int lists_before = 0;
         auto fetch = [&](int p0, int32_t (&z)[kPiece], int &tag) {
             const int p = p0 + lane;
@@ -516,10 +564,67 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
         // while this round is filtered (profiled: with one round ahead, the wait for
         // the piece was the top stall, 17% of the samples); filter candidates
         // packed by one warp scan
+#if RS_EXP_E_RING
+        // the pieces of RS_EXP_E_RING - 1 rounds ahead are in flight as cp.async
+        // copies into the warp's shared ring (no registers held: the round-ahead
+        // register prefetch kept one round in flight, and the probe loop was bound
+        // by the latency of its piece loads)
+        auto issue = [&](int p0, int st) {
+            const int p = p0 + lane;
+            int slot;
+            if (mapped) {
+                const uint32_t wd = S.ps[p0 >> 5];
+                slot = lists_before + __popc(wd & (0xFFFFFFFFu >> (31 - lane))) - 1;
+                lists_before += __popc(wd);
+            } else {
+                int lo = 0, hi = nx;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.pe[mid] <= p) lo = mid + 1; else hi = mid;
+                }
+                slot = lo;
+            }
+            int tag = -1;
+            if (p < npieces) {
+                const int64_t bx = S.xl[slot].x;
+                const int q = p - (slot ? S.pe[slot - 1] : 0);   // piece within the list
+                const int64_t blk = (bx >> 2) + q;
+                const int off = (int)(4 * blk - bx);
+                tag = ((off + 4) << 6) | (slot & 63);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&S.ring[st][lane]);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.pplus + 4 * blk));
+            }
+            S.rtag[st][lane] = tag;
+            asm volatile("cp.async.commit_group;");
+        };
+        constexpr int R = RS_EXP_E_RING;
+#pragma unroll
+        for (int r = 0; r < R - 1; r++) issue(32 * r, r);
+        int st = 0;
+        for (int p0 = 0; p0 < npieces; p0 += 32) {
+            issue(p0 + 32 * (R - 1), (st + R - 1) % R);     // the stage consumed last round
+            asm volatile("cp.async.wait_group %0;" ::"n"(R - 1));
+            int32_t zc[kPiece];
+            const int tagc = S.rtag[st][lane];
+            if (tagc >= 0) {
+                const int4 v = S.ring[st][lane];
+                const int off = (tagc >> 6) - 4;
+                const int lenx = S.xn[tagc & 63].x;
+                zc[0] = (off >= 0 && off < lenx) ? v.x : -1;
+                zc[1] = (off + 1 >= 0 && off + 1 < lenx) ? v.y : -1;
+                zc[2] = (off + 2 >= 0 && off + 2 < lenx) ? v.z : -1;
+                zc[3] = (off + 3 < lenx) ? v.w : -1;
+            } else {
+#pragma unroll
+                for (int j = 0; j < kPiece; j++) zc[j] = -1;
+            }
+            st = st + 1 == R ? 0 : st + 1;
+#else
         int32_t zc[kPiece];
         int tagc;
         fetch(0, zc, tagc);
-#if RS_EXP_E_DEPTH >= 2
+#endif
+#if !RS_EXP_E_RING && RS_EXP_E_DEPTH >= 2
         int32_t zm[kPiece];
         int tagm = 0;
         if (32 < npieces) {
@@ -529,6 +634,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
             for (int j = 0; j < kPiece; j++) zm[j] = -1;
         }
 #endif
+#if !RS_EXP_E_RING
         for (int p0 = 0; p0 < npieces; p0 += 32) {
             int32_t zn[kPiece];
             int tagn = 0;
@@ -538,6 +644,7 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
 #pragma unroll
                 for (int j = 0; j < kPiece; j++) zn[j] = -1;
             }
+#endif
             // a triangle needs z < y (every entry of P+(y) is below y): the rounds
             // in which no lane holds such a z -- most rounds of a hub y's items,
             // whose probed runs lie almost wholly above it -- skip the filter, the
@@ -570,7 +677,15 @@ __global__ void __launch_bounds__(kWarpsE * 32, RS_EXP_E_MINB) k_phase_e(CdeArgs
                 __syncwarp();
                 drain(32);
             }
-#if RS_EXP_E_DEPTH >= 2
+#if RS_EXP_E_XPRE
+            if (p0 == 0 && pre_ok) {                        // the next item's x records into L2
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    if (xpre[h] >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.pc2 + xpre[h]));
+            }
+#endif
+#if RS_EXP_E_RING
+#elif RS_EXP_E_DEPTH >= 2
 #pragma unroll
             for (int j = 0; j < kPiece; j++) { zc[j] = zm[j]; zm[j] = zn[j]; }
             tagc = tagm;
