@@ -13,6 +13,7 @@ namespace rs {
 constexpr int kTkBlocks = 148 * 4;
 constexpr int kTkThreads = 256;
 constexpr int kTkSortMax = 4096;   // in-smem bitonic sort capacity
+constexpr int kTkGatherSlot = 2040; // tk_hist word: the compact path's candidate count
 
 // state slots at scal + kScalTk: [0] prefix, [1] krem (keys still to take at
 // the threshold), [2] count of keys strictly above the current prefix
@@ -41,9 +42,18 @@ __device__ __forceinline__ void tk_digit(int pass, int &shift, int &width) {
     shift = hi - width;
 }
 
+// the compact path (k_tk_gather): once the keys sharing the threshold's top
+// 22 bits -- and every key above them -- fit the final sort, the remaining
+// passes over all n scores are skipped (*skip = how many were gathered)
+__device__ __forceinline__ bool tk_skipped(const unsigned long long *skip) {
+    return skip && *skip <= (unsigned long long)kTkSortMax;
+}
+
 __global__ void __launch_bounds__(kTkThreads) k_tk_pass(const double *__restrict__ score, int64_t lo, int64_t hi,
                                                         int pass, unsigned long long *st, unsigned int *hist,
-                                                        unsigned int *ticket, TkFilter flt) {
+                                                        unsigned int *ticket, TkFilter flt,
+                                                        const unsigned long long *skip) {
+    if (tk_skipped(skip)) return;
     __shared__ unsigned int h[kTkBins];
     __shared__ unsigned long long s_sum[kTkThreads];
     __shared__ bool s_last;
@@ -110,7 +120,9 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_pass(const double *__restrict
 __global__ void __launch_bounds__(kTkThreads) k_tk_above(const double *__restrict__ score, int64_t lo, int64_t hi,
                                                          const unsigned long long *st, unsigned long long *cand_key,
                                                          int32_t *cand_id, unsigned long long *cursor,
-                                                         unsigned int *tie_cnt, int64_t chunk, TkFilter flt) {
+                                                         unsigned int *tie_cnt, int64_t chunk, TkFilter flt,
+                                                         const unsigned long long *skip) {
+    if (tk_skipped(skip)) return;
     __shared__ unsigned int s_ties;
     if (threadIdx.x == 0) s_ties = 0;
     __syncthreads();
@@ -139,7 +151,8 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_above(const double *__restric
 __global__ void __launch_bounds__(kTkThreads) k_tk_ties(const double *__restrict__ score, int64_t lo, int64_t hi,
                                                         const unsigned long long *st, unsigned long long *cand_key,
                                                         int32_t *cand_id, const unsigned int *tie_cnt, int64_t chunk,
-                                                        TkFilter flt) {
+                                                        TkFilter flt, const unsigned long long *skip) {
+    if (tk_skipped(skip)) return;
     __shared__ unsigned long long s_pre;
     __shared__ int s_w[kTkThreads / 32];
     const unsigned long long T = st[0];
@@ -175,15 +188,38 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_ties(const double *__restrict
     }
 }
 
+// after the first two digit passes (the top 22 key bits of the threshold are
+// known): every key whose top 22 bits are >= the threshold's -- the keys above
+// it and those sharing its digits -- appended to the candidates (any order);
+// *cnt counts them all. When they fit kTkSortMax the sort picks the K first by
+// (key desc, id asc) and the later passes return at once
+__global__ void __launch_bounds__(kTkThreads) k_tk_gather(const double *__restrict__ score, int64_t lo, int64_t hi,
+                                                          const unsigned long long *st, unsigned long long *cand_key,
+                                                          int32_t *cand_id, unsigned long long *cnt) {
+    const unsigned long long top = st[0] >> 42;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = score_key(score[i]);
+        if ((key >> 42) >= top) {
+            const unsigned long long p = atomicAdd(cnt, 1ull);
+            if (p < (unsigned long long)kTkSortMax) {
+                cand_key[p] = key;
+                cand_id[p] = (int32_t)i;
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ bool tk_before(unsigned long long ka, int32_t ia, unsigned long long kb, int32_t ib) {
     return ka > kb || (ka == kb && ia < ib);
 }
 
 // single CTA bitonic sort of cnt <= kTkSortMax candidates, writes the first `out` entries
 __global__ void __launch_bounds__(1024) k_tk_sort(const unsigned long long *cand_key, const int32_t *cand_id,
-                                                  int64_t cnt, int64_t out, int32_t *ids_out, double *scores_out) {
+                                                  int64_t cnt, int64_t out, int32_t *ids_out, double *scores_out,
+                                                  const unsigned long long *dev_cnt) {
     __shared__ unsigned long long sk[kTkSortMax];
     __shared__ int32_t si[kTkSortMax];
+    if (tk_skipped(dev_cnt)) cnt = (int64_t)*dev_cnt;   // the compact path's candidates
     int size = 1;
     while (size < cnt) size <<= 1;
     for (int i = threadIdx.x; i < size; i += blockDim.x) {
@@ -223,9 +259,10 @@ __global__ void k_tk_copy_out(const unsigned long long *key, const int32_t *id, 
 
 // sort `cnt` (key, id) candidates by (key desc, id asc) and emit the first `out`
 cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
-                         double *scores_out) {
+                         double *scores_out, bool compact) {
     if (cnt <= kTkSortMax) {
-        k_tk_sort<<<1, 1024, 0, c.stream>>>(key, id, cnt, out, ids_out, scores_out);
+        const unsigned long long *dev_cnt = compact ? c.tk_hist + kTkGatherSlot : nullptr;
+        k_tk_sort<<<1, 1024, 0, c.stream>>>(key, id, cnt, out, ids_out, scores_out, dev_cnt);
         c.launches++;
         return cudaGetLastError();
     }
@@ -247,7 +284,8 @@ cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t c
 
 // local top-K of score[lo, hi) into (cand_key, cand_id)[0, K') sorted, K' = min(K, hi-lo)
 cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
-                               int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi) {
+                               int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi,
+                               bool compact) {
     TkFilter flt{own_inv, own_lo, own_hi};
     unsigned long long *st = c.scal + kScalTk;
     // tk_hist (2048 u64): digit histogram u32[kTkBins] | ticket | cursor | per-block tie counts
@@ -259,18 +297,26 @@ cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsign
     unsigned long long init[3] = {0ull, (unsigned long long)K, 0ull};
     cudaMemcpyAsync(st, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
     cudaMemsetAsync(c.tk_hist, 0, sizeof(unsigned long long) * (kTkBins / 2 + 2), c.stream);
+    unsigned long long *gcnt = c.tk_hist + kTkGatherSlot;
+    const unsigned long long *skip = compact ? gcnt : nullptr;
+    if (compact) cudaMemsetAsync(gcnt, 0, sizeof(unsigned long long), c.stream);
     int blocks = (int)std::min<int64_t>((range + kTkThreads - 1) / kTkThreads, kTkBlocks);
     if (blocks < 1) blocks = 1;
     for (int pass = 0; pass < kTkPasses; pass++) {
-        k_tk_pass<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist, ticket, flt);
+        k_tk_pass<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, pass, st, hist, ticket, flt,
+                                                      pass >= 2 ? skip : nullptr);
         c.launches++;
+        if (compact && pass == 1) {
+            k_tk_gather<<<blocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, gcnt);
+            c.launches++;
+        }
     }
     const int64_t chunk = (range + kTkBlocks - 1) / kTkBlocks;
     const int cblocks = (int)std::max<int64_t>(1, (range + chunk - 1) / std::max<int64_t>(chunk, 1));
     k_tk_above<<<cblocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, cursor, tie_cnt,
-                                                     std::max<int64_t>(chunk, 1), flt);
+                                                     std::max<int64_t>(chunk, 1), flt, skip);
     k_tk_ties<<<cblocks, kTkThreads, 0, c.stream>>>(c.score, lo, hi, st, cand_key, cand_id, tie_cnt,
-                                                    std::max<int64_t>(chunk, 1), flt);
+                                                    std::max<int64_t>(chunk, 1), flt, skip);
     c.launches += 2;
     return cudaGetLastError();
 }

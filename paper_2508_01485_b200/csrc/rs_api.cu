@@ -15,9 +15,10 @@ namespace rs {
 cudaError_t launch_log2_table(Ctx &c, double *t, int64_t len);
 cudaError_t launch_phase_a_impl(Ctx &c, const double *l2t, int64_t l2n, bool parity, int64_t lo, int64_t hi);
 cudaError_t launch_topk_select(Ctx &c, int64_t K, int64_t lo, int64_t hi, unsigned long long *cand_key,
-                               int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi);
+                               int32_t *cand_id, const int32_t *own_inv, int64_t own_lo, int64_t own_hi,
+                               bool compact = false);
 cudaError_t tk_sort_emit(Ctx &c, unsigned long long *key, int32_t *id, int64_t cnt, int64_t out, int32_t *ids_out,
-                         double *scores_out);
+                         double *scores_out, bool compact = false);
 cudaError_t launch_partition(Ctx &c);
 }  // namespace rs
 
@@ -871,8 +872,16 @@ extern "C" rs_status rs_topk(rs_ctx *ctx, int64_t K, int32_t *ids_out, double *s
         if (scores_out && !dev_sc) sc_d = ctx->stage_f64;
     }
     if (c.world == 1) {
-        CK(rs::launch_topk_select(c, Kc, 0, c.n, ctx->cand_key, ctx->cand_id, nullptr, 0, 0));
-        CK(rs::tk_sort_emit(c, ctx->cand_key, ctx->cand_id, Kc, Kc, ids_d, sc_d));
+        // K <= 4096: the compact path (after two digit passes the keys sharing the
+        // threshold's top 22 bits, and those above, usually fit the final sort:
+        // the other four passes and the above / ties scans are skipped)
+        const bool compact = Kc <= 4096 && !getenv("RS_EXP_TK_FULL");
+        if (compact) {
+            s = ensure_cand(ctx, 4096);
+            if (s != RS_OK) return s;
+        }
+        CK(rs::launch_topk_select(c, Kc, 0, c.n, ctx->cand_key, ctx->cand_id, nullptr, 0, 0, compact));
+        CK(rs::tk_sort_emit(c, ctx->cand_key, ctx->cand_id, Kc, Kc, ids_d, sc_d, compact));
     } else {
         // local top-K of the owned head range, padded with sentinels, all-gathered,
         // then the same deterministic merge on every rank
