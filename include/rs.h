@@ -137,6 +137,17 @@ rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream, int rank, 
                          const uint8_t nccl_id[128]);
 /* Fill `id_out` (128 bytes, host) with a fresh ncclUniqueId. */
 rs_status rs_nccl_unique_id(uint8_t id_out[128]);
+/* Test hook: run every collective of the NCCL transport (the one rs_create_dist
+ * uses: all-reduce sum and max, all-gather, the grouped-broadcast all-gather of
+ * segments, the grouped-reduce reduce-scatter of segments) on a one-rank NCCL
+ * communicator on `device`, on `cuda_stream` (NULL: a stream of its own), over
+ * `bytes` (>= 64, multiple of 8) of device memory it allocates and frees, and
+ * check every result bit for bit on the host. Only one GPU is available to this
+ * build's tests; a world of one still resolves the library, creates a
+ * communicator and runs each call through NCCL's kernels. RS_OK, RS_ENCCL (no
+ * NCCL / a call failed), RS_ECUDA, RS_EINVAL (bad size); a wrong result is
+ * RS_ECUDA with the mismatch in rs_last_error(NULL). */
+rs_status rs_nccl_selftest(int device, void *cuda_stream, size_t bytes);
 
 /* Emulated multi-GPU world (tests, one GPU): `world` ranks are host threads of
  * one process, each with its own context from rs_create_emulated on the same

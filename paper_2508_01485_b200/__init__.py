@@ -69,6 +69,7 @@ SIGNATURES = [
     ("rs_create", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P]),
     ("rs_create_dist", ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, _P]),
     ("rs_nccl_unique_id", ctypes.c_int, [_P]),
+    ("rs_nccl_selftest", ctypes.c_int, [ctypes.c_int, _P, ctypes.c_size_t]),
     ("rs_destroy", None, [_P]),
     ("rs_last_error", ctypes.c_char_p, [_P]),
     ("rs_load_csr", ctypes.c_int, [_P, ctypes.c_int64, _P, _P, ctypes.c_uint32]),
@@ -162,6 +163,15 @@ def rs_nccl_unique_id() -> bytes:
     if st != RS_OK:
         raise RsError(st, load_library().rs_last_error(None).decode())
     return bytes(buf)
+
+
+def rs_nccl_selftest(device: int, stream=None, nbytes: int = 1 << 20) -> None:
+    """include/rs.h rs_nccl_selftest: every NCCL-transport collective on a
+    one-rank communicator, checked bit for bit; raises RsError on failure."""
+    lib = load_library()
+    st = lib.rs_nccl_selftest(int(device), _P(stream) if stream else None, int(nbytes))
+    if st != RS_OK:
+        raise RsError(st, lib.rs_last_error(None).decode())
 
 
 def rs_create_dist(device: int, stream, rank: int, world: int, nccl_id: bytes):

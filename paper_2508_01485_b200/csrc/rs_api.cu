@@ -189,6 +189,89 @@ extern "C" rs_status rs_nccl_unique_id(uint8_t id_out[128]) {
 #endif
 }
 
+#ifdef RS_WITH_NCCL
+// rs_nccl_selftest: each NcclXport collective on a one-rank communicator, results
+// checked bit for bit (world 1: every collective leaves / copies its input)
+static rs_status nccl_selftest_run(rs::Xport &xp, cudaStream_t s, size_t bytes) {
+    rs_ctx *ctx = nullptr;
+    const size_t nw = bytes / 8;
+    std::vector<unsigned long long> h(nw), back(nw);
+    for (size_t i = 0; i < nw; i++) h[i] = 0x9E3779B97F4A7C15ull * (i + 1) ^ (i << 7);
+    unsigned long long *a = nullptr, *b = nullptr;
+    CK(cudaMalloc((void **)&a, bytes));
+    rs_status st = RS_OK;
+    auto check = [&](const unsigned long long *d, const char *what) -> rs_status {
+        cudaError_t e = cudaMemcpyAsync(back.data(), d, bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return fail(nullptr, RS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        for (size_t i = 0; i < nw; i++)
+            if (back[i] != h[i])
+                return fail(nullptr, RS_ECUDA, std::string("rs_nccl_selftest: ") + what + " changed word " +
+                                                   std::to_string(i));
+        return RS_OK;
+    };
+    auto xk = [&](cudaError_t e, const char *what) -> rs_status {
+        if (e == cudaSuccess) return RS_OK;
+        return fail(nullptr, RS_ENCCL, std::string(what) + ": " + xp.msg);
+    };
+    const size_t off[1] = {0}, len_b[1] = {bytes}, len_w[1] = {nw};
+    cudaError_t e = cudaMalloc((void **)&b, bytes);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a, h.data(), bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) st = fail(nullptr, RS_ECUDA, std::string("rs_nccl_selftest: ") + cudaGetErrorString(e));
+    if (st == RS_OK) st = xk(xp.allreduce_u64(a, nw, false, s), "allreduce sum");
+    if (st == RS_OK) st = check(a, "allreduce sum");
+    if (st == RS_OK) st = xk(xp.allreduce_u64(a, nw, true, s), "allreduce max");
+    if (st == RS_OK) st = check(a, "allreduce max");
+    if (st == RS_OK) st = xk(xp.allgatherv(a, off, len_b, s), "allgatherv");
+    if (st == RS_OK) st = check(a, "allgatherv");
+    if (st == RS_OK) st = xk(xp.reduce_scatterv_u64(a, off, len_w, s), "reduce_scatterv");
+    if (st == RS_OK) st = check(a, "reduce_scatterv");
+    if (st == RS_OK) {
+        e = cudaMemsetAsync(b, 0, bytes, s);
+        if (e != cudaSuccess) st = fail(nullptr, RS_ECUDA, cudaGetErrorString(e));
+    }
+    if (st == RS_OK) st = xk(xp.allgather(a, b, bytes, s), "allgather");
+    if (st == RS_OK) st = check(b, "allgather");
+    cudaStreamSynchronize(s);
+    cudaFree(a);
+    if (b) cudaFree(b);
+    return st;
+}
+#endif
+
+extern "C" rs_status rs_nccl_selftest(int device, void *cuda_stream, size_t bytes) {
+#ifdef RS_WITH_NCCL
+    rs_ctx *ctx = nullptr;
+    if (bytes < 64 || bytes % 8) return fail(nullptr, RS_EINVAL, "rs_nccl_selftest: bytes must be >= 64, a multiple of 8");
+    std::string why;
+    if (!rs::nccl_api(&why)) return fail(nullptr, RS_ENCCL, why);
+    CK(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)cuda_stream, own = nullptr;
+    if (!s) {
+        CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+        s = own;
+    }
+    ncclUniqueId id;
+    ncclComm_t comm = nullptr;
+    rs_status st = RS_OK;
+    ncclResult_t r = NCCL.GetUniqueId(&id);
+    if (r == ncclSuccess) r = NCCL.CommInitRank(&comm, 1, id, 0);
+    if (r != ncclSuccess) {
+        st = fail(nullptr, RS_ENCCL, std::string("rs_nccl_selftest: communicator: ") + NCCL.GetErrorString(r));
+    } else {
+        rs::Xport *xp = rs::make_nccl_xport(comm, 1);
+        st = nccl_selftest_run(*xp, s, bytes);
+        delete xp;
+        NCCL.CommDestroy(comm);
+    }
+    if (own) cudaStreamDestroy(own);
+    return st;
+#else
+    (void)device; (void)cuda_stream; (void)bytes;
+    return fail(nullptr, RS_ENCCL, "librs built without NCCL");
+#endif
+}
+
 extern "C" rs_status rs_create_dist(rs_ctx **out, int device, void *cuda_stream, int rank, int world,
                                     const uint8_t nccl_id[128]) {
     if (world < 1 || rank < 0 || rank >= world || !nccl_id)

@@ -191,3 +191,19 @@ def test_emulated_world_serial_mode_repeats():
     for R, ph in out:
         assert np.array_equal(R.view(np.uint64), ref["R"].view(np.uint64))
         assert ph[0] > 0 and ph[2] > 0
+
+
+@pytest.mark.parametrize("nbytes", [64, 8 << 20])
+def test_nccl_transport_world1(nbytes):
+    """The NCCL transport of rs_create_dist on real hardware: a one-rank
+    communicator (only one GPU is available to these tests) runs every
+    collective the exchange uses -- all-reduce sum / max, all-gather, the
+    grouped-broadcast all-gather of segments, the grouped-reduce reduce-scatter
+    of segments -- through NCCL's kernels on a torch stream; librs checks each
+    result bit for bit (a world of one leaves / copies its input)."""
+    import torch
+    s = torch.cuda.Stream()
+    rsb.rs_nccl_selftest(torch.cuda.current_device(), s.cuda_stream, nbytes)
+    rsb.rs_nccl_selftest(torch.cuda.current_device(), None, nbytes)   # a stream of its own
+    with pytest.raises(rsb.RsError):
+        rsb.rs_nccl_selftest(torch.cuda.current_device(), None, 12)
