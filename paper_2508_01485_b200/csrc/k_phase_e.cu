@@ -34,7 +34,6 @@
 // the lanes. COUNT mode (parity getter) counts the ordered (head, mid) target
 // pairs instead.
 #include "rs_phase.cuh"
-#include <cub/cub.cuh>
 #include <cstdlib>
 
 namespace rs {
@@ -871,72 +870,146 @@ __global__ void __launch_bounds__(256, RS_EXP_LIGHT_MINB) k_phase_e_light(CdeArg
 // ---------------------------------------------------------------- work items (per step)
 // Heavy middle vertices (degree >= 128) are cut into chunks of e_chunk
 // positions of P(y); the chunk counts depend on the communities, so the item
-// list is rebuilt every step (count, scan, scatter), heaviest vertices first.
+// list is rebuilt every step (count, then scan + scatter), heaviest vertices first.
 // One GPU: chunks of kChunkE = 64 positions. Multi-GPU: shorter ones -- a
 // rank's share of the probes is 1/N, and a 64-position item can take ~16 K
 // probes (Orkut shape), about a whole warp's share at N = 8, so the last items
 // would set the kernel's length
-__global__ void k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t lo, int64_t hi, int chunk,
-                          int32_t *cnt) {
-    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= n_heavy; y += (int64_t)gridDim.x * blockDim.x) {
-        int c = 0;
-        if (y < n_heavy && y >= lo && y < hi) {   // multi-GPU: this rank's middle vertices only
-            const PRec p = pc2[y];
-            if (pr_plus(p) > 0 && p.y > pr_plus(p)) c = (p.y - pr_plus(p) + chunk - 1) / chunk;   // chunks of P-(y)
-        }
+// Block b of the item build owns the contiguous heavy vertices
+// [b * per, (b + 1) * per): k_e_count writes each y's chunk count and the
+// block's total; k_e_scatter adds the totals of the blocks before it (at most
+// kEItemBlocks values), scans its own range tile by tile and writes the items --
+// two launches of our own instead of count + CUB's device scan (two launches)
+// + scatter. A thread per y writes its first 8 items; the rare y with more
+// (hubs: up to hundreds of chunks) are written by a warp each, so no thread
+// serialises a hub's whole item list.
+constexpr int kEItemBlocks = 148 * 4, kEItemThreads = 256;
+__device__ __forceinline__ int e_chunks(const PRec &p, int chunk) {
+    return (pr_plus(p) > 0 && p.y > pr_plus(p)) ? (p.y - pr_plus(p) + chunk - 1) / chunk : 0;   // chunks of P-(y)
+}
+__global__ void __launch_bounds__(kEItemThreads) k_e_count(const PRec *__restrict__ pc2, int64_t n_heavy, int64_t per,
+                                                          int chunk, int32_t *cnt, int32_t *bsum) {
+    __shared__ int s_w[kEItemThreads / 32];
+    const int64_t lo = blockIdx.x * per, hi = min(n_heavy, lo + per);
+    int acc = 0;
+    for (int64_t y = lo + threadIdx.x; y < hi; y += blockDim.x) {
+        const int c = e_chunks(pc2[y], chunk);
         cnt[y] = c;
+        acc += c;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kEItemThreads / 32; w++) t += s_w[w];
+        bsum[blockIdx.x] = t;
     }
 }
-// a thread per heavy y writes its first 8 items; the rare y with more (hubs:
-// up to hundreds of chunks) hand the rest to a warp each (second loop), so no
-// thread serialises a hub's whole item list
-// (multi-GPU, gpre / gm non-null: y's runs are read packed)
 // multi-GPU (world > 1, items dealt one by one): only this rank's items g = rank
 // mod world are written, at g / world (the rank's heavy kernel reads them in order)
 __device__ __forceinline__ void e_put(EItem *items, int g, const EItem &e, int rank, int world) {
     if (world == 1) items[g] = e;
     else if (g % world == rank) items[g / world] = e;
 }
-__global__ void k_e_scatter(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
-                            const PRec *__restrict__ pc2, const int64_t *__restrict__ rowptr,
-                            const int64_t *__restrict__ gpre, const int64_t *__restrict__ gm, int64_t n_heavy,
-                            EItem *items, int rank, int world) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n_heavy; y += stride) {
-        const int c = cnt[y], o = off[y];
-        if (c == 0) continue;
-        const PRec p = pc2[y];
-        EItem e;
-        e.by = gpre ? gpre[y] : rowptr[y];
-        e.y = (int32_t)y;
-        e.pyl = p.x;                                  // |P+(y)| | lab(y) << 24
-        e.pm = p.y - pr_plus(p);
-        e.pyt = pr_plus_t(p);
-        e.mbase = gm ? (uint32_t)gm[y] : 0u;
-        for (int j = 0; j < c && j < 8; j++) {
-            e.chunk = j;
-            e_put(items, o + j, e, rank, world);
-        }
+// (multi-GPU, gpre / gm non-null: y's runs are read packed)
+__global__ void __launch_bounds__(kEItemThreads) k_e_scatter(const int32_t *__restrict__ cnt,
+                                                            const int32_t *__restrict__ bsum, int nblk,
+                                                            const PRec *__restrict__ pc2,
+                                                            const int64_t *__restrict__ rowptr,
+                                                            const int64_t *__restrict__ gpre,
+                                                            const int64_t *__restrict__ gm, int64_t n_heavy,
+                                                            int64_t per, int32_t *total, EItem *items, int rank,
+                                                            int world) {
+    __shared__ int s_w[kEItemThreads / 32];
+    __shared__ int s_off[kEItemThreads];
+    __shared__ unsigned s_big[kEItemThreads / 32];
+    __shared__ int s_base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // the block's base: the totals of the blocks before it
+    int pre = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += blockDim.x) pre += bsum[b];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if (lane == 0) s_w[wid] = pre;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kEItemThreads / 32; w++) t += s_w[w];
+        s_base = t;
     }
-    // a warp per y with more than 8 chunks
-    const int lane = threadIdx.x & 31;
-    for (int64_t y = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; y < n_heavy; y += stride >> 5) {
-        const int c = cnt[y];
-        if (c <= 8) continue;
-        const int o = off[y];
-        const PRec p = pc2[y];
-        EItem e;
-        e.by = gpre ? gpre[y] : rowptr[y];
-        e.y = (int32_t)y;
-        e.pyl = p.x;
-        e.pm = p.y - pr_plus(p);
-        e.pyt = pr_plus_t(p);
-        e.mbase = gm ? (uint32_t)gm[y] : 0u;
-        for (int j = 8 + lane; j < c; j += 32) {
-            e.chunk = j;
-            e_put(items, o + j, e, rank, world);
+    __syncthreads();
+    int base = s_base;
+    const int64_t lo = blockIdx.x * per, hi = min(n_heavy, lo + per);
+    for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
+        const int64_t y = t0 + threadIdx.x;
+        const int c = y < hi ? cnt[y] : 0;
+        // block exclusive scan of c
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
+        __syncthreads();                                  // s_w / s_off of the previous tile are read
+        if (lane == 31) s_w[wid] = incl;
+        __syncthreads();
+        int wpre = 0, tile = 0;
+#pragma unroll
+        for (int w = 0; w < kEItemThreads / 32; w++) {
+            const int v = s_w[w];
+            wpre += w < wid ? v : 0;
+            tile += v;
+        }
+        const int o = base + wpre + incl - c;
+        s_off[threadIdx.x] = o;
+        EItem e;
+        if (c > 0) {
+            const PRec p = pc2[y];
+            e.by = gpre ? gpre[y] : rowptr[y];
+            e.y = (int32_t)y;
+            e.pyl = p.x;                                  // |P+(y)| | lab(y) << 24
+            e.pm = p.y - pr_plus(p);
+            e.pyt = pr_plus_t(p);
+            e.mbase = gm ? (uint32_t)gm[y] : 0u;
+            for (int j = 0; j < c && j < 8; j++) {
+                e.chunk = j;
+                e_put(items, o + j, e, rank, world);
+            }
+        }
+        // the tile's y with more than 8 chunks: a warp each (each warp publishes
+        // its mask of them; the warps take them round robin)
+        const unsigned big = __ballot_sync(0xffffffffu, c > 8);
+        if (lane == 0) s_big[wid] = big;
+        __syncthreads();                                  // s_off and s_big of this tile written
+        int seen = 0;
+        for (int w = 0; w < kEItemThreads / 32; w++) {
+            unsigned m = s_big[w];
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1;
+                if (seen++ % (kEItemThreads / 32) != wid) continue;
+                const int ti = 32 * w + bit;
+                const int64_t yb = t0 + ti;
+                const int cb = cnt[yb], ob = s_off[ti];
+                const PRec p = pc2[yb];
+                EItem eb;
+                eb.by = gpre ? gpre[yb] : rowptr[yb];
+                eb.y = (int32_t)yb;
+                eb.pyl = p.x;
+                eb.pm = p.y - pr_plus(p);
+                eb.pyt = pr_plus_t(p);
+                eb.mbase = gm ? (uint32_t)gm[yb] : 0u;
+                for (int j = 8 + lane; j < cb; j += 32) {
+                    eb.chunk = j;
+                    e_put(items, ob + j, eb, rank, world);
+                }
+            }
+        }
+        base += tile;
     }
+    if (blockIdx.x == nblk - 1 && threadIdx.x == 0) *total = base;   // the last block ends at the total
 }
 
 // load time: buffers sized for any community assignment (grow-only)
@@ -953,8 +1026,8 @@ cudaError_t launch_e_items(Ctx &c) {
     c.e_chunk = c.world >= 5 ? 16 : c.world >= 2 ? 32 : kChunkE;
     if (const char *ev = getenv("RS_EXP_ECHUNK")) c.e_chunk = std::min(kChunkE, std::max(1, atoi(ev)));
     c.e_extra = nh + c.nnz / c.e_chunk + 1;       // item capacity
-    // layout: cnt[nh+1] | off[nh+1] | items[cap] (EItem)
-    const size_t bytes = sizeof(int32_t) * 2 * (size_t)(nh + 1) + sizeof(EItem) * (size_t)c.e_extra + 16;
+    // layout: cnt[nh+1] | block totals[kEItemBlocks] | total | items[cap] (EItem)
+    const size_t bytes = sizeof(int32_t) * ((size_t)(nh + 1) + kEItemBlocks + 1) + sizeof(EItem) * (size_t)c.e_extra + 16;
     if (bytes <= c.e_bytes) return cudaSuccess;
     if (c.e_pre) cudaFree(c.e_pre);
     c.e_pre = nullptr;
@@ -967,23 +1040,20 @@ cudaError_t launch_e_items(Ctx &c) {
 static cudaError_t build_e_items(Ctx &c, EItems &it, int deal_rank, int deal_world) {
     const int64_t nh = c.e_nbig;
     int32_t *cnt = (int32_t *)c.e_pre;
-    int32_t *off = cnt + (nh + 1);
-    EItem *items = (EItem *)(((uintptr_t)(off + (nh + 1)) + 15) & ~(uintptr_t)15);
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nh + 256) / 256, 148 * 4));
+    int32_t *bsum = cnt + (nh + 1);
+    int32_t *total = bsum + kEItemBlocks;
+    EItem *items = (EItem *)(((uintptr_t)(total + 1) + 15) & ~(uintptr_t)15);
     // every heavy middle vertex (multi-GPU too: their P-(y) lists are exchanged,
     // and the ranks stride over the items)
-    k_e_count<<<blocks, 256, 0, c.stream>>>(c.pc2, nh, 0, c.n, c.e_chunk, cnt);
-    // the prefix is CUB's device scan (a few microseconds; a one-CTA scan of our
-    // own measured 0.27 ms: one block cannot keep enough loads in flight)
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(nh + 1), c.stream);
-    if (need > c.scratch_bytes) return cudaErrorMemoryAllocation;
-    cub::DeviceScan::ExclusiveSum(c.scratch, need, cnt, off, (int)(nh + 1), c.stream);
+    const int64_t per = std::max<int64_t>(1, (nh + kEItemBlocks - 1) / kEItemBlocks);
+    const int nblk = (int)std::max<int64_t>(1, (nh + per - 1) / per);
+    k_e_count<<<nblk, kEItemThreads, 0, c.stream>>>(c.pc2, nh, per, c.e_chunk, cnt, bsum);
     const int64_t *gm = c.mg_packed ? c.xg : nullptr, *gpre = c.mg_packed ? c.xg + (c.n + 1) : nullptr;
-    k_e_scatter<<<blocks, 256, 0, c.stream>>>(cnt, off, c.pc2, c.rowptr, gpre, gm, nh, items, deal_rank, deal_world);
-    c.launches += 3;
+    k_e_scatter<<<nblk, kEItemThreads, 0, c.stream>>>(cnt, bsum, nblk, c.pc2, c.rowptr, gpre, gm, nh, per, total,
+                                                      items, deal_rank, deal_world);
+    c.launches += 2;
     it.items = items;
-    it.total = off + nh;
+    it.total = total;
     return cudaGetLastError();
 }
 
