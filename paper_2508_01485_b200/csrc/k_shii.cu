@@ -15,6 +15,7 @@
 // Both processes are monotone, so the final set does not depend on the order of
 // the atomics. Per (seed, run) the device returns {influenced, outside}.
 #include "rs_internal.cuh"
+#include <vector>
 
 namespace rs {
 
@@ -118,6 +119,172 @@ cudaError_t launch_shii_run(Ctx &c, int32_t seed_o, int model, double p, uint64_
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((tail + 255) / 256, 148 * 8));
     k_sh_reset<<<(unsigned)blocks, 256, 0, c.stream>>>(act, list, tail);   // act back to all-zero
     c.launches++;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- IC, batched
+// Up to 64 (seed, run) diffusions of the IC model at once, bit j of a vertex's
+// word = diffusion j: act[v] the diffusions in which v is active, fr[v] those in
+// which v became active in the last level. A level takes every frontier vertex
+// u (a warp each) and every edge u -> b: the diffusions j active at u, not yet
+// at b, whose coin of u -> b succeeds (run r_j's salt, the same coin as one
+// diffusion at a time) activate b. IC's influenced set is reachability over the
+// succeeding edges, so it does not depend on the order of the atomics; the
+// adjacency of a frontier vertex is read once per level for all 64 diffusions
+// instead of once per diffusion.
+struct ShBatchArgs {
+    const int64_t *rowptr;
+    const int32_t *col;
+    const int32_t *perm;
+    int all_live;
+    uint64_t thr;
+    uint64_t st[64];            // run salt of diffusion j
+    unsigned long long *act;    // n
+    unsigned long long *fr;     // n, this level's new bits (read and cleared)
+    unsigned long long *fn;     // n, the next level's new bits
+    const int32_t *cur;         // this level's frontier vertices
+    int32_t *nxt;               // the next level's
+    unsigned long long *ctr;    // next frontier length
+};
+
+__global__ void __launch_bounds__(256) k_shb_level(ShBatchArgs a, int64_t len) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t f = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); f < len; f += nw) {
+        const int32_t u = a.cur[f];
+        const unsigned long long F = a.fr[u];
+        __syncwarp();
+        if (lane == 0) a.fr[u] = 0ull;               // written only by this level's readers
+        const uint64_t uo = (uint64_t)(uint32_t)a.perm[u];
+        for (int64_t e = a.rowptr[u] + lane; e < a.rowptr[u + 1]; e += 32) {
+            const int32_t b = a.col[e];
+            unsigned long long cand = F & ~*(volatile unsigned long long *)(a.act + b);
+            if (!cand) continue;
+            unsigned long long live = cand;
+            if (!a.all_live) {
+                const uint64_t key = (uo << 32) | (uint64_t)(uint32_t)a.perm[b];
+                live = 0ull;
+                while (cand) {
+                    const int j = __ffsll((long long)cand) - 1;
+                    cand &= cand - 1ull;
+                    if (sh_mix64(a.st[j] ^ key) < a.thr) live |= 1ull << j;
+                }
+            }
+            if (!live) continue;
+            const unsigned long long old = atomicOr(a.act + b, live);
+            const unsigned long long newly = live & ~old;
+            if (!newly) continue;
+            const unsigned long long oldn = atomicOr(a.fn + b, newly);
+            if (oldn == 0ull) a.nxt[atomicAdd(a.ctr, 1ull)] = b;
+        }
+    }
+}
+
+// the seeds: diffusion j starts at internal vertex seed[j]
+__global__ void k_shb_seed(const int32_t *seed, int nb, unsigned long long *act, unsigned long long *fr, int32_t *cur,
+                           unsigned long long *ctr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ctr[0] = 0ull;
+    for (int j = 0; j < nb; j++) {
+        const int32_t u = seed[j];
+        act[u] |= 1ull << j;
+        if (fr[u] == 0ull) cur[ctr[0]++] = u;
+        fr[u] |= 1ull << j;
+    }
+}
+
+// per diffusion j: influenced = active vertices, outside = those whose community
+// differs from the seed's (c0[j]); lane l counts bits l and l + 32
+__global__ void __launch_bounds__(256) k_shb_count(const unsigned long long *__restrict__ act,
+                                                   const int32_t *__restrict__ perm,
+                                                   const int32_t *__restrict__ comm_orig, int64_t n,
+                                                   const int32_t *__restrict__ c0, int nb,
+                                                   unsigned long long *out) {
+    __shared__ unsigned int s_cnt[4 * 32];
+    for (int i = threadIdx.x; i < 4 * 32; i += blockDim.x) s_cnt[i] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int32_t c0a = lane < nb ? c0[lane] : 0, c0b = lane + 32 < nb ? c0[lane + 32] : 0;
+    unsigned int ia = 0, oa = 0, ib = 0, ob = 0;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += warps * 32) {
+        const int64_t v0 = base + lane;
+        const unsigned long long A0 = v0 < n ? act[v0] : 0ull;
+        const int32_t cv0 = A0 ? comm_orig[perm[v0]] : 0;
+        unsigned nzm = __ballot_sync(0xffffffffu, A0 != 0ull);
+        while (nzm) {
+            const int src = __ffs(nzm) - 1;
+            nzm &= nzm - 1u;
+            const unsigned long long A = __shfl_sync(0xffffffffu, A0, src);
+            const int32_t cv = __shfl_sync(0xffffffffu, cv0, src);
+            const unsigned a1 = (unsigned)(A >> lane) & 1u, a2 = (unsigned)(A >> (lane + 32)) & 1u;
+            ia += a1;
+            oa += a1 & (unsigned)(cv != c0a);
+            ib += a2;
+            ob += a2 & (unsigned)(cv != c0b);
+        }
+    }
+    atomicAdd(&s_cnt[lane], ia);
+    atomicAdd(&s_cnt[32 + lane], ib);
+    atomicAdd(&s_cnt[64 + lane], oa);
+    atomicAdd(&s_cnt[96 + lane], ob);
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        const int j = threadIdx.x;
+        if (j < nb) {
+            atomicAdd(out + 2 * j, (unsigned long long)s_cnt[j]);
+            atomicAdd(out + 2 * j + 1, (unsigned long long)s_cnt[64 + j]);
+        }
+    }
+}
+
+// nb <= 64 IC diffusions: diffusion j from internal seed seed_d[j] (device) with
+// run salt st[j]; c0_d[j] its community; {influenced, outside} per diffusion to
+// out2 (host, 2 nb). buf: 3 n u64 + 2 n int32 + 64 B counters, device.
+cudaError_t launch_shii_ic_batch(Ctx &c, int nb, const int32_t *seed_d, const int32_t *c0_d, const uint64_t *st,
+                                 double p, unsigned long long *buf, int64_t *out2) {
+    cudaError_t e;
+    const int64_t n = c.n;
+    unsigned long long *act = buf, *fa = buf + n, *fb = buf + 2 * n;
+    int32_t *la = (int32_t *)(buf + 3 * n), *lb = la + n;
+    unsigned long long *ctr = (unsigned long long *)(lb + n);   // [0] list length, [2, 2 + 2 nb) counts
+    if ((e = cudaMemsetAsync(buf, 0, sizeof(unsigned long long) * 3 * n, c.stream))) return e;
+    if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (2 + 128), c.stream))) return e;
+    k_shb_seed<<<1, 32, 0, c.stream>>>(seed_d, nb, act, fa, la, ctr);
+    c.launches++;
+    ShBatchArgs a;
+    a.rowptr = c.rowptr; a.col = c.col; a.perm = c.perm;
+    a.all_live = p >= 1.0;
+    a.thr = p >= 1.0 ? 0ull : (uint64_t)ldexp(p, 64);
+    for (int j = 0; j < 64; j++) a.st[j] = j < nb ? st[j] : 0ull;
+    a.act = act;
+    a.ctr = ctr;
+    unsigned long long len = 0;
+    if ((e = cudaMemcpyAsync(&len, ctr, sizeof(len), cudaMemcpyDeviceToHost, c.stream))) return e;
+    if ((e = cudaStreamSynchronize(c.stream))) return e;
+    bool flip = false;
+    while (len > 0) {
+        a.fr = flip ? fb : fa;
+        a.fn = flip ? fa : fb;
+        a.cur = flip ? lb : la;
+        a.nxt = flip ? la : lb;
+        if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), c.stream))) return e;
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(((int64_t)len + 7) / 8, 148 * 16));
+        k_shb_level<<<(unsigned)blocks, 256, 0, c.stream>>>(a, (int64_t)len);
+        c.launches++;
+        if ((e = cudaMemcpyAsync(&len, ctr, sizeof(len), cudaMemcpyDeviceToHost, c.stream))) return e;
+        if ((e = cudaStreamSynchronize(c.stream))) return e;
+        flip = !flip;
+    }
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_shb_count<<<(unsigned)blocks, 256, 0, c.stream>>>(act, c.perm, c.comm_in, n, c0_d, nb, ctr + 2);
+    c.launches++;
+    std::vector<unsigned long long> h(2 * (size_t)nb);
+    if ((e = cudaMemcpyAsync(h.data(), ctr + 2, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost,
+                             c.stream)))
+        return e;
+    if ((e = cudaStreamSynchronize(c.stream))) return e;
+    for (int j = 0; j < 2 * nb; j++) out2[j] = (int64_t)h[j];
     return cudaGetLastError();
 }
 

@@ -1095,6 +1095,61 @@ extern "C" rs_status rs_shii(rs_ctx *ctx, const int32_t *S, int64_t nS, int32_t 
     CK(cudaMemcpy(hS.data(), S, sizeof(int32_t) * nS, is_device_ptr(S) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
     for (int64_t i = 0; i < nS; i++)
         if (hS[i] < 0 || hS[i] >= c.n) return fail(ctx, RS_EINVAL, "rs_shii: vertex id out of range");
+    if (model == RS_DIFFUSE_IC) {
+        // IC: up to 64 (seed, run) diffusions at once (k_shii.cu, launch_shii_ic_batch),
+        // diffusion j = (s, r) in seed-major order; the means summed in run order as below
+        const int64_t total = nS * (int64_t)runs;
+        std::vector<int64_t> res(2 * total);
+        std::vector<int32_t> hu(64), hc(64);
+        std::vector<uint64_t> st(64);
+        unsigned long long *bb = nullptr;
+        const size_t nbb = 3 * (size_t)c.n + (2 * sizeof(int32_t) * (size_t)c.n + 7) / 8 + 2 + 128 + 64;
+        CK(rs::dmalloc(&bb, sizeof(unsigned long long) * nbb));
+        int32_t *dsc = (int32_t *)(bb + nbb - 64);          // seeds | communities (64 each)
+        cudaError_t e = cudaSuccess;
+        std::vector<int32_t> hinv(1), hcomm(1);
+        for (int64_t j0 = 0; j0 < total && e == cudaSuccess; j0 += 64) {
+            const int nb = (int)std::min<int64_t>(64, total - j0);
+            for (int j = 0; j < nb && e == cudaSuccess; j++) {
+                const int64_t s = (j0 + j) / runs, r = (j0 + j) % runs;
+                st[j] = host_mix64(seed + (uint64_t)(2 * r + model + 1) * 0xD1B54A32D192ED03ull);
+                if (r == 0 || j == 0) {
+                    e = cudaMemcpyAsync(hinv.data(), c.inv + hS[s], sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
+                    if (e == cudaSuccess)
+                        e = cudaMemcpyAsync(hcomm.data(), c.comm_in + hS[s], sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                            c.stream);
+                    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+                }
+                hu[j] = hinv[0];
+                hc[j] = hcomm[0];
+            }
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(dsc, hu.data(), sizeof(int32_t) * 64, cudaMemcpyHostToDevice, c.stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(dsc + 64, hc.data(), sizeof(int32_t) * 64, cudaMemcpyHostToDevice, c.stream);
+            if (e == cudaSuccess)
+                e = rs::launch_shii_ic_batch(c, nb, dsc, dsc + 64, st.data(), p, bb, res.data() + 2 * j0);
+        }
+        cudaFree(bb);
+        if (e != cudaSuccess) return fail(ctx, RS_ECUDA, std::string("rs_shii: ") + cudaGetErrorString(e));
+        double setmean = 0.0;
+        for (int64_t s = 0; s < nS; s++) {
+            double acc = 0.0;
+            for (int32_t r = 0; r < runs; r++) {
+                const int64_t j = s * runs + r;
+                if (influenced_out) {
+                    influenced_out[j * 2] = res[2 * j];
+                    influenced_out[j * 2 + 1] = res[2 * j + 1];
+                }
+                acc += (double)res[2 * j + 1] / (double)res[2 * j];
+            }
+            const double sh = acc / (double)runs;
+            if (shii_out) shii_out[s] = sh;
+            setmean += sh;
+        }
+        if (mean_out) *mean_out = setmean / (double)nS;
+        return RS_OK;
+    }
     char *buf = nullptr;
     const size_t nb = sizeof(unsigned int) * c.n + 2 * sizeof(int32_t) * c.n + 64;
     CK(rs::dmalloc(&buf, nb));

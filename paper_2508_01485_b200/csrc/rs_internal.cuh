@@ -332,6 +332,8 @@ cudaError_t launch_phase_e(Ctx &c);
 cudaError_t launch_phase_d(Ctx &c);
 cudaError_t launch_finalize(Ctx &c);
 size_t awcc_scratch_bytes(int64_t M, int J1, int64_t cap, int64_t nS);
+cudaError_t launch_shii_ic_batch(Ctx &c, int nb, const int32_t *seed_d, const int32_t *c0_d, const uint64_t *st,
+                                 double p, unsigned long long *buf, int64_t *out2);
 cudaError_t launch_shii_run(Ctx &c, int32_t seed_o, int model, double p, uint64_t st, unsigned int *act,
                             int32_t *cnt, int32_t *list, unsigned long long *ctr, int64_t out2[2]);
 cudaError_t launch_awcc_degrees(Ctx &c, const int32_t *S_dev, int64_t nS, int64_t *deg_dev);
