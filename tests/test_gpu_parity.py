@@ -312,6 +312,26 @@ def test_shii_parity(model, p, name, scale):
     assert mg == mo
 
 
+@pytest.mark.parametrize("model,p", [("ic", 0.1), ("ic", 1.0), ("lt", 0.0)])
+def test_shii_parity_many_diffusions(model, p):
+    """more (seed, run) diffusions than one IC batch holds (64): 29 seeds x 3 runs
+    = 87, the second batch starting inside seed 21's runs; counts per (seed, run)
+    exact, means bitwise the oracle's (DESIGN C-31)"""
+    g = gen.config_graph("orkut", 0.003)
+    s = rsb.Scorer(0)
+    s.load_csr(g.rowptr, g.col)
+    s.set_communities(g.comm, 5)
+    rng = np.random.default_rng(29)
+    S = rng.choice(g.n, size=29, replace=False).astype(np.int32)
+    S[7] = S[3]                                    # a repeated seed
+    og, pg, mg = s.shii(S, model, p, 3, 0xC0FFEE)
+    s.close()
+    oo, po, mo = oracle.shii(g, S, model, p, 3, 0xC0FFEE)
+    assert np.array_equal(og, oo)
+    assert np.array_equal(pg.view(np.uint64), po.view(np.uint64))
+    assert mg == mo
+
+
 def test_shii_errors():
     g, _ = gen.load_fixture("karate")
     s = rsb.Scorer(0)
